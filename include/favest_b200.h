@@ -1,0 +1,103 @@
+/*
+ * favest_b200.h — C ABI of the B200-native FaVeST forward / adjoint vector
+ * spherical harmonic transforms (VSHT).
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (pure Python, /root/reference/pkg/src/favest) dispatches its scalar
+ * backends from two entry points; each function below replaces one of them:
+ *
+ *   fv_forward_grid    <- forward_favest(..., path="fast-scalar"|"auto")
+ *                         favest/transforms.py:79-147, with its scalar stage
+ *                         _forward_fast_values favest/scalar.py:146-154 and the
+ *                         CG assembly favest/transforms.py:120-146
+ *   fv_adjoint_grid    <- adjoint_favest(coeffs, rule|TensorGrid, ...)
+ *                         favest/transforms.py:150-181 with
+ *                         build_adjoint_coupling favest/coupling.py:200-240 and
+ *                         _adjoint_fast_values favest/scalar.py:170-179
+ *   fv_adjoint_points  <- adjoint_favest(coeffs, points) (direct route)
+ *                         favest/transforms.py:150-181 with
+ *                         _adjoint_direct_values favest/scalar.py:120-128
+ *   fv_plan_create_grid <- the per-grid state the reference rebuilds on every
+ *                         call: TensorGrid (favest/scalar.py:29-84),
+ *                         legendre_table (favest/legendre.py:36-75),
+ *                         build_cg_tables (favest/coupling.py:143-170)
+ *
+ * Data layout (all device pointers, caller-owned, contiguous, float64):
+ *   samples T   complex128 [B][N][3], N = n_theta * n_phi ring-major points
+ *               (favest/scalar.py:66-74), components x, y, z
+ *   coeffs a, b complex128 [B][(L+1)^2], flat index l*l + l + m
+ *               (favest/core.py:23-37); entry 0 must be 0
+ *   points      float64 [M][3] unit vectors
+ * Complex numbers are interleaved (re, im) doubles.
+ *
+ * Semantics: pure functions of their inputs, asynchronous on `stream`
+ * (a cudaStream_t, may be NULL for the legacy stream).  A plan is not safe for
+ * concurrent calls; distinct plans are independent.  Reductions run in a fixed
+ * order: results are bitwise reproducible run to run on the same device.
+ *
+ * Status codes: FV_OK; FV_EINVAL mirrors the reference's ValueError
+ * conditions (message via fv_last_error(), same wording); FV_ECUDA, FV_ENOMEM
+ * and FV_ENCCL are runtime failures (RuntimeError on the Python side).
+ */
+#ifndef FAVEST_B200_H
+#define FAVEST_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FV_OK 0
+#define FV_EINVAL 1
+#define FV_ECUDA 2
+#define FV_ENCCL 3
+#define FV_ENOMEM 4
+
+typedef struct fvPlan fvPlan;
+
+/* Version string of the library ("favest_b200 <version> sm_100a"). */
+const char* fv_version(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* fv_last_error(void);
+
+/*
+ * Grid plan for vector degree L on an iso-latitude tensor grid.
+ * ring_theta_host / ring_weight_host: n_theta host doubles, colatitudes
+ * strictly increasing in (0, pi) and per-point weights including the 2*pi/n_phi
+ * factor (TensorGrid, favest/scalar.py:29-61) — passed through verbatim, never
+ * recomputed.  Requires n_phi >= 2(L+1)+1
+ * (favest/transforms.py:63-72).  max_batch bounds B of later calls.
+ */
+int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const double* ring_theta_host,
+                        const double* ring_weight_host, int max_batch, int device);
+
+/* Plan for the scattered-point adjoint at vector degree L. */
+int fv_plan_create_points(fvPlan** out, int L, int max_batch, int device);
+
+void fv_plan_destroy(fvPlan* plan);
+
+/* Plan properties: 1 if the grid was folded about the equator (mirror pairs). */
+int fv_plan_info(const fvPlan* plan, int* L, int* n_theta, int* n_phi, int* n_pairs, int* paired);
+
+/* Forward VSHT of B tangent fields on the plan's grid: T -> (a, b). */
+int fv_forward_grid(fvPlan* plan, const double* T, double* a, double* b, int B, void* stream);
+
+/* Adjoint VSHT on the plan's grid: (a, b) -> T (Cartesian components). */
+int fv_adjoint_grid(fvPlan* plan, const double* a, const double* b, double* T, int B, void* stream);
+
+/* Adjoint VSHT at M scattered unit points: (a, b) -> T [B][M][3]. */
+int fv_adjoint_points(fvPlan* plan, const double* xyz, long long M, const double* a, const double* b,
+                      double* T, int B, void* stream);
+
+/*
+ * Stage timing of the last call on this plan (milliseconds, CUDA events on
+ * the call's stream; only filled when fv_set_profiling(plan, 1)).
+ * stage: 0 fft, 1 fold, 2 legendre, 3 cg.  Returns -1 if unavailable.
+ */
+int fv_set_profiling(fvPlan* plan, int enable);
+double fv_stage_ms(const fvPlan* plan, int stage);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FAVEST_B200_H */

@@ -1,0 +1,72 @@
+"""ctypes binding of ``libfavest_b200.so`` (C ABI: include/favest_b200.h).
+
+The library is the only compute path: if it is missing or cannot be loaded
+the calls raise — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .build import LIBPATH
+
+FV_OK, FV_EINVAL, FV_ECUDA, FV_ENCCL, FV_ENOMEM = 0, 1, 2, 3, 4
+
+#: every symbol include/favest_b200.h declares
+EXPORTED = (
+    "fv_version", "fv_last_error", "fv_plan_create_grid", "fv_plan_create_points",
+    "fv_plan_destroy", "fv_plan_info", "fv_forward_grid", "fv_adjoint_grid",
+    "fv_adjoint_points", "fv_set_profiling", "fv_stage_ms",
+)
+
+_lib = None
+
+
+def load(path: str | None = None) -> ctypes.CDLL:
+    """Load (once) and prototype the shared library."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIBPATH
+    if not os.path.exists(p):
+        raise RuntimeError(
+            f"{os.path.basename(p)} is not built; run `python -m paper_1908_00041_b200.build` "
+            "(the CUDA extension is the only compute path, there is no CPU fallback)"
+        )
+    lib = ctypes.CDLL(p)
+    vp, i, d, ll = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_longlong
+    dp = ctypes.POINTER(ctypes.c_double)
+    ip = ctypes.POINTER(ctypes.c_int)
+    sig = {
+        "fv_version": (ctypes.c_char_p, []),
+        "fv_last_error": (ctypes.c_char_p, []),
+        "fv_plan_create_grid": (i, [ctypes.POINTER(vp), i, i, i, dp, dp, i, i]),
+        "fv_plan_create_points": (i, [ctypes.POINTER(vp), i, i, i]),
+        "fv_plan_destroy": (None, [vp]),
+        "fv_plan_info": (i, [vp, ip, ip, ip, ip, ip]),
+        "fv_forward_grid": (i, [vp, vp, vp, vp, i, vp]),
+        "fv_adjoint_grid": (i, [vp, vp, vp, vp, i, vp]),
+        "fv_adjoint_points": (i, [vp, vp, ll, vp, vp, vp, i, vp]),
+        "fv_set_profiling": (i, [vp, i]),
+        "fv_stage_ms": (d, [vp, i]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    """Map a C status code to the reference's exception types."""
+    if rc == FV_OK:
+        return
+    msg = load().fv_last_error().decode() or f"favest_b200 error {rc}"
+    if rc == FV_EINVAL:
+        raise ValueError(msg)
+    if rc == FV_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)

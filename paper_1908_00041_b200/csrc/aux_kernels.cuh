@@ -1,0 +1,279 @@
+// Setup, layout and Clebsch-Gordan kernels around the Legendre contraction.
+//
+//   seeds_kernel      Pbar_m^m(t_p) for every order and ring pair, extended
+//                     range (favest/legendre.py:60-65)
+//   ab_kernel         recurrence coefficients a_lm, b_lm (favest/legendre.py:70-71)
+//   fold_fwd_kernel   ring spectra -> folded, weighted U/V/W combos in DMMA
+//                     fragment order (favest/transforms.py:109-112,
+//                     favest/scalar.py:149-152)
+//   cg_fwd_kernel     F^U, F^V, F^W -> a_lm, b_lm (favest/transforms.py:120-146)
+//   cg_adj_kernel     a_lm, b_lm -> merged g^X, g^Y, g^Z in fragment order
+//                     (favest/coupling.py:200-240, favest/transforms.py:165-175)
+#pragma once
+#include "common.cuh"
+
+namespace fv {
+
+constexpr double INV_SQRT_4PI_D = 0.28209479177387814;  // 1/sqrt(4*pi), favest/legendre.py:24
+
+// One thread per ring pair; sequential over m exactly like the reference's
+// diagonal loop, renormalising by 2^512 below 2^-512 (oracle.seed_table).
+__global__ void seeds_kernel(const double* __restrict__ pair_s, int nPpad, int Lt, double* seed_x,
+                             int* seed_e) {
+  int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nPpad) return;
+  const double s = pair_s[p];
+  double cur = INV_SQRT_4PI_D;
+  int e = 0;
+  seed_x[p] = cur;
+  seed_e[p] = 0;
+  for (int m = 1; m <= Lt; ++m) {
+    const double c = sqrt((2 * m + 1) / (2.0 * m));
+    cur = __dmul_rn(__dmul_rn(-c, s), cur);
+    if (fabs(cur) < 0x1p-512 && cur != 0.0) {
+      cur *= 0x1p512;
+      e -= XR_SHIFT;
+    }
+    seed_x[(size_t)m * nPpad + p] = cur;
+    seed_e[(size_t)m * nPpad + p] = e;
+  }
+}
+
+// a_l, b_l for l = m+2..Lt, stored m-major at abofs[m] + (l - m - 2).
+__global__ void ab_kernel(int Lt, const long long* __restrict__ abofs, double2* ab) {
+  const int m = blockIdx.y;
+  const int l = m + 2 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (l > Lt) return;
+  const long long L2 = (long long)l * l, M2 = (long long)m * m;
+  const double lf = (double)l;
+  const double a = sqrt((4.0 * lf * lf - 1.0) / (double)(L2 - M2));
+  const double lm1 = lf - 1.0;
+  const double b = sqrt((lm1 * lm1 - (double)M2) / (4.0 * (lm1 * lm1) - 1.0));
+  ab[abofs[m] + (l - m - 2)] = make_double2(a, b);
+}
+
+// Forward fold.  Thread per (local order mi, pair p, field b):
+//   C_n = combo of the three Cartesian ring spectra at bin +-m of the north ring,
+//   E = w_n C_n + w_s C_s, O = w_n C_n - w_s C_s, times sigma_{-m} for the -m bin,
+// written at X[mi][chunk][par][ks][nt][lane] (B operand fragment order).
+struct FoldArgs {
+  const double2* S;     // [comp][field][ring][n_phi], all B_total fields
+  double* X;
+  const int* pair_n;
+  const int* pair_s;
+  const double* ring_w;
+  int n_phi, n_theta, B_total, b0, nfields, NT, nPpad, nchunks, m_begin, m_count;
+};
+
+__global__ void fold_fwd_kernel(FoldArgs a) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int mi = blockIdx.y;
+  const int b = blockIdx.z;  // 0..nfields (== nfields: padding columns)
+  if (p >= a.nPpad) return;
+  const int m = a.m_begin + mi;
+  const int chunk = p >> 5, ks = (p >> 2) & 7, q = p & 3;
+  const size_t xbase = ((size_t)mi * a.nchunks + chunk) * (2 * 8 * a.NT * 32);
+  auto put = [&](int par, int n, double v) {
+    a.X[xbase + ((size_t)(par * 8 + ks) * a.NT + (n >> 3)) * 32 + ((n & 7) << 2) + q] = v;
+  };
+  if (b == a.nfields) {  // zero the padding columns of this pair
+    for (int n = 12 * a.nfields; n < 8 * a.NT; ++n) {
+      put(0, n, 0.0);
+      put(1, n, 0.0);
+    }
+    return;
+  }
+  const int rn = a.pair_n[p], rs = a.pair_s[p];
+  for (int sgn = 0; sgn < 2; ++sgn) {
+    double2 E[3], O[3];
+    if (rn < 0 || (sgn == 1 && m == 0)) {
+      for (int c = 0; c < 3; ++c) E[c] = O[c] = make_double2(0.0, 0.0);
+    } else {
+      const int bin = sgn ? (a.n_phi - m) % a.n_phi : m;
+      const double sig = (sgn == 1 && (m & 1)) ? -1.0 : 1.0;
+      double2 Tn[3], Ts[3];
+      for (int k = 0; k < 3; ++k) {
+        const size_t base = ((size_t)k * a.B_total + a.b0 + b) * a.n_theta;
+        Tn[k] = a.S[(base + rn) * a.n_phi + bin];
+        Ts[k] = rs >= 0 ? a.S[(base + rs) * a.n_phi + bin] : make_double2(0.0, 0.0);
+      }
+      const double wn = a.ring_w[rn];
+      const double ws = rs >= 0 ? a.ring_w[rs] : 0.0;
+      // U = -T1 + i T2, V = T1 + i T2, W = T3 (favest/transforms.py:112), after the FFT
+      double2 Cn[3], Cs[3];
+      Cn[0] = make_double2(-Tn[0].x - Tn[1].y, -Tn[0].y + Tn[1].x);
+      Cn[1] = make_double2(Tn[0].x - Tn[1].y, Tn[0].y + Tn[1].x);
+      Cn[2] = Tn[2];
+      Cs[0] = make_double2(-Ts[0].x - Ts[1].y, -Ts[0].y + Ts[1].x);
+      Cs[1] = make_double2(Ts[0].x - Ts[1].y, Ts[0].y + Ts[1].x);
+      Cs[2] = Ts[2];
+      for (int c = 0; c < 3; ++c) {
+        const double nr = wn * Cn[c].x, ni = wn * Cn[c].y;
+        if (rs >= 0) {
+          const double sr = ws * Cs[c].x, si = ws * Cs[c].y;
+          E[c] = make_double2(sig * (nr + sr), sig * (ni + si));
+          O[c] = make_double2(sig * (nr - sr), sig * (ni - si));
+        } else {  // unpaired ring: both parities see the ring itself
+          E[c] = O[c] = make_double2(sig * nr, sig * ni);
+        }
+      }
+    }
+    for (int c = 0; c < 3; ++c) {
+      const int n = 12 * b + 4 * c + 2 * sgn;
+      put(0, n, E[c].x);
+      put(0, n + 1, E[c].y);
+      put(1, n, O[c].x);
+      put(1, n + 1, O[c].y);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward Clebsch-Gordan assembly: favest/transforms.py:120-146
+// ---------------------------------------------------------------------------
+struct CgFwdArgs {
+  const double* F;      // rows tri(l, |m|), ncolF doubles: col 12b + 4c + 2s + ri
+  double2* A;           // (B_total, K) div coefficients
+  double2* Bc;          // (B_total, K) curl coefficients
+  int L, ncolF, B_total, b0, nfields;
+};
+
+__device__ __forceinline__ double2 f_read(const CgFwdArgs& a, int b, int comp, long long l, long long m) {
+  // scalar coefficient F^comp_{l,m}, zero outside 0 <= l <= L+1, |m| <= l
+  if (l < 0 || l > a.L + 1 || llabs(m) > l) return make_double2(0.0, 0.0);
+  const long long am = llabs(m);
+  const int sgn = (m < 0) ? 1 : 0;
+  const double* row = a.F + ((size_t)l * (l + 1) / 2 + am) * a.ncolF;
+  return *reinterpret_cast<const double2*>(row + 12 * b + 4 * comp + 2 * sgn);
+}
+
+__global__ void cg_fwd_kernel(CgFwdArgs a) {
+  const long long l = blockIdx.y;
+  const long long am = blockIdx.x * blockDim.x + threadIdx.x;
+  if (am > l) return;
+  const double is2 = 0.7071067811865475;  // favest/transforms.py:46 (1/np.sqrt(2.0))
+  const long long K = (long long)(a.L + 1) * (a.L + 1);
+  for (int sg = 0; sg < (am == 0 ? 1 : 2); ++sg) {
+    const long long M = sg ? -am : am;
+    // table values at the source positions (l+dl, M+dm); zero if out of range
+    auto xi_at = [&](int i, long long ls, long long ms) -> double {
+      if (ls < 0 || ls > a.L + 1 || llabs(ms) > ls) return 0.0;
+      return xi_coef(i, ls, ms);
+    };
+    auto mu_at = [&](int i, long long ls, long long ms) -> double {
+      if (ls < 0 || ls > a.L + 1 || llabs(ms) > ls) return 0.0;
+      return mu_coef(i, ls, ms);
+    };
+    const double x1 = xi_at(1, l - 1, M - 1), x2 = xi_at(2, l + 1, M - 1);
+    const double x3 = xi_at(3, l - 1, M + 1), x4 = xi_at(4, l + 1, M + 1);
+    const double x5 = xi_at(5, l - 1, M), x6 = xi_at(6, l + 1, M);
+    const double u1 = mu_at(1, l, M - 1), u2 = mu_at(2, l, M), u3 = mu_at(3, l, M + 1);
+    for (int b = 0; b < a.nfields; ++b) {
+      const double2 fu_a = f_read(a, b, 0, l - 1, M - 1), fu_b = f_read(a, b, 0, l + 1, M - 1);
+      const double2 fv_a = f_read(a, b, 1, l - 1, M + 1), fv_b = f_read(a, b, 1, l + 1, M + 1);
+      const double2 fw_a = f_read(a, b, 2, l - 1, M), fw_b = f_read(a, b, 2, l + 1, M);
+      const double2 fu_c = f_read(a, b, 0, l, M - 1), fv_c = f_read(a, b, 1, l, M + 1);
+      const double2 fw_c = f_read(a, b, 2, l, M);
+      // a = 1/sqrt2 * (x1 fu + x2 fu + x3 fv + x4 fv) + x5 fw + x6 fw
+      double ar = is2 * (((x1 * fu_a.x + x2 * fu_b.x) + x3 * fv_a.x) + x4 * fv_b.x) + x5 * fw_a.x + x6 * fw_b.x;
+      double ai = is2 * (((x1 * fu_a.y + x2 * fu_b.y) + x3 * fv_a.y) + x4 * fv_b.y) + x5 * fw_a.y + x6 * fw_b.y;
+      // b = -i/sqrt2 (u1 fu + u3 fv) - i u2 fw
+      const double sr = u1 * fu_c.x + u3 * fv_c.x, si = u1 * fu_c.y + u3 * fv_c.y;
+      double br = is2 * si + u2 * fw_c.y;
+      double bi = -is2 * sr - u2 * fw_c.x;
+      if (l == 0) ar = ai = br = bi = 0.0;  // favest/transforms.py:145-146
+      const size_t o = (size_t)(a.b0 + b) * K + l * l + l + M;
+      a.A[o] = make_double2(ar, ai);
+      a.Bc[o] = make_double2(br, bi);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// adjoint Clebsch-Gordan: favest/coupling.py:227-239 and transforms.py:168-175.
+// Thread per (table degree l <= L+1, order |m|) and row slot; writes sigma_m * g
+// into the fragment-ordered G tiles of order |m| (padding rows / columns -> 0).
+// ---------------------------------------------------------------------------
+struct CgAdjArgs {
+  const double2* A;     // (B_total, K) div
+  const double2* Bc;    // (B_total, K) curl
+  double* G;
+  const long long* gofs;    // fragment mode: tile offset (units of 512*NT doubles) per order
+  const long long* rowofs;  // row mode: row offset per order (rows of 12*nfields doubles)
+  int L, NT, B_total, b0, nfields, m_begin;
+  int rows_mode;            // 0: DMMA fragment tiles (grid path), 1: plain rows (points path)
+};
+
+__device__ __forceinline__ double2 c_read(const double2* t, const CgAdjArgs& a, int b, long long l, long long m) {
+  if (l < 0 || l > a.L || llabs(m) > l) return make_double2(0.0, 0.0);
+  return t[(size_t)(a.b0 + b) * (a.L + 1) * (a.L + 1) + l * l + l + m];
+}
+
+__global__ void cg_adj_kernel(CgAdjArgs a) {
+  const int mi = blockIdx.y;
+  const long long am = a.m_begin + mi;
+  const int Lt = a.L + 1;
+  const int nrows = Lt + 1 - (int)am;
+  const int nlc = (nrows + 63) / 64;
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;  // 0 .. 64*nlc-1
+  if (row >= (a.rows_mode ? nrows : 64 * nlc)) return;
+  const long long l = am + row;
+  const int lc = row >> 6, idx = row & 63;
+  const int par = idx & 1, k = idx >> 1, ks = k >> 2, q = k & 3;
+  double* Gt = a.rows_mode ? a.G + (size_t)(a.rowofs[am] + row) * (12 * a.nfields)
+                           : a.G + (size_t)(a.gofs[am] + lc) * (2 * 8 * a.NT * 32);
+  auto put = [&](int n, double v) {
+    if (a.rows_mode)
+      Gt[n] = v;
+    else
+      Gt[((size_t)(par * 8 + ks) * a.NT + (n >> 3)) * 32 + ((n & 7) << 2) + q] = v;
+  };
+  if (!a.rows_mode)
+    for (int n = 12 * a.nfields; n < 8 * a.NT; ++n) put(n, 0.0);
+  const bool live = l <= Lt;
+  const double is2 = 0.7071067811865475;
+  for (int sg = 0; sg < 2; ++sg) {
+    const long long m = sg ? -am : am;
+    const bool on = live && !(sg == 1 && am == 0);
+    double x1 = 0, x2 = 0, x3 = 0, x4 = 0, x5 = 0, x6 = 0, u1 = 0, u2 = 0, u3 = 0;
+    if (on) {
+      x1 = xi_coef(1, l, m); x2 = xi_coef(2, l, m); x3 = xi_coef(3, l, m);
+      x4 = xi_coef(4, l, m); x5 = xi_coef(5, l, m); x6 = xi_coef(6, l, m);
+      u1 = mu_coef(1, l, m); u2 = mu_coef(2, l, m); u3 = mu_coef(3, l, m);
+    }
+    const double sig = (m < 0 && (am & 1)) ? -1.0 : 1.0;  // favest/legendre.py:101-103
+    for (int b = 0; b < a.nfields; ++b) {
+      double2 gx = make_double2(0, 0), gy = make_double2(0, 0), gz = make_double2(0, 0);
+      if (on) {
+        const double2 ap1p = c_read(a.A, a, b, l + 1, m + 1), ap1m = c_read(a.A, a, b, l + 1, m - 1);
+        const double2 am1p = c_read(a.A, a, b, l - 1, m + 1), am1m = c_read(a.A, a, b, l - 1, m - 1);
+        const double2 ap10 = c_read(a.A, a, b, l + 1, m), am10 = c_read(a.A, a, b, l - 1, m);
+        const double2 bp = c_read(a.Bc, a, b, l, m + 1), bm = c_read(a.Bc, a, b, l, m - 1);
+        const double2 b0 = c_read(a.Bc, a, b, l, m);
+        // nu1..nu6, eta1..eta3 (favest/coupling.py:227-239)
+        const double2 nu1 = make_double2(ap1p.x * x1 - ap1m.x * x3, ap1p.y * x1 - ap1m.y * x3);
+        const double2 nu2 = make_double2(am1p.x * x2 - am1m.x * x4, am1p.y * x2 - am1m.y * x4);
+        const double2 s3 = make_double2(ap1p.x * x1 + ap1m.x * x3, ap1p.y * x1 + ap1m.y * x3);
+        const double2 nu3 = make_double2(-s3.y, s3.x);
+        const double2 s4 = make_double2(am1p.x * x2 + am1m.x * x4, am1p.y * x2 + am1m.y * x4);
+        const double2 nu4 = make_double2(-s4.y, s4.x);
+        const double2 nu5 = make_double2(ap10.x * x5, ap10.y * x5);
+        const double2 nu6 = make_double2(am10.x * x6, am10.y * x6);
+        const double2 d1 = make_double2(bp.x * u1 - bm.x * u3, bp.y * u1 - bm.y * u3);
+        const double2 eta1 = make_double2(-d1.y, d1.x);
+        const double2 eta2 = make_double2(bp.x * u1 + bm.x * u3, bp.y * u1 + bm.y * u3);
+        const double2 eta3 = make_double2(-(b0.y * u2), b0.x * u2);
+        // merge (favest/transforms.py:168-175)
+        gx = make_double2(-is2 * ((nu1.x + nu2.x) + eta1.x), -is2 * ((nu1.y + nu2.y) + eta1.y));
+        gy = make_double2(-is2 * ((nu3.x + nu4.x) - eta2.x), -is2 * ((nu3.y + nu4.y) - eta2.y));
+        gz = make_double2((nu5.x + nu6.x) + eta3.x, (nu5.y + nu6.y) + eta3.y);
+      }
+      const int n0 = 12 * b + 2 * sg;
+      put(n0 + 0, sig * gx.x); put(n0 + 1, sig * gx.y);
+      put(n0 + 4, sig * gy.x); put(n0 + 5, sig * gy.y);
+      put(n0 + 8, sig * gz.x); put(n0 + 9, sig * gz.y);
+    }
+  }
+}
+
+}  // namespace fv

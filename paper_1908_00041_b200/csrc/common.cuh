@@ -1,0 +1,136 @@
+// Shared device helpers for the FaVeST VSHT kernels (sm_100a).
+//
+// - FP64 tensor-core tile: mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4); B200 has no
+//   tcgen05 kind for f64, and DMMA measured 37.0 TF/s vs DFMA 33.6 TF/s on
+//   this pool (tools/fp64_microbench.cu, profiles/r01_fp64_microbench.txt).
+// - mbarrier + cp.async.bulk (TMA 1-D bulk copy) producer/consumer pipeline.
+// - extended-range ("X-number") scale handling for the Legendre recurrence.
+// - the nine closed-form Clebsch-Gordan coefficients, same expression order as
+//   the reference (favest/coupling.py:39-78), so xi/mu are bitwise equal.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fv {
+
+constexpr int XR_SHIFT = 512;  // value = x * 2^e, e a multiple of 512 (oracle/favest_oracle.py)
+
+__device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\t"
+      "mbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\t"
+      "mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+
+// 1-D bulk copy global -> shared, completion counted on an mbarrier (TMA engine).
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// value of an extended-range number x * 2^e (e <= 0, multiple of 512); below
+// 2^-1024 the value is flushed to zero, matching oracle._xr_value.
+__device__ __forceinline__ double xr_value(double x, int e) {
+  if (e == 0) return x;
+  if (e == -XR_SHIFT) return x * 0x1p-512;
+  if (e == -2 * XR_SHIFT) return x * 0x1p-1024;
+  return 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// Clebsch-Gordan closed forms: favest/coupling.py:25-78 (same operation order)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double coupling_c(long long l) {  // coupling.py:25-29
+  return sqrt((l + 1.0) / (2.0 * l + 1.0));
+}
+__device__ __forceinline__ double coupling_d(long long l) {  // coupling.py:32-36
+  return sqrt(l / (2.0 * l + 1.0));
+}
+
+__device__ __forceinline__ double cg_explicit(int dl, int m2, long long l, long long m) {
+  long long j1 = l + dl;
+  long long m1 = m - m2;
+  if (l < 0 || j1 < 0 || llabs(m) > l || llabs(m1) > j1) return 0.0;
+  double lf = (double)l, mf = (double)m;
+  if (dl == -1) {
+    if (m2 == 1) return sqrt((double)(l + m) * (lf + mf - 1.0) / ((2.0 * lf) * (2.0 * lf - 1.0)));
+    if (m2 == 0) return sqrt((double)((l + m) * (l - m)) / (lf * (2.0 * lf - 1.0)));
+    return sqrt((double)(l - m) * (lf - mf - 1.0) / ((2.0 * lf) * (2.0 * lf - 1.0)));
+  }
+  if (dl == 1) {
+    if (m2 == 1) return sqrt((lf - mf + 1.0) * (lf - mf + 2.0) / ((2.0 * lf + 2.0) * (2.0 * lf + 3.0)));
+    if (m2 == 0) return -sqrt((lf - mf + 1.0) * (lf + mf + 1.0) / ((2.0 * lf + 3.0) * (lf + 1.0)));
+    return sqrt((lf + mf + 1.0) * (lf + mf + 2.0) / ((2.0 * lf + 3.0) * (2.0 * lf + 2.0)));
+  }
+  if (l == 0) return 0.0;
+  if (m2 == 1) return -sqrt((double)(l + m) * (lf - mf + 1.0) / (lf * (2.0 * lf + 2.0)));
+  if (m2 == 0) return mf / sqrt(lf * (lf + 1.0));
+  return sqrt((lf + mf + 1.0) * (double)(l - m) / (lf * (2.0 * lf + 2.0)));
+}
+
+// xi^1..6 and mu^1..3 at table position (l, m): favest/coupling.py:159-167.
+// Only valid table positions (0 <= l <= lmax+1, |m| <= l) are ever requested;
+// positions outside read as zero through the callers' range checks
+// (favest/coupling.py:173-184).
+__device__ __forceinline__ double xi_coef(int i, long long l, long long m) {
+  switch (i) {
+    case 1: return coupling_c(l + 1) * cg_explicit(-1, 1, l + 1, m + 1);
+    case 2: return l >= 1 ? coupling_d(l - 1) * cg_explicit(1, 1, l - 1, m + 1) : 0.0;
+    case 3: return coupling_c(l + 1) * cg_explicit(-1, -1, l + 1, m - 1);
+    case 4: return l >= 1 ? coupling_d(l - 1) * cg_explicit(1, -1, l - 1, m - 1) : 0.0;
+    case 5: return coupling_c(l + 1) * cg_explicit(-1, 0, l + 1, m);
+    default: return l >= 1 ? coupling_d(l - 1) * cg_explicit(1, 0, l - 1, m) : 0.0;
+  }
+}
+__device__ __forceinline__ double mu_coef(int i, long long l, long long m) {
+  if (i == 1) return cg_explicit(0, 1, l, m + 1);
+  if (i == 2) return cg_explicit(0, 0, l, m);
+  return cg_explicit(0, -1, l, m - 1);
+}
+
+}  // namespace fv

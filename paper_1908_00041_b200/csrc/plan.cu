@@ -1,0 +1,540 @@
+// C ABI (include/favest_b200.h): plans, workspaces, cuFFT and the kernel
+// sequence of the forward / adjoint VSHT on B200 (sm_100a).
+#include <cuda_runtime.h>
+#include <cufft.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/favest_b200.h"
+#include "aux_kernels.cuh"
+#include "legendre.cuh"
+#include "points.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define FV_CUDA(x)                                                                            \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess) {                                                                  \
+      return fail(e_ == cudaErrorMemoryAllocation ? FV_ENOMEM : FV_ECUDA,                    \
+                  std::string("CUDA error in ") + #x + ": " + cudaGetErrorString(e_));        \
+    }                                                                                         \
+  } while (0)
+
+#define FV_CUFFT(x)                                                                           \
+  do {                                                                                        \
+    cufftResult r_ = (x);                                                                     \
+    if (r_ != CUFFT_SUCCESS) {                                                                \
+      return fail(r_ == CUFFT_ALLOC_FAILED ? FV_ENOMEM : FV_ECUDA,                            \
+                  std::string("cuFFT error ") + std::to_string((int)r_) + " in " + #x);       \
+    }                                                                                         \
+  } while (0)
+
+#define FV_TRY(x)          \
+  do {                     \
+    int rc_ = (x);         \
+    if (rc_ != FV_OK) return rc_; \
+  } while (0)
+
+inline int ntiles_for(int nfields) { return (12 * nfields + 7) / 8; }
+
+}  // namespace
+
+struct fvPlan {
+  int kind = 0;  // 0 grid, 1 points
+  int L = 0, Lt = 0, n_theta = 0, n_phi = 0, nP = 0, nPpad = 0, nchunks = 0, nrc = 0;
+  int max_batch = 0, device = 0, paired = 0;
+  // grid tables
+  double* pair_t = nullptr;
+  double* pair_sin = nullptr;
+  int* pair_n = nullptr;
+  int* pair_s = nullptr;
+  double* ring_w = nullptr;
+  double* seed_x = nullptr;
+  int* seed_e = nullptr;
+  double2* ab = nullptr;
+  long long* abofs = nullptr;
+  long long* gofs = nullptr;    // tile offsets per order (grid G layout)
+  long long* rowofs = nullptr;  // row offsets per order (points G layout)
+  long long g_tiles = 0;
+  // workspaces
+  double2* Sf = nullptr;
+  double2* Sa = nullptr;
+  double* X = nullptr;
+  double* F = nullptr;
+  double* G = nullptr;
+  std::map<int, std::pair<cufftHandle, cufftHandle>> ffts;
+  // profiling
+  bool profiling = false;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+};
+
+namespace {
+
+template <typename T>
+int dalloc(T** p, size_t n) {
+  if (n == 0) n = 1;
+  FV_CUDA(cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T)));
+  return FV_OK;
+}
+
+void free_plan(fvPlan* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  void* ptrs[] = {p->pair_t, p->pair_sin, p->pair_n, p->pair_s, p->ring_w, p->seed_x, p->seed_e,
+                  p->ab,     p->abofs,    p->gofs,   p->rowofs, p->Sf,     p->Sa,     p->X,
+                  p->F,      p->G};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  for (auto& kv : p->ffts) {
+    cufftDestroy(kv.second.first);
+    cufftDestroy(kv.second.second);
+  }
+  for (auto e : p->ev_pool) cudaEventDestroy(e);
+  delete p;
+}
+
+int ab_tables(fvPlan* p) {
+  const int Lt = p->Lt;
+  std::vector<long long> abofs(Lt + 2, 0);
+  for (int m = 0; m <= Lt; ++m) abofs[m + 1] = abofs[m] + std::max(0, Lt - m - 1);
+  FV_TRY(dalloc(&p->abofs, Lt + 1));
+  FV_TRY(dalloc(&p->ab, abofs[Lt + 1]));
+  FV_CUDA(cudaMemcpy(p->abofs, abofs.data(), (Lt + 1) * sizeof(long long), cudaMemcpyHostToDevice));
+  if (Lt >= 2) {
+    dim3 grid((Lt + 127) / 128, Lt + 1);
+    fv::ab_kernel<<<grid, 128>>>(Lt, p->abofs, p->ab);
+    FV_CUDA(cudaGetLastError());
+  }
+  return FV_OK;
+}
+
+cudaEvent_t next_event(fvPlan* p) {
+  if (p->ev_used == p->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    p->ev_pool.push_back(e);
+  }
+  return p->ev_pool[p->ev_used++];
+}
+
+struct StageMark {
+  fvPlan* p;
+  int stage;
+  cudaStream_t s;
+  cudaEvent_t e0 = nullptr;
+  StageMark(fvPlan* p_, int st, cudaStream_t s_) : p(p_), stage(st), s(s_) {
+    if (p->profiling) {
+      e0 = next_event(p);
+      cudaEventRecord(e0, s);
+    }
+  }
+  ~StageMark() {
+    if (p->profiling) {
+      cudaEvent_t e1 = next_event(p);
+      cudaEventRecord(e1, s);
+      p->marks.push_back({stage, {e0, e1}});
+    }
+  }
+};
+
+int get_ffts(fvPlan* p, int B, cufftHandle* fwd, cufftHandle* inv) {
+  auto it = p->ffts.find(B);
+  if (it == p->ffts.end()) {
+    int n = p->n_phi;
+    cufftHandle hf, hi;
+    // forward: component c of T [B][N][3] (stride 3) -> S[c][b][ring][q] (contiguous rings)
+    FV_CUFFT(cufftPlanMany(&hf, 1, &n, &n, 3, 3 * n, &n, 1, n, CUFFT_Z2Z, B * p->n_theta));
+    // inverse: S[c][b][ring][q] -> component c of T (stride 3); unnormalised = ifft * n_phi
+    FV_CUFFT(cufftPlanMany(&hi, 1, &n, &n, 1, n, &n, 3, 3 * n, CUFFT_Z2Z, B * p->n_theta));
+    it = p->ffts.emplace(B, std::make_pair(hf, hi)).first;
+  }
+  *fwd = it->second.first;
+  *inv = it->second.second;
+  return FV_OK;
+}
+
+// cudaFuncSetAttribute once per (kernel instantiation, device)
+bool first_use(unsigned long long* mask, int device) {
+  const unsigned long long bit = 1ull << (device & 63);
+  if (*mask & bit) return false;
+  *mask |= bit;
+  return true;
+}
+
+template <int NT>
+int launch_fwd(fvPlan* p, const fv::FwdArgs& args, int m_count, cudaStream_t s) {
+  static unsigned long long attr = 0;
+  const size_t bytes = fv::FwdSmem<NT>::bytes(p->nPpad);
+  if (bytes > 227 * 1024) return fail(FV_EINVAL, "grid too large for the forward kernel's shared memory");
+  if (first_use(&attr, p->device)) {
+    FV_CUDA(cudaFuncSetAttribute(fv::legendre_fwd_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 227 * 1024));
+  }
+  fv::legendre_fwd_kernel<NT><<<m_count, fv::kThreads, bytes, s>>>(args);
+  FV_CUDA(cudaGetLastError());
+  return FV_OK;
+}
+
+template <int NT>
+int launch_adj(fvPlan* p, const fv::AdjArgs& args, int m_count, cudaStream_t s) {
+  static unsigned long long attr = 0;
+  const size_t bytes = fv::AdjSmem<NT>::bytes();
+  if (first_use(&attr, p->device)) {
+    FV_CUDA(cudaFuncSetAttribute(fv::legendre_adj_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 227 * 1024));
+  }
+  fv::legendre_adj_kernel<NT><<<m_count * p->nrc, fv::kThreads, bytes, s>>>(args);
+  FV_CUDA(cudaGetLastError());
+  return FV_OK;
+}
+
+int dispatch_fwd(fvPlan* p, int NT, const fv::FwdArgs& a, int mc, cudaStream_t s) {
+  switch (NT) {
+    case 2: return launch_fwd<2>(p, a, mc, s);
+    case 3: return launch_fwd<3>(p, a, mc, s);
+    case 5: return launch_fwd<5>(p, a, mc, s);
+    case 6: return launch_fwd<6>(p, a, mc, s);
+  }
+  return fail(FV_EINVAL, "unsupported field group");
+}
+
+int dispatch_adj(fvPlan* p, int NT, const fv::AdjArgs& a, int mc, cudaStream_t s) {
+  switch (NT) {
+    case 2: return launch_adj<2>(p, a, mc, s);
+    case 3: return launch_adj<3>(p, a, mc, s);
+    case 5: return launch_adj<5>(p, a, mc, s);
+    case 6: return launch_adj<6>(p, a, mc, s);
+  }
+  return fail(FV_EINVAL, "unsupported field group");
+}
+
+int begin_call(fvPlan* p) {
+  if (!p) return fail(FV_EINVAL, "null plan");
+  FV_CUDA(cudaSetDevice(p->device));
+  p->marks.clear();
+  p->ev_used = 0;
+  g_err.clear();
+  return FV_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fv_version(void) { return "favest_b200 0.1.0 sm_100a"; }
+
+const char* fv_last_error(void) { return g_err.c_str(); }
+
+int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const double* ring_theta_host,
+                        const double* ring_weight_host, int max_batch, int device) {
+  if (!out) return fail(FV_EINVAL, "null output pointer");
+  *out = nullptr;
+  if (L < 1) return fail(FV_EINVAL, "vector transforms need lmax >= 1, got " + std::to_string(L));
+  if (n_theta < 1) return fail(FV_EINVAL, "grid needs at least one ring");
+  if (n_phi < 1) return fail(FV_EINVAL, "n_phi must be positive, got " + std::to_string(n_phi));
+  const int needed = 2 * (L + 1) + 1;  // favest/transforms.py:63
+  if (n_phi < needed)
+    return fail(FV_EINVAL, "fast-scalar path needs n_phi >= " + std::to_string(needed) + " for degree " +
+                               std::to_string(L) + ", grid has n_phi=" + std::to_string(n_phi));
+  if (max_batch < 1) return fail(FV_EINVAL, "max_batch must be positive");
+  for (int r = 0; r < n_theta; ++r) {
+    if (!(ring_theta_host[r] > 0.0 && ring_theta_host[r] < M_PI))
+      return fail(FV_EINVAL, "ring colatitudes must lie strictly inside (0, pi)");
+    if (r > 0 && !(ring_theta_host[r] > ring_theta_host[r - 1]))
+      return fail(FV_EINVAL, "ring colatitudes must be strictly increasing");
+  }
+  fvPlan* p = new fvPlan();
+  p->kind = 0;
+  p->L = L;
+  p->Lt = L + 1;
+  p->n_theta = n_theta;
+  p->n_phi = n_phi;
+  p->max_batch = max_batch;
+  p->device = device;
+  auto bail = [&](int rc) {
+    free_plan(p);
+    return rc;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return bail(fail(FV_ECUDA, "cannot select device"));
+
+  // ring cosines exactly as favest/scalar.py:133 + favest/legendre.py:53-57
+  std::vector<double> t(n_theta), w(ring_weight_host, ring_weight_host + n_theta);
+  for (int r = 0; r < n_theta; ++r) t[r] = std::min(1.0, std::max(-1.0, std::cos(ring_theta_host[r])));
+  // equatorial folding when the grid is mirror symmetric (GL: cos mirrors to 3e-16, weights bitwise)
+  bool sym = true;
+  for (int r = 0; r < n_theta / 2 && sym; ++r) {
+    const int r2 = n_theta - 1 - r;
+    if (std::fabs(t[r] + t[r2]) > 1e-13) sym = false;
+    if (std::fabs(w[r] - w[r2]) > 1e-13 * std::fabs(w[r])) sym = false;
+  }
+  std::vector<int> pn, ps;
+  if (sym) {
+    for (int r = 0; r < n_theta / 2; ++r) {
+      pn.push_back(r);
+      ps.push_back(n_theta - 1 - r);
+    }
+    if (n_theta & 1) {
+      pn.push_back(n_theta / 2);
+      ps.push_back(-1);
+    }
+  } else {
+    for (int r = 0; r < n_theta; ++r) {
+      pn.push_back(r);
+      ps.push_back(-1);
+    }
+  }
+  p->paired = sym ? 1 : 0;
+  p->nP = (int)pn.size();
+  p->nPpad = (p->nP + 63) / 64 * 64;
+  p->nchunks = p->nPpad / 32;
+  p->nrc = p->nPpad / 64;
+  std::vector<double> pt(p->nPpad, 0.0), psn(p->nPpad, 0.0);
+  pn.resize(p->nPpad, -1);
+  ps.resize(p->nPpad, -1);
+  for (int i = 0; i < p->nP; ++i) {
+    pt[i] = t[pn[i]];
+    psn[i] = std::sqrt(std::max(0.0, 1.0 - pt[i] * pt[i]));
+  }
+  const int Lt = p->Lt;
+  int rc;
+  if ((rc = dalloc(&p->pair_t, p->nPpad)) || (rc = dalloc(&p->pair_sin, p->nPpad)) ||
+      (rc = dalloc(&p->pair_n, p->nPpad)) || (rc = dalloc(&p->pair_s, p->nPpad)) ||
+      (rc = dalloc(&p->ring_w, n_theta)) || (rc = dalloc(&p->seed_x, (size_t)(Lt + 1) * p->nPpad)) ||
+      (rc = dalloc(&p->seed_e, (size_t)(Lt + 1) * p->nPpad)))
+    return bail(rc);
+  cudaMemcpy(p->pair_t, pt.data(), p->nPpad * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(p->pair_sin, psn.data(), p->nPpad * 8, cudaMemcpyHostToDevice);
+  cudaMemcpy(p->pair_n, pn.data(), p->nPpad * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(p->pair_s, ps.data(), p->nPpad * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(p->ring_w, w.data(), n_theta * 8, cudaMemcpyHostToDevice);
+  fv::seeds_kernel<<<(p->nPpad + 127) / 128, 128>>>(p->pair_sin, p->nPpad, Lt, p->seed_x, p->seed_e);
+  if (cudaGetLastError() != cudaSuccess) return bail(fail(FV_ECUDA, "seed kernel launch failed"));
+  if ((rc = ab_tables(p))) return bail(rc);
+  // G layout tile offsets: nlc(m) = ceil((Lt+1-m)/64) tiles per order
+  std::vector<long long> gofs(Lt + 2, 0);
+  for (int m = 0; m <= Lt; ++m) gofs[m + 1] = gofs[m] + (Lt + 1 - m + 63) / 64;
+  p->g_tiles = gofs[Lt + 1];
+  if ((rc = dalloc(&p->gofs, Lt + 1))) return bail(rc);
+  cudaMemcpy(p->gofs, gofs.data(), (Lt + 1) * 8, cudaMemcpyHostToDevice);
+  // workspaces (field groups of <= 4 -> NT <= 6)
+  const int gs = std::min(4, max_batch);
+  const int NTmax = ntiles_for(gs);
+  const size_t spec = (size_t)3 * max_batch * n_theta * n_phi;
+  if ((rc = dalloc(&p->Sf, spec)) || (rc = dalloc(&p->Sa, spec)) ||
+      (rc = dalloc(&p->X, (size_t)(Lt + 1) * p->nchunks * (2 * 8 * NTmax * 32))) ||
+      (rc = dalloc(&p->F, (size_t)(Lt + 1) * (Lt + 2) / 2 * 8 * NTmax)) ||
+      (rc = dalloc(&p->G, (size_t)p->g_tiles * (2 * 8 * NTmax * 32))))
+    return bail(rc);
+  if (cudaMemset(p->Sa, 0, spec * sizeof(double2)) != cudaSuccess) return bail(fail(FV_ECUDA, "memset failed"));
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return bail(fail(FV_ECUDA, std::string("plan setup: ") + cudaGetErrorString(e)));
+  *out = p;
+  return FV_OK;
+}
+
+int fv_plan_create_points(fvPlan** out, int L, int max_batch, int device) {
+  if (!out) return fail(FV_EINVAL, "null output pointer");
+  *out = nullptr;
+  if (L < 1) return fail(FV_EINVAL, "vector coefficients need lmax >= 1");
+  if (max_batch < 1) return fail(FV_EINVAL, "max_batch must be positive");
+  fvPlan* p = new fvPlan();
+  p->kind = 1;
+  p->L = L;
+  p->Lt = L + 1;
+  p->max_batch = max_batch;
+  p->device = device;
+  auto bail = [&](int rc) {
+    free_plan(p);
+    return rc;
+  };
+  if (cudaSetDevice(device) != cudaSuccess) return bail(fail(FV_ECUDA, "cannot select device"));
+  int rc;
+  if ((rc = ab_tables(p))) return bail(rc);
+  const int Lt = p->Lt;
+  std::vector<long long> rowofs(Lt + 2, 0);
+  for (int m = 0; m <= Lt; ++m) rowofs[m + 1] = rowofs[m] + (Lt + 1 - m);
+  if ((rc = dalloc(&p->rowofs, Lt + 1))) return bail(rc);
+  cudaMemcpy(p->rowofs, rowofs.data(), (Lt + 1) * 8, cudaMemcpyHostToDevice);
+  const int gs = std::min(4, max_batch);
+  if ((rc = dalloc(&p->G, (size_t)rowofs[Lt + 1] * 12 * gs))) return bail(rc);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return bail(fail(FV_ECUDA, std::string("plan setup: ") + cudaGetErrorString(e)));
+  *out = p;
+  return FV_OK;
+}
+
+void fv_plan_destroy(fvPlan* plan) { free_plan(plan); }
+
+int fv_plan_info(const fvPlan* p, int* L, int* n_theta, int* n_phi, int* n_pairs, int* paired) {
+  if (!p) return fail(FV_EINVAL, "null plan");
+  if (L) *L = p->L;
+  if (n_theta) *n_theta = p->n_theta;
+  if (n_phi) *n_phi = p->n_phi;
+  if (n_pairs) *n_pairs = p->nP;
+  if (paired) *paired = p->paired;
+  return FV_OK;
+}
+
+int fv_set_profiling(fvPlan* p, int enable) {
+  if (!p) return fail(FV_EINVAL, "null plan");
+  p->profiling = enable != 0;
+  return FV_OK;
+}
+
+double fv_stage_ms(const fvPlan* p, int stage) {
+  if (!p || !p->profiling || p->marks.empty()) return -1.0;
+  cudaEventSynchronize(p->marks.back().second.second);
+  double tot = 0.0;
+  for (auto& mk : p->marks) {
+    if (mk.first != stage) continue;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, mk.second.first, mk.second.second);
+    tot += ms;
+  }
+  return tot;
+}
+
+int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, void* stream) {
+  FV_TRY(begin_call(p));
+  if (p->kind != 0) return fail(FV_EINVAL, "fast-scalar path requires a rule with tensor-grid structure");
+  if (B < 1 || B > p->max_batch)
+    return fail(FV_EINVAL, "batch " + std::to_string(B) + " outside 1.." + std::to_string(p->max_batch));
+  if (!T || !a || !b) return fail(FV_EINVAL, "null data pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cufftHandle hf, hi;
+  FV_TRY(get_ffts(p, B, &hf, &hi));
+  const size_t per_comp = (size_t)B * p->n_theta * p->n_phi;
+  {
+    StageMark mk(p, 0, s);
+    FV_CUFFT(cufftSetStream(hf, s));
+    for (int c = 0; c < 3; ++c) {
+      auto* in = reinterpret_cast<cufftDoubleComplex*>(const_cast<double*>(T)) + c;
+      auto* outp = reinterpret_cast<cufftDoubleComplex*>(p->Sf + c * per_comp);
+      FV_CUFFT(cufftExecZ2Z(hf, in, outp, CUFFT_FORWARD));
+    }
+  }
+  const int Lt = p->Lt;
+  for (int b0 = 0; b0 < B; b0 += 4) {
+    const int nf = std::min(4, B - b0);
+    const int NT = ntiles_for(nf);
+    {
+      StageMark mk(p, 1, s);
+      fv::FoldArgs fa{p->Sf, p->X, p->pair_n, p->pair_s, p->ring_w, p->n_phi, p->n_theta, B, b0, nf, NT,
+                      p->nPpad, p->nchunks, 0, Lt + 1};
+      dim3 grid((p->nPpad + 127) / 128, Lt + 1, nf + 1);
+      fv::fold_fwd_kernel<<<grid, 128, 0, s>>>(fa);
+      FV_CUDA(cudaGetLastError());
+    }
+    {
+      StageMark mk(p, 2, s);
+      fv::FwdArgs args{p->X, p->F, p->seed_x, p->seed_e, p->ab, p->abofs, p->pair_t, Lt, p->nPpad, p->nchunks, 0};
+      FV_TRY(dispatch_fwd(p, NT, args, Lt + 1, s));
+    }
+    {
+      StageMark mk(p, 3, s);
+      fv::CgFwdArgs ca{p->F, reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), p->L, 8 * NT, B, b0, nf};
+      dim3 grid((p->L + 1 + 127) / 128, p->L + 1);
+      fv::cg_fwd_kernel<<<grid, 128, 0, s>>>(ca);
+      FV_CUDA(cudaGetLastError());
+    }
+  }
+  return FV_OK;
+}
+
+int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int B, void* stream) {
+  FV_TRY(begin_call(p));
+  if (p->kind != 0) return fail(FV_EINVAL, "fast-scalar path requires a rule with tensor-grid structure");
+  if (B < 1 || B > p->max_batch)
+    return fail(FV_EINVAL, "batch " + std::to_string(B) + " outside 1.." + std::to_string(p->max_batch));
+  if (!T || !a || !b) return fail(FV_EINVAL, "null data pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  cufftHandle hf, hi;
+  FV_TRY(get_ffts(p, B, &hf, &hi));
+  const int Lt = p->Lt;
+  for (int b0 = 0; b0 < B; b0 += 4) {
+    const int nf = std::min(4, B - b0);
+    const int NT = ntiles_for(nf);
+    {
+      StageMark mk(p, 3, s);
+      fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), p->G, p->gofs,
+                       nullptr, p->L, NT, B, b0, nf, 0, 0};
+      const int rows = (Lt + 1 + 63) / 64 * 64;
+      dim3 grid((rows + 127) / 128, Lt + 1);
+      fv::cg_adj_kernel<<<grid, 128, 0, s>>>(ca);
+      FV_CUDA(cudaGetLastError());
+    }
+    {
+      StageMark mk(p, 2, s);
+      fv::AdjArgs args{p->G, p->gofs, p->Sa, p->seed_x, p->seed_e, p->ab, p->abofs, p->pair_t, p->pair_n,
+                       p->pair_s, Lt, p->nPpad, p->nrc, p->n_phi, p->n_theta, B, b0, nf, 0};
+      FV_TRY(dispatch_adj(p, NT, args, Lt + 1, s));
+    }
+  }
+  {
+    StageMark mk(p, 0, s);
+    FV_CUFFT(cufftSetStream(hi, s));
+    const size_t per_comp = (size_t)B * p->n_theta * p->n_phi;
+    for (int c = 0; c < 3; ++c) {
+      auto* in = reinterpret_cast<cufftDoubleComplex*>(p->Sa + c * per_comp);
+      auto* outp = reinterpret_cast<cufftDoubleComplex*>(T) + c;
+      FV_CUFFT(cufftExecZ2Z(hi, in, outp, CUFFT_INVERSE));
+    }
+  }
+  return FV_OK;
+}
+
+int fv_adjoint_points(fvPlan* p, const double* xyz, long long M, const double* a, const double* b, double* T,
+                      int B, void* stream) {
+  FV_TRY(begin_call(p));
+  if (p->kind != 1) return fail(FV_EINVAL, "plan was not created for scattered points");
+  if (B < 1 || B > p->max_batch)
+    return fail(FV_EINVAL, "batch " + std::to_string(B) + " outside 1.." + std::to_string(p->max_batch));
+  if (M < 0) return fail(FV_EINVAL, "negative point count");
+  if (M == 0) return FV_OK;
+  if (!xyz || !T || !a || !b) return fail(FV_EINVAL, "null data pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int Lt = p->Lt;
+  for (int b0 = 0; b0 < B; b0 += 4) {
+    const int nf = std::min(4, B - b0);
+    {
+      StageMark mk(p, 3, s);
+      fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), p->G, nullptr,
+                       p->rowofs, p->L, 0, B, b0, nf, 0, 1};
+      dim3 grid((Lt + 1 + 127) / 128, Lt + 1);
+      fv::cg_adj_kernel<<<grid, 128, 0, s>>>(ca);
+      FV_CUDA(cudaGetLastError());
+    }
+    {
+      StageMark mk(p, 2, s);
+      fv::PtsArgs pa{xyz, M, p->G, p->rowofs, p->ab, p->abofs, reinterpret_cast<double2*>(T), Lt, B, b0};
+      const unsigned grid = (unsigned)((M + 127) / 128);
+      switch (nf) {
+        case 1: fv::adjoint_points_kernel<1><<<grid, 128, 0, s>>>(pa); break;
+        case 2: fv::adjoint_points_kernel<2><<<grid, 128, 0, s>>>(pa); break;
+        case 3: fv::adjoint_points_kernel<3><<<grid, 128, 0, s>>>(pa); break;
+        default: fv::adjoint_points_kernel<4><<<grid, 128, 0, s>>>(pa); break;
+      }
+      FV_CUDA(cudaGetLastError());
+    }
+  }
+  return FV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+"""Generate the golden parity fixtures from the REFERENCE implementation.
+
+Run in the build container (the only place /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the unmodified reference package from /root/reference/pkg/src
+(read-only; nothing is copied) and writes small .npz fixtures next to this
+script.  The fixtures pin both the numpy oracle (tests/test_oracle.py) and
+the CUDA path (tests/test_gpu_parity.py) to the reference's own outputs.
+"""
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def main():
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, REF)
+    import favest
+    from favest.core import ScalarCoefficients, TangentFieldSamples, VectorCoefficients, degrees_orders
+    from favest.coupling import build_cg_tables
+    from favest.legendre import legendre_table
+    from favest.quadrature import gen_gl_tensor
+    from favest.transforms import adjoint_favest, forward_favest
+
+    def coef(rng, lmax, law):
+        K = (lmax + 1) ** 2
+        ls, _ = degrees_orders(lmax)
+        lf = ls.astype(np.float64)
+        if law == "inv":
+            scale = np.where(ls >= 1, 1.0 / np.maximum(lf * (lf + 1.0), 1.0), 0.0)
+        else:
+            scale = (1.0 + lf) ** -2
+        out = []
+        for _ in range(2):
+            v = (rng.standard_normal(K) + 1j * rng.standard_normal(K)) * scale
+            v[0] = 0.0
+            out.append(v)
+        return out
+
+    def vc(a, b, lmax):
+        return VectorCoefficients(ScalarCoefficients(lmax, a), ScalarCoefficients(lmax, b))
+
+    # 1. Legendre values (bitwise pin of the recurrence) on a GL ring set and frozen args
+    grid, _ = gen_gl_tensor(2 * 38 + 3)
+    t = np.concatenate([np.cos(grid.ring_thetas), [1.0, 0.0, -0.37]])
+    np.savez_compressed(os.path.join(HERE, "legendre_l40.npz"), t=t, p=legendre_table(40, t))
+
+    # 2. CG tables (bitwise pin of the closed forms)
+    tab = build_cg_tables(12)
+    np.savez_compressed(
+        os.path.join(HERE, "cg_tables_l12.npz"),
+        **{f"xi{i}": tab.xi[i] for i in range(1, 7)},
+        **{f"mu{i}": tab.mu[i] for i in range(1, 4)},
+    )
+
+    # 3. grid round trips: C1 (L=32, seed 1, 1/(l(l+1)) law) plus odd/small L
+    for lmax, seed in ((32, 1), (8, 101), (17, 117)):
+        grid, rule = gen_gl_tensor(2 * lmax + 3)
+        rng = np.random.default_rng(seed)
+        a, b = coef(rng, lmax, "inv")
+        tables = build_cg_tables(lmax)
+        T = adjoint_favest(vc(a, b, lmax), rule, tables=tables)
+        F = forward_favest(T, rule, lmax, tables=tables)
+        # a noisy (non-bandlimited) tangent field through the forward
+        pts = rule.points
+        raw = 1e-3 * (rng.standard_normal(pts.shape) + 1j * rng.standard_normal(pts.shape))
+        raw -= np.sum(raw * pts, axis=1)[:, None] * pts
+        Tn = TangentFieldSamples(pts, T.values + raw)
+        Fn = forward_favest(Tn, rule, lmax, tables=tables)
+        np.savez_compressed(
+            os.path.join(HERE, f"roundtrip_l{lmax}.npz"),
+            lmax=lmax, ring_thetas=grid.ring_thetas, ring_weights=grid.ring_weights,
+            n_phi=grid.n_phi, a=a, b=b, T=T.values, fa=F.div.values, fb=F.curl.values,
+            Tn=Tn.values, fna=Fn.div.values, fnb=Fn.curl.values,
+        )
+
+    # 4. scattered-point adjoint (direct route), C5 recipe at small size
+    for lmax, M, seed in ((16, 300, 5), (9, 64, 55)):
+        rng = np.random.default_rng(seed)
+        v = rng.standard_normal((M, 3))
+        pts = v / np.linalg.norm(v, axis=1, keepdims=True)
+        a, b = coef(rng, lmax, "inv")
+        out = adjoint_favest(vc(a, b, lmax), pts)
+        np.savez_compressed(
+            os.path.join(HERE, f"scattered_l{lmax}_m{M}.npz"),
+            lmax=lmax, points=pts, a=a, b=b, T=out.values,
+        )
+    print("reference favest", getattr(favest, "__version__", "?"), "numpy", np.__version__)
+
+
+if __name__ == "__main__":
+    main()
