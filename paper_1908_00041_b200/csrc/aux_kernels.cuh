@@ -39,7 +39,67 @@ __global__ void seeds_kernel(const double* __restrict__ pair_s, int nPpad, int L
   }
 }
 
-// a_l, b_l for l = m+2..Lt, stored m-major at abofs[m] + (l - m - 2).
+// Polar start (legendre.cuh): per (order m, ring pair p) the first degree
+// l_s >= m with |Pbar_{l_s}^m(t_p)| >= 2^-100 and the values (P_ls, P_ls+1),
+// found by running the recurrence in extended range from the diagonal seed.
+// l_s = Lt+1 when no degree <= Lt reaches the threshold (and for padding pairs).
+// Uses the same FMA-form step as the hot loop (legendre.cuh rec_step).
+__device__ __forceinline__ bool xr_significant(double x, int e) {
+  return e == 0 ? fabs(x) >= 0x1p-100 : (e == -XR_SHIFT ? fabs(x) >= 0x1p412 : false);
+}
+
+__global__ void start_kernel(const double* __restrict__ seed_x, const int* __restrict__ seed_e,
+                             const double* __restrict__ pair_t, const int* __restrict__ pair_n,
+                             const double2* __restrict__ ab, const long long* __restrict__ abofs, int nPpad,
+                             int Lt, int* start_l, double2* start_v) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int m = blockIdx.y;
+  if (p >= nPpad) return;
+  const size_t o = (size_t)m * nPpad + p;
+  int ls = Lt + 1;
+  double A = 0.0, B = 0.0;
+  if (pair_n[p] >= 0) {
+    const double t = pair_t[p];
+    const double2* abm = ab + abofs[m];
+    int e = seed_e[o];
+    double p2 = seed_x[o];                                        // P_m^m
+    double p1 = (m < Lt) ? (sqrt(2 * m + 3.0) * t) * p2 : 0.0;   // P_{m+1}^m
+    auto step = [&](int l, double q1, double q2) {                // P_l from P_{l-1}, P_{l-2}
+      const double2 ac = abm[l - m - 2];
+      return fma(ac.x * t, q1, -(ac.y * q2));
+    };
+    if (xr_significant(p2, e)) {
+      ls = m;
+      A = xr_value(p2, e);
+      B = (m < Lt) ? xr_value(p1, e) : 0.0;
+    } else if (m < Lt && xr_significant(p1, e)) {
+      ls = m + 1;
+      A = xr_value(p1, e);
+      B = (m + 2 <= Lt) ? xr_value(step(m + 2, p1, p2), e) : 0.0;
+    } else {
+      for (int l = m + 2; l <= Lt; ++l) {
+        const double pn = step(l, p1, p2);
+        p2 = p1;
+        p1 = pn;
+        if (e < 0 && fabs(p1) >= 0x1p512) {
+          p1 *= 0x1p-512;
+          p2 *= 0x1p-512;
+          e += XR_SHIFT;
+        }
+        if (xr_significant(p1, e)) {
+          ls = l;
+          A = xr_value(p1, e);
+          B = (l + 1 <= Lt) ? xr_value(step(l + 1, p1, p2), e) : 0.0;
+          break;
+        }
+      }
+    }
+  }
+  start_l[o] = ls;
+  start_v[o] = make_double2(A, B);
+}
+
+// (a_l, a_l * b_l) for l = m+2..Lt, stored m-major at abofs[m] + (l - m - 2).
 __global__ void ab_kernel(int Lt, const long long* __restrict__ abofs, double2* ab) {
   const int m = blockIdx.y;
   const int l = m + 2 + blockIdx.x * blockDim.x + threadIdx.x;
@@ -49,7 +109,7 @@ __global__ void ab_kernel(int Lt, const long long* __restrict__ abofs, double2* 
   const double a = sqrt((4.0 * lf * lf - 1.0) / (double)(L2 - M2));
   const double lm1 = lf - 1.0;
   const double b = sqrt((lm1 * lm1 - (double)M2) / (4.0 * (lm1 * lm1) - 1.0));
-  ab[abofs[m] + (l - m - 2)] = make_double2(a, b);
+  ab[abofs[m] + (l - m - 2)] = make_double2(a, a * b);  // FMA-form recurrence (legendre.cuh)
 }
 
 // Forward fold.  Thread per (local order mi, pair p, field b):
@@ -214,19 +274,20 @@ __global__ void cg_adj_kernel(CgAdjArgs a) {
   const long long am = a.m_begin + mi;
   const int Lt = a.L + 1;
   const int nrows = Lt + 1 - (int)am;
-  const int nlc = (nrows + 63) / 64;
-  const int row = blockIdx.x * blockDim.x + threadIdx.x;  // 0 .. 64*nlc-1
-  if (row >= (a.rows_mode ? nrows : 64 * nlc)) return;
+  constexpr int LC = 32, KS = LC / 8;  // legendre.cuh ADJ_LC / ADJ_KS
+  const int nlc = (nrows + LC - 1) / LC;
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;  // 0 .. LC*nlc-1
+  if (row >= (a.rows_mode ? nrows : LC * nlc)) return;
   const long long l = am + row;
-  const int lc = row >> 6, idx = row & 63;
+  const int lc = row / LC, idx = row % LC;
   const int par = idx & 1, k = idx >> 1, ks = k >> 2, q = k & 3;
   double* Gt = a.rows_mode ? a.G + (size_t)(a.rowofs[am] + row) * (12 * a.nfields)
-                           : a.G + (size_t)(a.gofs[am] + lc) * (2 * 8 * a.NT * 32);
+                           : a.G + (size_t)(a.gofs[am] + lc) * (2 * KS * a.NT * 32);
   auto put = [&](int n, double v) {
     if (a.rows_mode)
       Gt[n] = v;
     else
-      Gt[((size_t)(par * 8 + ks) * a.NT + (n >> 3)) * 32 + ((n & 7) << 2) + q] = v;
+      Gt[((size_t)(par * KS + ks) * a.NT + (n >> 3)) * 32 + ((n & 7) << 2) + q] = v;
   };
   if (!a.rows_mode)
     for (int n = 12 * a.nfields; n < 8 * a.NT; ++n) put(n, 0.0);

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -50,6 +51,12 @@ int fail(int code, const std::string& msg) {
     if (rc_ != FV_OK) return rc_; \
   } while (0)
 
+// FV_DEBUG_MODE=1/2 isolates the consumer / producer halves of the Legendre kernels (timing only)
+int dbg_mode() {
+  static int v = [] { const char* e = std::getenv("FV_DEBUG_MODE"); return e ? std::atoi(e) : 0; }();
+  return v;
+}
+
 inline int ntiles_for(int nfields) { return (12 * nfields + 7) / 8; }
 
 }  // namespace
@@ -64,8 +71,10 @@ struct fvPlan {
   int* pair_n = nullptr;
   int* pair_s = nullptr;
   double* ring_w = nullptr;
-  double* seed_x = nullptr;
+  double* seed_x = nullptr;  // plan-time only (freed after the polar-start tables)
   int* seed_e = nullptr;
+  int* start_l = nullptr;
+  double2* start_v = nullptr;
   double2* ab = nullptr;
   long long* abofs = nullptr;
   long long* gofs = nullptr;    // tile offsets per order (grid G layout)
@@ -97,9 +106,9 @@ int dalloc(T** p, size_t n) {
 void free_plan(fvPlan* p) {
   if (!p) return;
   cudaSetDevice(p->device);
-  void* ptrs[] = {p->pair_t, p->pair_sin, p->pair_n, p->pair_s, p->ring_w, p->seed_x, p->seed_e,
-                  p->ab,     p->abofs,    p->gofs,   p->rowofs, p->Sf,     p->Sa,     p->X,
-                  p->F,      p->G};
+  void* ptrs[] = {p->pair_t, p->pair_sin, p->pair_n, p->pair_s, p->ring_w, p->seed_x,
+                  p->seed_e, p->start_l,  p->start_v, p->ab,   p->abofs,  p->gofs,
+                  p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->G};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (auto& kv : p->ffts) {
@@ -181,7 +190,7 @@ bool first_use(unsigned long long* mask, int device) {
 template <int NT>
 int launch_fwd(fvPlan* p, const fv::FwdArgs& args, int m_count, cudaStream_t s) {
   static unsigned long long attr = 0;
-  const size_t bytes = fv::FwdSmem<NT>::bytes(p->nPpad);
+  const size_t bytes = fv::FwdSmem<NT>::bytes(p->nchunks * fv::FWD_RC);
   if (bytes > 227 * 1024) return fail(FV_EINVAL, "grid too large for the forward kernel's shared memory");
   if (first_use(&attr, p->device)) {
     FV_CUDA(cudaFuncSetAttribute(fv::legendre_fwd_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -302,9 +311,9 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
   }
   p->paired = sym ? 1 : 0;
   p->nP = (int)pn.size();
-  p->nPpad = (p->nP + 63) / 64 * 64;
-  p->nchunks = p->nPpad / 32;
-  p->nrc = p->nPpad / 64;
+  p->nPpad = (p->nP + fv::ADJ_RC - 1) / fv::ADJ_RC * fv::ADJ_RC;
+  p->nchunks = (p->nP + fv::FWD_RC - 1) / fv::FWD_RC;  // forward chunks (pairs beyond nP are zero)
+  p->nrc = p->nPpad / fv::ADJ_RC;
   std::vector<double> pt(p->nPpad, 0.0), psn(p->nPpad, 0.0);
   pn.resize(p->nPpad, -1);
   ps.resize(p->nPpad, -1);
@@ -327,9 +336,23 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
   fv::seeds_kernel<<<(p->nPpad + 127) / 128, 128>>>(p->pair_sin, p->nPpad, Lt, p->seed_x, p->seed_e);
   if (cudaGetLastError() != cudaSuccess) return bail(fail(FV_ECUDA, "seed kernel launch failed"));
   if ((rc = ab_tables(p))) return bail(rc);
-  // G layout tile offsets: nlc(m) = ceil((Lt+1-m)/64) tiles per order
+  // polar-start tables (legendre.cuh), then the extended-range seeds are no longer needed
+  if ((rc = dalloc(&p->start_l, (size_t)(Lt + 1) * p->nPpad)) ||
+      (rc = dalloc(&p->start_v, (size_t)(Lt + 1) * p->nPpad)))
+    return bail(rc);
+  {
+    dim3 grid((p->nPpad + 127) / 128, Lt + 1);
+    fv::start_kernel<<<grid, 128>>>(p->seed_x, p->seed_e, p->pair_t, p->pair_n, p->ab, p->abofs, p->nPpad, Lt,
+                                    p->start_l, p->start_v);
+    if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(FV_ECUDA, "polar-start kernel failed"));
+    cudaFree(p->seed_x);
+    cudaFree(p->seed_e);
+    p->seed_x = nullptr;
+    p->seed_e = nullptr;
+  }
+  // G layout tile offsets: nlc(m) = ceil((Lt+1-m)/ADJ_LC) tiles per order
   std::vector<long long> gofs(Lt + 2, 0);
-  for (int m = 0; m <= Lt; ++m) gofs[m + 1] = gofs[m] + (Lt + 1 - m + 63) / 64;
+  for (int m = 0; m <= Lt; ++m) gofs[m + 1] = gofs[m] + (Lt + 1 - m + fv::ADJ_LC - 1) / fv::ADJ_LC;
   p->g_tiles = gofs[Lt + 1];
   if ((rc = dalloc(&p->gofs, Lt + 1))) return bail(rc);
   cudaMemcpy(p->gofs, gofs.data(), (Lt + 1) * 8, cudaMemcpyHostToDevice);
@@ -340,7 +363,7 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
   if ((rc = dalloc(&p->Sf, spec)) || (rc = dalloc(&p->Sa, spec)) ||
       (rc = dalloc(&p->X, (size_t)(Lt + 1) * p->nchunks * (2 * 8 * NTmax * 32))) ||
       (rc = dalloc(&p->F, (size_t)(Lt + 1) * (Lt + 2) / 2 * 8 * NTmax)) ||
-      (rc = dalloc(&p->G, (size_t)p->g_tiles * (2 * 8 * NTmax * 32))))
+      (rc = dalloc(&p->G, (size_t)p->g_tiles * (2 * fv::ADJ_KS * NTmax * 32))))
     return bail(rc);
   if (cudaMemset(p->Sa, 0, spec * sizeof(double2)) != cudaSuccess) return bail(fail(FV_ECUDA, "memset failed"));
   cudaError_t e = cudaDeviceSynchronize();
@@ -437,14 +460,14 @@ int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, voi
     {
       StageMark mk(p, 1, s);
       fv::FoldArgs fa{p->Sf, p->X, p->pair_n, p->pair_s, p->ring_w, p->n_phi, p->n_theta, B, b0, nf, NT,
-                      p->nPpad, p->nchunks, 0, Lt + 1};
-      dim3 grid((p->nPpad + 127) / 128, Lt + 1, nf + 1);
+                      p->nchunks * fv::FWD_RC, p->nchunks, 0, Lt + 1};
+      dim3 grid((p->nchunks * fv::FWD_RC + 127) / 128, Lt + 1, nf + 1);
       fv::fold_fwd_kernel<<<grid, 128, 0, s>>>(fa);
       FV_CUDA(cudaGetLastError());
     }
     {
       StageMark mk(p, 2, s);
-      fv::FwdArgs args{p->X, p->F, p->seed_x, p->seed_e, p->ab, p->abofs, p->pair_t, Lt, p->nPpad, p->nchunks, 0};
+      fv::FwdArgs args{p->X, p->F, p->start_l, p->start_v, p->ab, p->abofs, p->pair_t, Lt, p->nP, p->nPpad, p->nchunks, 0, dbg_mode()};
       FV_TRY(dispatch_fwd(p, NT, args, Lt + 1, s));
     }
     {
@@ -475,15 +498,15 @@ int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int 
       StageMark mk(p, 3, s);
       fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), p->G, p->gofs,
                        nullptr, p->L, NT, B, b0, nf, 0, 0};
-      const int rows = (Lt + 1 + 63) / 64 * 64;
+      const int rows = (Lt + 1 + fv::ADJ_LC - 1) / fv::ADJ_LC * fv::ADJ_LC;
       dim3 grid((rows + 127) / 128, Lt + 1);
       fv::cg_adj_kernel<<<grid, 128, 0, s>>>(ca);
       FV_CUDA(cudaGetLastError());
     }
     {
       StageMark mk(p, 2, s);
-      fv::AdjArgs args{p->G, p->gofs, p->Sa, p->seed_x, p->seed_e, p->ab, p->abofs, p->pair_t, p->pair_n,
-                       p->pair_s, Lt, p->nPpad, p->nrc, p->n_phi, p->n_theta, B, b0, nf, 0};
+      fv::AdjArgs args{p->G, p->gofs, p->Sa, p->start_l, p->start_v, p->ab, p->abofs, p->pair_t, p->pair_n,
+                       p->pair_s, Lt, p->nP, p->nPpad, p->nrc, p->n_phi, p->n_theta, B, b0, nf, 0, dbg_mode()};
       FV_TRY(dispatch_adj(p, NT, args, Lt + 1, s));
     }
   }

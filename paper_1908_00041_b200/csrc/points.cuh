@@ -66,8 +66,8 @@ __global__ void __launch_bounds__(128) adjoint_points_kernel(PtsArgs a) {
       } else if (l == m + 1) {
         v = p1;
       } else {
-        const double2 abv = abm[l - m - 2];
-        const double pn = __dmul_rn(abv.x, __dsub_rn(__dmul_rn(t, p1), __dmul_rn(abv.y, p2)));
+        const double2 abv = abm[l - m - 2];  // (a_l, a_l * b_l)
+        const double pn = fma(abv.x * t, p1, -(abv.y * p2));
         p2 = p1;
         p1 = pn;
         if (e < 0 && fabs(p1) >= 0x1p512) {
