@@ -246,7 +246,7 @@ def sht_forward_grid(f, ring_thetas, ring_weights, n_phi, lt, orders=None):
     return out
 
 
-def sht_adjoint_grid(g, lt, ring_thetas, n_phi, orders=None):
+def sht_adjoint_grid(g, lt, ring_thetas, n_phi, orders=None, spectrum=False):
     """Scalar adjoint on a tensor grid (favest/scalar.py:170-179):
     spectrum[r, m mod n_phi] = sum_l Pbar_l^{|m|}(t_r) sigma_m g_{l,m}, then
     ifft * n_phi.  ``g`` is (flat_size(lt), C).  Returns (N, C)."""
@@ -268,6 +268,8 @@ def sht_adjoint_grid(g, lt, ring_thetas, n_phi, orders=None):
             mm = sgn * m
             cols = _sigma(mm) * g[ls * ls + ls + mm]  # (n_l, C)
             spec[:, mm % n_phi, :] = P.T @ cols.real + 1j * (P.T @ cols.imag)
+    if spectrum:  # ring spectra before the inverse DFT: (n_theta, n_phi, C)
+        return spec
     out = np.fft.ifft(spec, axis=1) * n_phi
     return out.reshape(n_theta * n_phi, C)
 
@@ -457,11 +459,12 @@ def vsht_adjoint_merged(a, b, lmax):
     )
 
 
-def vsht_adjoint_grid(a, b, lmax, ring_thetas, n_phi, orders=None):
+def vsht_adjoint_grid(a, b, lmax, ring_thetas, n_phi, orders=None, spectrum=False):
     """Adjoint FaVeST on a GL grid (favest/transforms.py:150-181, fast path).
-    Returns (N, 3) complex Cartesian components."""
+    Returns (N, 3) complex Cartesian components, or with ``spectrum`` the ring
+    spectra (n_theta, n_phi, 3) of which only the bins of ``orders`` are filled."""
     merged = vsht_adjoint_merged(a, b, lmax)
-    return sht_adjoint_grid(merged, lmax + 1, ring_thetas, n_phi, orders=orders)
+    return sht_adjoint_grid(merged, lmax + 1, ring_thetas, n_phi, orders=orders, spectrum=spectrum)
 
 
 def vsht_adjoint_points(a, b, lmax, points):

@@ -1,0 +1,107 @@
+"""The numpy oracle (oracle/) pinned against the reference's own outputs.
+
+Golden vectors come from the unmodified reference (tests/golden/make_golden.py);
+known-answer values are those of the reference's tests
+(pkg/tests/test_legendre.py:23-29, pkg/tests/test_coupling.py:16-20).
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import oracle.favest_oracle as FO
+
+
+def test_legendre_bitwise_against_reference(golden):
+    d = golden("legendre_l40")
+    p = O.legendre_table(40, d["t"])
+    assert np.array_equal(p, d["p"])
+
+
+def test_legendre_known_answers():
+    # pkg/tests/test_legendre.py:23-29
+    p = O.legendre_table(2, np.array([1.0, 0.0, -0.37]))
+    assert np.allclose(p[:, O.tri_index(0, 0)], 0.28209479177387814, atol=1e-15)
+    assert p[0, O.tri_index(1, 0)] == pytest.approx(0.4886025119029199, abs=1e-12)
+    assert p[0, O.tri_index(1, 1)] == pytest.approx(0.0, abs=1e-15)
+    assert p[1, O.tri_index(2, 0)] == pytest.approx(-0.3153915652525201, abs=1e-12)
+
+
+def test_coupling_weights_known_answers():
+    # pkg/tests/test_coupling.py:16-20: c_1, d_1
+    assert FO._coupling_c(1) == pytest.approx(0.8164965809277260, abs=1e-15)
+    assert FO._coupling_d(1) == pytest.approx(0.5773502691896258, abs=1e-15)
+
+
+def test_cg_tables_bitwise_against_reference(golden):
+    d = golden("cg_tables_l12")
+    xi, mu = O.cg_tables(12)
+    for i in range(1, 7):
+        assert np.array_equal(xi[i], d[f"xi{i}"]), i
+    for i in range(1, 4):
+        assert np.array_equal(mu[i], d[f"mu{i}"]), i
+
+
+@pytest.mark.parametrize("lmax", [8, 17, 32])
+def test_grid_roundtrip_against_reference(golden, lmax):
+    g = golden(f"roundtrip_l{lmax}")
+    th, w, nphi = O.gl_grid(lmax)
+    assert np.array_equal(th, g["ring_thetas"]) and np.array_equal(w, g["ring_weights"])
+    assert nphi == int(g["n_phi"])
+    T = O.vsht_adjoint_grid(g["a"], g["b"], lmax, th, nphi)
+    assert O.rel_l2(T, g["T"]) <= 1e-14
+    fa, fb = O.vsht_forward_grid(g["T"], th, w, nphi, lmax)
+    assert O.rel_l2(np.concatenate([fa, fb]), np.concatenate([g["fa"], g["fb"]])) <= 1e-14
+    fa, fb = O.vsht_forward_grid(g["Tn"], th, w, nphi, lmax)
+    assert O.rel_l2(np.concatenate([fa, fb]), np.concatenate([g["fna"], g["fnb"]])) <= 1e-14
+
+
+@pytest.mark.parametrize("name", ["scattered_l16_m300", "scattered_l9_m64"])
+def test_scattered_adjoint_against_reference(golden, name):
+    g = golden(name)
+    T = O.vsht_adjoint_points(g["a"], g["b"], int(g["lmax"]), g["points"])
+    assert O.rel_l2(T, g["T"]) <= 1e-14
+
+
+def test_forward_is_weighted_adjoint_of_adjoint():
+    # <F T, c> = <T, S c>_w for the scalar transforms (pkg/tests/test_scalar.py:72-82)
+    rng = np.random.default_rng(4)
+    L = 12
+    th, w, nphi = O.gl_grid(L)
+    N = len(th) * nphi
+    f = rng.standard_normal((N, 1)) + 1j * rng.standard_normal((N, 1))
+    g = rng.standard_normal((O.flat_size(L), 1)) + 1j * rng.standard_normal((O.flat_size(L), 1))
+    Ff = O.sht_forward_grid(f, th, w, nphi, L)
+    Sg = O.sht_adjoint_grid(g, L, th, nphi)
+    lhs = np.vdot(g, Ff)
+    wts = np.repeat(w, nphi)[:, None]
+    rhs = np.vdot(Sg * wts, f)
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+
+
+def test_extended_range_orthonormal_at_l4096():
+    # X-number recurrence stays finite and orthonormal where the reference underflows
+    L = 4096
+    th, w, nphi = O.gl_grid(L)
+    t, s = O.ring_cos_sin(th)
+    sx, se = O.seed_table(L + 1, s)
+    assert se.min() < -1024  # seeds far below the double range
+    gw = w * nphi / (2 * np.pi)
+    for m in (1500, 4000):
+        P = O.legendre_m(m, L + 1, t, sx[m], se[m])
+        assert np.all(np.isfinite(P))
+        G = (P * gw) @ P.T * 2 * np.pi
+        assert np.max(np.abs(G - np.eye(len(G)))) < 1e-11
+
+
+def test_partial_orders_match_full():
+    L = 20
+    th, w, nphi = O.gl_grid(L)
+    rng = np.random.default_rng(9)
+    a, b = O.coef(rng, L, "inv")
+    T = O.vsht_adjoint_grid(a, b, L, th, nphi)
+    fa, fb = O.vsht_forward_grid(T, th, w, nphi, L)
+    pa, pb = O.vsht_forward_grid(T, th, w, nphi, L, orders=[0, 5, 20])
+    ls, ms = O.degrees_orders(L)
+    sel = np.isin(np.abs(ms), [0, 5, 20])
+    assert np.array_equal(pa[sel], fa[sel]) and np.array_equal(pb[sel], fb[sel])
