@@ -1,0 +1,419 @@
+#!/usr/bin/env python
+"""bench.py — FaVeST forward+adjoint VSHT throughput on B200.
+
+Metric (BASELINE.json): fp64 forward+adjoint VSHT transforms/sec at L=1024,
+and the fraction of the FP64 roofline.  One step = forward then adjoint of
+every field of the batch (BASELINE configs[2]: L=1024, Gauss-Legendre
+1026 x 2052 grid, 4 fields per GPU, coefficients CN(0,1)(1+l)^-2, field =
+adjoint(coefficients) + tangent N(0, 1e-3) noise).  value = fields pushed
+through forward+adjoint per second over all ranks.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N > 1: launched by torchrun, one process per GPU, fields sharded by batch
+(weak scaling, no data-path collective); max over ranks of the CUDA-event
+time.  --impl reference times the reference algorithm's CPU implementation
+(the numpy oracle port in oracle/, all host cores) on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 forward+adjoint VSHT transforms/sec at L=1024; fraction of FP64/HBM roofline"
+UNIT = "fields/s (forward+adjoint per field)"
+# FP64 peaks: DMMA.8x8x4 measured on this pool's B200 (tools/fp64_microbench.cu,
+# profiles/r01_fp64_microbench.txt); the datasheet figure is 40 TFLOP/s.
+FP64_PEAK_MEASURED = 37.0
+FP64_PEAK_DATASHEET = 40.0
+
+
+def canonical_flops(L: int, B: int) -> dict:
+    """SURVEY §8(d) canonical count per direction: folded Legendre contraction
+    6*B*n_theta*(L+2)^2 plus three complex ring FFTs 15*B*n_theta*n_phi*log2(n_phi)."""
+    nth, nph = L + 2, 2 * L + 4
+    leg = 6.0 * B * nth * (L + 2) ** 2
+    fft = 15.0 * B * nth * nph * np.log2(nph)
+    return {"legendre": leg, "fft": fft, "total": leg + fft}
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """Polls NVML (SM clock, max clock, clock-event reasons) every ~2 ms in a
+    thread while the timed region runs (the B200_PROFILING.md clocks line)."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, torch_device):
+        self.dev = torch_device
+        self.samples = []
+        self.max_mhz = None
+        self.stop = threading.Event()
+        self.ok = False
+
+    def __enter__(self):
+        try:
+            import pynvml as nv
+            import torch
+
+            nv.nvmlInit()
+            h = None
+            try:
+                bus = torch.cuda.get_device_properties(self.dev).pci_bus_id
+                h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = nv.nvmlDeviceGetHandleByIndex(self.dev.index or 0)
+            self.nv, self.h = nv, h
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self.ok = True
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        except Exception as exc:  # pragma: no cover - NVML missing
+            self.err = str(exc)
+        return self
+
+    def _run(self):
+        nv, h = self.nv, self.h
+        while not self.stop.is_set():
+            try:
+                clk = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                try:
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:
+                    rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append((float(clk), int(rs)))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if self.ok:
+            self.t.join(timeout=1)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"], "samples": 0}
+        reasons = set()
+        for _, rs in self.samples:
+            for bit, name in self.REASONS.items():
+                if rs & bit:
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median([c for c, _ in self.samples])), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(self.samples), "source": "NVML, 2 ms polling"}
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+def make_inputs(L: int, B: int, seed: int):
+    """BASELINE configs[2] recipe: coefficients first (div then curl per field), then
+    tangent noise sigma=1e-3 on top of the adjoint field."""
+    import oracle.favest_oracle as O  # only the seeded generators (no oracle compute)
+
+    rng = np.random.default_rng(seed)
+    ab = [O.coef(rng, L, "pow2") for _ in range(B)]
+    return rng, np.stack([x[0] for x in ab]), np.stack([x[1] for x in ab])
+
+
+def cpu_port_rate(L: int, sample_orders_every: int):
+    """Time the numpy port of the reference algorithm (oracle/) on one field.
+
+    The order-independent parts (ring FFTs, Clebsch-Gordan stages, tables) run in
+    full; the per-order Legendre stage runs on every k-th order and is scaled by
+    the sampled fraction of the per-order work.  Returns (fields/s, seconds for
+    the extrapolated full forward+adjoint, description)."""
+    import oracle.favest_oracle as O
+
+    th, w, nph = O.gl_grid(L)
+    rng = np.random.default_rng(3)
+    a, b = O.coef(rng, L, "pow2")
+    T = O.tangent_noise(rng, O.grid_points(th, nph), 1.0)
+    Lt = L + 1
+    orders = list(range(0, Lt + 1, sample_orders_every))
+    frac = sum(Lt + 1 - m for m in orders) / sum(Lt + 1 - m for m in range(Lt + 1))
+
+    def clock(fn):
+        t0 = time.perf_counter()
+        out = fn()
+        return time.perf_counter() - t0, out
+
+    t1, t2, t3 = T[:, 0], T[:, 1], T[:, 2]
+    combos = np.stack([-t1 + 1j * t2, t1 + 1j * t2, t3], axis=1)        # favest/transforms.py:109-112
+    tf0, _ = clock(lambda: O.sht_forward_grid(combos, th, w, nph, Lt, orders=[]))
+    tfs, f = clock(lambda: O.sht_forward_grid(combos, th, w, nph, Lt, orders=orders))
+    tcf, _ = clock(lambda: O.cg_forward_assemble(f, L))
+    tca, g = clock(lambda: O.vsht_adjoint_merged(a, b, L))
+    ta0, _ = clock(lambda: O.sht_adjoint_grid(g, Lt, th, nph, orders=[]))
+    tas, _ = clock(lambda: O.sht_adjoint_grid(g, Lt, th, nph, orders=orders))
+    total = tf0 + max(tfs - tf0, 0.0) / frac + tcf + tca + ta0 + max(tas - ta0, 0.0) / frac
+    desc = (f"numpy oracle port (oracle/favest_oracle.py, OpenBLAS) of one field at L={L}: ring FFTs and "
+            f"CG stages in full, per-order Legendre stage on every {sample_orders_every}th order "
+            f"(work fraction {frac:.3f}) scaled to all orders; forward+adjoint")
+    return 1.0 / total, total, desc
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+
+        return sum(int(x.get("num_threads", 0)) for x in threadpool_info() if x.get("user_api") == "blas") or None
+    except Exception:
+        return None
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the path's CPU implementation on the host cores, rank 0 only
+    (the reference is pure Python/numpy and cannot travel to the GPU box, so the
+    numpy port in oracle/ stands in for it)."""
+    if rank != 0:
+        return
+    L = args.L
+    for _ in range(args.warmup):
+        cpu_port_rate(L, args.ref_every * 4)
+    rates, secs = [], []
+    desc = ""
+    for _ in range(args.steps):
+        r, dt, desc = cpu_port_rate(L, args.ref_every)
+        rates.append(r)
+        secs.append(dt)
+    rate = float(np.median(rates))
+    cores = os.cpu_count()
+    line = {
+        "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": float(np.median(secs)) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(L, args.batch, world), "impl": "reference",
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc,
+                         "blas_threads": blas_threads(), "numpy": np.__version__},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(L, B, world):
+    return {"workload": f"C3 (BASELINE configs[2]): L={L} Gauss-Legendre {L + 2}x{2 * L + 4} grid, "
+                        f"{B} fields per GPU, forward then adjoint per step",
+            "L": L, "fields_per_gpu": B, "global_batch": B * world, "n_theta": L + 2, "n_phi": 2 * L + 4,
+            "parallelism": f"batch-sharded x{world} (no collective)",
+            "l2": "inputs exceed the 126 MB L2 (404 MB field batch per GPU), no explicit flush"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    import oracle.favest_oracle as O
+    from paper_1908_00041_b200.grid import gl_grid_for
+    from paper_1908_00041_b200.plan import GridPlan
+
+    L, B = args.L, args.batch
+    grid, _ = gl_grid_for(L)
+    plan = GridPlan.from_grid(grid, L, max_batch=B, device=dev)
+    rng, A, Bc = make_inputs(L, B, seed=3 + rank)
+    A_d = torch.from_numpy(A).to(dev)
+    B_d = torch.from_numpy(Bc).to(dev)
+    T0 = plan.adjoint(A_d, B_d)
+    pts = torch.from_numpy(O.grid_points(grid.ring_thetas, grid.n_phi)).to(dev)
+    # tangent N(0, 1e-3) noise, generated on the device
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    noise = 1e-3 * torch.complex(torch.randn(T0.shape, generator=g, device=dev, dtype=torch.float64),
+                                 torch.randn(T0.shape, generator=g, device=dev, dtype=torch.float64))
+    noise -= (noise * pts).sum(-1, keepdim=True) * pts
+    T = (T0 + noise).contiguous()
+    del T0, noise
+    a = torch.empty((B, plan.n_coeffs), dtype=torch.complex128, device=dev)
+    b = torch.empty_like(a)
+    Tout = torch.empty_like(T)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        plan.forward(T, a, b)
+        plan.adjoint(a, b, Tout)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    plan.set_profiling(True)  # CUDA events around each stage on the call's stream
+    with ClockSampler(dev) as clocks:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    ms_total = max_over_ranks(e0.elapsed_time(e1))
+    stage_ms = plan.stage_ms()
+    stage_n = plan.stage_counts()
+    plan.set_profiling(False)
+    ms_step = ms_total / args.steps
+    value = world * B * args.steps / (ms_total / 1e3)
+
+    # forward-only / adjoint-only device times (separate short loops)
+    def timed(fn, n):
+        barrier()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(n):
+            fn()
+        s1.record(stream)
+        barrier()
+        return max_over_ranks(s0.elapsed_time(s1)) / n
+
+    n_sub = max(3, args.steps // 2)
+    ms_fwd = timed(lambda: plan.forward(T, a, b), n_sub)
+    ms_adj = timed(lambda: plan.adjoint(a, b, Tout), n_sub)
+
+    # roofline of the dominant kernel: the Legendre contraction (forward + adjoint launches)
+    fl = canonical_flops(L, B)
+    n_leg = max(1, stage_n["legendre"])
+    leg_ms = stage_ms["legendre"] / n_leg  # average launch (forward and adjoint alternate)
+    achieved = fl["legendre"] / (leg_ms / 1e3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "legendre_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_MEASURED, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_MEASURED, "traffic": traffic,
+                "kernel": "legendre_fwd_kernel / legendre_adj_kernel (FP64 DMMA.8x8x4)",
+                "flops_per_launch": fl["legendre"],
+                "flops_basis": "6*B*n_theta*(L+2)^2 canonical folded contraction (SURVEY §8(d))",
+                "peak_source": "DMMA microbenchmark on this pool (profiles/r01_fp64_microbench.txt); "
+                               "datasheet 40 TFLOP/s; MEASURED_PEAKS.json has no FP64 entry",
+                "avg_launch_ms": leg_ms, "share_of_step": stage_ms["legendre"] / ms_total}
+    hbm, hbm_src = hbm_peak()
+    step_frac = (2 * fl["total"] / (ms_step / 1e3)) / (FP64_PEAK_DATASHEET * 1e12)
+
+    # end to end: pinned host buffers through the public API, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        Th = torch.empty(T.shape, dtype=T.dtype, pin_memory=True)
+        Th.copy_(T)
+        Toh = torch.empty_like(Th, pin_memory=True)
+        Td = torch.empty_like(T)
+
+        def e2e_step():
+            Td.copy_(Th, non_blocking=True)
+            plan.forward(Td, a, b)
+            plan.adjoint(a, b, Tout)
+            Toh.copy_(Tout, non_blocking=True)
+
+        e2e_step()
+        n_e = max(2, min(args.steps, 5))
+        ms_e = timed(e2e_step, n_e)
+        bytes_io = T.numel() * 16
+        e2e = {"value": world * B / (ms_e / 1e3), "unit": UNIT, "h2d_bytes_per_step": bytes_io,
+               "d2h_bytes_per_step": bytes_io, "ms_per_step": ms_e,
+               "path": "pinned host (B,N,3) -> GridPlan.forward -> GridPlan.adjoint -> pinned host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, dt, desc = cpu_port_rate(L, args.ref_every)
+        cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": desc,
+               "seconds": dt, "blas_threads": blas_threads(), "numpy": np.__version__}
+
+    if rank == 0:
+        groups = (B + 3) // 4
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(L, B, world),
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks.summary(),
+            "gpu_launches": args.steps * groups * 5,
+            "detail": {
+                "forward_ms": ms_fwd, "adjoint_ms": ms_adj,
+                "forward_fields_per_s": world * B / (ms_fwd / 1e3),
+                "adjoint_fields_per_s": world * B / (ms_adj / 1e3),
+                "stage_ms_per_step": {k: v / args.steps for k, v in stage_ms.items()},
+                "canonical_gflop_per_direction": fl["total"] / 1e9,
+                "step_fraction_of_fp64_roofline_datasheet": step_frac,
+                "forward_fraction_of_roofline": (fl["total"] / (ms_fwd / 1e3)) / (FP64_PEAK_DATASHEET * 1e12),
+                "adjoint_fraction_of_roofline": (fl["total"] / (ms_adj / 1e3)) / (FP64_PEAK_DATASHEET * 1e12),
+                "hbm_peak_gbs": hbm, "hbm_peak_source": hbm_src,
+                "polar_skip_threshold": "2^-100 (values below are exact zeros; SURVEY §7 hard part 2)",
+                "launches_note": "per step per 4-field group: fold, legendre_fwd, cg_fwd, cg_adj, "
+                                 "legendre_adj (ring FFTs are cuFFT library kernels)",
+            },
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--L", type=int, default=1024)
+    ap.add_argument("--batch", type=int, default=4, help="fields per GPU")
+    ap.add_argument("--ref-every", type=int, default=8, help="order stride of the CPU sample")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

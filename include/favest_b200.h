@@ -90,12 +90,15 @@ int fv_adjoint_points(fvPlan* plan, const double* xyz, long long M, const double
                       double* T, int B, void* stream);
 
 /*
- * Stage timing of the last call on this plan (milliseconds, CUDA events on
- * the call's stream; only filled when fv_set_profiling(plan, 1)).
- * stage: 0 fft, 1 fold, 2 legendre, 3 cg.  Returns -1 if unavailable.
+ * Stage timing (milliseconds, CUDA events recorded on each call's stream):
+ * fv_set_profiling(plan, 1) starts accumulating over all following calls,
+ * fv_stage_ms sums one stage (0 fft, 1 fold, 2 legendre, 3 cg) and the number
+ * of launches of that stage is fv_stage_count.  fv_set_profiling(plan, 0)
+ * stops and resets.  Returns -1 if nothing was recorded.
  */
 int fv_set_profiling(fvPlan* plan, int enable);
 double fv_stage_ms(const fvPlan* plan, int stage);
+int fv_stage_count(const fvPlan* plan, int stage);
 
 #ifdef __cplusplus
 }

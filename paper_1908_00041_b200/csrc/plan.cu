@@ -237,8 +237,6 @@ int dispatch_adj(fvPlan* p, int NT, const fv::AdjArgs& a, int mc, cudaStream_t s
 int begin_call(fvPlan* p) {
   if (!p) return fail(FV_EINVAL, "null plan");
   FV_CUDA(cudaSetDevice(p->device));
-  p->marks.clear();
-  p->ev_used = 0;
   g_err.clear();
   return FV_OK;
 }
@@ -417,12 +415,15 @@ int fv_plan_info(const fvPlan* p, int* L, int* n_theta, int* n_phi, int* n_pairs
 
 int fv_set_profiling(fvPlan* p, int enable) {
   if (!p) return fail(FV_EINVAL, "null plan");
+  if (p->profiling && !p->marks.empty()) cudaEventSynchronize(p->marks.back().second.second);
   p->profiling = enable != 0;
+  p->marks.clear();  // stage times accumulate over all calls until the next fv_set_profiling
+  p->ev_used = 0;
   return FV_OK;
 }
 
 double fv_stage_ms(const fvPlan* p, int stage) {
-  if (!p || !p->profiling || p->marks.empty()) return -1.0;
+  if (!p || p->marks.empty()) return -1.0;
   cudaEventSynchronize(p->marks.back().second.second);
   double tot = 0.0;
   for (auto& mk : p->marks) {
@@ -432,6 +433,13 @@ double fv_stage_ms(const fvPlan* p, int stage) {
     tot += ms;
   }
   return tot;
+}
+
+int fv_stage_count(const fvPlan* p, int stage) {
+  if (!p) return 0;
+  int n = 0;
+  for (auto& mk : p->marks) n += mk.first == stage;
+  return n;
 }
 
 int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, void* stream) {

@@ -98,9 +98,14 @@ class GridPlan:
     def set_profiling(self, enable: bool = True):
         _lib.check(self.lib.fv_set_profiling(self._h, int(bool(enable))))
 
+    STAGES = ("fft", "fold", "legendre", "cg")
+
     def stage_ms(self) -> dict:
-        names = ("fft", "fold", "legendre", "cg")
-        return {n: self.lib.fv_stage_ms(self._h, i) for i, n in enumerate(names)}
+        """Accumulated stage times (ms) since set_profiling(True)."""
+        return {n: self.lib.fv_stage_ms(self._h, i) for i, n in enumerate(self.STAGES)}
+
+    def stage_counts(self) -> dict:
+        return {n: self.lib.fv_stage_count(self._h, i) for i, n in enumerate(self.STAGES)}
 
     def forward(self, T, a=None, b=None):
         """T (B, N, 3) complex128 -> (a, b), each (B, (lmax+1)**2) complex128."""
