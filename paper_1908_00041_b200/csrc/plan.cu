@@ -15,6 +15,7 @@
 
 #include "../../include/favest_b200.h"
 #include "aux_kernels.cuh"
+#include "fft.cuh"
 #include "legendre.cuh"
 #include "points.cuh"
 
@@ -87,6 +88,11 @@ struct fvPlan {
   double* F = nullptr;
   double* G = nullptr;
   std::map<int, std::pair<cufftHandle, cufftHandle>> ffts;
+  // hand-written ring FFT (fft.cuh) when every prime factor of n_phi is <= 19
+  bool custom_fft = false;
+  int fft_nst = 0;
+  int fft_radix[fv::FFT_MAXST] = {};
+  double2* fft_tw = nullptr;
   // profiling
   bool profiling = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
@@ -108,7 +114,8 @@ void free_plan(fvPlan* p) {
   cudaSetDevice(p->device);
   void* ptrs[] = {p->pair_t, p->pair_sin, p->pair_n, p->pair_s, p->ring_w, p->seed_x,
                   p->seed_e, p->start_l,  p->start_v, p->ab,   p->abofs,  p->gofs,
-                  p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->G};
+                  p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->G,
+                  p->fft_tw};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (auto& kv : p->ffts) {
@@ -234,6 +241,83 @@ int dispatch_adj(fvPlan* p, int NT, const fv::AdjArgs& a, int mc, cudaStream_t s
   return fail(FV_EINVAL, "unsupported field group");
 }
 
+// radix sequence for the hand-written FFT: 4s, then 2, then odd primes <= 19
+bool fft_factor(int n, int* radix, int* nst) {
+  if (n < 2 || n > fv::FFT_NMAX) return false;
+  int k = 0;
+  auto push = [&](int r) {
+    if (k >= fv::FFT_MAXST) return false;
+    radix[k++] = r;
+    return true;
+  };
+  while (n % 4 == 0) { if (!push(4)) return false; n /= 4; }
+  while (n % 2 == 0) { if (!push(2)) return false; n /= 2; }
+  for (int p : {3, 5, 7, 11, 13, 17, 19})
+    while (n % p == 0) { if (!push(p)) return false; n /= p; }
+  *nst = k;
+  return n == 1;
+}
+
+int setup_fft(fvPlan* p) {
+  const char* env = std::getenv("FV_FFT");
+  const bool force_cufft = env && std::string(env) == "cufft";
+  if (force_cufft || !fft_factor(p->n_phi, p->fft_radix, &p->fft_nst)) return FV_OK;
+  // roots of the odd-prime butterflies (per device: __constant__ lives in each context)
+  double rc[75], rs[75];
+  for (int R : {3, 5, 7, 11, 13, 17, 19})
+    for (int m = 0; m < R; ++m) {
+      const long double a = 2.0L * 3.141592653589793238462643383279502884L * m / R;
+      rc[fv::root_offset(R) + m] = (double)cosl(a);
+      rs[fv::root_offset(R) + m] = (double)sinl(a);
+    }
+  FV_CUDA(cudaMemcpyToSymbol(fv::kRootCos, rc, sizeof(rc)));
+  FV_CUDA(cudaMemcpyToSymbol(fv::kRootSin, rs, sizeof(rs)));
+  std::vector<double2> tw(p->n_phi);
+  for (int k = 0; k < p->n_phi; ++k) {
+    const long double a = 2.0L * 3.141592653589793238462643383279502884L * k / p->n_phi;
+    tw[k] = make_double2((double)cosl(a), -(double)sinl(a));
+  }
+  FV_TRY(dalloc(&p->fft_tw, p->n_phi));
+  FV_CUDA(cudaMemcpy(p->fft_tw, tw.data(), p->n_phi * sizeof(double2), cudaMemcpyHostToDevice));
+  const size_t smem = 2 * (size_t)p->n_phi * sizeof(double2);
+  FV_CUDA(cudaFuncSetAttribute(fv::ring_fft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  FV_CUDA(cudaFuncSetAttribute(fv::ring_fft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  p->custom_fft = true;
+  return FV_OK;
+}
+
+// forward: T [B][N][3] (AoS) -> S[c][b][ring][q]; inverse: S -> T
+int ring_fft(fvPlan* p, bool inverse, const double2* in, double2* out, int B, cudaStream_t s) {
+  fv::RingFftArgs a{};
+  const long long n = p->n_phi, spec_cs = (long long)B * p->n_theta * n;
+  a.in = in;
+  a.out = out;
+  if (!inverse) {
+    a.in_cs = 1; a.in_rs = 3 * n; a.in_es = 3;
+    a.out_cs = spec_cs; a.out_rs = n; a.out_es = 1;
+  } else {
+    a.in_cs = spec_cs; a.in_rs = n; a.in_es = 1;
+    a.out_cs = 1; a.out_rs = 3 * n; a.out_es = 3;
+  }
+  a.tw = p->fft_tw;
+  a.n = p->n_phi;
+  a.nst = p->fft_nst;
+  int ns = 1;
+  for (int i = 0; i < p->fft_nst; ++i) {
+    a.radix[i] = p->fft_radix[i];
+    a.ns[i] = ns;
+    a.nsmagic[i] = ns == 1 ? 0u : (unsigned)((0x100000000ull + ns - 1) / ns);  // exact j/ns for j < 2^16
+    a.tstride[i] = p->n_phi / (ns * p->fft_radix[i]);
+    ns *= p->fft_radix[i];
+  }
+  dim3 grid(3, B * p->n_theta);
+  const size_t smem = 2 * (size_t)n * sizeof(double2);
+  if (inverse) fv::ring_fft_kernel<true><<<grid, fv::FFT_THREADS, smem, s>>>(a);
+  else fv::ring_fft_kernel<false><<<grid, fv::FFT_THREADS, smem, s>>>(a);
+  FV_CUDA(cudaGetLastError());
+  return FV_OK;
+}
+
 int begin_call(fvPlan* p) {
   if (!p) return fail(FV_EINVAL, "null plan");
   FV_CUDA(cudaSetDevice(p->device));
@@ -354,6 +438,7 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
   p->g_tiles = gofs[Lt + 1];
   if ((rc = dalloc(&p->gofs, Lt + 1))) return bail(rc);
   cudaMemcpy(p->gofs, gofs.data(), (Lt + 1) * 8, cudaMemcpyHostToDevice);
+  if ((rc = setup_fft(p))) return bail(rc);
   // workspaces (field groups of <= 4 -> NT <= 6)
   const int gs = std::min(4, max_batch);
   const int NTmax = ntiles_for(gs);
@@ -449,10 +534,13 @@ int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, voi
     return fail(FV_EINVAL, "batch " + std::to_string(B) + " outside 1.." + std::to_string(p->max_batch));
   if (!T || !a || !b) return fail(FV_EINVAL, "null data pointer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  cufftHandle hf, hi;
-  FV_TRY(get_ffts(p, B, &hf, &hi));
   const size_t per_comp = (size_t)B * p->n_theta * p->n_phi;
-  {
+  if (p->custom_fft) {
+    StageMark mk(p, 0, s);
+    FV_TRY(ring_fft(p, false, reinterpret_cast<const double2*>(T), p->Sf, B, s));
+  } else {
+    cufftHandle hf, hi;
+    FV_TRY(get_ffts(p, B, &hf, &hi));
     StageMark mk(p, 0, s);
     FV_CUFFT(cufftSetStream(hf, s));
     for (int c = 0; c < 3; ++c) {
@@ -496,8 +584,6 @@ int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int 
     return fail(FV_EINVAL, "batch " + std::to_string(B) + " outside 1.." + std::to_string(p->max_batch));
   if (!T || !a || !b) return fail(FV_EINVAL, "null data pointer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  cufftHandle hf, hi;
-  FV_TRY(get_ffts(p, B, &hf, &hi));
   const int Lt = p->Lt;
   for (int b0 = 0; b0 < B; b0 += 4) {
     const int nf = std::min(4, B - b0);
@@ -518,7 +604,12 @@ int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int 
       FV_TRY(dispatch_adj(p, NT, args, Lt + 1, s));
     }
   }
-  {
+  if (p->custom_fft) {
+    StageMark mk(p, 0, s);
+    FV_TRY(ring_fft(p, true, p->Sa, reinterpret_cast<double2*>(T), B, s));
+  } else {
+    cufftHandle hf, hi;
+    FV_TRY(get_ffts(p, B, &hf, &hi));
     StageMark mk(p, 0, s);
     FV_CUFFT(cufftSetStream(hi, s));
     const size_t per_comp = (size_t)B * p->n_theta * p->n_phi;
