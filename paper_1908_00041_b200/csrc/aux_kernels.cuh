@@ -50,7 +50,8 @@ __device__ __forceinline__ bool xr_significant(double x, int e) {
 
 __global__ void start_kernel(const double* __restrict__ seed_x, const int* __restrict__ seed_e,
                              const double* __restrict__ pair_t, const int* __restrict__ pair_n,
-                             const double2* __restrict__ ab, const long long* __restrict__ abofs, int nPpad,
+                             const double2* __restrict__ ab, const long long* __restrict__ abofs,
+                             const double2* __restrict__ dg, const long long* __restrict__ dgofs, int nPpad,
                              int Lt, int* start_l, double2* start_v) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   const int m = blockIdx.y;
@@ -95,8 +96,56 @@ __global__ void start_kernel(const double* __restrict__ seed_x, const int* __res
       }
     }
   }
+  // injected in block-rescaled units R = P / gamma (legendre.cuh)
+  if (ls <= Lt) {
+    const double2* dgm = dg + dgofs[m];
+    A = A / dgm[ls - m].y;
+    B = (ls + 1 <= Lt) ? B / dgm[ls + 1 - m].y : 0.0;
+  }
   start_l[o] = ls;
   start_v[o] = make_double2(A, B);
+}
+
+// Block-rescaled recurrence coefficients (legendre.cuh): for each order m the
+// degrees are cut into 32-blocks starting at l = m; inside a block
+//   P_l = gamma_l R_l,  R_l = t R_{l-1} - d_l R_{l-2},
+//   gamma_l = gamma_{l-1} a_l, d_l = b_l / a_{l-1}        (interior rows)
+//   gamma_l = a_l, d_l = b_l                              (first recurrence row of a block:
+//                                                          l = m+2 or (l-m) % 32 == 0)
+// with a_l, b_l of favest/legendre.py:70-71; rows l = m, m+1 (seeds) have
+// (d, gamma) = (0, 1).  At block ends the state is converted back to P.
+// One thread per (m, block).  dg[dgofs[m] + (l - m)] = (d_l, gamma_l).
+__global__ void dg_kernel(int Lt, const long long* __restrict__ dgofs, double2* dg) {
+  const int m = blockIdx.y;
+  const int blk = blockIdx.x * blockDim.x + threadIdx.x;
+  const int l0 = m + 32 * blk;
+  if (l0 > Lt) return;
+  double2* out = dg + dgofs[m];
+  auto ab_of = [&](int l, double& a, double& b) {
+    const long long L2 = (long long)l * l, M2 = (long long)m * m;
+    const double lf = (double)l;
+    a = sqrt((4.0 * lf * lf - 1.0) / (double)(L2 - M2));
+    const double lm1 = lf - 1.0;
+    b = sqrt((lm1 * lm1 - (double)M2) / (4.0 * (lm1 * lm1) - 1.0));
+  };
+  double gam = 1.0;
+  for (int l = l0; l <= min(Lt, l0 + 31); ++l) {
+    if (l < m + 2) {
+      out[l - m] = make_double2(0.0, 1.0);
+      continue;
+    }
+    double a, b;
+    ab_of(l, a, b);
+    if (l == m + 2 || l == l0) {
+      gam = a;
+      out[l - m] = make_double2(b, gam);
+    } else {
+      double ap, bp;
+      ab_of(l - 1, ap, bp);
+      gam *= a;
+      out[l - m] = make_double2(b / ap, gam);
+    }
+  }
 }
 
 // (a_l, a_l * b_l) for l = m+2..Lt, stored m-major at abofs[m] + (l - m - 2).
@@ -257,6 +306,8 @@ __global__ void cg_fwd_kernel(CgFwdArgs a) {
 struct CgAdjArgs {
   const double2* A;     // (B_total, K) div
   const double2* Bc;    // (B_total, K) curl
+  const double2* dg;    // grid mode: (d, gamma) of the block-rescaled recurrence, G is scaled by gamma_l
+  const long long* dgofs;
   double* G;
   const long long* gofs;    // fragment mode: tile offset (units of 512*NT doubles) per order
   const long long* rowofs;  // row mode: row offset per order (rows of 12*nfields doubles)
@@ -302,7 +353,8 @@ __global__ void cg_adj_kernel(CgAdjArgs a) {
       x4 = xi_coef(4, l, m); x5 = xi_coef(5, l, m); x6 = xi_coef(6, l, m);
       u1 = mu_coef(1, l, m); u2 = mu_coef(2, l, m); u3 = mu_coef(3, l, m);
     }
-    const double sig = (m < 0 && (am & 1)) ? -1.0 : 1.0;  // favest/legendre.py:101-103
+    double sig = (m < 0 && (am & 1)) ? -1.0 : 1.0;  // favest/legendre.py:101-103
+    if (!a.rows_mode && live) sig *= a.dg[a.dgofs[am] + (l - am)].y;  // gamma_l (legendre.cuh)
     for (int b = 0; b < a.nfields; ++b) {
       double2 gx = make_double2(0, 0), gy = make_double2(0, 0), gz = make_double2(0, 0);
       if (on) {

@@ -33,22 +33,43 @@ namespace fv {
 constexpr int kConsumerWarps = 8;
 constexpr int kProducerWarps = 4;  // one per SMSP: the recurrence chain is latency bound
 constexpr int kThreads = 32 * (kConsumerWarps + kProducerWarps);
+#ifndef FV_PRODUCERS_FIRST
+#define FV_PRODUCERS_FIRST 0
+#endif
+// warp roles: producers take warps 0..3 (one per SMSP) when FV_PRODUCERS_FIRST,
+// otherwise the last four warps; the issue arbiter's warp ordering decides how
+// the producer's FP64 ops interleave with the consumers' DMMAs.
+__device__ __forceinline__ bool is_producer(int warp) {
+  return FV_PRODUCERS_FIRST ? warp < kProducerWarps : warp >= kConsumerWarps;
+}
+__device__ __forceinline__ int producer_index(int warp) {
+  return FV_PRODUCERS_FIRST ? warp : warp - kConsumerWarps;
+}
+__device__ __forceinline__ int consumer_index(int warp) {
+  return FV_PRODUCERS_FIRST ? warp - kProducerWarps : warp;
+}
 
-// Recurrence step in FMA form: with (a_l, c_l = a_l * b_l) precomputed,
-//   P_l = a_l t P_{l-1} - c_l P_{l-2} = fma(a_l t, P_{l-1}, -(c_l P_{l-2})).
-// Only the FMA is on the loop-carried chain (a_l t and c_l P_{l-2} are known one
-// step early).  Rounding differs from the reference's a*(t*P1 - b*P2) by an ulp
-// per step (checked against the oracle at 1e-11 relative; typically 1e-15..1e-13).
-// MIXED tiles inject the polar-start values: P = A at l == l_s, B at l_s + 1; before
-// l_s the state is (0, 0) and the recurrence yields exact zeros.
+// Block-rescaled recurrence (two FP64 ops per step, one on the loop-carried
+// chain): inside 32-degree blocks P_l = gamma_l R_l with
+//   R_l = fma(t, R_{l-1}, -(d_l R_{l-2}))
+// (d_l, gamma_l from aux_kernels.cuh dg_kernel); the state is converted back to
+// P at each block end.  gamma is folded into the consumers instead of the
+// producer: the forward scales its output rows by gamma_l, the adjoint's
+// coefficient tiles are pre-scaled by gamma_l (cg_adj_kernel).  The producer
+// shares the SM sub-partition's FP64 datapath with the DMMA warps, so its op
+// count per step bounds how far ahead of them it can run.  Rounding differs from
+// the reference's a*(t*P1 - b*P2) at the ulp level per step (checked against the
+// oracle at 1e-11 relative; typically 1e-15..1e-13).
+// MIXED tiles inject the polar-start values (pre-divided by gamma): R = A at
+// l == l_s, B at l_s + 1; before l_s the state is (0, 0) and stays exactly zero.
 struct Inject {
   int ls;
   double A, B;
 };
 
 template <bool MIXED>
-__device__ __forceinline__ double rec_step(double& p1, double& p2, double at, double c, int l, const Inject& in) {
-  double pn = fma(at, p1, -(c * p2));
+__device__ __forceinline__ double rec_step(double& p1, double& p2, double tt, double d, int l, const Inject& in) {
+  double pn = fma(tt, p1, -(d * p2));
   if (MIXED) {
     pn = (l == in.ls) ? in.A : pn;
     pn = (l == in.ls + 1) ? in.B : pn;
@@ -66,23 +87,31 @@ constexpr int FWD_RC = 32;       // ring pairs per chunk (8 k-steps)
 constexpr int FWD_STAGES = 5;
 constexpr int FWD_PTILE = 2 * 4 * 8 * 32;  // doubles: [par][Mtile 4][ks 8][lane]
 
+struct __align__(16) StageMeta {
+  int kmin[8];  // per k-step: smallest polar start among its four pairs (16-byte aligned for LDS.128)
+  int zero;     // 1: every Pbar in the tile is below the polar threshold
+  int pad[7];
+};
+
 struct FwdArgs {
   const double* X;          // [m][chunk][par][ks 8][NT][32]
   double* F;                // rows tri(l, m) (l-major), 8*NT doubles each
   const int* start_l;       // [m][nPpad] polar start degree (Lt+1: never)
   const double2* start_v;   // [m][nPpad] (P_ls, P_ls+1)
-  const double2* ab;        // (a_l, a_l*b_l), m-major: abofs[m] + (l - m - 2)
-  const long long* abofs;
+  const double2* dg;        // (d_l, gamma_l), m-major: dgofs[m] + (l - m)
+  const long long* dgofs;
   const double* pair_t;     // [nPpad] cos(theta) of the north ring of each pair
   int Lt, nP, nPpad, nchunks, m_begin;
   int dbg;  // 0 normal; 1: consumers skip MMAs; 2: producers skip the recurrence; 3: both
+  long long* trace;  // optional pipeline timeline of CTA trace_cta (clock64 stamps), normally null
+  int trace_cta;
+  // table mode (plan-time Legendre tiles, ptab_fwd_kernel): null -> on-the-fly producer
+  const double* ptab;         // [tile][FWD_PTILE], tile = tofs[m] + j * nchunks + c
+  const StageMeta* mtab;
+  const long long* tofs;
 };
 
-struct StageMeta {
-  int zero;     // 1: every Pbar in the tile is below the polar threshold
-  int kmin[8];  // per k-step: smallest polar start among its four pairs
-  int pad[7];
-};
+
 
 template <int NT>
 struct FwdSmem {
@@ -95,10 +124,10 @@ struct FwdSmem {
 };
 
 // rows idx = 0..63 of one (l-block, chunk) tile; lane = ring pair 4s+q of the chunk.
-// Coefficients are pulled from shared memory 8 steps at a time and a_l*t is
-// formed off the loop-carried chain.
+// (d, gamma) for the 64 rows are staged in shared memory and pulled 8 at a time;
+// rows 31 and 63 end a 32-degree block: the state goes back to P units there.
 template <bool MIXED>
-__device__ __forceinline__ void fwd_produce(double* Ps, const double2* abw, double tt, double& p1, double& p2,
+__device__ __forceinline__ void fwd_produce(double* Ps, const double2* dgw, double tt, double& p1, double& p2,
                                             int lane, int l0, const Inject& in) {
   const int s = lane >> 2, q = lane & 3, sx = s & 3;
   double* bp[8];
@@ -106,20 +135,146 @@ __device__ __forceinline__ void fwd_produce(double* Ps, const double2* abw, doub
   for (int g = 0; g < 8; ++g) bp[g] = Ps + s * 32 + q + ((g ^ sx) << 2);
 #pragma unroll
   for (int b0 = 0; b0 < FWD_LB; b0 += 8) {
-    double at[8], cc[8];
+    double dd[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const double2 ac = abw[b0 + k];
-      at[k] = ac.x * tt;
-      cc[k] = ac.y;
-    }
+    for (int k = 0; k < 8; ++k) dd[k] = dgw[b0 + k].x;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int idx = b0 + k;
-      const double v = rec_step<MIXED>(p1, p2, at[k], cc[k], l0 + idx, in);
+      const double v = rec_step<MIXED>(p1, p2, tt, dd[k], l0 + idx, in);
       const int par = idx & 1, rp = idx >> 1, i = rp >> 3, g = rp & 7;
       bp[g][(par * 4 + i) * 8 * 32] = v;
+      if ((idx & 31) == 31) {
+        p1 *= dgw[idx].y;
+        p2 *= dgw[idx - 1].y;
+      }
     }
+  }
+}
+
+// Per-CTA producer state of the forward (one order m): pair cos(theta), polar
+// start, recurrence state carried across l-blocks.
+struct FwdState {
+  double* p1;
+  double* p2;
+  const double* t;
+  const int* ls;
+};
+
+struct TileClass {
+  bool zero, mixed;
+  int km;  // smallest polar start of the lane's k-step
+};
+
+__device__ __forceinline__ TileClass fwd_classify(const FwdState& st, int p, int l0, int lane) {
+  TileClass tc;
+  const int ls = st.ls[p];
+  const bool before = ls > l0 + FWD_LB - 1;          // tile entirely below start
+  const bool inject = !before && ls + 1 >= l0;        // start value(s) land in this tile
+  tc.zero = __all_sync(0xffffffffu, before);
+  tc.mixed = __any_sync(0xffffffffu, inject);
+  int km = min(ls, __shfl_xor_sync(0xffffffffu, ls, 1));
+  tc.km = min(km, __shfl_xor_sync(0xffffffffu, km, 2));
+  return tc;
+}
+
+// rows of one (l-block j, chunk c) tile into Ps (shared or global), state update
+__device__ __forceinline__ void fwd_compute(const FwdArgs& args, const FwdState& st, const TileClass& tc, double* Ps,
+                                            const double2* abw, int m, int j, int nlb, int p, int l0, int lane) {
+  Inject in;
+  in.ls = st.ls[p];
+  in.A = in.B = 0.0;
+  if (tc.mixed) {
+    const double2 v = args.start_v[(size_t)m * args.nPpad + p];
+    in.A = v.x;
+    in.B = v.y;
+  }
+  double p1 = st.p1[p], p2 = st.p2[p];
+  const double tt = st.t[p];
+  if (tc.mixed) fwd_produce<true>(Ps, abw, tt, p1, p2, lane, l0, in);
+  else fwd_produce<false>(Ps, abw, tt, p1, p2, lane, l0, in);
+  if (j + 1 < nlb) {
+    st.p1[p] = p1;
+    st.p2[p] = p2;
+  }
+}
+
+__device__ __forceinline__ void fwd_stage_coefs(double2* abw, const FwdArgs& args, int m, int l0, int lane) {
+  const double2* dgm = args.dg + args.dgofs[m];
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {  // (d, gamma) for rows l0..l0+63; rows past Lt are never stored
+    const int l = l0 + 32 * h + lane;
+    abw[32 * h + lane] = (l <= args.Lt) ? dgm[l - m] : make_double2(0.0, 1.0);
+  }
+  __syncwarp();
+}
+
+// Plan-time table of forward Legendre tiles (table mode): exactly the tiles the
+// on-the-fly producer would build, in the same shared-memory fragment layout,
+// plus their StageMeta.  One CTA (4 producer warps) per order m.
+__global__ void __launch_bounds__(32 * kProducerWarps) ptab_fwd_kernel(FwdArgs args, double* ptab, StageMeta* mtab) {
+  extern __shared__ __align__(128) double smem[];
+  const int nPx = args.nchunks * FWD_RC;
+  double2* abw_all = reinterpret_cast<double2*>(smem);
+  FwdState st;
+  double* sp1 = reinterpret_cast<double*>(abw_all + kProducerWarps * FWD_LB);
+  st.p1 = sp1;
+  st.p2 = sp1 + nPx;
+  double* st_t = sp1 + 2 * nPx;
+  int* st_ls = reinterpret_cast<int*>(st_t + nPx);
+  st.t = st_t;
+  st.ls = st_ls;
+  const int m = args.m_begin + blockIdx.x;
+  const int nlb = (args.Lt + 1 - m + FWD_LB - 1) / FWD_LB;
+  for (int p = threadIdx.x; p < nPx; p += blockDim.x) {
+    st_t[p] = args.pair_t[p];
+    st_ls[p] = args.start_l[(size_t)m * args.nPpad + p];
+    st.p1[p] = 0.0;
+    st.p2[p] = 0.0;
+  }
+  __syncthreads();
+  const int pw = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* abw = abw_all + pw * FWD_LB;
+  const long long base = args.tofs[m];
+  for (int j = 0; j < nlb; ++j) {
+    const int l0 = m + FWD_LB * j;
+    fwd_stage_coefs(abw, args, m, l0, lane);
+    for (int c = pw; c < args.nchunks; c += kProducerWarps) {
+      const long long tile = base + (long long)j * args.nchunks + c;
+      const int p = c * FWD_RC + lane;
+      const TileClass tc = fwd_classify(st, p, l0, lane);
+      if (lane == 0) mtab[tile].zero = tc.zero;
+      if ((lane & 3) == 0) mtab[tile].kmin[lane >> 2] = tc.km;
+      if (!tc.zero) fwd_compute(args, st, tc, ptab + tile * FWD_PTILE, abw, m, j, nlb, p, l0, lane);
+    }
+  }
+}
+
+template <int KS0, int NTW, int NT>
+__device__ __forceinline__ void fwd_mtile_run(int nt0, double (&acc)[NTW][2], const double (&a)[8],
+                                              const double (&bb)[8][NTW]) {
+#pragma unroll
+  for (int ks = KS0; ks < 8; ++ks)
+#pragma unroll
+    for (int jn = 0; jn < NTW; ++jn)
+      if (nt0 + jn < NT) dmma_m8n8k4(acc[jn][0], acc[jn][1], a[ks], bb[ks][jn]);
+}
+
+// DMMAs of one M-tile from its first active k-step on (switch = real branch)
+template <int NTW, int NT>
+__device__ __forceinline__ void fwd_mtile_dmma(int kfirst, int nt0, double (&acc)[NTW][2], const double (&a)[8],
+                                               const double (&bb)[8][NTW]) {
+  switch (kfirst) {
+    case 0: fwd_mtile_run<0, NTW, NT>(nt0, acc, a, bb); break;
+    case 1: fwd_mtile_run<1, NTW, NT>(nt0, acc, a, bb); break;
+    case 2: fwd_mtile_run<2, NTW, NT>(nt0, acc, a, bb); break;
+    case 3: fwd_mtile_run<3, NTW, NT>(nt0, acc, a, bb); break;
+    case 4: fwd_mtile_run<4, NTW, NT>(nt0, acc, a, bb); break;
+    case 5: fwd_mtile_run<5, NTW, NT>(nt0, acc, a, bb); break;
+    case 6: fwd_mtile_run<6, NTW, NT>(nt0, acc, a, bb); break;
+    case 7: fwd_mtile_run<7, NTW, NT>(nt0, acc, a, bb); break;
+    default: break;
   }
 }
 
@@ -158,68 +313,51 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
     st_p1[p] = 0.0;
     st_p2[p] = 0.0;
   }
+  unsigned long long gt0 = 0;
+  if (args.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
   __syncthreads();
 
-  if (warp >= kConsumerWarps) {
+  if (is_producer(warp)) {
     // ------------------------------ producer ------------------------------
-    const int pw = warp - kConsumerWarps;
+    const int pw = producer_index(warp);
     double2* abw = abw_all + pw * FWD_LB;
-    const double2* abm = args.ab + args.abofs[m];
+    FwdState st{st_p1, st_p2, st_t, st_ls};
+    const bool table = args.ptab != nullptr;
     for (int j = 0; j < nlb; ++j) {
       const int l0 = m + FWD_LB * j;
-      __syncwarp();
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {  // (a, a*b) for rows l0..l0+63; zero past Lt (rows become 0)
-        const int l = l0 + 32 * h + lane;
-        abw[32 * h + lane] = (l >= m + 2 && l <= Lt) ? abm[l - m - 2] : make_double2(0.0, 0.0);
-      }
-      __syncwarp();
+      if (!table) fwd_stage_coefs(abw, args, m, l0, lane);
       for (int c = pw; c < nchunks; c += kProducerWarps) {
         const int t = j * nchunks + c;
         const int stage = t % FWD_STAGES;
         const uint32_t round = t / FWD_STAGES;
         const int p = c * FWD_RC + lane;
-        const double tt = st_t[p];
-        Inject in;
-        in.ls = st_ls[p];
-        const bool before = in.ls > l0 + FWD_LB - 1;             // tile entirely below start
-        const bool inject = !before && in.ls + 1 >= l0;           // start value(s) land in this tile
-        const bool zero = __all_sync(0xffffffffu, before);
-        const bool mixed = __any_sync(0xffffffffu, inject);
-        in.A = in.B = 0.0;
-        if (mixed) {
-          const double2 v = args.start_v[(size_t)m * args.nPpad + p];
-          in.A = v.x;
-          in.B = v.y;
-        }
-        double p1 = st_p1[p], p2 = st_p2[p];
-        // smallest polar start of the k-step (4 consecutive lanes)
-        int km = min(in.ls, __shfl_xor_sync(0xffffffffu, in.ls, 1));
-        km = min(km, __shfl_xor_sync(0xffffffffu, km, 2));
+        const TileClass tc = fwd_classify(st, p, l0, lane);
+        const bool tr = args.trace && blockIdx.x == args.trace_cta && lane == 0 && t < 4096;
+        if (tr) args.trace[t * 8 + 0] = clock64();
         mbar_wait(&empty[stage], (round & 1) ^ 1);
+        if (tr) args.trace[t * 8 + 1] = clock64();
         double* Ps = smem + stage * SM::STAGE;
         double* Xs = Ps + FWD_PTILE;
-        if (lane == 0) meta[stage].zero = zero;
-        if ((lane & 3) == 0) meta[stage].kmin[lane >> 2] = km;
-        if (!zero) {
+        if (tc.zero || !table) {
+          if (lane == 0) meta[stage].zero = tc.zero;
+          if ((lane & 3) == 0) meta[stage].kmin[lane >> 2] = tc.km;
+        }
+        if (!tc.zero) {
           if (lane == 0) {
-            asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])),
-                         "r"((uint32_t)(SM::XTILE * 8))
+            const uint32_t bytes = SM::XTILE * 8 + (table ? FWD_PTILE * 8 + (uint32_t)sizeof(StageMeta) : 0u);
+            asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])), "r"(bytes)
                          : "memory");
             bulk_g2s(Xs, args.X + ((size_t)(m - args.m_begin) * nchunks + c) * SM::XTILE, SM::XTILE * 8,
                      &full[stage]);
+            if (table) {
+              const long long tile = args.tofs[m] + t;
+              bulk_g2s(Ps, args.ptab + tile * FWD_PTILE, FWD_PTILE * 8, &full[stage]);
+              bulk_g2s(&meta[stage], args.mtab + tile, sizeof(StageMeta), &full[stage]);
+            }
           }
-          if (args.dbg & 2) {
-          } else if (mixed) {
-            fwd_produce<true>(Ps, abw, tt, p1, p2, lane, l0, in);
-          } else {
-            fwd_produce<false>(Ps, abw, tt, p1, p2, lane, l0, in);
-          }
-          if (j + 1 < nlb) {
-            st_p1[p] = p1;
-            st_p2[p] = p2;
-          }
+          if (!table && !(args.dbg & 2)) fwd_compute(args, st, tc, Ps, abw, m, j, nlb, p, l0, lane);
         }
+        if (tr) args.trace[t * 8 + 2] = clock64() | ((long long)tc.zero << 62) | ((long long)tc.mixed << 61);
         mbar_arrive(&full[stage]);
       }
     }
@@ -228,9 +366,10 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
 
   // -------------------------------- consumers --------------------------------
   constexpr int NTW = (NT + 1) / 2;
-  const int par = warp >> 2;
-  const int mh = (warp >> 1) & 1;
-  const int nh = warp & 1;
+  const int cw = consumer_index(warp);
+  const int par = cw >> 2;
+  const int mh = (cw >> 1) & 1;
+  const int nh = cw & 1;
   const int nt0 = nh * NTW;
   const int g = lane >> 2, q = lane & 3;
   const int ncolF = 8 * NT;
@@ -242,32 +381,47 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
 
   for (int j = 0; j < nlb; ++j) {
     const int l0 = m + FWD_LB * j;
-    const int lhi = l0 + 32 * mh + 31;  // last row of this warp's two M-tiles
     for (int c = 0; c < nchunks; ++c) {
       const int t = j * nchunks + c;
       const int stage = t % FWD_STAGES;
       const uint32_t round = t / FWD_STAGES;
+      const bool tr = args.trace && blockIdx.x == args.trace_cta && lane == 0 && cw == 0 && t < 4096;
+      if (tr) args.trace[t * 8 + 3] = clock64();
       mbar_wait(&full[stage], round & 1);
+      if (tr) args.trace[t * 8 + 4] = clock64();
       const double* Ps = smem + stage * SM::STAGE;
       const double* Xs = Ps + FWD_PTILE;
+      const int4 km0 = *reinterpret_cast<const int4*>(&meta[stage].kmin[0]);
+      const int4 km1 = *reinterpret_cast<const int4*>(&meta[stage].kmin[4]);
+      const int kmin[8] = {km0.x, km0.y, km0.z, km0.w, km1.x, km1.y, km1.z, km1.w};
       if (!meta[stage].zero && !(args.dbg & 1)) {
+        // all fragments of the tile first (unconditional loads, hoisted), then the
+        // DMMAs.  M-tile i = 2*mh + ii holds rows l0 + 16 i .. l0 + 16 i + 15 (one
+        // parity); its k-steps below the polar start form a prefix (pairs further
+        // from the pole start earlier) and M-tiles past Lt are padding, so each
+        // M-tile runs its DMMAs from its first active k-step on, selected with a
+        // real branch (a predicated-off DMMA still occupies the FP64 tensor pipe).
+        double a0[8], a1[8], bb[8][NTW];
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
-          if (meta[stage].kmin[ks] <= lhi) {
-            const int sw = ((g ^ (ks & 3)) << 2) + q;
-            const double a0 = Ps[((par * 4 + 2 * mh + 0) * 8 + ks) * 32 + sw];
-            const double a1 = Ps[((par * 4 + 2 * mh + 1) * 8 + ks) * 32 + sw];
+          const int sw = ((g ^ (ks & 3)) << 2) + q;
+          a0[ks] = lds_f64(&Ps[((par * 4 + 2 * mh + 0) * 8 + ks) * 32 + sw]);
+          a1[ks] = lds_f64(&Ps[((par * 4 + 2 * mh + 1) * 8 + ks) * 32 + sw]);
 #pragma unroll
-            for (int jn = 0; jn < NTW; ++jn) {
-              if (nt0 + jn < NT) {
-                const double b = Xs[((par * 8 + ks) * NT + nt0 + jn) * 32 + lane];
-                dmma_m8n8k4(acc[0][jn][0], acc[0][jn][1], a0, b);
-                dmma_m8n8k4(acc[1][jn][0], acc[1][jn][1], a1, b);
-              }
-            }
-          }
+          for (int jn = 0; jn < NTW; ++jn)
+            bb[ks][jn] = (nt0 + jn < NT) ? lds_f64(&Xs[((par * 8 + ks) * NT + nt0 + jn) * 32 + lane]) : 0.0;
         }
+        const int r0 = l0 + 32 * mh, r1 = r0 + 16;
+        int kf0 = 8, kf1 = 8;
+#pragma unroll
+        for (int ks = 7; ks >= 0; --ks) {
+          if (r0 <= Lt && kmin[ks] <= r0 + 15) kf0 = ks;
+          if (r1 <= Lt && kmin[ks] <= r1 + 15) kf1 = ks;
+        }
+        fwd_mtile_dmma<NTW, NT>(kf0, nt0, acc[0], a0, bb);
+        fwd_mtile_dmma<NTW, NT>(kf1, nt0, acc[1], a1, bb);
       }
+      if (tr) args.trace[t * 8 + 5] = clock64();
       mbar_arrive(&empty[stage]);
     }
     // epilogue for this l-block: rows l = l0 + 2*(8*i + g) + par
@@ -277,17 +431,28 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       const int l = l0 + 2 * (8 * i + g) + par;
       if (l <= Lt) {
         double* row = args.F + ((size_t)l * (l + 1) / 2 + m) * ncolF;
+        const double gam = args.dg[args.dgofs[m] + (l - m)].y;  // P_l = gamma_l R_l
 #pragma unroll
         for (int jn = 0; jn < NTW; ++jn) {
           if (nt0 + jn < NT) {
             *reinterpret_cast<double2*>(row + (nt0 + jn) * 8 + 2 * q) =
-                make_double2(acc[ii][jn][0], acc[ii][jn][1]);
+                make_double2(gam * acc[ii][jn][0], gam * acc[ii][jn][1]);
           }
         }
       }
 #pragma unroll
       for (int jn = 0; jn < NTW; ++jn) acc[ii][jn][0] = acc[ii][jn][1] = 0.0;
     }
+  }
+  if (args.trace && cw == 0 && lane == 0 && blockIdx.x < 4096) {
+    unsigned long long gt1;
+    unsigned smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt1));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    long long* ct = args.trace + 4096 * 8 + blockIdx.x * 4;
+    ct[0] = (long long)gt0;
+    ct[1] = (long long)gt1;
+    ct[2] = smid;
   }
 }
 
@@ -307,13 +472,16 @@ struct AdjArgs {
   double2* S;               // spectrum [comp][field][ring][n_phi] (all fields)
   const int* start_l;
   const double2* start_v;
-  const double2* ab;
-  const long long* abofs;
+  const double2* dg;
+  const long long* dgofs;
   const double* pair_t;
   const int* pair_n;        // north ring of each pair (-1: padding)
   const int* pair_s;        // south ring (-1: unpaired)
   int Lt, nP, nPpad, nrc, n_phi, n_theta, B_total, b0, nfields, m_begin;
   int dbg;
+  // table mode: P^T stage tiles [aofs[m] + rc * nlc(m) + lc][ADJ_PTILE] (ptab_adj_kernel)
+  const double* ptab;
+  const long long* aofs;
 };
 
 template <int NT>
@@ -329,9 +497,10 @@ __device__ __forceinline__ int adj_swz(int g, int q, int i) {
   return (g << 2) + (q ^ ((g >> 2) | ((i & 1) << 1)));
 }
 
-// l values idx = 0..ADJ_LC-1 of one stage for the lane's pair (M-tile i, row g)
+// l values idx = 0..ADJ_LC-1 of one stage (= one 32-degree block) for the lane's
+// pair (M-tile i, row g); the state goes back to P units after the last row.
 template <bool MIXED>
-__device__ __forceinline__ void adj_produce(double* Ps, const double2* abw, double tt, double& p1, double& p2,
+__device__ __forceinline__ void adj_produce(double* Ps, const double2* dgw, double tt, double& p1, double& p2,
                                             int i, int g, int l0, const Inject& in) {
   const int cx = (g >> 2) | ((i & 1) << 1);
   double* bp[4];
@@ -339,20 +508,76 @@ __device__ __forceinline__ void adj_produce(double* Ps, const double2* abw, doub
   for (int q = 0; q < 4; ++q) bp[q] = Ps + i * 32 + (g << 2) + (q ^ cx);
 #pragma unroll
   for (int b0 = 0; b0 < ADJ_LC; b0 += 8) {
-    double at[8], cc[8];
+    double dd[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const double2 ac = abw[b0 + k];
-      at[k] = ac.x * tt;
-      cc[k] = ac.y;
-    }
+    for (int k = 0; k < 8; ++k) dd[k] = dgw[b0 + k].x;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int idx = b0 + k;
-      const double v = rec_step<MIXED>(p1, p2, at[k], cc[k], l0 + idx, in);
+      const double v = rec_step<MIXED>(p1, p2, tt, dd[k], l0 + idx, in);
       const int par = idx & 1, kk = idx >> 1, ks = kk >> 2, q = kk & 3;
       bp[q][(par * ADJ_KS + ks) * ADJ_MT * 32] = v;
     }
+  }
+  p1 *= dgw[ADJ_LC - 1].y;
+  p2 *= dgw[ADJ_LC - 2].y;
+}
+
+// Plan-time table of adjoint P^T stage tiles (table mode); all-zero warps leave
+// their M-tiles unwritten, exactly as the on-the-fly producer does.
+__global__ void __launch_bounds__(32 * kProducerWarps) ptab_adj_kernel(AdjArgs args, double* ptab) {
+  __shared__ double2 abw_all[kProducerWarps * ADJ_LC];
+  const int m = args.m_begin + blockIdx.x / args.nrc;
+  const int rc = blockIdx.x % args.nrc;
+  const int Lt = args.Lt;
+  const int nlc = (Lt + 1 - m + ADJ_LC - 1) / ADJ_LC;
+  const int pw = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* abw = abw_all + pw * ADJ_LC;
+  const int rho = 32 * pw + lane;
+  const int p = rc * ADJ_RC + rho;
+  const int i = rho >> 3, g = rho & 7;
+  const double tt = args.pair_t[p];
+  Inject in;
+  in.ls = args.start_l[(size_t)m * args.nPpad + p];
+  const double2 v = args.start_v[(size_t)m * args.nPpad + p];
+  in.A = v.x;
+  in.B = v.y;
+  double p1 = 0.0, p2 = 0.0;
+  const double2* dgm = args.dg + args.dgofs[m];
+  double* base = ptab + (size_t)(args.aofs[m] + (long long)rc * nlc) * ADJ_PTILE;
+  for (int lc = 0; lc < nlc; ++lc) {
+    const int l0 = m + ADJ_LC * lc;
+    const bool before = in.ls > l0 + ADJ_LC - 1;
+    const bool zero = __all_sync(0xffffffffu, before);
+    const bool mixed = __any_sync(0xffffffffu, !before && in.ls + 1 >= l0);
+    if (zero) continue;
+    __syncwarp();
+    const int l = l0 + lane;
+    abw[lane] = (l <= Lt) ? dgm[l - m] : make_double2(0.0, 1.0);
+    __syncwarp();
+    double* Ps = base + (size_t)lc * ADJ_PTILE;
+    if (mixed) adj_produce<true>(Ps, abw, tt, p1, p2, i, g, l0, in);
+    else adj_produce<false>(Ps, abw, tt, p1, p2, i, g, l0, in);
+  }
+}
+
+template <int I0, int NT>
+__device__ __forceinline__ void adj_ks_run(double (&acc)[4][NT][2], const double (&a)[4], const double (&b)[NT]) {
+#pragma unroll
+  for (int jn = 0; jn < NT; ++jn)
+#pragma unroll
+    for (int ii = I0; ii < 4; ++ii) dmma_m8n8k4(acc[ii][jn][0], acc[ii][jn][1], a[ii], b[jn]);
+}
+
+template <int NT>
+__device__ __forceinline__ void adj_ks_dmma(int ifirst, double (&acc)[4][NT][2], const double (&a)[4],
+                                            const double (&b)[NT]) {
+  switch (ifirst) {
+    case 0: adj_ks_run<0, NT>(acc, a, b); break;
+    case 1: adj_ks_run<1, NT>(acc, a, b); break;
+    case 2: adj_ks_run<2, NT>(acc, a, b); break;
+    case 3: adj_ks_run<3, NT>(acc, a, b); break;
+    default: break;
   }
 }
 
@@ -381,9 +606,9 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
   }
   __syncthreads();
 
-  if (warp >= kConsumerWarps) {
+  if (is_producer(warp)) {
     // ------------------------------ producer ------------------------------
-    const int pw = warp - kConsumerWarps;
+    const int pw = producer_index(warp);
     double2* abw = abw_all + pw * ADJ_LC;
     const int rho = 32 * pw + lane;            // pair within the CTA's chunk
     const int p = rc * ADJ_RC + rho;
@@ -397,8 +622,9 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
       in.B = v.y;
     }
     double p1 = 0.0, p2 = 0.0;
-    const double2* abm = args.ab + args.abofs[m];
+    const double2* dgm = args.dg + args.dgofs[m];
     const double* Gm = args.G + (size_t)args.gofs[m] * SM::GTILE;
+    const bool table = args.ptab != nullptr;
     for (int lc = 0; lc < nlc; ++lc) {
       const int stage = lc % ADJ_STAGES;
       const uint32_t round = lc / ADJ_STAGES;
@@ -406,23 +632,26 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
       const bool before = in.ls > l0 + ADJ_LC - 1;
       const bool zero = __all_sync(0xffffffffu, before);
       const bool mixed = __any_sync(0xffffffffu, !before && in.ls + 1 >= l0);
-      if (!zero) {
+      if (!zero && !table) {
         __syncwarp();
         const int l = l0 + lane;
-        abw[lane] = (l >= m + 2 && l <= Lt) ? abm[l - m - 2] : make_double2(0.0, 0.0);
+        abw[lane] = (l <= Lt) ? dgm[l - m] : make_double2(0.0, 1.0);
         __syncwarp();
       }
       mbar_wait(&empty[stage], (round & 1) ^ 1);
       double* Ps = smem + stage * SM::STAGE;
       double* Gs = Ps + ADJ_PTILE;
       if (pw == 0 && lane == 0) {
-        asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])),
-                     "r"((uint32_t)(SM::GTILE * 8))
+        const uint32_t bytes = SM::GTILE * 8 + (table ? ADJ_PTILE * 8 : 0u);
+        asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])), "r"(bytes)
                      : "memory");
         bulk_g2s(Gs, Gm + (size_t)lc * SM::GTILE, SM::GTILE * 8, &full[stage]);
+        if (table)
+          bulk_g2s(Ps, args.ptab + (size_t)(args.aofs[m] + (long long)rc * nlc + lc) * ADJ_PTILE, ADJ_PTILE * 8,
+                   &full[stage]);
       }
       // all-zero warps write nothing: the consumers skip their M-tiles (polar start)
-      if (zero || (args.dbg & 2)) {
+      if (zero || table || (args.dbg & 2)) {
       } else if (mixed) {
         adj_produce<true>(Ps, abw, tt, p1, p2, i, g, l0, in);
       } else {
@@ -435,8 +664,9 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
 
   // -------------------------------- consumers --------------------------------
   // warp (par, mq): M-tiles 4mq..4mq+3 (32 pairs) x all NT n-tiles of parity par
-  const int par = warp >> 2;
-  const int mq = warp & 3;
+  const int cw = consumer_index(warp);
+  const int par = cw >> 2;
+  const int mq = cw & 3;
   const int g = lane >> 2, q = lane & 3;
   // first degree at which each of the warp's M-tiles has a pair above the polar threshold
   int mt_start[4];
@@ -464,21 +694,36 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
 #pragma unroll
     for (int ii = 0; ii < 4; ++ii) act[ii] = mt_start[ii] <= lhi;
     if (!(args.dbg & 1) && (act[0] || act[1] || act[2] || act[3])) {
-#pragma unroll
-      for (int ks = 0; ks < ADJ_KS; ++ks) {
-        double a[4];
+      // k-step fragments double-buffered in registers: the loads of step ks+1
+      // are in flight while the 24 DMMAs of step ks issue
+      double a[2][4], b[2][NT];
+      auto load = [&](int ks, int bufi) {
 #pragma unroll
         for (int ii = 0; ii < 4; ++ii) {
           const int i = 4 * mq + ii;
-          a[ii] = act[ii] ? Ps[((par * ADJ_KS + ks) * ADJ_MT + i) * 32 + adj_swz(g, q, i)] : 0.0;
+          a[bufi][ii] = lds_f64(&Ps[((par * ADJ_KS + ks) * ADJ_MT + i) * 32 + adj_swz(g, q, i)]);
         }
 #pragma unroll
-        for (int jn = 0; jn < NT; ++jn) {
-          const double b = Gs[((par * ADJ_KS + ks) * NT + jn) * 32 + lane];
+        for (int jn = 0; jn < NT; ++jn) b[bufi][jn] = lds_f64(&Gs[((par * ADJ_KS + ks) * NT + jn) * 32 + lane]);
+      };
+      load(0, 0);
+      const int l0s = m + ADJ_LC * lc;
 #pragma unroll
-          for (int ii = 0; ii < 4; ++ii)
-            if (act[ii]) dmma_m8n8k4(acc[ii][jn][0], acc[ii][jn][1], a[ii], b);
+      for (int ks = 0; ks < ADJ_KS; ++ks) {
+        if (ks + 1 < ADJ_KS) load(ks + 1, (ks + 1) & 1);
+        // k-step ks holds degrees l0s + 8 ks .. + 7 (one parity): skip M-tiles whose
+        // pairs start later, and the k-steps past Lt (zero coefficient rows)
+        const int khi = l0s + 8 * ks + 7;
+        // active M-tiles form a suffix (pairs nearer the equator start earlier):
+        // dispatch on the first one with a real branch (predicated-off DMMAs
+        // would still occupy the pipe)
+        int ifirst = 4;
+        if (l0s + 8 * ks <= Lt) {
+#pragma unroll
+          for (int ii = 3; ii >= 0; --ii)
+            if (mt_start[ii] <= khi) ifirst = ii;
         }
+        adj_ks_dmma<NT>(ifirst, acc, a[ks & 1], b[ks & 1]);
       }
     }
     mbar_arrive(&empty[stage]);

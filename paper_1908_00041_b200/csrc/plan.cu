@@ -58,6 +58,21 @@ int dbg_mode() {
   return v;
 }
 
+// FV_TRACE_CTA=<m> records the forward pipeline timeline of that CTA (tools/trace_fwd.py)
+long long* g_trace = nullptr;
+int trace_cta() {
+  static int v = [] { const char* e = std::getenv("FV_TRACE_CTA"); return e ? std::atoi(e) : -1; }();
+  return v;
+}
+long long* trace_buf() {
+  if (trace_cta() < 0) return nullptr;
+  if (!g_trace) {
+    cudaMalloc(&g_trace, 4096 * 12 * sizeof(long long));
+    cudaMemset(g_trace, 0, 4096 * 12 * sizeof(long long));
+  }
+  return g_trace;
+}
+
 inline int ntiles_for(int nfields) { return (12 * nfields + 7) / 8; }
 
 }  // namespace
@@ -78,6 +93,15 @@ struct fvPlan {
   double2* start_v = nullptr;
   double2* ab = nullptr;
   long long* abofs = nullptr;
+  double2* dg = nullptr;        // block-rescaled recurrence (d, gamma) (grid plans)
+  long long* dgofs = nullptr;
+  // table mode: plan-time Legendre tiles streamed by TMA instead of the on-the-fly producer
+  double* ptab_f = nullptr;
+  fv::StageMeta* mtab_f = nullptr;
+  long long* tofs = nullptr;
+  double* ptab_a = nullptr;
+  long long* aofs = nullptr;
+  size_t ptab_bytes = 0;
   long long* gofs = nullptr;    // tile offsets per order (grid G layout)
   long long* rowofs = nullptr;  // row offsets per order (points G layout)
   long long g_tiles = 0;
@@ -114,6 +138,7 @@ void free_plan(fvPlan* p) {
   cudaSetDevice(p->device);
   void* ptrs[] = {p->pair_t, p->pair_sin, p->pair_n, p->pair_s, p->ring_w, p->seed_x,
                   p->seed_e, p->start_l,  p->start_v, p->ab,   p->abofs,  p->gofs,
+                  p->dg,     p->dgofs,  p->ptab_f,  p->mtab_f, p->tofs,   p->ptab_a, p->aofs,
                   p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->G,
                   p->fft_tw};
   for (void* q : ptrs)
@@ -138,6 +163,78 @@ int ab_tables(fvPlan* p) {
     fv::ab_kernel<<<grid, 128>>>(Lt, p->abofs, p->ab);
     FV_CUDA(cudaGetLastError());
   }
+  return FV_OK;
+}
+
+int dg_tables(fvPlan* p) {
+  const int Lt = p->Lt;
+  std::vector<long long> ofs(Lt + 2, 0);
+  for (int m = 0; m <= Lt; ++m) ofs[m + 1] = ofs[m] + (Lt + 1 - m);
+  FV_TRY(dalloc(&p->dgofs, Lt + 1));
+  FV_TRY(dalloc(&p->dg, ofs[Lt + 1]));
+  FV_CUDA(cudaMemcpy(p->dgofs, ofs.data(), (Lt + 1) * sizeof(long long), cudaMemcpyHostToDevice));
+  dim3 grid((Lt + 1 + 31) / 32, Lt + 1);
+  fv::dg_kernel<<<grid, 32>>>(Lt, p->dgofs, p->dg);
+  FV_CUDA(cudaGetLastError());
+  return FV_OK;
+}
+
+// Table mode (legendre.cuh): precompute every forward tile and adjoint stage tile
+// once per plan when they fit the budget FV_PTAB_GB (default 32 GB; FV_PTAB=0
+// disables).  At L=1024 this is ~5 GB; at L=4096 it would be ~250 GB, so large
+// degrees keep the on-the-fly recurrence producer.
+int ptab_tables(fvPlan* p) {
+  const char* en = std::getenv("FV_PTAB");
+  if (en && std::atoi(en) == 0) return FV_OK;
+  const char* gb = std::getenv("FV_PTAB_GB");
+  const double budget = (gb ? std::atof(gb) : 32.0) * 1e9;
+  const int Lt = p->Lt;
+  std::vector<long long> tofs(Lt + 2, 0), aofs(Lt + 2, 0);
+  for (int m = 0; m <= Lt; ++m) {
+    tofs[m + 1] = tofs[m] + (long long)((Lt + 1 - m + fv::FWD_LB - 1) / fv::FWD_LB) * p->nchunks;
+    aofs[m + 1] = aofs[m] + (long long)((Lt + 1 - m + fv::ADJ_LC - 1) / fv::ADJ_LC) * p->nrc;
+  }
+  const size_t bytes = (size_t)tofs[Lt + 1] * (fv::FWD_PTILE * 8 + sizeof(fv::StageMeta)) +
+                       (size_t)aofs[Lt + 1] * fv::ADJ_PTILE * 8;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  if ((double)bytes > budget || bytes > free_b / 2) return FV_OK;
+  FV_TRY(dalloc(&p->tofs, Lt + 1));
+  FV_TRY(dalloc(&p->aofs, Lt + 1));
+  FV_TRY(dalloc(&p->ptab_f, (size_t)tofs[Lt + 1] * fv::FWD_PTILE));
+  FV_TRY(dalloc(&p->mtab_f, (size_t)tofs[Lt + 1]));
+  FV_TRY(dalloc(&p->ptab_a, (size_t)aofs[Lt + 1] * fv::ADJ_PTILE));
+  FV_CUDA(cudaMemcpy(p->tofs, tofs.data(), (Lt + 1) * 8, cudaMemcpyHostToDevice));
+  FV_CUDA(cudaMemcpy(p->aofs, aofs.data(), (Lt + 1) * 8, cudaMemcpyHostToDevice));
+  fv::FwdArgs fa{};
+  fa.start_l = p->start_l;
+  fa.start_v = p->start_v;
+  fa.dg = p->dg;
+  fa.dgofs = p->dgofs;
+  fa.pair_t = p->pair_t;
+  fa.Lt = Lt;
+  fa.nP = p->nP;
+  fa.nPpad = p->nPpad;
+  fa.nchunks = p->nchunks;
+  fa.tofs = p->tofs;
+  const size_t smem_f = fv::kProducerWarps * fv::FWD_LB * 16 + (size_t)p->nchunks * fv::FWD_RC * 28;
+  FV_CUDA(cudaFuncSetAttribute(fv::ptab_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
+  fv::ptab_fwd_kernel<<<Lt + 1, 32 * fv::kProducerWarps, smem_f>>>(fa, p->ptab_f, p->mtab_f);
+  FV_CUDA(cudaGetLastError());
+  fv::AdjArgs aa{};
+  aa.start_l = p->start_l;
+  aa.start_v = p->start_v;
+  aa.dg = p->dg;
+  aa.dgofs = p->dgofs;
+  aa.pair_t = p->pair_t;
+  aa.Lt = Lt;
+  aa.nP = p->nP;
+  aa.nPpad = p->nPpad;
+  aa.nrc = p->nrc;
+  aa.aofs = p->aofs;
+  fv::ptab_adj_kernel<<<(Lt + 1) * p->nrc, 32 * fv::kProducerWarps>>>(aa, p->ptab_a);
+  FV_CUDA(cudaGetLastError());
+  p->ptab_bytes = bytes;
   return FV_OK;
 }
 
@@ -331,6 +428,14 @@ extern "C" {
 
 const char* fv_version(void) { return "favest_b200 0.1.0 sm_100a"; }
 
+// debug: copy the forward pipeline trace (4096 tiles x 8 stamps) to the host
+int fv_debug_trace(long long* host) {
+  if (!g_trace) return FV_EINVAL;
+  cudaDeviceSynchronize();
+  cudaMemcpy(host, g_trace, 4096 * 12 * sizeof(long long), cudaMemcpyDeviceToHost);
+  return FV_OK;
+}
+
 const char* fv_last_error(void) { return g_err.c_str(); }
 
 int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const double* ring_theta_host,
@@ -417,21 +522,22 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
   cudaMemcpy(p->ring_w, w.data(), n_theta * 8, cudaMemcpyHostToDevice);
   fv::seeds_kernel<<<(p->nPpad + 127) / 128, 128>>>(p->pair_sin, p->nPpad, Lt, p->seed_x, p->seed_e);
   if (cudaGetLastError() != cudaSuccess) return bail(fail(FV_ECUDA, "seed kernel launch failed"));
-  if ((rc = ab_tables(p))) return bail(rc);
+  if ((rc = ab_tables(p)) || (rc = dg_tables(p))) return bail(rc);
   // polar-start tables (legendre.cuh), then the extended-range seeds are no longer needed
   if ((rc = dalloc(&p->start_l, (size_t)(Lt + 1) * p->nPpad)) ||
       (rc = dalloc(&p->start_v, (size_t)(Lt + 1) * p->nPpad)))
     return bail(rc);
   {
     dim3 grid((p->nPpad + 127) / 128, Lt + 1);
-    fv::start_kernel<<<grid, 128>>>(p->seed_x, p->seed_e, p->pair_t, p->pair_n, p->ab, p->abofs, p->nPpad, Lt,
-                                    p->start_l, p->start_v);
+    fv::start_kernel<<<grid, 128>>>(p->seed_x, p->seed_e, p->pair_t, p->pair_n, p->ab, p->abofs, p->dg, p->dgofs,
+                                    p->nPpad, Lt, p->start_l, p->start_v);
     if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(FV_ECUDA, "polar-start kernel failed"));
     cudaFree(p->seed_x);
     cudaFree(p->seed_e);
     p->seed_x = nullptr;
     p->seed_e = nullptr;
   }
+  if ((rc = ptab_tables(p))) return bail(rc);
   // G layout tile offsets: nlc(m) = ceil((Lt+1-m)/ADJ_LC) tiles per order
   std::vector<long long> gofs(Lt + 2, 0);
   for (int m = 0; m <= Lt; ++m) gofs[m + 1] = gofs[m] + (Lt + 1 - m + fv::ADJ_LC - 1) / fv::ADJ_LC;
@@ -563,7 +669,8 @@ int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, voi
     }
     {
       StageMark mk(p, 2, s);
-      fv::FwdArgs args{p->X, p->F, p->start_l, p->start_v, p->ab, p->abofs, p->pair_t, Lt, p->nP, p->nPpad, p->nchunks, 0, dbg_mode()};
+      fv::FwdArgs args{p->X, p->F, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, Lt, p->nP, p->nPpad, p->nchunks, 0, dbg_mode(), trace_buf(), trace_cta(),
+                       p->ptab_f, p->mtab_f, p->tofs};
       FV_TRY(dispatch_fwd(p, NT, args, Lt + 1, s));
     }
     {
@@ -590,8 +697,8 @@ int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int 
     const int NT = ntiles_for(nf);
     {
       StageMark mk(p, 3, s);
-      fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), p->G, p->gofs,
-                       nullptr, p->L, NT, B, b0, nf, 0, 0};
+      fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), p->dg, p->dgofs,
+                       p->G, p->gofs, nullptr, p->L, NT, B, b0, nf, 0, 0};
       const int rows = (Lt + 1 + fv::ADJ_LC - 1) / fv::ADJ_LC * fv::ADJ_LC;
       dim3 grid((rows + 127) / 128, Lt + 1);
       fv::cg_adj_kernel<<<grid, 128, 0, s>>>(ca);
@@ -599,8 +706,9 @@ int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int 
     }
     {
       StageMark mk(p, 2, s);
-      fv::AdjArgs args{p->G, p->gofs, p->Sa, p->start_l, p->start_v, p->ab, p->abofs, p->pair_t, p->pair_n,
-                       p->pair_s, Lt, p->nP, p->nPpad, p->nrc, p->n_phi, p->n_theta, B, b0, nf, 0, dbg_mode()};
+      fv::AdjArgs args{p->G, p->gofs, p->Sa, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, p->pair_n,
+                       p->pair_s, Lt, p->nP, p->nPpad, p->nrc, p->n_phi, p->n_theta, B, b0, nf, 0, dbg_mode(),
+                       p->ptab_a, p->aofs};
       FV_TRY(dispatch_adj(p, NT, args, Lt + 1, s));
     }
   }
@@ -637,8 +745,8 @@ int fv_adjoint_points(fvPlan* p, const double* xyz, long long M, const double* a
     const int nf = std::min(4, B - b0);
     {
       StageMark mk(p, 3, s);
-      fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), p->G, nullptr,
-                       p->rowofs, p->L, 0, B, b0, nf, 0, 1};
+      fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), nullptr, nullptr,
+                       p->G, nullptr, p->rowofs, p->L, 0, B, b0, nf, 0, 1};
       dim3 grid((Lt + 1 + 127) / 128, Lt + 1);
       fv::cg_adj_kernel<<<grid, 128, 0, s>>>(ca);
       FV_CUDA(cudaGetLastError());
