@@ -75,15 +75,16 @@ class ClockSampler:
     def __enter__(self):
         try:
             import pynvml as nv
-            import torch
 
             nv.nvmlInit()
-            h = None
-            try:
-                bus = torch.cuda.get_device_properties(self.dev).pci_bus_id
-                h = nv.nvmlDeviceGetHandleByPciBusId(bus)
-            except Exception:
-                h = nv.nvmlDeviceGetHandleByIndex(self.dev.index or 0)
+            # NVML enumerates physical GPUs; map through CUDA_VISIBLE_DEVICES when set
+            idx = self.dev.index or 0
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                ids = [x.strip() for x in vis.split(",") if x.strip()]
+                if idx < len(ids) and ids[idx].isdigit():
+                    idx = int(ids[idx])
+            h = nv.nvmlDeviceGetHandleByIndex(idx)
             self.nv, self.h = nv, h
             self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
             self.ok = True
