@@ -103,6 +103,7 @@ struct FwdArgs {
   const double* pair_t;     // [nPpad] cos(theta) of the north ring of each pair
   int Lt, nP, nPpad, nchunks, m_begin;
   int dbg;  // 0 normal; 1: consumers skip MMAs; 2: producers skip the recurrence; 3: both
+  int m_count;  // orders m_begin .. m_begin + m_count - 1 (persistent CTAs walk them)
   long long* trace;  // optional pipeline timeline of CTA trace_cta (clock64 stamps), normally null
   int trace_cta;
   // table mode (plan-time Legendre tiles, ptab_fwd_kernel): null -> on-the-fly producer
@@ -278,6 +279,10 @@ __device__ __forceinline__ void fwd_mtile_dmma(int kfirst, int nt0, double (&acc
   }
 }
 
+// Persistent forward: CTA b walks orders in snake order over rounds of gridDim
+// (m ascending = work descending), which balances the per-order work (L+2-m).
+__device__ __forceinline__ int fwd_item(int k, int b, int G) { return (k & 1) ? k * G + (G - 1 - b) : k * G + b; }
+
 template <int NT>
 __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args) {
   extern __shared__ __align__(128) double smem[];
@@ -292,10 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
   double* st_t = st_p2 + nPx;
   int* st_ls = reinterpret_cast<int*>(st_t + nPx);
 
-  const int m = args.m_begin + blockIdx.x;
   const int Lt = args.Lt;
-  const int nrows = Lt + 1 - m;
-  const int nlb = (nrows + FWD_LB - 1) / FWD_LB;
   const int nchunks = args.nchunks;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -307,12 +309,6 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
     }
     fence_barrier_init();
   }
-  for (int p = threadIdx.x; p < nPx; p += blockDim.x) {
-    st_t[p] = args.pair_t[p];
-    st_ls[p] = args.start_l[(size_t)m * args.nPpad + p];
-    st_p1[p] = 0.0;
-    st_p2[p] = 0.0;
-  }
   unsigned long long gt0 = 0;
   if (args.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
   __syncthreads();
@@ -323,43 +319,61 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
     double2* abw = abw_all + pw * FWD_LB;
     FwdState st{st_p1, st_p2, st_t, st_ls};
     const bool table = args.ptab != nullptr;
-    for (int j = 0; j < nlb; ++j) {
-      const int l0 = m + FWD_LB * j;
-      if (!table) fwd_stage_coefs(abw, args, m, l0, lane);
+    uint32_t tbase = 0;  // tile counter across this CTA's orders
+    for (int k = 0;; ++k) {
+      const int item = fwd_item(k, blockIdx.x, gridDim.x);
+      if (item >= args.m_count) break;
+      const int m = args.m_begin + item;
+      const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
+      // this warp's chunks only: no other warp touches these state entries
       for (int c = pw; c < nchunks; c += kProducerWarps) {
-        const int t = j * nchunks + c;
-        const int stage = t % FWD_STAGES;
-        const uint32_t round = t / FWD_STAGES;
         const int p = c * FWD_RC + lane;
-        const TileClass tc = fwd_classify(st, p, l0, lane);
-        const bool tr = args.trace && blockIdx.x == args.trace_cta && lane == 0 && t < 4096;
-        if (tr) args.trace[t * 8 + 0] = clock64();
-        mbar_wait(&empty[stage], (round & 1) ^ 1);
-        if (tr) args.trace[t * 8 + 1] = clock64();
-        double* Ps = smem + stage * SM::STAGE;
-        double* Xs = Ps + FWD_PTILE;
-        if (tc.zero || !table) {
-          if (lane == 0) meta[stage].zero = tc.zero;
-          if ((lane & 3) == 0) meta[stage].kmin[lane >> 2] = tc.km;
-        }
-        if (!tc.zero) {
-          if (lane == 0) {
-            const uint32_t bytes = SM::XTILE * 8 + (table ? FWD_PTILE * 8 + (uint32_t)sizeof(StageMeta) : 0u);
-            asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])), "r"(bytes)
-                         : "memory");
-            bulk_g2s(Xs, args.X + ((size_t)(m - args.m_begin) * nchunks + c) * SM::XTILE, SM::XTILE * 8,
-                     &full[stage]);
-            if (table) {
-              const long long tile = args.tofs[m] + t;
-              bulk_g2s(Ps, args.ptab + tile * FWD_PTILE, FWD_PTILE * 8, &full[stage]);
-              bulk_g2s(&meta[stage], args.mtab + tile, sizeof(StageMeta), &full[stage]);
-            }
-          }
-          if (!table && !(args.dbg & 2)) fwd_compute(args, st, tc, Ps, abw, m, j, nlb, p, l0, lane);
-        }
-        if (tr) args.trace[t * 8 + 2] = clock64() | ((long long)tc.zero << 62) | ((long long)tc.mixed << 61);
-        mbar_arrive(&full[stage]);
+        st_t[p] = args.pair_t[p];
+        st_ls[p] = args.start_l[(size_t)m * args.nPpad + p];
+        st_p1[p] = 0.0;
+        st_p2[p] = 0.0;
       }
+      __syncwarp();
+      for (int j = 0; j < nlb; ++j) {
+        const int l0 = m + FWD_LB * j;
+        if (!table) fwd_stage_coefs(abw, args, m, l0, lane);
+        for (int c = pw; c < nchunks; c += kProducerWarps) {
+          const int tl = j * nchunks + c;
+          const uint32_t t = tbase + tl;
+          const int stage = t % FWD_STAGES;
+          const uint32_t round = t / FWD_STAGES;
+          const int p = c * FWD_RC + lane;
+          const TileClass tc = fwd_classify(st, p, l0, lane);
+          const bool tr = args.trace && blockIdx.x == args.trace_cta && lane == 0 && t < 4096;
+          if (tr) args.trace[t * 8 + 0] = clock64();
+          mbar_wait(&empty[stage], (round & 1) ^ 1);
+          if (tr) args.trace[t * 8 + 1] = clock64();
+          double* Ps = smem + stage * SM::STAGE;
+          double* Xs = Ps + FWD_PTILE;
+          if (tc.zero || !table) {
+            if (lane == 0) meta[stage].zero = tc.zero;
+            if ((lane & 3) == 0) meta[stage].kmin[lane >> 2] = tc.km;
+          }
+          if (!tc.zero) {
+            if (lane == 0) {
+              const uint32_t bytes = SM::XTILE * 8 + (table ? FWD_PTILE * 8 + (uint32_t)sizeof(StageMeta) : 0u);
+              asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])), "r"(bytes)
+                           : "memory");
+              bulk_g2s(Xs, args.X + ((size_t)(m - args.m_begin) * nchunks + c) * SM::XTILE, SM::XTILE * 8,
+                       &full[stage]);
+              if (table) {
+                const long long tile = args.tofs[m] + tl;
+                bulk_g2s(Ps, args.ptab + tile * FWD_PTILE, FWD_PTILE * 8, &full[stage]);
+                bulk_g2s(&meta[stage], args.mtab + tile, sizeof(StageMeta), &full[stage]);
+              }
+            }
+            if (!table && !(args.dbg & 2)) fwd_compute(args, st, tc, Ps, abw, m, j, nlb, p, l0, lane);
+          }
+          if (tr) args.trace[t * 8 + 2] = clock64() | ((long long)tc.zero << 62) | ((long long)tc.mixed << 61);
+          mbar_arrive(&full[stage]);
+        }
+      }
+      tbase += nlb * nchunks;
     }
     return;
   }
@@ -379,10 +393,16 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
 #pragma unroll
     for (int b = 0; b < NTW; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
+  uint32_t tbase = 0;
+  for (int k = 0;; ++k) {
+  const int item = fwd_item(k, blockIdx.x, gridDim.x);
+  if (item >= args.m_count) break;
+  const int m = args.m_begin + item;
+  const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
   for (int j = 0; j < nlb; ++j) {
     const int l0 = m + FWD_LB * j;
     for (int c = 0; c < nchunks; ++c) {
-      const int t = j * nchunks + c;
+      const uint32_t t = tbase + j * nchunks + c;
       const int stage = t % FWD_STAGES;
       const uint32_t round = t / FWD_STAGES;
       const bool tr = args.trace && blockIdx.x == args.trace_cta && lane == 0 && cw == 0 && t < 4096;
@@ -444,6 +464,8 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       for (int jn = 0; jn < NTW; ++jn) acc[ii][jn][0] = acc[ii][jn][1] = 0.0;
     }
   }
+  tbase += nlb * nchunks;
+  }
   if (args.trace && cw == 0 && lane == 0 && blockIdx.x < 4096) {
     unsigned long long gt1;
     unsigned smid;
@@ -479,6 +501,7 @@ struct AdjArgs {
   const int* pair_s;        // south ring (-1: unpaired)
   int Lt, nP, nPpad, nrc, n_phi, n_theta, B_total, b0, nfields, m_begin;
   int dbg;
+  int m_count;  // orders m_begin .. m_begin + m_count - 1
   // table mode: P^T stage tiles [aofs[m] + rc * nlc(m) + lc][ADJ_PTILE] (ptab_adj_kernel)
   const double* ptab;
   const long long* aofs;
@@ -488,8 +511,9 @@ template <int NT>
 struct AdjSmem {
   static constexpr int GTILE = 2 * ADJ_KS * NT * 32;
   static constexpr int STAGE = ADJ_PTILE + GTILE;
+  static constexpr int XCH = 4 * 4 * NT * 32 * 2;  // epilogue parity exchange
   static constexpr size_t bytes() {
-    return (size_t)ADJ_STAGES * STAGE * 8 + 2 * ADJ_STAGES * 8 + kProducerWarps * ADJ_LC * 16;
+    return (size_t)(ADJ_STAGES * STAGE + XCH) * 8 + 2 * ADJ_STAGES * 8 + kProducerWarps * ADJ_LC * 16;
   }
 };
 
@@ -581,19 +605,22 @@ __device__ __forceinline__ void adj_ks_dmma(int ifirst, double (&acc)[4][NT][2],
   }
 }
 
+// Persistent: one CTA per SM walks the (order m, 128-pair chunk) items in
+// descending-work order (item = blockIdx.x + k * gridDim.x; m ascending), with
+// one stage counter across items, so the producers fill the next item's stages
+// while the consumers run the previous item's epilogue.  The parity exchange of
+// the epilogue has its own shared buffer for the same reason.
 template <int NT>
 __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args) {
   extern __shared__ __align__(128) double smem[];
   using SM = AdjSmem<NT>;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ADJ_STAGES * SM::STAGE);
+  double* xch = smem + ADJ_STAGES * SM::STAGE;  // [mq][ii][jn][lane][2]
+  uint64_t* full = reinterpret_cast<uint64_t*>(xch + SM::XCH);
   uint64_t* empty = full + ADJ_STAGES;
   double2* abw_all = reinterpret_cast<double2*>(empty + ADJ_STAGES);
 
-  const int m = args.m_begin + blockIdx.x / args.nrc;
-  const int rc = blockIdx.x % args.nrc;
   const int Lt = args.Lt;
-  const int nrows = Lt + 1 - m;
-  const int nlc = (nrows + ADJ_LC - 1) / ADJ_LC;
+  const int nitems = args.m_count * args.nrc;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
@@ -610,54 +637,60 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
     // ------------------------------ producer ------------------------------
     const int pw = producer_index(warp);
     double2* abw = abw_all + pw * ADJ_LC;
-    const int rho = 32 * pw + lane;            // pair within the CTA's chunk
-    const int p = rc * ADJ_RC + rho;
+    const int rho = 32 * pw + lane;            // pair within the item's chunk
     const int i = rho >> 3, g = rho & 7;
-    const double tt = args.pair_t[p];
-    Inject in;
-    in.ls = args.start_l[(size_t)m * args.nPpad + p];
-    {
-      const double2 v = args.start_v[(size_t)m * args.nPpad + p];
-      in.A = v.x;
-      in.B = v.y;
-    }
-    double p1 = 0.0, p2 = 0.0;
-    const double2* dgm = args.dg + args.dgofs[m];
-    const double* Gm = args.G + (size_t)args.gofs[m] * SM::GTILE;
     const bool table = args.ptab != nullptr;
-    for (int lc = 0; lc < nlc; ++lc) {
-      const int stage = lc % ADJ_STAGES;
-      const uint32_t round = lc / ADJ_STAGES;
-      const int l0 = m + ADJ_LC * lc;
-      const bool before = in.ls > l0 + ADJ_LC - 1;
-      const bool zero = __all_sync(0xffffffffu, before);
-      const bool mixed = __any_sync(0xffffffffu, !before && in.ls + 1 >= l0);
-      if (!zero && !table) {
-        __syncwarp();
-        const int l = l0 + lane;
-        abw[lane] = (l <= Lt) ? dgm[l - m] : make_double2(0.0, 1.0);
-        __syncwarp();
+    uint32_t sc = 0;                           // stage counter across items
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+      const int m = args.m_begin + item / args.nrc;
+      const int rc = item % args.nrc;
+      const int nlc = (Lt + 1 - m + ADJ_LC - 1) / ADJ_LC;
+      const int p = rc * ADJ_RC + rho;
+      const double tt = args.pair_t[p];
+      Inject in;
+      in.ls = args.start_l[(size_t)m * args.nPpad + p];
+      {
+        const double2 v = args.start_v[(size_t)m * args.nPpad + p];
+        in.A = v.x;
+        in.B = v.y;
       }
-      mbar_wait(&empty[stage], (round & 1) ^ 1);
-      double* Ps = smem + stage * SM::STAGE;
-      double* Gs = Ps + ADJ_PTILE;
-      if (pw == 0 && lane == 0) {
-        const uint32_t bytes = SM::GTILE * 8 + (table ? ADJ_PTILE * 8 : 0u);
-        asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])), "r"(bytes)
-                     : "memory");
-        bulk_g2s(Gs, Gm + (size_t)lc * SM::GTILE, SM::GTILE * 8, &full[stage]);
-        if (table)
-          bulk_g2s(Ps, args.ptab + (size_t)(args.aofs[m] + (long long)rc * nlc + lc) * ADJ_PTILE, ADJ_PTILE * 8,
-                   &full[stage]);
+      double p1 = 0.0, p2 = 0.0;
+      const double2* dgm = args.dg + args.dgofs[m];
+      const double* Gm = args.G + (size_t)args.gofs[m] * SM::GTILE;
+      for (int lc = 0; lc < nlc; ++lc, ++sc) {
+        const int stage = sc % ADJ_STAGES;
+        const uint32_t round = sc / ADJ_STAGES;
+        const int l0 = m + ADJ_LC * lc;
+        const bool before = in.ls > l0 + ADJ_LC - 1;
+        const bool zero = __all_sync(0xffffffffu, before);
+        const bool mixed = __any_sync(0xffffffffu, !before && in.ls + 1 >= l0);
+        if (!zero && !table) {
+          __syncwarp();
+          const int l = l0 + lane;
+          abw[lane] = (l <= Lt) ? dgm[l - m] : make_double2(0.0, 1.0);
+          __syncwarp();
+        }
+        mbar_wait(&empty[stage], (round & 1) ^ 1);
+        double* Ps = smem + stage * SM::STAGE;
+        double* Gs = Ps + ADJ_PTILE;
+        if (pw == 0 && lane == 0) {
+          const uint32_t bytes = SM::GTILE * 8 + (table ? ADJ_PTILE * 8 : 0u);
+          asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])), "r"(bytes)
+                       : "memory");
+          bulk_g2s(Gs, Gm + (size_t)lc * SM::GTILE, SM::GTILE * 8, &full[stage]);
+          if (table)
+            bulk_g2s(Ps, args.ptab + (size_t)(args.aofs[m] + (long long)rc * nlc + lc) * ADJ_PTILE,
+                     ADJ_PTILE * 8, &full[stage]);
+        }
+        // all-zero warps write nothing: the consumers skip their M-tiles (polar start)
+        if (zero || table || (args.dbg & 2)) {
+        } else if (mixed) {
+          adj_produce<true>(Ps, abw, tt, p1, p2, i, g, l0, in);
+        } else {
+          adj_produce<false>(Ps, abw, tt, p1, p2, i, g, l0, in);
+        }
+        mbar_arrive(&full[stage]);
       }
-      // all-zero warps write nothing: the consumers skip their M-tiles (polar start)
-      if (zero || table || (args.dbg & 2)) {
-      } else if (mixed) {
-        adj_produce<true>(Ps, abw, tt, p1, p2, i, g, l0, in);
-      } else {
-        adj_produce<false>(Ps, abw, tt, p1, p2, i, g, l0, in);
-      }
-      mbar_arrive(&full[stage]);
     }
     return;
   }
@@ -668,102 +701,105 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
   const int par = cw >> 2;
   const int mq = cw & 3;
   const int g = lane >> 2, q = lane & 3;
-  // first degree at which each of the warp's M-tiles has a pair above the polar threshold
-  int mt_start[4];
-  {
-    int v = args.start_l[(size_t)m * args.nPpad + rc * ADJ_RC + 32 * mq + lane];
+  uint32_t sc = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int m = args.m_begin + item / args.nrc;
+    const int rc = item % args.nrc;
+    const int nlc = (Lt + 1 - m + ADJ_LC - 1) / ADJ_LC;
+    // first degree at which each of the warp's M-tiles has a pair above the polar threshold
+    int mt_start[4];
+    {
+      int v = args.start_l[(size_t)m * args.nPpad + rc * ADJ_RC + 32 * mq + lane];
 #pragma unroll
-    for (int o = 1; o < 8; o <<= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+      for (int o = 1; o < 8; o <<= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
 #pragma unroll
-    for (int ii = 0; ii < 4; ++ii) mt_start[ii] = __shfl_sync(0xffffffffu, v, 8 * ii);
-  }
-  double acc[4][NT][2];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-
-  for (int lc = 0; lc < nlc; ++lc) {
-    const int stage = lc % ADJ_STAGES;
-    const uint32_t round = lc / ADJ_STAGES;
-    const int lhi = m + ADJ_LC * lc + ADJ_LC - 1;
-    mbar_wait(&full[stage], round & 1);
-    const double* Ps = smem + stage * SM::STAGE;
-    const double* Gs = Ps + ADJ_PTILE;
-    bool act[4];
-#pragma unroll
-    for (int ii = 0; ii < 4; ++ii) act[ii] = mt_start[ii] <= lhi;
-    if (!(args.dbg & 1) && (act[0] || act[1] || act[2] || act[3])) {
-      // k-step fragments double-buffered in registers: the loads of step ks+1
-      // are in flight while the 24 DMMAs of step ks issue
-      double a[2][4], b[2][NT];
-      auto load = [&](int ks, int bufi) {
-#pragma unroll
-        for (int ii = 0; ii < 4; ++ii) {
-          const int i = 4 * mq + ii;
-          a[bufi][ii] = lds_f64(&Ps[((par * ADJ_KS + ks) * ADJ_MT + i) * 32 + adj_swz(g, q, i)]);
-        }
-#pragma unroll
-        for (int jn = 0; jn < NT; ++jn) b[bufi][jn] = lds_f64(&Gs[((par * ADJ_KS + ks) * NT + jn) * 32 + lane]);
-      };
-      load(0, 0);
-      const int l0s = m + ADJ_LC * lc;
-#pragma unroll
-      for (int ks = 0; ks < ADJ_KS; ++ks) {
-        if (ks + 1 < ADJ_KS) load(ks + 1, (ks + 1) & 1);
-        // k-step ks holds degrees l0s + 8 ks .. + 7 (one parity): skip M-tiles whose
-        // pairs start later, and the k-steps past Lt (zero coefficient rows)
-        const int khi = l0s + 8 * ks + 7;
-        // active M-tiles form a suffix (pairs nearer the equator start earlier):
-        // dispatch on the first one with a real branch (predicated-off DMMAs
-        // would still occupy the pipe)
-        int ifirst = 4;
-        if (l0s + 8 * ks <= Lt) {
-#pragma unroll
-          for (int ii = 3; ii >= 0; --ii)
-            if (mt_start[ii] <= khi) ifirst = ii;
-        }
-        adj_ks_dmma<NT>(ifirst, acc, a[ks & 1], b[ks & 1]);
-      }
+      for (int ii = 0; ii < 4; ++ii) mt_start[ii] = __shfl_sync(0xffffffffu, v, 8 * ii);
     }
-    mbar_arrive(&empty[stage]);
-  }
+    double acc[4][NT][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-  // epilogue: combine parities through shared memory (odd warps publish, even warps finish)
-  asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps));
-  double* xch = smem;  // reuse stage buffers: [mq][ii][jn][lane][2]
-  if (par == 1) {
+    for (int lc = 0; lc < nlc; ++lc, ++sc) {
+      const int stage = sc % ADJ_STAGES;
+      const uint32_t round = sc / ADJ_STAGES;
+      const int l0s = m + ADJ_LC * lc;
+      mbar_wait(&full[stage], round & 1);
+      const double* Ps = smem + stage * SM::STAGE;
+      const double* Gs = Ps + ADJ_PTILE;
+      const int mts = min(min(mt_start[0], mt_start[1]), min(mt_start[2], mt_start[3]));
+      if (!(args.dbg & 1) && mts <= l0s + ADJ_LC - 1 && l0s <= Lt) {
+        // k-step fragments double-buffered in registers: the loads of step ks+1
+        // are in flight while the DMMAs of step ks issue
+        double a[2][4], b[2][NT];
+        auto load = [&](int ks, int bufi) {
 #pragma unroll
-    for (int ii = 0; ii < 4; ++ii)
+          for (int ii = 0; ii < 4; ++ii) {
+            const int i = 4 * mq + ii;
+            a[bufi][ii] = lds_f64(&Ps[((par * ADJ_KS + ks) * ADJ_MT + i) * 32 + adj_swz(g, q, i)]);
+          }
 #pragma unroll
-      for (int jn = 0; jn < NT; ++jn) {
-        double* d = xch + ((size_t)((mq * 4 + ii) * NT + jn) * 32 + lane) * 2;
-        d[0] = acc[ii][jn][0];
-        d[1] = acc[ii][jn][1];
+          for (int jn = 0; jn < NT; ++jn) b[bufi][jn] = lds_f64(&Gs[((par * ADJ_KS + ks) * NT + jn) * 32 + lane]);
+        };
+        load(0, 0);
+#pragma unroll
+        for (int ks = 0; ks < ADJ_KS; ++ks) {
+          if (ks + 1 < ADJ_KS) load(ks + 1, (ks + 1) & 1);
+          // k-step ks holds degrees l0s + 8 ks .. + 7 (one parity).  Active M-tiles
+          // form a suffix (pairs nearer the equator start earlier; padding pairs at
+          // the end never start, their accumulators are discarded): dispatch on the
+          // first active one with a real branch (a predicated-off DMMA still
+          // occupies the pipe); k-steps past Lt hold zero coefficient rows.
+          const int khi = l0s + 8 * ks + 7;
+          int ifirst = 4;
+          if (l0s + 8 * ks <= Lt) {
+#pragma unroll
+            for (int ii = 3; ii >= 0; --ii)
+              if (mt_start[ii] <= khi) ifirst = ii;
+          }
+          adj_ks_dmma<NT>(ifirst, acc, a[ks & 1], b[ks & 1]);
+        }
       }
-  }
-  asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps));
-  if (par == 0 && rc * ADJ_RC + 32 * mq < args.nP) {
+      mbar_arrive(&empty[stage]);
+    }
+
+    // epilogue: combine parities through the exchange buffer (odd warps publish,
+    // even warps finish); the first barrier also retires the previous item's reads
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps));
+    if (par == 1) {
 #pragma unroll
-    for (int ii = 0; ii < 4; ++ii) {
-      const int rho = (4 * mq + ii) * 8 + g;
-      const int p = rc * ADJ_RC + rho;
-      const int rn = args.pair_n[p];
-      const int rs = args.pair_s[p];
-      if (rn < 0) continue;
+      for (int ii = 0; ii < 4; ++ii)
 #pragma unroll
-      for (int jn = 0; jn < NT; ++jn) {
-        const double* d = xch + ((size_t)((mq * 4 + ii) * NT + jn) * 32 + lane) * 2;
-        const int ser = (jn * 8 + 2 * q) >> 1;  // 6*field + 2*comp + sign
-        const int b = ser / 6, comp = (ser % 6) >> 1, sgn = ser & 1;
-        if (b >= args.nfields) continue;
-        if (sgn == 1 && m == 0) continue;
-        const int bin = sgn ? (args.n_phi - m) % args.n_phi : m;
-        const double er = acc[ii][jn][0], ei = acc[ii][jn][1];
-        const double orr = d[0], oi = d[1];
-        const size_t base = ((size_t)comp * args.B_total + args.b0 + b) * args.n_theta;
-        args.S[(base + rn) * args.n_phi + bin] = make_double2(er + orr, ei + oi);
-        if (rs >= 0) args.S[(base + rs) * args.n_phi + bin] = make_double2(er - orr, ei - oi);
+        for (int jn = 0; jn < NT; ++jn) {
+          double* d = xch + ((size_t)((mq * 4 + ii) * NT + jn) * 32 + lane) * 2;
+          d[0] = acc[ii][jn][0];
+          d[1] = acc[ii][jn][1];
+        }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps));
+    if (par == 0 && rc * ADJ_RC + 32 * mq < args.nP) {
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) {
+        const int rho = (4 * mq + ii) * 8 + g;
+        const int p = rc * ADJ_RC + rho;
+        const int rn = args.pair_n[p];
+        const int rs = args.pair_s[p];
+        if (rn < 0) continue;
+#pragma unroll
+        for (int jn = 0; jn < NT; ++jn) {
+          const double* d = xch + ((size_t)((mq * 4 + ii) * NT + jn) * 32 + lane) * 2;
+          const int ser = (jn * 8 + 2 * q) >> 1;  // 6*field + 2*comp + sign
+          const int b = ser / 6, comp = (ser % 6) >> 1, sgn = ser & 1;
+          if (b >= args.nfields) continue;
+          if (sgn == 1 && m == 0) continue;
+          const int bin = sgn ? (args.n_phi - m) % args.n_phi : m;
+          const double er = acc[ii][jn][0], ei = acc[ii][jn][1];
+          const double orr = d[0], oi = d[1];
+          const size_t base = ((size_t)comp * args.B_total + args.b0 + b) * args.n_theta;
+          args.S[(base + rn) * args.n_phi + bin] = make_double2(er + orr, ei + oi);
+          if (rs >= 0) args.S[(base + rs) * args.n_phi + bin] = make_double2(er - orr, ei - oi);
+        }
       }
     }
   }

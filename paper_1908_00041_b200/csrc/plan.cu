@@ -80,7 +80,7 @@ inline int ntiles_for(int nfields) { return (12 * nfields + 7) / 8; }
 struct fvPlan {
   int kind = 0;  // 0 grid, 1 points
   int L = 0, Lt = 0, n_theta = 0, n_phi = 0, nP = 0, nPpad = 0, nchunks = 0, nrc = 0;
-  int max_batch = 0, device = 0, paired = 0;
+  int max_batch = 0, device = 0, paired = 0, num_sms = 148;
   // grid tables
   double* pair_t = nullptr;
   double* pair_sin = nullptr;
@@ -300,7 +300,11 @@ int launch_fwd(fvPlan* p, const fv::FwdArgs& args, int m_count, cudaStream_t s) 
     FV_CUDA(cudaFuncSetAttribute(fv::legendre_fwd_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  227 * 1024));
   }
-  fv::legendre_fwd_kernel<NT><<<m_count, fv::kThreads, bytes, s>>>(args);
+  fv::FwdArgs a2 = args;
+  a2.m_count = m_count;
+  // one CTA per order: the hardware block scheduler hands out orders in ascending m
+  // (descending work) dynamically, which balances better than a static persistent split
+  fv::legendre_fwd_kernel<NT><<<m_count, fv::kThreads, bytes, s>>>(a2);
   FV_CUDA(cudaGetLastError());
   return FV_OK;
 }
@@ -313,7 +317,11 @@ int launch_adj(fvPlan* p, const fv::AdjArgs& args, int m_count, cudaStream_t s) 
     FV_CUDA(cudaFuncSetAttribute(fv::legendre_adj_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  227 * 1024));
   }
-  fv::legendre_adj_kernel<NT><<<m_count * p->nrc, fv::kThreads, bytes, s>>>(args);
+  if (bytes > 227 * 1024) return fail(FV_EINVAL, "adjoint kernel shared memory exceeds 227 KB");
+  fv::AdjArgs a2 = args;
+  a2.m_count = m_count;
+  const int items = m_count * p->nrc;
+  fv::legendre_adj_kernel<NT><<<std::min(items, p->num_sms), fv::kThreads, bytes, s>>>(a2);
   FV_CUDA(cudaGetLastError());
   return FV_OK;
 }
@@ -469,6 +477,7 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
     return rc;
   };
   if (cudaSetDevice(device) != cudaSuccess) return bail(fail(FV_ECUDA, "cannot select device"));
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
 
   // ring cosines exactly as favest/scalar.py:133 + favest/legendre.py:53-57
   std::vector<double> t(n_theta), w(ring_weight_host, ring_weight_host + n_theta);
@@ -669,8 +678,8 @@ int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, voi
     }
     {
       StageMark mk(p, 2, s);
-      fv::FwdArgs args{p->X, p->F, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, Lt, p->nP, p->nPpad, p->nchunks, 0, dbg_mode(), trace_buf(), trace_cta(),
-                       p->ptab_f, p->mtab_f, p->tofs};
+      fv::FwdArgs args{p->X, p->F, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, Lt, p->nP, p->nPpad, p->nchunks, 0, dbg_mode(), Lt + 1, trace_buf(),
+                       trace_cta(), p->ptab_f, p->mtab_f, p->tofs};
       FV_TRY(dispatch_fwd(p, NT, args, Lt + 1, s));
     }
     {
@@ -708,7 +717,7 @@ int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int 
       StageMark mk(p, 2, s);
       fv::AdjArgs args{p->G, p->gofs, p->Sa, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, p->pair_n,
                        p->pair_s, Lt, p->nP, p->nPpad, p->nrc, p->n_phi, p->n_theta, B, b0, nf, 0, dbg_mode(),
-                       p->ptab_a, p->aofs};
+                       Lt + 1, p->ptab_a, p->aofs};
       FV_TRY(dispatch_adj(p, NT, args, Lt + 1, s));
     }
   }
