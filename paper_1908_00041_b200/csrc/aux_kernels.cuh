@@ -238,12 +238,32 @@ __global__ void fold_fwd_kernel(FoldArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// Clebsch-Gordan factor table: xi^1..6, mu^1..3 (favest/coupling.py:143-170) at
+// every flat position k = l*l + l + m, l <= L+1, stored as 9 arrays of K_t
+// doubles (plan time; same closed forms, so bitwise the reference's values).
+// ---------------------------------------------------------------------------
+__global__ void cg_table_kernel(int Lt, double* cgt) {
+  const long long Kt = (long long)(Lt + 1) * (Lt + 1);
+  const long long k = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= Kt) return;
+  long long l = (long long)sqrt((double)k);
+  while (l * l > k) --l;
+  while ((l + 1) * (l + 1) <= k) ++l;
+  const long long m = k - l * l - l;
+#pragma unroll
+  for (int i = 1; i <= 6; ++i) cgt[(i - 1) * Kt + k] = xi_coef(i, l, m);
+#pragma unroll
+  for (int i = 1; i <= 3; ++i) cgt[(5 + i) * Kt + k] = mu_coef(i, l, m);
+}
+
+// ---------------------------------------------------------------------------
 // forward Clebsch-Gordan assembly: favest/transforms.py:120-146
 // ---------------------------------------------------------------------------
 struct CgFwdArgs {
   const double* F;      // rows tri(l, |m|), ncolF doubles: col 12b + 4c + 2s + ri
   double2* A;           // (B_total, K) div coefficients
   double2* Bc;          // (B_total, K) curl coefficients
+  const double* cgt;    // cg_table_kernel: 9 x K_t (xi1..6, mu1..3)
   int L, ncolF, B_total, b0, nfields;
 };
 
@@ -265,13 +285,14 @@ __global__ void cg_fwd_kernel(CgFwdArgs a) {
   for (int sg = 0; sg < (am == 0 ? 1 : 2); ++sg) {
     const long long M = sg ? -am : am;
     // table values at the source positions (l+dl, M+dm); zero if out of range
+    const long long Kt = (long long)(a.L + 2) * (a.L + 2);
     auto xi_at = [&](int i, long long ls, long long ms) -> double {
       if (ls < 0 || ls > a.L + 1 || llabs(ms) > ls) return 0.0;
-      return xi_coef(i, ls, ms);
+      return __ldg(&a.cgt[(i - 1) * Kt + ls * ls + ls + ms]);
     };
     auto mu_at = [&](int i, long long ls, long long ms) -> double {
       if (ls < 0 || ls > a.L + 1 || llabs(ms) > ls) return 0.0;
-      return mu_coef(i, ls, ms);
+      return __ldg(&a.cgt[(5 + i) * Kt + ls * ls + ls + ms]);
     };
     const double x1 = xi_at(1, l - 1, M - 1), x2 = xi_at(2, l + 1, M - 1);
     const double x3 = xi_at(3, l - 1, M + 1), x4 = xi_at(4, l + 1, M + 1);
@@ -308,6 +329,7 @@ struct CgAdjArgs {
   const double2* Bc;    // (B_total, K) curl
   const double2* dg;    // grid mode: (d, gamma) of the block-rescaled recurrence, G is scaled by gamma_l
   const long long* dgofs;
+  const double* cgt;    // cg_table_kernel: 9 x K_t (xi1..6, mu1..3)
   double* G;
   const long long* gofs;    // fragment mode: tile offset (units of 512*NT doubles) per order
   const long long* rowofs;  // row mode: row offset per order (rows of 12*nfields doubles)
@@ -349,9 +371,10 @@ __global__ void cg_adj_kernel(CgAdjArgs a) {
     const bool on = live && !(sg == 1 && am == 0);
     double x1 = 0, x2 = 0, x3 = 0, x4 = 0, x5 = 0, x6 = 0, u1 = 0, u2 = 0, u3 = 0;
     if (on) {
-      x1 = xi_coef(1, l, m); x2 = xi_coef(2, l, m); x3 = xi_coef(3, l, m);
-      x4 = xi_coef(4, l, m); x5 = xi_coef(5, l, m); x6 = xi_coef(6, l, m);
-      u1 = mu_coef(1, l, m); u2 = mu_coef(2, l, m); u3 = mu_coef(3, l, m);
+      const long long Kt = (long long)(Lt + 1) * (Lt + 1), k = l * l + l + m;
+      x1 = __ldg(&a.cgt[0 * Kt + k]); x2 = __ldg(&a.cgt[1 * Kt + k]); x3 = __ldg(&a.cgt[2 * Kt + k]);
+      x4 = __ldg(&a.cgt[3 * Kt + k]); x5 = __ldg(&a.cgt[4 * Kt + k]); x6 = __ldg(&a.cgt[5 * Kt + k]);
+      u1 = __ldg(&a.cgt[6 * Kt + k]); u2 = __ldg(&a.cgt[7 * Kt + k]); u3 = __ldg(&a.cgt[8 * Kt + k]);
     }
     double sig = (m < 0 && (am & 1)) ? -1.0 : 1.0;  // favest/legendre.py:101-103
     if (!a.rows_mode && live) sig *= a.dg[a.dgofs[am] + (l - am)].y;  // gamma_l (legendre.cuh)

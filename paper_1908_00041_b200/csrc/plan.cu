@@ -93,6 +93,7 @@ struct fvPlan {
   double2* start_v = nullptr;
   double2* ab = nullptr;
   long long* abofs = nullptr;
+  double* cgt = nullptr;        // Clebsch-Gordan factors xi1..6, mu1..3 (9 x K_t)
   double2* dg = nullptr;        // block-rescaled recurrence (d, gamma) (grid plans)
   long long* dgofs = nullptr;
   // table mode: plan-time Legendre tiles streamed by TMA instead of the on-the-fly producer
@@ -138,7 +139,7 @@ void free_plan(fvPlan* p) {
   cudaSetDevice(p->device);
   void* ptrs[] = {p->pair_t, p->pair_sin, p->pair_n, p->pair_s, p->ring_w, p->seed_x,
                   p->seed_e, p->start_l,  p->start_v, p->ab,   p->abofs,  p->gofs,
-                  p->dg,     p->dgofs,  p->ptab_f,  p->mtab_f, p->tofs,   p->ptab_a, p->aofs,
+                  p->dg,     p->dgofs,  p->cgt,     p->ptab_f,  p->mtab_f, p->tofs,   p->ptab_a, p->aofs,
                   p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->G,
                   p->fft_tw};
   for (void* q : ptrs)
@@ -163,6 +164,14 @@ int ab_tables(fvPlan* p) {
     fv::ab_kernel<<<grid, 128>>>(Lt, p->abofs, p->ab);
     FV_CUDA(cudaGetLastError());
   }
+  return FV_OK;
+}
+
+int cg_tables(fvPlan* p) {
+  const long long Kt = (long long)(p->Lt + 1) * (p->Lt + 1);
+  FV_TRY(dalloc(&p->cgt, (size_t)(9 * Kt)));
+  fv::cg_table_kernel<<<(unsigned)((Kt + 255) / 256), 256>>>(p->Lt, p->cgt);
+  FV_CUDA(cudaGetLastError());
   return FV_OK;
 }
 
@@ -531,7 +540,7 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
   cudaMemcpy(p->ring_w, w.data(), n_theta * 8, cudaMemcpyHostToDevice);
   fv::seeds_kernel<<<(p->nPpad + 127) / 128, 128>>>(p->pair_sin, p->nPpad, Lt, p->seed_x, p->seed_e);
   if (cudaGetLastError() != cudaSuccess) return bail(fail(FV_ECUDA, "seed kernel launch failed"));
-  if ((rc = ab_tables(p)) || (rc = dg_tables(p))) return bail(rc);
+  if ((rc = ab_tables(p)) || (rc = dg_tables(p)) || (rc = cg_tables(p))) return bail(rc);
   // polar-start tables (legendre.cuh), then the extended-range seeds are no longer needed
   if ((rc = dalloc(&p->start_l, (size_t)(Lt + 1) * p->nPpad)) ||
       (rc = dalloc(&p->start_v, (size_t)(Lt + 1) * p->nPpad)))
@@ -587,7 +596,7 @@ int fv_plan_create_points(fvPlan** out, int L, int max_batch, int device) {
   };
   if (cudaSetDevice(device) != cudaSuccess) return bail(fail(FV_ECUDA, "cannot select device"));
   int rc;
-  if ((rc = ab_tables(p))) return bail(rc);
+  if ((rc = ab_tables(p)) || (rc = cg_tables(p))) return bail(rc);
   const int Lt = p->Lt;
   std::vector<long long> rowofs(Lt + 2, 0);
   for (int m = 0; m <= Lt; ++m) rowofs[m + 1] = rowofs[m] + (Lt + 1 - m);
@@ -684,7 +693,8 @@ int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, voi
     }
     {
       StageMark mk(p, 3, s);
-      fv::CgFwdArgs ca{p->F, reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), p->L, 8 * NT, B, b0, nf};
+      fv::CgFwdArgs ca{p->F, reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), p->cgt, p->L, 8 * NT, B, b0,
+                       nf};
       dim3 grid((p->L + 1 + 127) / 128, p->L + 1);
       fv::cg_fwd_kernel<<<grid, 128, 0, s>>>(ca);
       FV_CUDA(cudaGetLastError());
@@ -707,7 +717,7 @@ int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int 
     {
       StageMark mk(p, 3, s);
       fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), p->dg, p->dgofs,
-                       p->G, p->gofs, nullptr, p->L, NT, B, b0, nf, 0, 0};
+                       p->cgt, p->G, p->gofs, nullptr, p->L, NT, B, b0, nf, 0, 0};
       const int rows = (Lt + 1 + fv::ADJ_LC - 1) / fv::ADJ_LC * fv::ADJ_LC;
       dim3 grid((rows + 127) / 128, Lt + 1);
       fv::cg_adj_kernel<<<grid, 128, 0, s>>>(ca);
@@ -755,7 +765,7 @@ int fv_adjoint_points(fvPlan* p, const double* xyz, long long M, const double* a
     {
       StageMark mk(p, 3, s);
       fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), nullptr, nullptr,
-                       p->G, nullptr, p->rowofs, p->L, 0, B, b0, nf, 0, 1};
+                       p->cgt, p->G, nullptr, p->rowofs, p->L, 0, B, b0, nf, 0, 1};
       dim3 grid((Lt + 1 + 127) / 128, Lt + 1);
       fv::cg_adj_kernel<<<grid, 128, 0, s>>>(ca);
       FV_CUDA(cudaGetLastError());
