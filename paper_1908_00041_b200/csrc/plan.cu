@@ -355,21 +355,40 @@ int dispatch_adj(fvPlan* p, int NT, const fv::AdjArgs& a, int mc, cudaStream_t s
   return fail(FV_EINVAL, "unsupported field group");
 }
 
-// radix sequence for the hand-written FFT: 4s, then 2, then odd primes <= 19
+// radix sequence for the hand-written FFT: each prime 11..19 is its own stage;
+// the small primes (2, 3, 5, 7) are packed greedily into composite radices
+// <= 16 (fewer, fatter stages: fewer shared-memory passes and barriers).
+// Largest radix first: the first stage has no twiddles.
 bool fft_factor(int n, int* radix, int* nst) {
   if (n < 2 || n > fv::FFT_NMAX) return false;
-  int k = 0;
-  auto push = [&](int r) {
-    if (k >= fv::FFT_MAXST) return false;
-    radix[k++] = r;
-    return true;
-  };
-  while (n % 4 == 0) { if (!push(4)) return false; n /= 4; }
-  while (n % 2 == 0) { if (!push(2)) return false; n /= 2; }
-  for (int p : {3, 5, 7, 11, 13, 17, 19})
-    while (n % p == 0) { if (!push(p)) return false; n /= p; }
-  *nst = k;
-  return n == 1;
+  std::vector<int> small, out;
+  for (int p : {2, 3, 5, 7, 11, 13, 17, 19})
+    while (n % p == 0) {
+      (p <= 7 ? small : out).push_back(p);
+      n /= p;
+    }
+  if (n != 1) return false;
+  std::sort(small.begin(), small.end(), std::greater<int>());
+  while (!small.empty()) {
+    int r = small.front();
+    small.erase(small.begin());
+    for (bool grew = true; grew;) {
+      grew = false;
+      for (size_t i = 0; i < small.size(); ++i)
+        if (r * small[i] <= 16) {
+          r *= small[i];
+          small.erase(small.begin() + i);
+          grew = true;
+          break;
+        }
+    }
+    out.push_back(r);
+  }
+  std::sort(out.begin(), out.end(), std::greater<int>());
+  if ((int)out.size() > fv::FFT_MAXST) return false;
+  for (size_t i = 0; i < out.size(); ++i) radix[i] = out[i];
+  *nst = (int)out.size();
+  return true;
 }
 
 int setup_fft(fvPlan* p) {
@@ -386,14 +405,26 @@ int setup_fft(fvPlan* p) {
     }
   FV_CUDA(cudaMemcpyToSymbol(fv::kRootCos, rc, sizeof(rc)));
   FV_CUDA(cudaMemcpyToSymbol(fv::kRootSin, rs, sizeof(rs)));
-  std::vector<double2> tw(p->n_phi);
-  for (int k = 0; k < p->n_phi; ++k) {
-    const long double a = 2.0L * 3.141592653589793238462643383279502884L * k / p->n_phi;
+  double cc[sizeof(fv::kCompCos) / sizeof(double)], cs[sizeof(fv::kCompSin) / sizeof(double)];
+  for (int R : fv::kCompR)
+    for (int e = 0; e < R; ++e) {
+      const long double a = 2.0L * 3.141592653589793238462643383279502884L * e / R;
+      cc[fv::comp_offset(R) + e] = (double)cosl(a);
+      cs[fv::comp_offset(R) + e] = (double)sinl(a);
+    }
+  FV_CUDA(cudaMemcpyToSymbol(fv::kCompCos, cc, sizeof(cc)));
+  FV_CUDA(cudaMemcpyToSymbol(fv::kCompSin, cs, sizeof(cs)));
+  // factored twiddles: lo[k] = w^k (k < 64), hi[j] = w^(64 j)
+  const int nhi = (p->n_phi + fv::FFT_TWLO - 1) / fv::FFT_TWLO;
+  std::vector<double2> tw(fv::FFT_TWLO + nhi);
+  for (int k = 0; k < (int)tw.size(); ++k) {
+    const long long e = k < fv::FFT_TWLO ? k : (long long)fv::FFT_TWLO * (k - fv::FFT_TWLO);
+    const long double a = 2.0L * 3.141592653589793238462643383279502884L * e / p->n_phi;
     tw[k] = make_double2((double)cosl(a), -(double)sinl(a));
   }
-  FV_TRY(dalloc(&p->fft_tw, p->n_phi));
-  FV_CUDA(cudaMemcpy(p->fft_tw, tw.data(), p->n_phi * sizeof(double2), cudaMemcpyHostToDevice));
-  const size_t smem = 2 * (size_t)p->n_phi * sizeof(double2);
+  FV_TRY(dalloc(&p->fft_tw, tw.size()));
+  FV_CUDA(cudaMemcpy(p->fft_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  const size_t smem = (3 * (size_t)p->n_phi + fv::FFT_TWN) * sizeof(double2);
   FV_CUDA(cudaFuncSetAttribute(fv::ring_fft_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   FV_CUDA(cudaFuncSetAttribute(fv::ring_fft_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   p->custom_fft = true;
@@ -424,8 +455,9 @@ int ring_fft(fvPlan* p, bool inverse, const double2* in, double2* out, int B, cu
     a.tstride[i] = p->n_phi / (ns * p->fft_radix[i]);
     ns *= p->fft_radix[i];
   }
-  dim3 grid(3, B * p->n_theta);
-  const size_t smem = 2 * (size_t)n * sizeof(double2);
+  a.nrings = B * p->n_theta;
+  const int grid = std::min(3 * a.nrings, 2 * p->num_sms);
+  const size_t smem = (3 * (size_t)n + fv::FFT_TWN) * sizeof(double2);
   if (inverse) fv::ring_fft_kernel<true><<<grid, fv::FFT_THREADS, smem, s>>>(a);
   else fv::ring_fft_kernel<false><<<grid, fv::FFT_THREADS, smem, s>>>(a);
   FV_CUDA(cudaGetLastError());

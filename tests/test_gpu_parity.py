@@ -201,6 +201,25 @@ def test_odd_and_asymmetric_grids():
         assert O.rel_l2(got, np.concatenate([ra, rb])) <= TOL
 
 
+@pytest.mark.parametrize("nphi", [24, 30, 36, 40, 42, 48, 49, 64, 75, 128, 286, 342, 2052, 46])
+def test_ring_fft_radix_plans(nphi):
+    """Every packed radix (2..16 composites, primes 11..19) and the cuFFT
+    fallback (46 = 2 * 23), forward and adjoint against the oracle."""
+    cuda_or_skip()
+    rng = np.random.default_rng(nphi)
+    L = 8
+    th, w, _ = O.gl_grid(L)
+    plan = _plan(L, th, w, nphi, B=2)
+    a, b = O.coef(rng, L, "inv")
+    T = plan.adjoint(_t(a[None]), _t(b[None])).cpu().numpy()[0]
+    assert O.rel_l2(T, O.vsht_adjoint_grid(a, b, L, th, nphi)) <= TOL
+    Tin = T + O.tangent_noise(rng, O.grid_points(th, nphi), 0.1)
+    fa, fb_ = plan.forward(_t(Tin[None]))
+    ra, rb = O.vsht_forward_grid(Tin, th, w, nphi, L)
+    got = np.concatenate([fa[0].cpu().numpy(), fb_[0].cpu().numpy()])
+    assert O.rel_l2(got, np.concatenate([ra, rb])) <= TOL
+
+
 def test_c5_scattered_subset_against_oracle():
     # BASELINE configs[4]: L=128, points first then 1/(l(l+1)) coefficients, seed 5
     from paper_1908_00041_b200.plan import PointsPlan
