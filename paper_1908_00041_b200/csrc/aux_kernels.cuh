@@ -319,6 +319,80 @@ __global__ void cg_fwd_kernel(CgFwdArgs a) {
   }
 }
 
+// Tiled forward CG: CTA per (degree l, block of 32 orders |m|).  The F rows it
+// reads (degrees l-1, l, l+1; orders m0-1 .. m0+32, contiguous in the tri
+// layout) are staged in shared memory with coalesced 16-byte loads; thread per
+// (order, field, sign).  Same arithmetic as cg_fwd_kernel (bitwise equal).
+// NF (fields in the group) is a template parameter so that every index
+// division is by a compile-time constant; all indices fit 32 bits.
+constexpr int CGF_THREADS = 256, CGF_MB = 32;
+__host__ __device__ constexpr int cgf_nt(int nf) { return (12 * nf + 7) / 8; }
+__host__ __device__ constexpr int cgf_rs(int nf) { return 4 * cgf_nt(nf) + 1; }  // odd double2 row stride
+template <int NF>
+__global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
+  constexpr int NV = 4 * cgf_nt(NF), RS = cgf_rs(NF), ROWS = CGF_MB + 2;
+  const int l = blockIdx.y;
+  const int m0 = blockIdx.x * CGF_MB;
+  if (m0 > l) return;
+  extern __shared__ __align__(16) double2 cgf_smem[];  // [3][ROWS][RS]
+  constexpr int NE = 3 * ROWS * NV, PER = (NE + CGF_THREADS - 1) / CGF_THREADS;
+  const int Lt = a.L + 1;
+  double2 x[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {  // all loads of the thread in flight before the stores
+    const int e = threadIdx.x + u * CGF_THREADS;
+    x[u] = make_double2(0.0, 0.0);
+    if (e < NE) {
+      const int i = e / (ROWS * NV), r = (e / NV) % ROWS, v = e % NV;
+      const int lp = l - 1 + i, mp = m0 - 1 + r;
+      if (lp >= 0 && lp <= Lt && mp >= 0 && mp <= lp)
+        x[u] = __ldg(reinterpret_cast<const double2*>(a.F) + ((size_t)(lp * (lp + 1) / 2 + mp) * NV + v));
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int e = threadIdx.x + u * CGF_THREADS;
+    if (e < NE) cgf_smem[e / NV * RS + e % NV] = x[u];
+  }
+  __syncthreads();
+  const double is2 = 0.7071067811865475;  // favest/transforms.py:46 (1/np.sqrt(2.0))
+  const int K = (a.L + 1) * (a.L + 1), Kt = (Lt + 1) * (Lt + 1);
+  constexpr int NW = CGF_MB * NF * 2;
+#pragma unroll 1
+  for (int w = threadIdx.x; w < NW; w += CGF_THREADS) {
+    const int mi = w % CGF_MB, b = (w / CGF_MB) % NF, sg = w / (CGF_MB * NF);
+    const int am = m0 + mi;
+    if (am > l || (sg == 1 && am == 0)) continue;
+    const int M = sg ? -am : am;
+    auto tab = [&](int i, int ls, int ms) -> double {
+      if (ls < 0 || ls > Lt || abs(ms) > ls) return 0.0;
+      return __ldg(&a.cgt[i * Kt + ls * ls + ls + ms]);
+    };
+    // staged F^comp_{l+dl, mm}: row |mm| - (m0 - 1); out-of-range rows were staged as 0
+    auto f = [&](int comp, int dl, int mm) -> double2 {
+      return cgf_smem[((dl + 1) * ROWS + abs(mm) - (m0 - 1)) * RS + 6 * b + 2 * comp + (mm < 0 ? 1 : 0)];
+    };
+    const double x1 = tab(0, l - 1, M - 1), x2 = tab(1, l + 1, M - 1);
+    const double x3 = tab(2, l - 1, M + 1), x4 = tab(3, l + 1, M + 1);
+    const double x5 = tab(4, l - 1, M), x6 = tab(5, l + 1, M);
+    const double u1 = tab(6, l, M - 1), u2 = tab(7, l, M), u3 = tab(8, l, M + 1);
+    const double2 fu_a = f(0, -1, M - 1), fu_b = f(0, 1, M - 1);
+    const double2 fv_a = f(1, -1, M + 1), fv_b = f(1, 1, M + 1);
+    const double2 fw_a = f(2, -1, M), fw_b = f(2, 1, M);
+    const double2 fu_c = f(0, 0, M - 1), fv_c = f(1, 0, M + 1);
+    const double2 fw_c = f(2, 0, M);
+    double ar = is2 * (((x1 * fu_a.x + x2 * fu_b.x) + x3 * fv_a.x) + x4 * fv_b.x) + x5 * fw_a.x + x6 * fw_b.x;
+    double ai = is2 * (((x1 * fu_a.y + x2 * fu_b.y) + x3 * fv_a.y) + x4 * fv_b.y) + x5 * fw_a.y + x6 * fw_b.y;
+    const double sr = u1 * fu_c.x + u3 * fv_c.x, si = u1 * fu_c.y + u3 * fv_c.y;
+    double br = is2 * si + u2 * fw_c.y;
+    double bi = -is2 * sr - u2 * fw_c.x;
+    if (l == 0) ar = ai = br = bi = 0.0;  // favest/transforms.py:145-146
+    const size_t o = (size_t)(a.b0 + b) * K + (l * l + l + M);
+    a.A[o] = make_double2(ar, ai);
+    a.Bc[o] = make_double2(br, bi);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // adjoint Clebsch-Gordan: favest/coupling.py:227-239 and transforms.py:168-175.
 // Thread per (table degree l <= L+1, order |m|) and row slot; writes sigma_m * g
@@ -335,7 +409,26 @@ struct CgAdjArgs {
   const long long* rowofs;  // row mode: row offset per order (rows of 12*nfields doubles)
   int L, NT, B_total, b0, nfields, m_begin;
   int rows_mode;            // 0: DMMA fragment tiles (grid path), 1: plain rows (points path)
+  const double* cga;        // cg_adj_tile_kernel: factors in G-row order ((i * 2 + sign) * nrow + row)
+  long long nrow;
 };
+
+// cgt -> G-row order: row (gofs[|m|] + chunk) * 32 + idx holds degree
+// l = |m| + 32 chunk + idx; entry (i, sign) = factor i at (l, +-|m|), zero for
+// l > L+1 and for the duplicate m = 0 sign.
+__global__ void cga_table_kernel(int Lt, const long long* __restrict__ gofs, const double* __restrict__ cgt,
+                                 double* cga, long long nrow) {
+  const int am = blockIdx.y, c = blockIdx.x, idx = threadIdx.x;
+  if (c * 32 >= Lt + 1 - am) return;
+  const long long l = am + 32LL * c + idx;
+  const long long row = (gofs[am] + c) * 32 + idx;
+  const long long Kt = (long long)(Lt + 1) * (Lt + 1);
+  for (int sg = 0; sg < 2; ++sg) {
+    const bool on = l <= Lt && !(sg == 1 && am == 0);
+    const long long k = l * l + l + (sg ? -am : am);
+    for (int i = 0; i < 9; ++i) cga[(i * 2 + sg) * nrow + row] = on ? cgt[i * Kt + k] : 0.0;
+  }
+}
 
 __device__ __forceinline__ double2 c_read(const double2* t, const CgAdjArgs& a, int b, long long l, long long m) {
   if (l < 0 || l > a.L || llabs(m) > l) return make_double2(0.0, 0.0);
@@ -409,6 +502,117 @@ __global__ void cg_adj_kernel(CgAdjArgs a) {
       put(n0 + 4, sig * gy.x); put(n0 + 5, sig * gy.y);
       put(n0 + 8, sig * gz.x); put(n0 + 9, sig * gz.y);
     }
+  }
+}
+
+// Grid-path adjoint CG, tiled: CTA per (order |m|, 32-row chunk) of the DMMA
+// G tiles.  The A / B entries the chunk needs (rows l0-1 .. l0+32, orders
+// +-|m|-1 .. +-|m|+1, all NF fields of the group) are staged in shared memory,
+// the chunk is assembled in shared memory in fragment order (padded blocks,
+// conflict-free stores) and written out as one contiguous block.  The nine
+// factors come from cga (G-row order, coalesced).  Same arithmetic as
+// cg_adj_kernel (bitwise equal results).
+constexpr int CGA_THREADS = 256;
+__host__ __device__ constexpr int cga_bstride(int nf) { return cgf_nt(nf) * 32 + 4; }
+template <int NF>
+__global__ void __launch_bounds__(CGA_THREADS) cg_adj_tile_kernel(CgAdjArgs a) {
+  constexpr int LC = 32, KS = LC / 8, NT = cgf_nt(NF), BS = cga_bstride(NF);
+  constexpr int TILE = 2 * KS * NT * 32;  // doubles
+  static_assert(LC * NF * 2 <= CGA_THREADS, "one (row, field, sign) per thread");
+  const int am = blockIdx.y;
+  const int Lt = a.L + 1;
+  const int c = blockIdx.x;
+  if (c * LC >= Lt + 1 - am) return;
+  const int l0 = am + c * LC;
+  extern __shared__ __align__(16) double cga_smem[];
+  double* Gs = cga_smem;                                           // 2 KS padded blocks
+  double2* As = reinterpret_cast<double2*>(Gs + 2 * KS * BS);      // [NF][34][7] (odd stride)
+  double2* Bs = As + NF * 34 * 7;
+  // this thread's output (row idx, field b, sign sg); its nine factors and
+  // gamma are loaded together with the staging loads (one memory round trip)
+  const int w = threadIdx.x;
+  const int idx = w % LC, b = (w / LC) % NF, sg = w / (LC * NF);
+  const int l = l0 + idx;
+  const bool work = w < LC * NF * 2 && l <= Lt && !(sg == 1 && am == 0);
+  double cfv[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double gam = 0.0;
+  if (work) {
+    const double* cf = a.cga + (a.gofs[am] + c) * 32 + sg * a.nrow + idx;  // coalesced over idx
+#pragma unroll
+    for (int i = 0; i < 9; ++i) cfv[i] = __ldg(cf + 2 * i * a.nrow);
+    gam = a.dg[a.dgofs[am] + (l - am)].y;
+  }
+  constexpr int NE = NF * 34 * 6, PER = (NE + CGA_THREADS - 1) / CGA_THREADS;
+  const int K = (a.L + 1) * (a.L + 1);
+  double2 va[PER], vb[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int e = threadIdx.x + u * CGA_THREADS;
+    va[u] = vb[u] = make_double2(0.0, 0.0);
+    if (e < NE) {
+      const int bb = e / (34 * 6), r = (e / 6) % 34, j = e % 6;
+      const int lp = l0 - 1 + r;
+      const int mp = (j < 3 ? am : -am) + (j % 3) - 1;
+      if (lp >= 0 && lp <= a.L && abs(mp) <= lp) {
+        const size_t o = (size_t)(a.b0 + bb) * K + (lp * lp + lp + mp);
+        va[u] = __ldg(&a.A[o]);
+        vb[u] = __ldg(&a.Bc[o]);
+      }
+    }
+  }
+  for (int i = threadIdx.x; i < 2 * KS * BS; i += CGA_THREADS) Gs[i] = 0.0;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int e = threadIdx.x + u * CGA_THREADS;
+    if (e < NE) {
+      As[e / 6 * 7 + e % 6] = va[u];
+      Bs[e / 6 * 7 + e % 6] = vb[u];
+    }
+  }
+  __syncthreads();
+  if (work) {
+    const double is2 = 0.7071067811865475;
+    const double x1 = cfv[0], x2 = cfv[1], x3 = cfv[2], x4 = cfv[3], x5 = cfv[4], x6 = cfv[5];
+    const double u1 = cfv[6], u2 = cfv[7], u3 = cfv[8];
+    const int m = sg ? -am : am;
+    double sig = (m < 0 && (am & 1)) ? -1.0 : 1.0;  // favest/legendre.py:101-103
+    sig *= gam;                                      // gamma_l (legendre.cuh)
+    // staged entries: row r = l - l0 + 1 (+-1), j = 3 sg + (M' - m + 1)
+    auto at = [&](const double2* t, int dr, int dm) { return t[(b * 34 + idx + 1 + dr) * 7 + 3 * sg + dm + 1]; };
+    const double2 ap1p = at(As, 1, 1), ap1m = at(As, 1, -1), am1p = at(As, -1, 1), am1m = at(As, -1, -1);
+    const double2 ap10 = at(As, 1, 0), am10 = at(As, -1, 0);
+    const double2 bp = at(Bs, 0, 1), bm = at(Bs, 0, -1), b0 = at(Bs, 0, 0);
+    // nu1..nu6, eta1..eta3 (favest/coupling.py:227-239)
+    const double2 nu1 = make_double2(ap1p.x * x1 - ap1m.x * x3, ap1p.y * x1 - ap1m.y * x3);
+    const double2 nu2 = make_double2(am1p.x * x2 - am1m.x * x4, am1p.y * x2 - am1m.y * x4);
+    const double2 s3 = make_double2(ap1p.x * x1 + ap1m.x * x3, ap1p.y * x1 + ap1m.y * x3);
+    const double2 nu3 = make_double2(-s3.y, s3.x);
+    const double2 s4 = make_double2(am1p.x * x2 + am1m.x * x4, am1p.y * x2 + am1m.y * x4);
+    const double2 nu4 = make_double2(-s4.y, s4.x);
+    const double2 nu5 = make_double2(ap10.x * x5, ap10.y * x5);
+    const double2 nu6 = make_double2(am10.x * x6, am10.y * x6);
+    const double2 d1 = make_double2(bp.x * u1 - bm.x * u3, bp.y * u1 - bm.y * u3);
+    const double2 eta1 = make_double2(-d1.y, d1.x);
+    const double2 eta2 = make_double2(bp.x * u1 + bm.x * u3, bp.y * u1 + bm.y * u3);
+    const double2 eta3 = make_double2(-(b0.y * u2), b0.x * u2);
+    // merge (favest/transforms.py:168-175)
+    const double2 gx = make_double2(-is2 * ((nu1.x + nu2.x) + eta1.x), -is2 * ((nu1.y + nu2.y) + eta1.y));
+    const double2 gy = make_double2(-is2 * ((nu3.x + nu4.x) - eta2.x), -is2 * ((nu3.y + nu4.y) - eta2.y));
+    const double2 gz = make_double2((nu5.x + nu6.x) + eta3.x, (nu5.y + nu6.y) + eta3.y);
+    const int par = idx & 1, kk = idx >> 1, ks = kk >> 2, q = kk & 3;
+    double* gb = Gs + (par * KS + ks) * BS + q;
+    auto put = [&](int n, double v) { gb[(n >> 3) * 32 + ((n & 7) << 2)] = v; };
+    const int n0 = 12 * b + 2 * sg;
+    put(n0 + 0, sig * gx.x); put(n0 + 1, sig * gx.y);
+    put(n0 + 4, sig * gy.x); put(n0 + 5, sig * gy.y);
+    put(n0 + 8, sig * gz.x); put(n0 + 9, sig * gz.y);
+  }
+  __syncthreads();
+  double2* dst = reinterpret_cast<double2*>(a.G + (size_t)(a.gofs[am] + c) * TILE);
+  constexpr int BH = NT * 16;  // double2 per block
+  for (int i = threadIdx.x; i < TILE / 2; i += CGA_THREADS) {
+    const int blk = i / BH, o = i - blk * BH;
+    dst[i] = reinterpret_cast<const double2*>(Gs + blk * BS)[o];
   }
 }
 

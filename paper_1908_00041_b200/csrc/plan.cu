@@ -94,6 +94,7 @@ struct fvPlan {
   double2* ab = nullptr;
   long long* abofs = nullptr;
   double* cgt = nullptr;        // Clebsch-Gordan factors xi1..6, mu1..3 (9 x K_t)
+  double* cga = nullptr;        // the same factors in G-row order for the adjoint (9 x 2 signs x 32 g_tiles)
   double2* dg = nullptr;        // block-rescaled recurrence (d, gamma) (grid plans)
   long long* dgofs = nullptr;
   // table mode: plan-time Legendre tiles streamed by TMA instead of the on-the-fly producer
@@ -139,7 +140,7 @@ void free_plan(fvPlan* p) {
   cudaSetDevice(p->device);
   void* ptrs[] = {p->pair_t, p->pair_sin, p->pair_n, p->pair_s, p->ring_w, p->seed_x,
                   p->seed_e, p->start_l,  p->start_v, p->ab,   p->abofs,  p->gofs,
-                  p->dg,     p->dgofs,  p->cgt,     p->ptab_f,  p->mtab_f, p->tofs,   p->ptab_a, p->aofs,
+                  p->dg,     p->dgofs,  p->cgt,     p->cga,     p->ptab_f,  p->mtab_f, p->tofs,   p->ptab_a, p->aofs,
                   p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->G,
                   p->fft_tw};
   for (void* q : ptrs)
@@ -594,6 +595,12 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
   p->g_tiles = gofs[Lt + 1];
   if ((rc = dalloc(&p->gofs, Lt + 1))) return bail(rc);
   cudaMemcpy(p->gofs, gofs.data(), (Lt + 1) * 8, cudaMemcpyHostToDevice);
+  if ((rc = dalloc(&p->cga, (size_t)18 * 32 * p->g_tiles))) return bail(rc);
+  {
+    dim3 grid((Lt + 1 + fv::ADJ_LC - 1) / fv::ADJ_LC, Lt + 1);
+    fv::cga_table_kernel<<<grid, 32>>>(Lt, p->gofs, p->cgt, p->cga, 32 * p->g_tiles);
+    FV_CUDA(cudaGetLastError());
+  }
   if ((rc = setup_fft(p))) return bail(rc);
   // workspaces (field groups of <= 4 -> NT <= 6)
   const int gs = std::min(4, max_batch);
@@ -727,8 +734,14 @@ int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, voi
       StageMark mk(p, 3, s);
       fv::CgFwdArgs ca{p->F, reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), p->cgt, p->L, 8 * NT, B, b0,
                        nf};
-      dim3 grid((p->L + 1 + 127) / 128, p->L + 1);
-      fv::cg_fwd_kernel<<<grid, 128, 0, s>>>(ca);
+      dim3 grid((p->L + 1 + fv::CGF_MB - 1) / fv::CGF_MB, p->L + 1);
+      const size_t smem = (size_t)3 * (fv::CGF_MB + 2) * fv::cgf_rs(nf) * sizeof(double2);
+      switch (nf) {
+        case 1: fv::cg_fwd_tile_kernel<1><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
+        case 2: fv::cg_fwd_tile_kernel<2><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
+        case 3: fv::cg_fwd_tile_kernel<3><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
+        default: fv::cg_fwd_tile_kernel<4><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
+      }
       FV_CUDA(cudaGetLastError());
     }
   }
@@ -749,10 +762,16 @@ int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int 
     {
       StageMark mk(p, 3, s);
       fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), p->dg, p->dgofs,
-                       p->cgt, p->G, p->gofs, nullptr, p->L, NT, B, b0, nf, 0, 0};
-      const int rows = (Lt + 1 + fv::ADJ_LC - 1) / fv::ADJ_LC * fv::ADJ_LC;
-      dim3 grid((rows + 127) / 128, Lt + 1);
-      fv::cg_adj_kernel<<<grid, 128, 0, s>>>(ca);
+                       p->cgt, p->G, p->gofs, nullptr, p->L, NT, B, b0, nf, 0, 0, p->cga, 32 * p->g_tiles};
+      dim3 grid((Lt + 1 + fv::ADJ_LC - 1) / fv::ADJ_LC, Lt + 1);
+      const size_t smem = (size_t)2 * fv::ADJ_KS * fv::cga_bstride(nf) * sizeof(double) +
+                          2 * (size_t)nf * 34 * 7 * sizeof(double2);
+      switch (nf) {
+        case 1: fv::cg_adj_tile_kernel<1><<<grid, fv::CGA_THREADS, smem, s>>>(ca); break;
+        case 2: fv::cg_adj_tile_kernel<2><<<grid, fv::CGA_THREADS, smem, s>>>(ca); break;
+        case 3: fv::cg_adj_tile_kernel<3><<<grid, fv::CGA_THREADS, smem, s>>>(ca); break;
+        default: fv::cg_adj_tile_kernel<4><<<grid, fv::CGA_THREADS, smem, s>>>(ca); break;
+      }
       FV_CUDA(cudaGetLastError());
     }
     {
