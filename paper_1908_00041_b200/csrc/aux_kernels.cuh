@@ -166,12 +166,13 @@ __global__ void ab_kernel(int Lt, const long long* __restrict__ abofs, double2* 
 //   E = w_n C_n + w_s C_s, O = w_n C_n - w_s C_s, times sigma_{-m} for the -m bin,
 // written at X[mi][chunk][par][ks][nt][lane] (B operand fragment order).
 struct FoldArgs {
-  const double2* S;     // [comp][field][ring][n_phi], all B_total fields
+  const double2* S;     // ring spectra, layout lay (common.cuh SLayout)
   double* X;
   const int* pair_n;
   const int* pair_s;
   const double* ring_w;
   int n_phi, n_theta, B_total, b0, nfields, NT, nPpad, nchunks, m_begin, m_count;
+  SLayout lay;
 };
 
 __global__ void fold_fwd_kernel(FoldArgs a) {
@@ -201,10 +202,10 @@ __global__ void fold_fwd_kernel(FoldArgs a) {
       const int bin = sgn ? (a.n_phi - m) % a.n_phi : m;
       const double sig = (sgn == 1 && (m & 1)) ? -1.0 : 1.0;
       double2 Tn[3], Ts[3];
-      for (int k = 0; k < 3; ++k) {
-        const size_t base = ((size_t)k * a.B_total + a.b0 + b) * a.n_theta;
-        Tn[k] = a.S[(base + rn) * a.n_phi + bin];
-        Ts[k] = rs >= 0 ? a.S[(base + rs) * a.n_phi + bin] : make_double2(0.0, 0.0);
+      for (int k = 0; k < 3; ++k) {  // bin-major layout: consecutive pairs -> consecutive rings (coalesced)
+        const double2* base = a.S + k * a.lay.cs + (long long)(a.b0 + b) * a.n_theta * a.lay.rs + bin * a.lay.bs;
+        Tn[k] = base[rn * a.lay.rs];
+        Ts[k] = rs >= 0 ? base[rs * a.lay.rs] : make_double2(0.0, 0.0);
       }
       const double wn = a.ring_w[rn];
       const double ws = rs >= 0 ? a.ring_w[rs] : 0.0;

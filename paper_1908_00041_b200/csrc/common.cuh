@@ -13,6 +13,15 @@
 
 namespace fv {
 
+// Ring-spectrum layout: element (component c, ring R = field * n_theta + t, bin q)
+// lives at c * cs + R * rs + q * bs (units of complex doubles).  Ring-major
+// (rs = n_phi, bs = 1) keeps each ring's FFT contiguous; bin-major (rs = 1,
+// bs = rings) makes one bin row of consecutive rings contiguous for the
+// per-order kernels.  Chosen per direction by the plan.
+struct SLayout {
+  long long cs, rs, bs;
+};
+
 constexpr int XR_SHIFT = 512;  // value = x * 2^e, e a multiple of 512 (oracle/favest_oracle.py)
 
 __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {

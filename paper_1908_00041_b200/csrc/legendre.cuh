@@ -486,12 +486,14 @@ constexpr int ADJ_KS = ADJ_LC / 8;
 constexpr int ADJ_RC = 128;      // ring pairs per CTA (16 M-tiles, one per producer lane)
 constexpr int ADJ_MT = ADJ_RC / 8;
 constexpr int ADJ_STAGES = 4;
-constexpr int ADJ_PTILE = 2 * ADJ_KS * ADJ_MT * 32;  // doubles: [par][ks][Mtile][lane]
+constexpr int ADJ_MTILE = 2 * ADJ_KS * 32;           // doubles per M-tile: [par][ks][lane]
+constexpr int ADJ_PTILE = ADJ_MT * ADJ_MTILE;         // doubles: [Mtile][par][ks][lane] (M-tile major, so
+                                                      // any run of M-tiles is one contiguous bulk copy)
 
 struct AdjArgs {
   const double* G;          // per m: (gofs[m] + lc) * GTILE, [par][ks ADJ_KS][NT][32]
   const long long* gofs;
-  double2* S;               // spectrum [comp][field][ring][n_phi] (all fields)
+  double2* S;               // ring spectra, layout lay (common.cuh SLayout)
   const int* start_l;
   const double2* start_v;
   const double2* dg;
@@ -505,6 +507,9 @@ struct AdjArgs {
   // table mode: P^T stage tiles [aofs[m] + rc * nlc(m) + lc][ADJ_PTILE] (ptab_adj_kernel)
   const double* ptab;
   const long long* aofs;
+  long long* trace;  // optional pipeline timeline of CTA trace_cta (clock64 stamps), normally null
+  int trace_cta;
+  SLayout lay;
 };
 
 template <int NT>
@@ -529,7 +534,7 @@ __device__ __forceinline__ void adj_produce(double* Ps, const double2* dgw, doub
   const int cx = (g >> 2) | ((i & 1) << 1);
   double* bp[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) bp[q] = Ps + i * 32 + (g << 2) + (q ^ cx);
+  for (int q = 0; q < 4; ++q) bp[q] = Ps + i * ADJ_MTILE + (g << 2) + (q ^ cx);
 #pragma unroll
   for (int b0 = 0; b0 < ADJ_LC; b0 += 8) {
     double dd[8];
@@ -540,7 +545,7 @@ __device__ __forceinline__ void adj_produce(double* Ps, const double2* dgw, doub
       const int idx = b0 + k;
       const double v = rec_step<MIXED>(p1, p2, tt, dd[k], l0 + idx, in);
       const int par = idx & 1, kk = idx >> 1, ks = kk >> 2, q = kk & 3;
-      bp[q][(par * ADJ_KS + ks) * ADJ_MT * 32] = v;
+      bp[q][(par * ADJ_KS + ks) * 32] = v;
     }
   }
   p1 *= dgw[ADJ_LC - 1].y;
@@ -670,17 +675,34 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
           abw[lane] = (l <= Lt) ? dgm[l - m] : make_double2(0.0, 1.0);
           __syncwarp();
         }
+        // table mode: each producer warp copies the run of its four M-tiles that
+        // holds a started pair in this stage (polar start, padding pairs) -- the
+        // consumers never read the others
+        uint32_t act = 0;
+        if (table) {
+          const unsigned bal = __ballot_sync(0xffffffffu, in.ls <= l0 + ADJ_LC - 1 && l0 <= Lt);
+#pragma unroll
+          for (int t = 0; t < 4; ++t) act |= ((bal >> (8 * t)) & 0xffu) ? (1u << t) : 0u;
+        }
+        const bool tr = args.trace && blockIdx.x == args.trace_cta && pw == 0 && lane == 0 && sc < 4096;
+        if (tr) args.trace[sc * 8 + 0] = clock64();
         mbar_wait(&empty[stage], (round & 1) ^ 1);
+        if (tr) args.trace[sc * 8 + 1] = clock64();
         double* Ps = smem + stage * SM::STAGE;
         double* Gs = Ps + ADJ_PTILE;
-        if (pw == 0 && lane == 0) {
-          const uint32_t bytes = SM::GTILE * 8 + (table ? ADJ_PTILE * 8 : 0u);
-          asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])), "r"(bytes)
-                       : "memory");
-          bulk_g2s(Gs, Gm + (size_t)lc * SM::GTILE, SM::GTILE * 8, &full[stage]);
-          if (table)
-            bulk_g2s(Ps, args.ptab + (size_t)(args.aofs[m] + (long long)rc * nlc + lc) * ADJ_PTILE,
-                     ADJ_PTILE * 8, &full[stage]);
+        if (lane == 0) {
+          const int lo = act ? __ffs(act) - 1 : 0, hi = act ? 32 - __clz(act) : 0;
+          const uint32_t bytes = (pw == 0 ? SM::GTILE * 8 : 0u) + (uint32_t)(hi - lo) * ADJ_MTILE * 8;
+          if (bytes) {
+            asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])), "r"(bytes)
+                         : "memory");
+            if (pw == 0) bulk_g2s(Gs, Gm + (size_t)lc * SM::GTILE, SM::GTILE * 8, &full[stage]);
+            if (hi > lo)
+              bulk_g2s(Ps + (4 * pw + lo) * ADJ_MTILE,
+                       args.ptab + (size_t)(args.aofs[m] + (long long)rc * nlc + lc) * ADJ_PTILE +
+                           (4 * pw + lo) * ADJ_MTILE,
+                       (uint32_t)(hi - lo) * ADJ_MTILE * 8, &full[stage]);
+          }
         }
         // all-zero warps write nothing: the consumers skip their M-tiles (polar start)
         if (zero || table || (args.dbg & 2)) {
@@ -690,13 +712,17 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
           adj_produce<false>(Ps, abw, tt, p1, p2, i, g, l0, in);
         }
         mbar_arrive(&full[stage]);
+        if (tr) args.trace[sc * 8 + 2] = clock64() | ((long long)item << 40);
       }
     }
     return;
   }
 
   // -------------------------------- consumers --------------------------------
-  // warp (par, mq): M-tiles 4mq..4mq+3 (32 pairs) x all NT n-tiles of parity par
+  // warp (par, mq): M-tiles mq, mq+4, mq+8, mq+12 x all NT n-tiles of parity
+  // par.  The interleave gives every SM sub-partition (warp % 4 == mq) the same
+  // mix of polar and equatorial pairs, so the polar skip shortens the stage
+  // instead of idling one sub-partition's DMMA pipe.
   const int cw = consumer_index(warp);
   const int par = cw >> 2;
   const int mq = cw & 3;
@@ -709,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
     // first degree at which each of the warp's M-tiles has a pair above the polar threshold
     int mt_start[4];
     {
-      int v = args.start_l[(size_t)m * args.nPpad + rc * ADJ_RC + 32 * mq + lane];
+      int v = args.start_l[(size_t)m * args.nPpad + rc * ADJ_RC + 8 * mq + 32 * (lane >> 3) + (lane & 7)];
 #pragma unroll
       for (int o = 1; o < 8; o <<= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
 #pragma unroll
@@ -725,7 +751,10 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
       const int stage = sc % ADJ_STAGES;
       const uint32_t round = sc / ADJ_STAGES;
       const int l0s = m + ADJ_LC * lc;
+      const bool tr = args.trace && blockIdx.x == args.trace_cta && (cw == 0 || cw == 3) && lane == 0 && sc < 4096;
+      if (tr) args.trace[sc * 8 + (cw == 0 ? 3 : 6)] = clock64();
       mbar_wait(&full[stage], round & 1);
+      if (tr && cw == 0) args.trace[sc * 8 + 4] = clock64();
       const double* Ps = smem + stage * SM::STAGE;
       const double* Gs = Ps + ADJ_PTILE;
       const int mts = min(min(mt_start[0], mt_start[1]), min(mt_start[2], mt_start[3]));
@@ -736,8 +765,8 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
         auto load = [&](int ks, int bufi) {
 #pragma unroll
           for (int ii = 0; ii < 4; ++ii) {
-            const int i = 4 * mq + ii;
-            a[bufi][ii] = lds_f64(&Ps[((par * ADJ_KS + ks) * ADJ_MT + i) * 32 + adj_swz(g, q, i)]);
+            const int i = mq + 4 * ii;
+            a[bufi][ii] = lds_f64(&Ps[i * ADJ_MTILE + (par * ADJ_KS + ks) * 32 + adj_swz(g, q, i)]);
           }
 #pragma unroll
           for (int jn = 0; jn < NT; ++jn) b[bufi][jn] = lds_f64(&Gs[((par * ADJ_KS + ks) * NT + jn) * 32 + lane]);
@@ -761,12 +790,16 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
           adj_ks_dmma<NT>(ifirst, acc, a[ks & 1], b[ks & 1]);
         }
       }
+      if (tr) args.trace[sc * 8 + (cw == 0 ? 5 : 7)] = clock64();
       mbar_arrive(&empty[stage]);
     }
+    const bool tre = args.trace && blockIdx.x == args.trace_cta && cw == 0 && lane == 0 && sc <= 1024;
+    if (tre) args.trace[4096 * 8 + (sc - 1) * 4] = clock64();
 
     // epilogue: combine parities through the exchange buffer (odd warps publish,
     // even warps finish); the first barrier also retires the previous item's reads
     asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps));
+    if (tre) args.trace[4096 * 8 + (sc - 1) * 4 + 1] = clock64();
     if (par == 1) {
 #pragma unroll
       for (int ii = 0; ii < 4; ++ii)
@@ -778,30 +811,44 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
         }
     }
     asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps));
-    if (par == 0 && rc * ADJ_RC + 32 * mq < args.nP) {
+    if (tre) args.trace[4096 * 8 + (sc - 1) * 4 + 2] = clock64();
+    if (par == 0 && rc * ADJ_RC + 8 * mq < args.nP && !(args.dbg & 4)) {
+      // per-lane column targets first (the column -> (field, comp, sign) map and
+      // the bin row depend only on jn and q), ring indices next, then only
+      // stores (bin-major layout: lanes g are 8 consecutive pairs -> 8 consecutive
+      // north (south) rings, i.e. 128-byte runs of one bin row)
+      const int bin1 = (args.n_phi - m) % args.n_phi;
+      double2* dst[NT];
+      bool ok[NT];
+#pragma unroll
+      for (int jn = 0; jn < NT; ++jn) {
+        const int ser = 4 * jn + q;  // 6*field + 2*comp + sign
+        const int b = ser / 6, comp = (ser % 6) >> 1, sgn = ser & 1;
+        ok[jn] = b < args.nfields && !(sgn == 1 && m == 0);
+        dst[jn] = args.S + comp * args.lay.cs + (long long)(args.b0 + b) * args.n_theta * args.lay.rs +
+                  (sgn ? bin1 : m) * args.lay.bs;
+      }
+      int rn[4], rs[4];
 #pragma unroll
       for (int ii = 0; ii < 4; ++ii) {
-        const int rho = (4 * mq + ii) * 8 + g;
-        const int p = rc * ADJ_RC + rho;
-        const int rn = args.pair_n[p];
-        const int rs = args.pair_s[p];
-        if (rn < 0) continue;
+        const int p = rc * ADJ_RC + (mq + 4 * ii) * 8 + g;
+        rn[ii] = args.pair_n[p];
+        rs[ii] = args.pair_s[p];
+      }
+#pragma unroll
+      for (int ii = 0; ii < 4; ++ii) {
+        if (rn[ii] < 0) continue;
 #pragma unroll
         for (int jn = 0; jn < NT; ++jn) {
-          const double* d = xch + ((size_t)((mq * 4 + ii) * NT + jn) * 32 + lane) * 2;
-          const int ser = (jn * 8 + 2 * q) >> 1;  // 6*field + 2*comp + sign
-          const int b = ser / 6, comp = (ser % 6) >> 1, sgn = ser & 1;
-          if (b >= args.nfields) continue;
-          if (sgn == 1 && m == 0) continue;
-          const int bin = sgn ? (args.n_phi - m) % args.n_phi : m;
+          if (!ok[jn]) continue;
+          const double2 o = *reinterpret_cast<const double2*>(xch + ((size_t)((mq * 4 + ii) * NT + jn) * 32 + lane) * 2);
           const double er = acc[ii][jn][0], ei = acc[ii][jn][1];
-          const double orr = d[0], oi = d[1];
-          const size_t base = ((size_t)comp * args.B_total + args.b0 + b) * args.n_theta;
-          args.S[(base + rn) * args.n_phi + bin] = make_double2(er + orr, ei + oi);
-          if (rs >= 0) args.S[(base + rs) * args.n_phi + bin] = make_double2(er - orr, ei - oi);
+          dst[jn][rn[ii] * args.lay.rs] = make_double2(er + o.x, ei + o.y);
+          if (rs[ii] >= 0) dst[jn][rs[ii] * args.lay.rs] = make_double2(er - o.x, ei - o.y);
         }
       }
     }
+    if (tre) args.trace[4096 * 8 + (sc - 1) * 4 + 3] = clock64();
   }
 }
 

@@ -68,7 +68,7 @@ long long* trace_buf() {
   if (trace_cta() < 0) return nullptr;
   if (!g_trace) {
     cudaMalloc(&g_trace, 4096 * 12 * sizeof(long long));
-    cudaMemset(g_trace, 0, 4096 * 12 * sizeof(long long));
+    cudaMemset(g_trace, 0, 4096 * 12 * sizeof(long long));  // forward: 4096 x 8 + CTA records; adjoint: 4096 x 8 + 4096 x 2
   }
   return g_trace;
 }
@@ -81,6 +81,7 @@ struct fvPlan {
   int kind = 0;  // 0 grid, 1 points
   int L = 0, Lt = 0, n_theta = 0, n_phi = 0, nP = 0, nPpad = 0, nchunks = 0, nrc = 0;
   int max_batch = 0, device = 0, paired = 0, num_sms = 148;
+  fv::SLayout lay_f{}, lay_a{};  // ring-spectrum layouts of the forward / adjoint (fixed for any B <= max_batch)
   // grid tables
   double* pair_t = nullptr;
   double* pair_sin = nullptr;
@@ -108,7 +109,7 @@ struct fvPlan {
   long long* rowofs = nullptr;  // row offsets per order (points G layout)
   long long g_tiles = 0;
   // workspaces
-  double2* Sf = nullptr;
+  double2* Sf = nullptr;        // ring spectra [comp][bin][ring of all max_batch fields] (ring fastest)
   double2* Sa = nullptr;
   double* X = nullptr;
   double* F = nullptr;
@@ -282,10 +283,12 @@ int get_ffts(fvPlan* p, int B, cufftHandle* fwd, cufftHandle* inv) {
   if (it == p->ffts.end()) {
     int n = p->n_phi;
     cufftHandle hf, hi;
-    // forward: component c of T [B][N][3] (stride 3) -> S[c][b][ring][q] (contiguous rings)
-    FV_CUFFT(cufftPlanMany(&hf, 1, &n, &n, 3, 3 * n, &n, 1, n, CUFFT_Z2Z, B * p->n_theta));
-    // inverse: S[c][b][ring][q] -> component c of T (stride 3); unnormalised = ifft * n_phi
-    FV_CUFFT(cufftPlanMany(&hi, 1, &n, &n, 1, n, &n, 3, 3 * n, CUFFT_Z2Z, B * p->n_theta));
+    // forward: component c of T [B][N][3] (stride 3) -> spectra in layout lay_f
+    FV_CUFFT(cufftPlanMany(&hf, 1, &n, &n, 3, 3 * n, &n, (int)p->lay_f.bs, (int)p->lay_f.rs, CUFFT_Z2Z,
+                           B * p->n_theta));
+    // inverse: spectra in layout lay_a -> component c of T (stride 3); unnormalised = ifft * n_phi
+    FV_CUFFT(cufftPlanMany(&hi, 1, &n, &n, (int)p->lay_a.bs, (int)p->lay_a.rs, &n, 3, 3 * n, CUFFT_Z2Z,
+                           B * p->n_theta));
     it = p->ffts.emplace(B, std::make_pair(hf, hi)).first;
   }
   *fwd = it->second.first;
@@ -432,17 +435,17 @@ int setup_fft(fvPlan* p) {
   return FV_OK;
 }
 
-// forward: T [B][N][3] (AoS) -> S[c][b][ring][q]; inverse: S -> T
+// forward: T [B][N][3] (AoS) -> spectra (layout lay_f); inverse: spectra (lay_a) -> T
 int ring_fft(fvPlan* p, bool inverse, const double2* in, double2* out, int B, cudaStream_t s) {
   fv::RingFftArgs a{};
-  const long long n = p->n_phi, spec_cs = (long long)B * p->n_theta * n;
+  const long long n = p->n_phi;
   a.in = in;
   a.out = out;
   if (!inverse) {
     a.in_cs = 1; a.in_rs = 3 * n; a.in_es = 3;
-    a.out_cs = spec_cs; a.out_rs = n; a.out_es = 1;
+    a.out_cs = p->lay_f.cs; a.out_rs = p->lay_f.rs; a.out_es = (int)p->lay_f.bs;
   } else {
-    a.in_cs = spec_cs; a.in_rs = n; a.in_es = 1;
+    a.in_cs = p->lay_a.cs; a.in_rs = p->lay_a.rs; a.in_es = (int)p->lay_a.bs;
     a.out_cs = 1; a.out_rs = 3 * n; a.out_es = 3;
   }
   a.tw = p->fft_tw;
@@ -605,6 +608,16 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
   // workspaces (field groups of <= 4 -> NT <= 6)
   const int gs = std::min(4, max_batch);
   const int NTmax = ntiles_for(gs);
+  {
+    // FV_SLAYOUT=<fwd><adj> digits, 0 ring-major / 1 bin-major (default 01: the
+    // forward FFT writes contiguous rings, the adjoint epilogue writes bin rows)
+    const char* sl = std::getenv("FV_SLAYOUT");
+    const bool fbin = sl && sl[0] == '1', abin = !(sl && sl[0] && sl[1] == '0');
+    const long long rings = (long long)max_batch * n_theta;
+    const fv::SLayout ringmajor{rings * n_phi, n_phi, 1}, binmajor{rings * n_phi, 1, rings};
+    p->lay_f = fbin ? binmajor : ringmajor;
+    p->lay_a = abin ? binmajor : ringmajor;
+  }
   const size_t spec = (size_t)3 * max_batch * n_theta * n_phi;
   if ((rc = dalloc(&p->Sf, spec)) || (rc = dalloc(&p->Sa, spec)) ||
       (rc = dalloc(&p->X, (size_t)(Lt + 1) * p->nchunks * (2 * 8 * NTmax * 32))) ||
@@ -697,7 +710,7 @@ int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, voi
     return fail(FV_EINVAL, "batch " + std::to_string(B) + " outside 1.." + std::to_string(p->max_batch));
   if (!T || !a || !b) return fail(FV_EINVAL, "null data pointer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const size_t per_comp = (size_t)B * p->n_theta * p->n_phi;
+  const size_t per_comp = (size_t)p->lay_f.cs;
   if (p->custom_fft) {
     StageMark mk(p, 0, s);
     FV_TRY(ring_fft(p, false, reinterpret_cast<const double2*>(T), p->Sf, B, s));
@@ -719,7 +732,7 @@ int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, voi
     {
       StageMark mk(p, 1, s);
       fv::FoldArgs fa{p->Sf, p->X, p->pair_n, p->pair_s, p->ring_w, p->n_phi, p->n_theta, B, b0, nf, NT,
-                      p->nchunks * fv::FWD_RC, p->nchunks, 0, Lt + 1};
+                      p->nchunks * fv::FWD_RC, p->nchunks, 0, Lt + 1, p->lay_f};
       dim3 grid((p->nchunks * fv::FWD_RC + 127) / 128, Lt + 1, nf + 1);
       fv::fold_fwd_kernel<<<grid, 128, 0, s>>>(fa);
       FV_CUDA(cudaGetLastError());
@@ -778,7 +791,7 @@ int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int 
       StageMark mk(p, 2, s);
       fv::AdjArgs args{p->G, p->gofs, p->Sa, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, p->pair_n,
                        p->pair_s, Lt, p->nP, p->nPpad, p->nrc, p->n_phi, p->n_theta, B, b0, nf, 0, dbg_mode(),
-                       Lt + 1, p->ptab_a, p->aofs};
+                       Lt + 1, p->ptab_a, p->aofs, trace_buf(), trace_cta(), p->lay_a};
       FV_TRY(dispatch_adj(p, NT, args, Lt + 1, s));
     }
   }
@@ -790,7 +803,7 @@ int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int 
     FV_TRY(get_ffts(p, B, &hf, &hi));
     StageMark mk(p, 0, s);
     FV_CUFFT(cufftSetStream(hi, s));
-    const size_t per_comp = (size_t)B * p->n_theta * p->n_phi;
+    const size_t per_comp = (size_t)p->lay_a.cs;
     for (int c = 0; c < 3; ++c) {
       auto* in = reinterpret_cast<cufftDoubleComplex*>(p->Sa + c * per_comp);
       auto* outp = reinterpret_cast<cufftDoubleComplex*>(T) + c;
