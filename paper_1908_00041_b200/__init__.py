@@ -16,11 +16,12 @@ from .core import (
 )
 from .grid import TensorGrid, gen_gl_tensor, gl_grid_for
 from .transforms import PATHS, adjoint_favest, forward_favest, grid_plan, points_plan
+from .pipeline import HostPipeline
 
 __version__ = "0.1.0"
 
 __all__ = [
     "QuadratureRule", "ScalarCoefficients", "TangentFieldSamples", "VectorCoefficients",
     "degrees_orders", "flat_index", "flat_size", "TensorGrid", "gen_gl_tensor", "gl_grid_for",
-    "PATHS", "adjoint_favest", "forward_favest", "grid_plan", "points_plan",
+    "PATHS", "adjoint_favest", "forward_favest", "grid_plan", "points_plan", "HostPipeline",
 ]

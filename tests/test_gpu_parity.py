@@ -253,3 +253,39 @@ def test_api_errors_on_device():
     with pytest.raises(ValueError):
         plan.adjoint(torch.zeros((1, 80), dtype=torch.complex128, device="cuda"),
                      torch.zeros((1, 81), dtype=torch.complex128, device="cuda"))
+
+
+def test_host_pipeline_matches_device_path():
+    """HostPipeline (overlapped pinned-host batches) returns exactly the device path's results."""
+    torch = cuda_or_skip()
+    from paper_1908_00041_b200.pipeline import HostPipeline
+
+    rng = np.random.default_rng(21)
+    L, B = 12, 3
+    th, w, nphi = O.gl_grid(L)
+    plan = _plan(L, th, w, nphi, B=B)
+    A = np.stack([O.coef(rng, L, "inv")[0] for _ in range(B)])
+    Bc = np.stack([O.coef(rng, L, "inv")[1] for _ in range(B)])
+    T = plan.adjoint(_t(A), _t(Bc))
+    fa, fb = plan.forward(T)
+    T2 = plan.adjoint(fa, fb)
+    pipe = HostPipeline(plan, depth=2)
+    Th = torch.empty(T.shape, dtype=T.dtype, pin_memory=True)
+    Th.copy_(T.cpu())
+    outs = [torch.empty_like(Th, pin_memory=True) for _ in range(3)]
+    for o in outs:  # three batches through two slots
+        pipe.submit_roundtrip(Th, o)
+    ah = torch.empty(fa.shape, dtype=fa.dtype, pin_memory=True)
+    bh = torch.empty_like(ah, pin_memory=True)
+    pipe.submit_forward(Th, ah, bh)
+    Tadj = torch.empty_like(Th, pin_memory=True)
+    Ah = torch.from_numpy(A).pin_memory()
+    Bh = torch.from_numpy(Bc).pin_memory()
+    pipe.submit_adjoint(Ah, Bh, Tadj)
+    pipe.synchronize()
+    for o in outs:
+        assert torch.equal(o, T2.cpu())
+    assert torch.equal(ah, fa.cpu()) and torch.equal(bh, fb.cpu())
+    assert torch.equal(Tadj, T.cpu())
+    with pytest.raises(ValueError):
+        pipe.submit_roundtrip(T, outs[0])  # device tensor, not pinned host
