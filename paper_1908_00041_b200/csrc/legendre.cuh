@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
     double2* abw = abw_all + pw * FWD_LB;
     FwdState st{st_p1, st_p2, st_t, st_ls};
     const bool table = args.ptab != nullptr;
+    const uint64_t pol_first = l2_evict_first(), pol_last = l2_evict_last();
     uint32_t tbase = 0;  // tile counter across this CTA's orders
     for (int k = 0;; ++k) {
       const int item = fwd_item(k, blockIdx.x, gridDim.x);
@@ -359,12 +360,14 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
               const uint32_t bytes = SM::XTILE * 8 + (table ? FWD_PTILE * 8 + (uint32_t)sizeof(StageMeta) : 0u);
               asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])), "r"(bytes)
                            : "memory");
-              bulk_g2s(Xs, args.X + ((size_t)(m - args.m_begin) * nchunks + c) * SM::XTILE, SM::XTILE * 8,
-                       &full[stage]);
+              // X chunks are re-read by every l-block of the order: keep them in L2;
+              // the table tiles are read once: let them go first
+              bulk_g2s_hint(Xs, args.X + ((size_t)(m - args.m_begin) * nchunks + c) * SM::XTILE, SM::XTILE * 8,
+                            &full[stage], pol_last);
               if (table) {
                 const long long tile = args.tofs[m] + tl;
-                bulk_g2s(Ps, args.ptab + tile * FWD_PTILE, FWD_PTILE * 8, &full[stage]);
-                bulk_g2s(&meta[stage], args.mtab + tile, sizeof(StageMeta), &full[stage]);
+                bulk_g2s_hint(Ps, args.ptab + tile * FWD_PTILE, FWD_PTILE * 8, &full[stage], pol_first);
+                bulk_g2s_hint(&meta[stage], args.mtab + tile, sizeof(StageMeta), &full[stage], pol_first);
               }
             }
             if (!table && !(args.dbg & 2)) fwd_compute(args, st, tc, Ps, abw, m, j, nlb, p, l0, lane);
@@ -645,6 +648,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
     const int rho = 32 * pw + lane;            // pair within the item's chunk
     const int i = rho >> 3, g = rho & 7;
     const bool table = args.ptab != nullptr;
+    const uint64_t pol_first = l2_evict_first(), pol_last = l2_evict_last();
     uint32_t sc = 0;                           // stage counter across items
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
       const int m = args.m_begin + item / args.nrc;
@@ -696,12 +700,13 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
           if (bytes) {
             asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[stage])), "r"(bytes)
                          : "memory");
-            if (pw == 0) bulk_g2s(Gs, Gm + (size_t)lc * SM::GTILE, SM::GTILE * 8, &full[stage]);
+            // G tiles are shared by the order's ring chunks (kept in L2), table tiles are read once
+            if (pw == 0) bulk_g2s_hint(Gs, Gm + (size_t)lc * SM::GTILE, SM::GTILE * 8, &full[stage], pol_last);
             if (hi > lo)
-              bulk_g2s(Ps + (4 * pw + lo) * ADJ_MTILE,
-                       args.ptab + (size_t)(args.aofs[m] + (long long)rc * nlc + lc) * ADJ_PTILE +
-                           (4 * pw + lo) * ADJ_MTILE,
-                       (uint32_t)(hi - lo) * ADJ_MTILE * 8, &full[stage]);
+              bulk_g2s_hint(Ps + (4 * pw + lo) * ADJ_MTILE,
+                            args.ptab + (size_t)(args.aofs[m] + (long long)rc * nlc + lc) * ADJ_PTILE +
+                                (4 * pw + lo) * ADJ_MTILE,
+                            (uint32_t)(hi - lo) * ADJ_MTILE * 8, &full[stage], pol_first);
           }
         }
         // all-zero warps write nothing: the consumers skip their M-tiles (polar start)
