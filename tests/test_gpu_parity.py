@@ -135,6 +135,37 @@ def test_c3_headline_spot_orders():
     torch.cuda.synchronize()
 
 
+def test_c4_l4096_spot_orders_and_roundtrip():
+    """BASELINE configs[3] (L=4096, one field, (1+l)^-2 spectrum, seed 4) on one GPU: on-the-fly
+    Legendre producer (the tables exceed the plan budget), cuFFT ring FFTs (8196 = 4*3*683).
+    Spot orders against the extended-range oracle, plus the adjoint -> forward round trip."""
+    torch = cuda_or_skip()
+    L = 4096
+    th, w, nphi = O.gl_grid(L)
+    rng = np.random.default_rng(4)
+    A, Bc = O.coef(rng, L, "pow2")
+    plan = _plan(L, th, w, nphi, 1)
+    T = plan.adjoint(_t(A[None]), _t(Bc[None]))
+    orders = [0, 1, 999, 2048, 4000, 4096, 4097]
+    spec = torch.fft.fft(T[0].reshape(L + 2, nphi, 3), dim=1).div_(nphi)
+    bins = sorted({m % nphi for m in orders} | {(-m) % nphi for m in orders})
+    spec = spec[:, bins].cpu().numpy()
+    ref = O.vsht_adjoint_grid(A, Bc, L, th, nphi, orders=orders, spectrum=True)
+    assert O.rel_l2(spec, ref[:, bins]) <= TOL
+    fa, fb_ = plan.forward(T)
+    ls, ms = O.degrees_orders(L)
+    out_orders = [0, 1, 999, 2048, 4000, 4096]
+    sel = np.isin(np.abs(ms), out_orders)
+    Tn = T[0].cpu().numpy()
+    del T
+    ra, rb = O.vsht_forward_grid(Tn, th, w, nphi, L, orders=out_orders)
+    got = np.concatenate([fa[0].cpu().numpy()[sel], fb_[0].cpu().numpy()[sel]])
+    assert O.rel_l2(got, np.concatenate([ra[sel], rb[sel]])) <= TOL
+    err = O.rel_l2(np.concatenate([fa[0].cpu().numpy(), fb_[0].cpu().numpy()]), np.concatenate([A, Bc]))
+    assert err <= 1e-9  # scipy GL weights at n=4098 bound the round trip, not the kernels
+    torch.cuda.synchronize()
+
+
 def test_linearity_determinism_and_batch_consistency():
     L = 48
     th, w, nphi = O.gl_grid(L)

@@ -68,3 +68,29 @@ if __name__ == "__main__":
     if "b256" in what: batch_check(256, 4, 2)
     if "t" in what:
         timing(256, 16); timing(1024, 4)
+
+def c4_timing(reps=3):
+    L = 4096
+    th, w, nphi = O.gl_grid(L)
+    t0 = time.time()
+    plan = GridPlan(L, th, w, nphi, max_batch=1)
+    torch.cuda.synchronize()
+    print("C4 plan", time.time() - t0, "s", flush=True)
+    rng = np.random.default_rng(4)
+    A, Bc = O.coef(rng, L, "pow2")
+    A = torch.from_numpy(A[None]).cuda(); Bc = torch.from_numpy(Bc[None]).cuda()
+    T = plan.adjoint(A, Bc); plan.forward(T); torch.cuda.synchronize()
+    plan.set_profiling(True)
+    for name, fn in (("fwd", lambda: plan.forward(T)), ("adj", lambda: plan.adjoint(A, Bc))):
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        before = plan.stage_ms()
+        e0.record()
+        for _ in range(reps): fn()
+        e1.record(); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        after = plan.stage_ms()
+        st = {k: (after[k] - before[k]) / reps for k in after}
+        print(f"C4 L=4096 B=1 {name}: {ms:.3f} ms  stages {st}", flush=True)
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "c4":
+    c4_timing()
