@@ -90,6 +90,39 @@ int fv_adjoint_points(fvPlan* plan, const double* xyz, long long M, const double
                       double* T, int B, void* stream);
 
 /*
+ * Order-sharded building blocks (ring-sharded fields,
+ * m-sharded contraction, one all-to-all transpose per direction; the Python
+ * driver is paper_1908_00041_b200/dist.py).  Together they are exactly
+ * fv_forward_grid / fv_adjoint_grid split at the transpose:
+ *   fv_forward_grid  = fv_ring_fft(forward) ; fv_forward_orders(all orders)
+ *   fv_adjoint_grid  = fv_adjoint_orders(all orders) ; fv_ring_fft(inverse)
+ *
+ * Spectra: element (component c, ring R, bin j) at c*cs + R*rs + j*bs complex
+ * units, R = field * n_theta + ring over ALL rings of the plan's grid.  nbins = 0:
+ * natural DFT bins (order m at bin m, -m at (n_phi - m) % n_phi); nbins > 0:
+ * compact bins holding orders bin_lo .. bin_lo + nbins - 1 (+m at m - bin_lo,
+ * -m at nbins + m - bin_lo).
+ */
+
+/* 3 x nrings ring DFTs of length n_phi (favest/scalar.py:149 forward, :178
+ * inverse unnormalised); element (c, ring, q) at c*cs + ring*rs + q*es. */
+int fv_ring_fft(fvPlan* plan, int inverse, const double* in, long long in_cs, long long in_rs, long long in_es,
+                double* out, long long out_cs, long long out_rs, long long out_es, int nrings, void* stream);
+
+/* Forward contraction for Legendre orders [m_lo, m_hi) and CG assembly of the
+ * coefficient orders [c_lo, c_hi) (favest/scalar.py:150-154 restricted to those
+ * orders, favest/transforms.py:120-146); entries of a, b for other orders are
+ * not touched.  Needs m_lo <= c_lo - 1 (or c_lo = 0 = m_lo) and c_hi <= m_hi - 1. */
+int fv_forward_orders(fvPlan* plan, const double* S, long long cs, long long rs, long long bs, int bin_lo, int nbins,
+                      double* a, double* b, int B, int m_lo, int m_hi, int c_lo, int c_hi, void* stream);
+
+/* Adjoint coupling + synthesis of orders [m_lo, m_hi) into the spectra
+ * (favest/coupling.py:227-239, favest/scalar.py:170-177 restricted to those
+ * orders); reads a, b at orders m_lo - 1 .. m_hi. */
+int fv_adjoint_orders(fvPlan* plan, const double* a, const double* b, int B, int m_lo, int m_hi, double* S,
+                      long long cs, long long rs, long long bs, int bin_lo, int nbins, void* stream);
+
+/*
  * Stage timing (milliseconds, CUDA events recorded on each call's stream):
  * fv_set_profiling(plan, 1) starts accumulating over all following calls,
  * fv_stage_ms sums one stage (0 fft, 1 fold, 2 legendre, 3 cg) and the number

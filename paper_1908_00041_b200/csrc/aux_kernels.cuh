@@ -199,7 +199,7 @@ __global__ void fold_fwd_kernel(FoldArgs a) {
     if (rn < 0 || (sgn == 1 && m == 0)) {
       for (int c = 0; c < 3; ++c) E[c] = O[c] = make_double2(0.0, 0.0);
     } else {
-      const int bin = sgn ? (a.n_phi - m) % a.n_phi : m;
+      const long long bin = spec_bin(a.lay, m, sgn, a.n_phi);
       const double sig = (sgn == 1 && (m & 1)) ? -1.0 : 1.0;
       double2 Tn[3], Ts[3];
       for (int k = 0; k < 3; ++k) {  // bin-major layout: consecutive pairs -> consecutive rings (coalesced)
@@ -266,6 +266,7 @@ struct CgFwdArgs {
   double2* Bc;          // (B_total, K) curl coefficients
   const double* cgt;    // cg_table_kernel: 9 x K_t (xi1..6, mu1..3)
   int L, ncolF, B_total, b0, nfields;
+  int c_lo, c_hi;       // orders |m| written: [c_lo, c_hi) (F rows of c_lo-1 .. c_hi must be current)
 };
 
 __device__ __forceinline__ double2 f_read(const CgFwdArgs& a, int b, int comp, long long l, long long m) {
@@ -363,7 +364,7 @@ __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
   for (int w = threadIdx.x; w < NW; w += CGF_THREADS) {
     const int mi = w % CGF_MB, b = (w / CGF_MB) % NF, sg = w / (CGF_MB * NF);
     const int am = m0 + mi;
-    if (am > l || (sg == 1 && am == 0)) continue;
+    if (am > l || (sg == 1 && am == 0) || am < a.c_lo || am >= a.c_hi) continue;
     const int M = sg ? -am : am;
     auto tab = [&](int i, int ls, int ms) -> double {
       if (ls < 0 || ls > Lt || abs(ms) > ls) return 0.0;
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(CGA_THREADS) cg_adj_tile_kernel(CgAdjArgs a) {
   constexpr int LC = 32, KS = LC / 8, NT = cgf_nt(NF), BS = cga_bstride(NF);
   constexpr int TILE = 2 * KS * NT * 32;  // doubles
   static_assert(LC * NF * 2 <= CGA_THREADS, "one (row, field, sign) per thread");
-  const int am = blockIdx.y;
+  const int am = a.m_begin + blockIdx.y;
   const int Lt = a.L + 1;
   const int c = blockIdx.x;
   if (c * LC >= Lt + 1 - am) return;

@@ -18,9 +18,18 @@ namespace fv {
 // (rs = n_phi, bs = 1) keeps each ring's FFT contiguous; bin-major (rs = 1,
 // bs = rings) makes one bin row of consecutive rings contiguous for the
 // per-order kernels.  Chosen per direction by the plan.
+// Compact bins (order-sharded spectra, nbins > 0): only the orders
+// bin_lo .. bin_lo + nbins - 1 are held, +m at bin m - bin_lo, -m at
+// nbins + m - bin_lo.  nbins == 0: natural DFT bins (m, (n_phi - m) % n_phi).
 struct SLayout {
   long long cs, rs, bs;
+  int bin_lo, nbins;
 };
+
+__device__ __forceinline__ long long spec_bin(const SLayout& l, int m, int sgn, int n_phi) {
+  if (l.nbins == 0) return sgn ? (n_phi - m) % n_phi : m;
+  return (sgn ? l.nbins : 0) + (m - l.bin_lo);
+}
 
 constexpr int XR_SHIFT = 512;  // value = x * 2^e, e a multiple of 512 (oracle/favest_oracle.py)
 

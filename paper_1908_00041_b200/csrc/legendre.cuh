@@ -822,7 +822,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
       // the bin row depend only on jn and q), ring indices next, then only
       // stores (bin-major layout: lanes g are 8 consecutive pairs -> 8 consecutive
       // north (south) rings, i.e. 128-byte runs of one bin row)
-      const int bin1 = (args.n_phi - m) % args.n_phi;
+      const long long bin0 = spec_bin(args.lay, m, 0, args.n_phi), bin1 = spec_bin(args.lay, m, 1, args.n_phi);
       double2* dst[NT];
       bool ok[NT];
 #pragma unroll
@@ -831,7 +831,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
         const int b = ser / 6, comp = (ser % 6) >> 1, sgn = ser & 1;
         ok[jn] = b < args.nfields && !(sgn == 1 && m == 0);
         dst[jn] = args.S + comp * args.lay.cs + (long long)(args.b0 + b) * args.n_theta * args.lay.rs +
-                  (sgn ? bin1 : m) * args.lay.bs;
+                  (sgn ? bin1 : bin0) * args.lay.bs;
       }
       int rn[4], rs[4];
 #pragma unroll

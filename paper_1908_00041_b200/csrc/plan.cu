@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <string>
 #include <utility>
 #include <vector>
@@ -114,7 +115,7 @@ struct fvPlan {
   double* X = nullptr;
   double* F = nullptr;
   double* G = nullptr;
-  std::map<int, std::pair<cufftHandle, cufftHandle>> ffts;
+  std::map<std::tuple<long long, long long, long long, long long, int>, cufftHandle> ffts;  // strided cuFFT plans
   // hand-written ring FFT (fft.cuh) when every prime factor of n_phi is <= 19
   bool custom_fft = false;
   int fft_nst = 0;
@@ -146,10 +147,7 @@ void free_plan(fvPlan* p) {
                   p->fft_tw};
   for (void* q : ptrs)
     if (q) cudaFree(q);
-  for (auto& kv : p->ffts) {
-    cufftDestroy(kv.second.first);
-    cufftDestroy(kv.second.second);
-  }
+  for (auto& kv : p->ffts) cufftDestroy(kv.second);
   for (auto e : p->ev_pool) cudaEventDestroy(e);
   delete p;
 }
@@ -278,21 +276,18 @@ struct StageMark {
   }
 };
 
-int get_ffts(fvPlan* p, int B, cufftHandle* fwd, cufftHandle* inv) {
-  auto it = p->ffts.find(B);
+// cuFFT fallback (lengths with a prime factor > 19): one strided batched plan per
+// (strides, ring count), cached in the plan; components are separate executions
+int get_fft_strided(fvPlan* p, long long irs, long long ies, long long ors, long long oes, int nrings, cufftHandle* h) {
+  const auto key = std::make_tuple(irs, ies, ors, oes, nrings);
+  auto it = p->ffts.find(key);
   if (it == p->ffts.end()) {
     int n = p->n_phi;
-    cufftHandle hf, hi;
-    // forward: component c of T [B][N][3] (stride 3) -> spectra in layout lay_f
-    FV_CUFFT(cufftPlanMany(&hf, 1, &n, &n, 3, 3 * n, &n, (int)p->lay_f.bs, (int)p->lay_f.rs, CUFFT_Z2Z,
-                           B * p->n_theta));
-    // inverse: spectra in layout lay_a -> component c of T (stride 3); unnormalised = ifft * n_phi
-    FV_CUFFT(cufftPlanMany(&hi, 1, &n, &n, (int)p->lay_a.bs, (int)p->lay_a.rs, &n, 3, 3 * n, CUFFT_Z2Z,
-                           B * p->n_theta));
-    it = p->ffts.emplace(B, std::make_pair(hf, hi)).first;
+    cufftHandle hh;
+    FV_CUFFT(cufftPlanMany(&hh, 1, &n, &n, (int)ies, (int)irs, &n, (int)oes, (int)ors, CUFFT_Z2Z, nrings));
+    it = p->ffts.emplace(key, hh).first;
   }
-  *fwd = it->second.first;
-  *inv = it->second.second;
+  *h = it->second;
   return FV_OK;
 }
 
@@ -435,19 +430,15 @@ int setup_fft(fvPlan* p) {
   return FV_OK;
 }
 
-// forward: T [B][N][3] (AoS) -> spectra (layout lay_f); inverse: spectra (lay_a) -> T
-int ring_fft(fvPlan* p, bool inverse, const double2* in, double2* out, int B, cudaStream_t s) {
+// 3 components x nrings ring DFTs with the hand-written kernel; element (c, ring, q) at
+// c * cs + ring * rs + q * es (complex units) on both sides
+int ring_fft_raw(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
+                 double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s) {
   fv::RingFftArgs a{};
-  const long long n = p->n_phi;
   a.in = in;
   a.out = out;
-  if (!inverse) {
-    a.in_cs = 1; a.in_rs = 3 * n; a.in_es = 3;
-    a.out_cs = p->lay_f.cs; a.out_rs = p->lay_f.rs; a.out_es = (int)p->lay_f.bs;
-  } else {
-    a.in_cs = p->lay_a.cs; a.in_rs = p->lay_a.rs; a.in_es = (int)p->lay_a.bs;
-    a.out_cs = 1; a.out_rs = 3 * n; a.out_es = 3;
-  }
+  a.in_cs = in_cs; a.in_rs = in_rs; a.in_es = (int)in_es;
+  a.out_cs = out_cs; a.out_rs = out_rs; a.out_es = (int)out_es;
   a.tw = p->fft_tw;
   a.n = p->n_phi;
   a.nst = p->fft_nst;
@@ -459,9 +450,9 @@ int ring_fft(fvPlan* p, bool inverse, const double2* in, double2* out, int B, cu
     a.tstride[i] = p->n_phi / (ns * p->fft_radix[i]);
     ns *= p->fft_radix[i];
   }
-  a.nrings = B * p->n_theta;
+  a.nrings = nrings;
   const int grid = std::min(3 * a.nrings, 2 * p->num_sms);
-  const size_t smem = (3 * (size_t)n + fv::FFT_TWN) * sizeof(double2);
+  const size_t smem = (3 * (size_t)p->n_phi + fv::FFT_TWN) * sizeof(double2);
   if (inverse) fv::ring_fft_kernel<true><<<grid, fv::FFT_THREADS, smem, s>>>(a);
   else fv::ring_fft_kernel<false><<<grid, fv::FFT_THREADS, smem, s>>>(a);
   FV_CUDA(cudaGetLastError());
@@ -703,51 +694,45 @@ int fv_stage_count(const fvPlan* p, int stage) {
   return n;
 }
 
-int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, void* stream) {
+namespace {
+
+int check_grid_call(fvPlan* p, int B, const void* x, const void* y, const void* z) {
   FV_TRY(begin_call(p));
   if (p->kind != 0) return fail(FV_EINVAL, "fast-scalar path requires a rule with tensor-grid structure");
   if (B < 1 || B > p->max_batch)
     return fail(FV_EINVAL, "batch " + std::to_string(B) + " outside 1.." + std::to_string(p->max_batch));
-  if (!T || !a || !b) return fail(FV_EINVAL, "null data pointer");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const size_t per_comp = (size_t)p->lay_f.cs;
-  if (p->custom_fft) {
-    StageMark mk(p, 0, s);
-    FV_TRY(ring_fft(p, false, reinterpret_cast<const double2*>(T), p->Sf, B, s));
-  } else {
-    cufftHandle hf, hi;
-    FV_TRY(get_ffts(p, B, &hf, &hi));
-    StageMark mk(p, 0, s);
-    FV_CUFFT(cufftSetStream(hf, s));
-    for (int c = 0; c < 3; ++c) {
-      auto* in = reinterpret_cast<cufftDoubleComplex*>(const_cast<double*>(T)) + c;
-      auto* outp = reinterpret_cast<cufftDoubleComplex*>(p->Sf + c * per_comp);
-      FV_CUFFT(cufftExecZ2Z(hf, in, outp, CUFFT_FORWARD));
-    }
-  }
+  if (!x || !y || !z) return fail(FV_EINVAL, "null data pointer");
+  return FV_OK;
+}
+
+// fold + Legendre over orders [m_lo, m_hi) and CG for orders [c_lo, c_hi), reading the
+// spectra of every ring of the grid in layout `lay` (natural or compact bins)
+int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* a, double* b, int B, int m_lo,
+                   int m_hi, int c_lo, int c_hi, cudaStream_t s) {
   const int Lt = p->Lt;
+  const int mc = m_hi - m_lo;
   for (int b0 = 0; b0 < B; b0 += 4) {
     const int nf = std::min(4, B - b0);
     const int NT = ntiles_for(nf);
     {
       StageMark mk(p, 1, s);
-      fv::FoldArgs fa{p->Sf, p->X, p->pair_n, p->pair_s, p->ring_w, p->n_phi, p->n_theta, B, b0, nf, NT,
-                      p->nchunks * fv::FWD_RC, p->nchunks, 0, Lt + 1, p->lay_f};
-      dim3 grid((p->nchunks * fv::FWD_RC + 127) / 128, Lt + 1, nf + 1);
+      fv::FoldArgs fa{S, p->X, p->pair_n, p->pair_s, p->ring_w, p->n_phi, p->n_theta, B, b0, nf, NT,
+                      p->nchunks * fv::FWD_RC, p->nchunks, m_lo, mc, lay};
+      dim3 grid((p->nchunks * fv::FWD_RC + 127) / 128, mc, nf + 1);
       fv::fold_fwd_kernel<<<grid, 128, 0, s>>>(fa);
       FV_CUDA(cudaGetLastError());
     }
     {
       StageMark mk(p, 2, s);
-      fv::FwdArgs args{p->X, p->F, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, Lt, p->nP, p->nPpad, p->nchunks, 0, dbg_mode(), Lt + 1, trace_buf(),
-                       trace_cta(), p->ptab_f, p->mtab_f, p->tofs};
-      FV_TRY(dispatch_fwd(p, NT, args, Lt + 1, s));
+      fv::FwdArgs args{p->X, p->F, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, Lt, p->nP, p->nPpad,
+                       p->nchunks, m_lo, dbg_mode(), mc, trace_buf(), trace_cta(), p->ptab_f, p->mtab_f, p->tofs};
+      FV_TRY(dispatch_fwd(p, NT, args, mc, s));
     }
-    {
+    if (c_hi > c_lo) {
       StageMark mk(p, 3, s);
       fv::CgFwdArgs ca{p->F, reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), p->cgt, p->L, 8 * NT, B, b0,
-                       nf};
-      dim3 grid((p->L + 1 + fv::CGF_MB - 1) / fv::CGF_MB, p->L + 1);
+                       nf, c_lo, c_hi};
+      dim3 grid((c_hi + fv::CGF_MB - 1) / fv::CGF_MB, p->L + 1);
       const size_t smem = (size_t)3 * (fv::CGF_MB + 2) * fv::cgf_rs(nf) * sizeof(double2);
       switch (nf) {
         case 1: fv::cg_fwd_tile_kernel<1><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
@@ -761,22 +746,19 @@ int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, voi
   return FV_OK;
 }
 
-int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int B, void* stream) {
-  FV_TRY(begin_call(p));
-  if (p->kind != 0) return fail(FV_EINVAL, "fast-scalar path requires a rule with tensor-grid structure");
-  if (B < 1 || B > p->max_batch)
-    return fail(FV_EINVAL, "batch " + std::to_string(B) + " outside 1.." + std::to_string(p->max_batch));
-  if (!T || !a || !b) return fail(FV_EINVAL, "null data pointer");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+// CG + Legendre synthesis for orders [m_lo, m_hi) into spectra of every ring (layout `lay`)
+int adjoint_orders(fvPlan* p, const double* a, const double* b, double2* S, const fv::SLayout& lay, int B, int m_lo,
+                   int m_hi, cudaStream_t s) {
   const int Lt = p->Lt;
+  const int mc = m_hi - m_lo;
   for (int b0 = 0; b0 < B; b0 += 4) {
     const int nf = std::min(4, B - b0);
     const int NT = ntiles_for(nf);
     {
       StageMark mk(p, 3, s);
       fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), p->dg, p->dgofs,
-                       p->cgt, p->G, p->gofs, nullptr, p->L, NT, B, b0, nf, 0, 0, p->cga, 32 * p->g_tiles};
-      dim3 grid((Lt + 1 + fv::ADJ_LC - 1) / fv::ADJ_LC, Lt + 1);
+                       p->cgt, p->G, p->gofs, nullptr, p->L, NT, B, b0, nf, m_lo, 0, p->cga, 32 * p->g_tiles};
+      dim3 grid((Lt + 1 - m_lo + fv::ADJ_LC - 1) / fv::ADJ_LC, mc);
       const size_t smem = (size_t)2 * fv::ADJ_KS * fv::cga_bstride(nf) * sizeof(double) +
                           2 * (size_t)nf * 34 * 7 * sizeof(double2);
       switch (nf) {
@@ -789,28 +771,95 @@ int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int 
     }
     {
       StageMark mk(p, 2, s);
-      fv::AdjArgs args{p->G, p->gofs, p->Sa, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, p->pair_n,
-                       p->pair_s, Lt, p->nP, p->nPpad, p->nrc, p->n_phi, p->n_theta, B, b0, nf, 0, dbg_mode(),
-                       Lt + 1, p->ptab_a, p->aofs, trace_buf(), trace_cta(), p->lay_a};
-      FV_TRY(dispatch_adj(p, NT, args, Lt + 1, s));
-    }
-  }
-  if (p->custom_fft) {
-    StageMark mk(p, 0, s);
-    FV_TRY(ring_fft(p, true, p->Sa, reinterpret_cast<double2*>(T), B, s));
-  } else {
-    cufftHandle hf, hi;
-    FV_TRY(get_ffts(p, B, &hf, &hi));
-    StageMark mk(p, 0, s);
-    FV_CUFFT(cufftSetStream(hi, s));
-    const size_t per_comp = (size_t)p->lay_a.cs;
-    for (int c = 0; c < 3; ++c) {
-      auto* in = reinterpret_cast<cufftDoubleComplex*>(p->Sa + c * per_comp);
-      auto* outp = reinterpret_cast<cufftDoubleComplex*>(T) + c;
-      FV_CUFFT(cufftExecZ2Z(hi, in, outp, CUFFT_INVERSE));
+      fv::AdjArgs args{p->G, p->gofs, S, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, p->pair_n,
+                       p->pair_s, Lt, p->nP, p->nPpad, p->nrc, p->n_phi, p->n_theta, B, b0, nf, m_lo, dbg_mode(),
+                       mc, p->ptab_a, p->aofs, trace_buf(), trace_cta(), lay};
+      FV_TRY(dispatch_adj(p, NT, args, mc, s));
     }
   }
   return FV_OK;
+}
+
+// three components x nrings ring DFTs of length n_phi, arbitrary strides (complex units)
+int ring_ffts(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
+              double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s) {
+  StageMark mk(p, 0, s);
+  if (p->custom_fft) return ring_fft_raw(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
+  cufftHandle h;
+  FV_TRY(get_fft_strided(p, in_rs, in_es, out_rs, out_es, nrings, &h));
+  FV_CUFFT(cufftSetStream(h, s));
+  for (int c = 0; c < 3; ++c) {
+    auto* i = reinterpret_cast<cufftDoubleComplex*>(const_cast<double2*>(in)) + c * in_cs;
+    auto* o = reinterpret_cast<cufftDoubleComplex*>(out) + c * out_cs;
+    FV_CUFFT(cufftExecZ2Z(h, i, o, inverse ? CUFFT_INVERSE : CUFFT_FORWARD));
+  }
+  return FV_OK;
+}
+
+}  // namespace
+
+int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, void* stream) {
+  FV_TRY(check_grid_call(p, B, T, a, b));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const long long n = p->n_phi;
+  FV_TRY(ring_ffts(p, false, reinterpret_cast<const double2*>(T), 1, 3 * n, 3, p->Sf, p->lay_f.cs, p->lay_f.rs,
+                   p->lay_f.bs, B * p->n_theta, s));
+  return forward_orders(p, p->Sf, p->lay_f, a, b, B, 0, p->Lt + 1, 0, p->L + 1, s);
+}
+
+int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int B, void* stream) {
+  FV_TRY(check_grid_call(p, B, T, a, b));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  FV_TRY(adjoint_orders(p, a, b, p->Sa, p->lay_a, B, 0, p->Lt + 1, s));
+  const long long n = p->n_phi;
+  return ring_ffts(p, true, p->Sa, p->lay_a.cs, p->lay_a.rs, p->lay_a.bs, reinterpret_cast<double2*>(T), 1, 3 * n, 3,
+                   B * p->n_theta, s);
+}
+
+// ---- order-sharded building blocks (paper_1908_00041_b200/dist.py) ----
+int fv_ring_fft(fvPlan* p, int inverse, const double* in, long long in_cs, long long in_rs, long long in_es,
+                double* out, long long out_cs, long long out_rs, long long out_es, int nrings, void* stream) {
+  FV_TRY(begin_call(p));
+  if (p->kind != 0) return fail(FV_EINVAL, "fast-scalar path requires a rule with tensor-grid structure");
+  if (!in || !out) return fail(FV_EINVAL, "null data pointer");
+  if (nrings < 0) return fail(FV_EINVAL, "negative ring count");
+  if (nrings == 0) return FV_OK;
+  return ring_ffts(p, inverse != 0, reinterpret_cast<const double2*>(in), in_cs, in_rs, in_es,
+                   reinterpret_cast<double2*>(out), out_cs, out_rs, out_es, nrings,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+namespace {
+int check_orders(fvPlan* p, long long rs, long long bs, int bin_lo, int nbins, int m_lo, int m_hi) {
+  if (m_lo < 0 || m_hi > p->Lt + 1 || m_lo >= m_hi)
+    return fail(FV_EINVAL, "order range [" + std::to_string(m_lo) + ", " + std::to_string(m_hi) + ") outside 0.." +
+                               std::to_string(p->Lt));
+  if (nbins < 0 || (nbins > 0 && (m_lo < bin_lo || m_hi > bin_lo + nbins)))
+    return fail(FV_EINVAL, "compact bins do not cover the order range");
+  if (rs <= 0 || bs <= 0) return fail(FV_EINVAL, "spectrum strides must be positive");
+  return FV_OK;
+}
+}  // namespace
+
+int fv_forward_orders(fvPlan* p, const double* S, long long cs, long long rs, long long bs, int bin_lo, int nbins,
+                      double* a, double* b, int B, int m_lo, int m_hi, int c_lo, int c_hi, void* stream) {
+  FV_TRY(check_grid_call(p, B, S, a, b));
+  FV_TRY(check_orders(p, rs, bs, bin_lo, nbins, m_lo, m_hi));
+  if (c_lo < 0 || c_hi > p->L + 1 || c_lo > c_hi) return fail(FV_EINVAL, "coefficient order range invalid");
+  if (c_hi > c_lo && ((c_lo > 0 && c_lo - 1 < m_lo) || c_hi > m_hi - 1 || (c_lo == 0 && m_lo > 0)))
+    return fail(FV_EINVAL, "coefficient orders need the Legendre orders c_lo-1 .. c_hi");
+  const fv::SLayout lay{cs, rs, bs, bin_lo, nbins};
+  return forward_orders(p, reinterpret_cast<const double2*>(S), lay, a, b, B, m_lo, m_hi, c_lo, c_hi,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+int fv_adjoint_orders(fvPlan* p, const double* a, const double* b, int B, int m_lo, int m_hi, double* S, long long cs,
+                      long long rs, long long bs, int bin_lo, int nbins, void* stream) {
+  FV_TRY(check_grid_call(p, B, S, a, b));
+  FV_TRY(check_orders(p, rs, bs, bin_lo, nbins, m_lo, m_hi));
+  const fv::SLayout lay{cs, rs, bs, bin_lo, nbins};
+  return adjoint_orders(p, a, b, reinterpret_cast<double2*>(S), lay, B, m_lo, m_hi,
+                        reinterpret_cast<cudaStream_t>(stream));
 }
 
 int fv_adjoint_points(fvPlan* p, const double* xyz, long long M, const double* a, const double* b, double* T,

@@ -1,0 +1,370 @@
+"""Order-sharded VSHT across GPUs (the C4 layout).
+
+Each rank owns a contiguous block of rings of the grid (its slice of every
+field) and a contiguous range of orders m, chosen so that the per-order
+Legendre work (∝ Lt+1−m) is balanced.  One transpose per direction:
+
+forward
+  1. local ring FFTs of the owned rings (``fv_ring_fft``);
+  2. all-to-all: bins ±m of every order owner h needs (its orders plus a
+     two-order halo) go to h, so h holds all rings at its orders;
+  3. ``fv_forward_orders``: fold + Legendre contraction + CG for h's orders
+     and the one-order halo either side that the adjoint's coupling reads.
+     a, b come back full-size with those orders filled (m-sharded).
+
+adjoint (input: a, b with the owner's orders ±1 valid — the forward's output,
+or full tables)
+  1. ``fv_adjoint_orders``: coupling + synthesis of the owned orders into
+     compact spectra of every ring;
+  2. all-to-all: every ring block goes back to its owner;
+  3. local inverse ring FFTs → the owned rings of T.
+
+``gather_coefficients`` turns m-sharded a, b into full tables on every rank
+(entries are disjoint: an all-reduce of zero-masked tables is exact).
+
+The transport is ``torch.distributed.all_to_all_single`` (NCCL on GPUs, one
+process per GPU); ``simulate_forward`` / ``simulate_adjoint`` drive several
+ranks' plans in one process with local copies in place of the collective
+(used to check the sharded path against the single-plan path on one GPU —
+nothing in it waits on another rank's kernels).  The per-rank arithmetic is
+the same kernels on the same values as ``GridPlan.forward/adjoint``, so the
+sharded results are bitwise identical to the unsharded ones.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from .shard import order_work
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+# ---------------------------------------------------------------------------
+# partition (host logic; gloo-tested)
+# ---------------------------------------------------------------------------
+def ring_blocks(n_theta: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous ring ranges [r0, r1) per rank, sizes differing by at most one."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    base, extra = divmod(n_theta, world)
+    out, r = [], 0
+    for k in range(world):
+        n = base + (1 if k < extra else 0)
+        out.append((r, r + n))
+        r += n
+    return out
+
+
+def order_ranges(Lt: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous order ranges [m0, m1) over 0..Lt with balanced Legendre work.
+
+    Work of order m is Lt+1−m degrees (plus one unit for its FFT bins / fold);
+    the cut points are placed at the cumulative-work quantiles.  Every rank gets
+    at least one order when world <= Lt+1.
+    """
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    n = Lt + 1
+    if world > n:
+        raise ValueError(f"{world} ranks for {n} orders")
+    w = [order_work(Lt, m) + 1 for m in range(n)]
+    total = float(sum(w))
+    cuts, acc, k = [0], 0.0, 1
+    for m in range(n):
+        acc += w[m]
+        while k < world and acc >= total * k / world:
+            cuts.append(m + 1)
+            k += 1
+    while len(cuts) < world:
+        cuts.append(n)
+    cuts.append(n)
+    # at least one order each (monotone repair from the right)
+    for i in range(world - 1, 0, -1):
+        cuts[i] = min(cuts[i], cuts[i + 1] - 1)
+    for i in range(1, world):
+        cuts[i] = max(cuts[i], cuts[i - 1] + 1)
+    return [(cuts[i], cuts[i + 1]) for i in range(world)]
+
+
+@dataclass(frozen=True)
+class RankLayout:
+    """What rank h owns and needs (orders are scalar orders 0..Lt)."""
+
+    rings: tuple[int, int]        # owned rings [r0, r1)
+    orders: tuple[int, int]       # owned orders [m0, m1): adjoint synthesis, gathered coefficients
+    coef: tuple[int, int]         # forward CG orders [c0, c1): owned ∩ 0..L, plus one halo order each side
+    legendre: tuple[int, int]     # forward Legendre orders [l0, l1) feeding coef (one more each side)
+
+
+def rank_layouts(n_theta: int, L: int, world: int) -> list[RankLayout]:
+    Lt = L + 1
+    rb = ring_blocks(n_theta, world)
+    ob = order_ranges(Lt, world)
+    out = []
+    for h in range(world):
+        m0, m1 = ob[h]
+        c0, c1 = max(0, m0 - 1), min(L + 1, m1 + 1)  # the synthesis of m0..m1-1 reads orders m0-1..m1
+        l0, l1 = max(0, c0 - 1), min(Lt + 1, c1 + 1)  # CG of order c reads F at c-1..c+1 (|-1| = 1)
+        out.append(RankLayout(rb[h], (m0, m1), (c0, c1), (l0, l1)))
+    return out
+
+
+def natural_bins(m0: int, m1: int, n_phi: int):
+    """(compact index, natural DFT bin) pairs of orders [m0, m1): +m then −m,
+    the −0 duplicate of m = 0 left out."""
+    nb = m1 - m0
+    pos = [(m - m0, m) for m in range(m0, m1)]
+    neg = [(nb + m - m0, (n_phi - m) % n_phi) for m in range(m0, m1) if m != 0]
+    return pos + neg
+
+
+# ---------------------------------------------------------------------------
+# kernels (C ABI) — a backend object so that tests can substitute a reference
+# ---------------------------------------------------------------------------
+class CudaStages:
+    """The four sharded building blocks on one GridPlan (``fv_ring_fft``,
+    ``fv_forward_orders``, ``fv_adjoint_orders``)."""
+
+    def __init__(self, plan):
+        from . import _lib
+
+        self.plan = plan
+        self.lib = plan.lib
+        self._check = _lib.check
+
+    def _stream(self):
+        torch = _torch()
+        return torch.cuda.current_stream(self.plan.device).cuda_stream
+
+    # spectra views: (3, B, rings, bins) slices of max-batch buffers, inner dims contiguous
+    def fft_fields(self, T_local, S_loc):
+        """T_local (B, nloc*n_phi, 3) -> S_loc (3, B, nloc, n_phi) ring spectra."""
+        n = self.plan.n_phi
+        B, nloc = S_loc.shape[1], S_loc.shape[2]
+        torch = _torch()
+        with torch.cuda.device(self.plan.device):
+            self._check(self.lib.fv_ring_fft(self.plan._h, 0, T_local.data_ptr(), 1, 3 * n, 3, S_loc.data_ptr(),
+                                             S_loc.stride(0), n, 1, B * nloc, self._stream()))
+
+    def ifft_fields(self, S_loc, T_local):
+        n = self.plan.n_phi
+        B, nloc = S_loc.shape[1], S_loc.shape[2]
+        torch = _torch()
+        with torch.cuda.device(self.plan.device):
+            self._check(self.lib.fv_ring_fft(self.plan._h, 1, S_loc.data_ptr(), S_loc.stride(0), n, 1,
+                                             T_local.data_ptr(), 1, 3 * n, 3, B * nloc, self._stream()))
+
+    def forward_orders(self, S_own, bin_lo, nb, a, b, legendre, coef):
+        """S_own (3, B, n_theta, 2*nb) compact spectra of all rings -> a, b at orders coef."""
+        B, nth = S_own.shape[1], S_own.shape[2]
+        torch = _torch()
+        with torch.cuda.device(self.plan.device):
+            self._check(self.lib.fv_forward_orders(
+                self.plan._h, S_own.data_ptr(), S_own.stride(0), 2 * nb, 1, bin_lo, nb, a.data_ptr(), b.data_ptr(),
+                B, legendre[0], legendre[1], coef[0], coef[1], self._stream()))
+
+    def adjoint_orders(self, a, b, orders, S_own):
+        """a, b (orders ±1 valid) -> S_own (3, B, n_theta, 2*nb) compact spectra of orders."""
+        B, nth, nb = S_own.shape[1], S_own.shape[2], S_own.shape[3] // 2
+        torch = _torch()
+        with torch.cuda.device(self.plan.device):
+            self._check(self.lib.fv_adjoint_orders(
+                self.plan._h, a.data_ptr(), b.data_ptr(), B, orders[0], orders[1], S_own.data_ptr(),
+                S_own.stride(0), 2 * nb, 1, orders[0], nb, self._stream()))
+
+
+# ---------------------------------------------------------------------------
+# per-rank plan
+# ---------------------------------------------------------------------------
+class OrderShardedPlan:
+    """Rank ``rank`` of ``world`` in the order-sharded transform of B fields.
+
+    ``stages`` performs the kernels (``CudaStages(GridPlan)`` in production);
+    ``n_theta``, ``n_phi``, ``L`` describe the grid; tensors are allocated on
+    ``device`` with ``max_batch`` fields.
+    """
+
+    def __init__(self, stages, L, n_theta, n_phi, max_batch, rank, world, device, group=None):
+        torch = _torch()
+        if not 0 <= rank < world:
+            raise ValueError(f"bad rank {rank} of {world}")
+        self.stages = stages
+        self.L, self.Lt = int(L), int(L) + 1
+        self.n_theta, self.n_phi = int(n_theta), int(n_phi)
+        self.max_batch = int(max_batch)
+        self.rank, self.world = int(rank), int(world)
+        self.device = torch.device(device)
+        self.group = group
+        self.layouts = rank_layouts(self.n_theta, self.L, self.world)
+        me = self.layouts[self.rank]
+        self.me = me
+        self.nloc = me.rings[1] - me.rings[0]
+        self.K = (self.L + 1) ** 2
+        c128 = torch.complex128
+        B, n = self.max_batch, self.n_phi
+        # local ring spectra: forward FFT output, and the adjoint's inverse-FFT input whose
+        # bins no rank owns (n_phi > 2 Lt + 1) must stay zero — hence two buffers
+        self.S_loc = torch.empty((3, B, self.nloc, n), dtype=c128, device=self.device)
+        self.S_loc_a = torch.zeros((3, B, self.nloc, n), dtype=c128, device=self.device)
+        # forward: compact bins of the Legendre orders; adjoint: compact bins of the owned orders
+        nbf = me.legendre[1] - me.legendre[0]
+        nba = me.orders[1] - me.orders[0]
+        self.S_fwd = torch.zeros((3, B, self.n_theta, 2 * nbf), dtype=c128, device=self.device)
+        self.S_adj = torch.zeros((3, B, self.n_theta, 2 * nba), dtype=c128, device=self.device)
+        # index tensors for the transposes
+        self._send_bins = []  # forward: natural bins destination h needs (its Legendre orders)
+        for h in range(self.world):
+            lo, hi = self.layouts[h].legendre
+            idx = list(range(lo, hi)) + [(n - m) % n for m in range(lo, hi)]
+            self._send_bins.append(torch.tensor(idx, dtype=torch.long, device=self.device))
+        self._recv_bins = []  # adjoint: (compact index, natural bin) of owner h's orders
+        for h in range(self.world):
+            m0, m1 = self.layouts[h].orders
+            pairs = natural_bins(m0, m1, n)
+            self._recv_bins.append((torch.tensor([p[0] for p in pairs], dtype=torch.long, device=self.device),
+                                    torch.tensor([p[1] for p in pairs], dtype=torch.long, device=self.device)))
+
+    # ---- transport -------------------------------------------------------
+    def _all_to_all(self, sends, out_splits):
+        """sends[h]: contiguous complex tensor for rank h; out_splits[g]: float64 count from rank g."""
+        torch = _torch()
+        import torch.distributed as dist
+
+        flat_in = torch.cat([torch.view_as_real(s).reshape(-1) for s in sends])
+        in_splits = [s.numel() * 2 for s in sends]
+        flat_out = torch.empty(sum(out_splits), dtype=torch.float64, device=self.device)
+        dist.all_to_all_single(flat_out, flat_in, out_splits, in_splits, group=self.group)
+        outs, o = [], 0
+        for k in out_splits:
+            outs.append(torch.view_as_complex(flat_out[o:o + k].view(-1, 2)))
+            o += k
+        return outs
+
+    # ---- forward ---------------------------------------------------------
+    def forward_send(self, T_local):
+        """Local FFTs, then the per-destination blocks (3, B, nloc, 2*nb_h)."""
+        B = int(T_local.shape[0])
+        S = self.S_loc[:, :B]
+        self.stages.fft_fields(T_local, S)
+        return [S.index_select(3, self._send_bins[h]).contiguous() for h in range(self.world)]
+
+    def forward_recv_sizes(self, B):
+        nb = self.me.legendre[1] - self.me.legendre[0]
+        return [3 * B * (l.rings[1] - l.rings[0]) * 2 * nb * 2 for l in self.layouts]
+
+    def forward_finish(self, recvs, B, a, b):
+        nb = self.me.legendre[1] - self.me.legendre[0]
+        S = self.S_fwd[:, :B]
+        for g, r in enumerate(recvs):
+            r0, r1 = self.layouts[g].rings
+            S[:, :, r0:r1, :] = r.view(3, B, r1 - r0, 2 * nb)
+        self.stages.forward_orders(S, self.me.legendre[0], nb, a, b, self.me.legendre, self.me.coef)
+        return a, b
+
+    def forward(self, T_local, a=None, b=None):
+        """T_local (B, nloc*n_phi, 3) -> a, b (B, (L+1)^2), valid at this rank's coef orders."""
+        torch = _torch()
+        B = int(T_local.shape[0])
+        if a is None:
+            a = torch.zeros((B, self.K), dtype=torch.complex128, device=self.device)
+        if b is None:
+            b = torch.zeros((B, self.K), dtype=torch.complex128, device=self.device)
+        sends = self.forward_send(T_local)
+        recvs = self._all_to_all(sends, self.forward_recv_sizes(B))
+        return self.forward_finish(recvs, B, a, b)
+
+    # ---- adjoint ---------------------------------------------------------
+    def adjoint_send(self, a, b):
+        B = int(a.shape[0])
+        S = self.S_adj[:, :B]
+        self.stages.adjoint_orders(a, b, self.me.orders, S)
+        return [S[:, :, l.rings[0]:l.rings[1], :].contiguous() for l in self.layouts]
+
+    def adjoint_recv_sizes(self, B):
+        return [3 * B * self.nloc * 2 * (l.orders[1] - l.orders[0]) * 2 for l in self.layouts]
+
+    def adjoint_finish(self, recvs, B, T_local):
+        S = self.S_loc_a[:, :B]
+        for h, r in enumerate(recvs):
+            nb = self.layouts[h].orders[1] - self.layouts[h].orders[0]
+            blk = r.view(3, B, self.nloc, 2 * nb)
+            ci, nat = self._recv_bins[h]
+            S.index_copy_(3, nat, blk.index_select(3, ci))
+        self.stages.ifft_fields(S, T_local)
+        return T_local
+
+    def adjoint(self, a, b, T_local=None):
+        """a, b (B, (L+1)^2) with this rank's orders ±1 valid -> T_local (B, nloc*n_phi, 3)."""
+        torch = _torch()
+        B = int(a.shape[0])
+        if T_local is None:
+            T_local = torch.empty((B, self.nloc * self.n_phi, 3), dtype=torch.complex128, device=self.device)
+        sends = self.adjoint_send(a, b)
+        recvs = self._all_to_all(sends, self.adjoint_recv_sizes(B))
+        return self.adjoint_finish(recvs, B, T_local)
+
+    # ---- coefficients ------------------------------------------------------
+    def order_mask(self, orders=None):
+        """Boolean (K,) mask of the flat entries l*l+l+m with |m| in ``orders`` (default: owned)."""
+        torch = _torch()
+        m0, m1 = orders or self.me.orders
+        k = torch.arange(self.K, device=self.device)
+        l = torch.sqrt(k.to(torch.float64)).floor().to(torch.long)
+        m = (k - l * l - l).abs()
+        return (m >= m0) & (m < m1)
+
+    def gather_coefficients(self, a, b):
+        """m-sharded a, b -> full tables on every rank (disjoint entries, exact all-reduce)."""
+        torch = _torch()
+        import torch.distributed as dist
+
+        mask = self.order_mask()
+        out = []
+        for x in (a, b):
+            y = torch.where(mask, x, torch.zeros((), dtype=x.dtype, device=x.device))
+            yr = torch.view_as_real(y).contiguous()
+            dist.all_reduce(yr, group=self.group)
+            out.append(torch.view_as_complex(yr))
+        return out[0], out[1]
+
+
+def make_plan(L, grid, max_batch, rank, world, device=None, group=None):
+    """Production constructor: one GridPlan on this rank's GPU + its shard layout."""
+    from .plan import GridPlan
+
+    plan = GridPlan.from_grid(grid, L, max_batch=max_batch, device=device)
+    return OrderShardedPlan(CudaStages(plan), L, grid.n_theta, grid.n_phi, max_batch, rank, world,
+                            plan.device, group)
+
+
+# ---------------------------------------------------------------------------
+# in-process simulation of several ranks (checks, one device)
+# ---------------------------------------------------------------------------
+def simulate_forward(plans, T_locals):
+    torch = _torch()
+    B = int(T_locals[0].shape[0])
+    sends = [p.forward_send(T) for p, T in zip(plans, T_locals)]
+    outs = []
+    for h, p in enumerate(plans):
+        recvs = [sends[g][h] for g in range(len(plans))]
+        a = torch.zeros((B, p.K), dtype=torch.complex128, device=p.device)
+        b = torch.zeros_like(a)
+        outs.append(p.forward_finish(recvs, B, a, b))
+    return outs
+
+
+def simulate_adjoint(plans, ab):
+    torch = _torch()
+    B = int(ab[0][0].shape[0])
+    sends = [p.adjoint_send(a, b) for p, (a, b) in zip(plans, ab)]
+    outs = []
+    for g, p in enumerate(plans):
+        recvs = [sends[h][g] for h in range(len(plans))]
+        T = torch.empty((B, p.nloc * p.n_phi, 3), dtype=torch.complex128, device=p.device)
+        outs.append(p.adjoint_finish(recvs, B, T))
+    return outs

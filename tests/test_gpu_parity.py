@@ -320,3 +320,53 @@ def test_host_pipeline_matches_device_path():
     assert torch.equal(Tadj, T.cpu())
     with pytest.raises(ValueError):
         pipe.submit_roundtrip(T, outs[0])  # device tensor, not pinned host
+
+
+@pytest.mark.parametrize("L,world", [(40, 1), (40, 2), (40, 3), (21, 2)])
+def test_order_sharded_path_matches_single_plan(L, world):
+    """The order-sharded building blocks (fv_ring_fft / fv_forward_orders / fv_adjoint_orders,
+    dist.py) with ranks simulated in one process reproduce GridPlan.forward/adjoint; with the
+    hand-written FFT (n_phi = 84) bitwise, with the cuFFT fallback (n_phi = 46) to rounding."""
+    torch = cuda_or_skip()
+    from paper_1908_00041_b200.dist import CudaStages, OrderShardedPlan, simulate_adjoint, simulate_forward
+
+    rng = np.random.default_rng(L + world)
+    B, maxB = 3, 4
+    th, w, nphi = O.gl_grid(L)
+    nth = len(th)
+    plan = _plan(L, th, w, nphi, B=maxB)
+    A = np.stack([O.coef(rng, L, "inv")[0] for _ in range(B)])
+    Bc = np.stack([O.coef(rng, L, "inv")[1] for _ in range(B)])
+    T = plan.adjoint(_t(A), _t(Bc))
+    T = T + _t(np.stack([O.tangent_noise(rng, O.grid_points(th, nphi), 0.1) for _ in range(B)]))
+    a_ref, b_ref = plan.forward(T)
+    T_ref = plan.adjoint(a_ref, b_ref)
+    plans = [OrderShardedPlan(CudaStages(plan), L, nth, nphi, maxB, r, world, plan.device) for r in range(world)]
+    T4 = T.view(B, nth, nphi, 3)
+    Tl = [T4[:, p.me.rings[0]:p.me.rings[1]].reshape(B, -1, 3).contiguous() for p in plans]
+    outs = simulate_forward(plans, Tl)
+    exact = nphi == 84
+    for p, (a, b) in zip(plans, outs):
+        sel = p.order_mask(p.me.coef)
+        for x, ref in ((a, a_ref), (b, b_ref)):
+            if exact:
+                assert torch.equal(x[:, sel], ref[:, sel])
+            else:
+                assert O.rel_l2(x[:, sel].cpu().numpy(), ref[:, sel].cpu().numpy()) <= 1e-14
+    Tout = simulate_adjoint(plans, outs)
+    Tfull = torch.cat([t.view(B, -1, nphi, 3) for t in Tout], 1).reshape(B, -1, 3)
+    if exact:
+        assert torch.equal(Tfull, T_ref)
+    else:
+        assert O.rel_l2(Tfull.cpu().numpy(), T_ref.cpu().numpy()) <= 1e-14
+    with pytest.raises(ValueError):
+        plans[0].stages.lib and _lib_check_bad_orders(plan)
+
+
+def _lib_check_bad_orders(plan):
+    import ctypes
+
+    from paper_1908_00041_b200 import _lib
+
+    buf = ctypes.c_void_p(1)
+    _lib.check(plan.lib.fv_forward_orders(plan._h, buf, 1, 1, 1, 0, 0, buf, buf, 1, 5, 3, 0, 0, None))
