@@ -419,6 +419,91 @@ def run_ours(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------------------
+# C4: one L=4096 field, order-sharded over the ranks (strong scaling)
+# ---------------------------------------------------------------------------
+def run_c4(args, rank, world, local_rank):
+    """BASELINE configs[3]: L=4096, one field, forward + adjoint per step, order-sharded
+    across the N ranks (paper_1908_00041_b200/dist.py: ring-sharded field, m-sharded
+    contraction, one NCCL all-to-all per direction)."""
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    os.environ.setdefault("RANK", str(rank))
+    os.environ.setdefault("WORLD_SIZE", str(world))
+    dist.init_process_group("nccl", device_id=dev)
+    import oracle.favest_oracle as O
+    from paper_1908_00041_b200.dist import make_plan
+    from paper_1908_00041_b200.grid import gl_grid_for
+
+    L = args.L if args.L != 1024 else 4096
+    grid, _ = gl_grid_for(L)
+    sp = make_plan(L, grid, 1, rank, world, dev)
+    rng = np.random.default_rng(4)
+    A, Bc = O.coef(rng, L, "pow2")
+    a_full = torch.from_numpy(A[None]).to(dev)
+    b_full = torch.from_numpy(Bc[None]).to(dev)
+    T_local = sp.adjoint(a_full, b_full)  # this rank's rings of adjoint(coefficients)
+    a = torch.zeros_like(a_full)
+    b = torch.zeros_like(b_full)
+    Tout = torch.empty_like(T_local)
+
+    def step():
+        sp.forward(T_local, a, b)
+        sp.adjoint(a, b, Tout)
+
+    def barrier():
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    stream = torch.cuda.current_stream(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clocks:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+    # parity guard on the timed outputs: adjoint(forward(adjoint(c))) vs adjoint(c) on this rank's rings
+    rel = float(torch.linalg.vector_norm(Tout - T_local) / torch.linalg.vector_norm(T_local))
+    rel = max_over_ranks(rel)
+    fl = canonical_flops(L, 1)
+    if rank == 0:
+        lay = sp.me
+        line = {
+            "metric": "fp64 forward+adjoint VSHT pairs/sec at L=4096 (order-sharded)",
+            "value": 1.0 / (ms / 1e3), "unit": "fields/s (forward+adjoint per field)", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C4 (BASELINE configs[3]): L=4096 Gauss-Legendre 4098x8196 grid, one field, "
+                                   "forward then adjoint per step, order-sharded", "L": L, "global_batch": 1,
+                       "parallelism": f"order-sharded x{world} (NCCL all-to-all per direction)",
+                       "rank0_rings": list(lay.rings), "rank0_orders": list(lay.orders)},
+            "clocks": clocks.summary(),
+            "detail": {"canonical_gflop_per_direction": fl["total"] / 1e9,
+                       "fraction_of_fp64_roofline_datasheet": (2 * fl["total"] / (ms / 1e3)) / (FP64_PEAK_DATASHEET * 1e12),
+                       "roundtrip_rel_l2": rel},
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--gpus", type=int, default=1)
@@ -430,12 +515,16 @@ def main():
     ap.add_argument("--ref-every", type=int, default=8, help="order stride of the CPU sample")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="c3", choices=["c3", "c4"],
+                    help="c3: batch-sharded L=1024 (the headline); c4: one L=4096 field, order-sharded")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.workload == "c4":
+        run_c4(args, rank, world, local_rank)
     else:
         run_ours(args, rank, world, local_rank)
 
