@@ -3,10 +3,13 @@
 //   seeds_kernel      Pbar_m^m(t_p) for every order and ring pair, extended
 //                     range (favest/legendre.py:60-65)
 //   ab_kernel         recurrence coefficients a_lm, b_lm (favest/legendre.py:70-71)
-//   fold_fwd_kernel   ring spectra -> folded, weighted U/V/W combos in DMMA
-//                     fragment order (favest/transforms.py:109-112,
-//                     favest/scalar.py:149-152)
-//   cg_fwd_kernel     F^U, F^V, F^W -> a_lm, b_lm (favest/transforms.py:120-146)
+//   fold_fwd_kernel   ring spectra -> folded, weighted Cartesian components in
+//                     DMMA fragment order (favest/scalar.py:149-152); used by
+//                     the order-sharded path, the grid path fuses it into the
+//                     FFT (fft2.cuh fft_fold_kernel)
+//   cg_fwd_kernel     F^x, F^y, F^z -> combos F^U, F^V, F^W
+//                     (favest/transforms.py:109-112, applied after the linear
+//                     scalar transform) -> a_lm, b_lm (favest/transforms.py:120-146)
 //   cg_adj_kernel     a_lm, b_lm -> merged g^X, g^Y, g^Z in fragment order
 //                     (favest/coupling.py:200-240, favest/transforms.py:165-175)
 #pragma once
@@ -161,10 +164,15 @@ __global__ void ab_kernel(int Lt, const long long* __restrict__ abofs, double2* 
   ab[abofs[m] + (l - m - 2)] = make_double2(a, a * b);  // FMA-form recurrence (legendre.cuh)
 }
 
-// Forward fold.  Thread per (local order mi, pair p, field b):
-//   C_n = combo of the three Cartesian ring spectra at bin +-m of the north ring,
-//   E = w_n C_n + w_s C_s, O = w_n C_n - w_s C_s, times sigma_{-m} for the -m bin,
-// written at X[mi][chunk][par][ks][nt][lane] (B operand fragment order).
+// Forward fold.  Thread per (local order mi, pair p, field b, component c):
+//   E = w_n S_n + w_s S_s, O = w_n S_n - w_s S_s of the Cartesian ring spectra
+//   at bins +m and -m (times sigma_{-m} on the -m bin), written as the four
+//   columns 12 b + 4 c + (2 sign + re/im) of X[mi][chunk][par][ks][nt][k 4][n 8]
+//   (B operand tiles; the consumer lane (k = lane & 3, n = lane >> 2) reads
+//   k * 8 + n), one aligned 32-byte sector per parity.  The U/V/W combos of
+//   favest/transforms.py:112 are formed after the (linear) scalar transform, in
+//   the CG stage.  blockIdx.z == 3 nfields zeroes the padding columns.  The
+//   grid path fuses this into the ring FFT (fft2.cuh fft_fold_kernel).
 struct FoldArgs {
   const double2* S;     // ring spectra, layout lay (common.cuh SLayout)
   double* X;
@@ -178,64 +186,49 @@ struct FoldArgs {
 __global__ void fold_fwd_kernel(FoldArgs a) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   const int mi = blockIdx.y;
-  const int b = blockIdx.z;  // 0..nfields (== nfields: padding columns)
+  const int z = blockIdx.z;  // 3 b + c, or 3 nfields: padding columns
   if (p >= a.nPpad) return;
   const int m = a.m_begin + mi;
   const int chunk = p >> 5, ks = (p >> 2) & 7, q = p & 3;
-  const size_t xbase = ((size_t)mi * a.nchunks + chunk) * (2 * 8 * a.NT * 32);
-  auto put = [&](int par, int n, double v) {
-    a.X[xbase + ((size_t)(par * 8 + ks) * a.NT + (n >> 3)) * 32 + ((n & 7) << 2) + q] = v;
+  double* xt = a.X + ((size_t)mi * a.nchunks + chunk) * (2 * 8 * a.NT * 32) + (size_t)ks * a.NT * 32 + q * 8;
+  const size_t par_stride = (size_t)8 * a.NT * 32;
+  auto put4 = [&](int col, double2 v0, double2 v1, double2 o0, double2 o1) {
+    double2* e = reinterpret_cast<double2*>(xt + (col >> 3) * 32 + (col & 7));
+    double2* o = reinterpret_cast<double2*>(xt + par_stride + (col >> 3) * 32 + (col & 7));
+    e[0] = v0;
+    e[1] = v1;
+    o[0] = o0;
+    o[1] = o1;
   };
-  if (b == a.nfields) {  // zero the padding columns of this pair
-    for (int n = 12 * a.nfields; n < 8 * a.NT; ++n) {
-      put(0, n, 0.0);
-      put(1, n, 0.0);
-    }
+  const double2 zero = make_double2(0.0, 0.0);
+  if (z == 3 * a.nfields) {  // padding columns 12 nf .. 8 NT - 1 (at most one group of 4)
+    if (12 * a.nfields < 8 * a.NT) put4(12 * a.nfields, zero, zero, zero, zero);
     return;
   }
+  const int b = z / 3, c = z % 3;
   const int rn = a.pair_n[p], rs = a.pair_s[p];
-  for (int sgn = 0; sgn < 2; ++sgn) {
-    double2 E[3], O[3];
-    if (rn < 0 || (sgn == 1 && m == 0)) {
-      for (int c = 0; c < 3; ++c) E[c] = O[c] = make_double2(0.0, 0.0);
-    } else {
+  double2 E[2] = {zero, zero}, O[2] = {zero, zero};
+  if (rn >= 0) {
+    const double wn = a.ring_w[rn];
+    const double ws = rs >= 0 ? a.ring_w[rs] : 0.0;
+    const double2* base = a.S + c * a.lay.cs + (long long)(a.b0 + b) * a.n_theta * a.lay.rs;
+    for (int sgn = 0; sgn < 2; ++sgn) {
+      if (sgn == 1 && m == 0) break;
       const long long bin = spec_bin(a.lay, m, sgn, a.n_phi);
       const double sig = (sgn == 1 && (m & 1)) ? -1.0 : 1.0;
-      double2 Tn[3], Ts[3];
-      for (int k = 0; k < 3; ++k) {  // bin-major layout: consecutive pairs -> consecutive rings (coalesced)
-        const double2* base = a.S + k * a.lay.cs + (long long)(a.b0 + b) * a.n_theta * a.lay.rs + bin * a.lay.bs;
-        Tn[k] = base[rn * a.lay.rs];
-        Ts[k] = rs >= 0 ? base[rs * a.lay.rs] : make_double2(0.0, 0.0);
+      const double2 Tn = base[rn * a.lay.rs + bin * a.lay.bs];
+      const double nr = wn * Tn.x, ni = wn * Tn.y;
+      if (rs >= 0) {
+        const double2 Ts = base[rs * a.lay.rs + bin * a.lay.bs];
+        const double sr = ws * Ts.x, si = ws * Ts.y;
+        E[sgn] = make_double2(sig * (nr + sr), sig * (ni + si));
+        O[sgn] = make_double2(sig * (nr - sr), sig * (ni - si));
+      } else {  // unpaired ring: both parities see the ring itself
+        E[sgn] = O[sgn] = make_double2(sig * nr, sig * ni);
       }
-      const double wn = a.ring_w[rn];
-      const double ws = rs >= 0 ? a.ring_w[rs] : 0.0;
-      // U = -T1 + i T2, V = T1 + i T2, W = T3 (favest/transforms.py:112), after the FFT
-      double2 Cn[3], Cs[3];
-      Cn[0] = make_double2(-Tn[0].x - Tn[1].y, -Tn[0].y + Tn[1].x);
-      Cn[1] = make_double2(Tn[0].x - Tn[1].y, Tn[0].y + Tn[1].x);
-      Cn[2] = Tn[2];
-      Cs[0] = make_double2(-Ts[0].x - Ts[1].y, -Ts[0].y + Ts[1].x);
-      Cs[1] = make_double2(Ts[0].x - Ts[1].y, Ts[0].y + Ts[1].x);
-      Cs[2] = Ts[2];
-      for (int c = 0; c < 3; ++c) {
-        const double nr = wn * Cn[c].x, ni = wn * Cn[c].y;
-        if (rs >= 0) {
-          const double sr = ws * Cs[c].x, si = ws * Cs[c].y;
-          E[c] = make_double2(sig * (nr + sr), sig * (ni + si));
-          O[c] = make_double2(sig * (nr - sr), sig * (ni - si));
-        } else {  // unpaired ring: both parities see the ring itself
-          E[c] = O[c] = make_double2(sig * nr, sig * ni);
-        }
-      }
-    }
-    for (int c = 0; c < 3; ++c) {
-      const int n = 12 * b + 4 * c + 2 * sgn;
-      put(0, n, E[c].x);
-      put(0, n + 1, E[c].y);
-      put(1, n, O[c].x);
-      put(1, n + 1, O[c].y);
     }
   }
+  put4(12 * b + 4 * c, E[0], E[1], O[0], O[1]);
 }
 
 // ---------------------------------------------------------------------------
@@ -269,13 +262,24 @@ struct CgFwdArgs {
   int c_lo, c_hi;       // orders |m| written: [c_lo, c_hi) (F rows of c_lo-1 .. c_hi must be current)
 };
 
+// U = -x + i y, V = x + i y, W = z (favest/transforms.py:112) from the
+// Cartesian scalar coefficients (the scalar transform is linear)
+__device__ __forceinline__ double2 combo_uvw(int comp, double2 x, double2 y, double2 z) {
+  if (comp == 0) return make_double2(-x.x - y.y, -x.y + y.x);
+  if (comp == 1) return make_double2(x.x - y.y, x.y + y.x);
+  return z;
+}
+
 __device__ __forceinline__ double2 f_read(const CgFwdArgs& a, int b, int comp, long long l, long long m) {
-  // scalar coefficient F^comp_{l,m}, zero outside 0 <= l <= L+1, |m| <= l
+  // scalar coefficient F^comp_{l,m} (comp 0 U, 1 V, 2 W), zero outside 0 <= l <= L+1, |m| <= l
   if (l < 0 || l > a.L + 1 || llabs(m) > l) return make_double2(0.0, 0.0);
   const long long am = llabs(m);
   const int sgn = (m < 0) ? 1 : 0;
-  const double* row = a.F + ((size_t)l * (l + 1) / 2 + am) * a.ncolF;
-  return *reinterpret_cast<const double2*>(row + 12 * b + 4 * comp + 2 * sgn);
+  const double* row = a.F + ((size_t)l * (l + 1) / 2 + am) * a.ncolF + 12 * b + 2 * sgn;
+  const double2 x = *reinterpret_cast<const double2*>(row);
+  const double2 y = *reinterpret_cast<const double2*>(row + 4);
+  const double2 z = *reinterpret_cast<const double2*>(row + 8);
+  return combo_uvw(comp, x, y, z);
 }
 
 __global__ void cg_fwd_kernel(CgFwdArgs a) {
@@ -370,9 +374,11 @@ __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
       if (ls < 0 || ls > Lt || abs(ms) > ls) return 0.0;
       return __ldg(&a.cgt[i * Kt + ls * ls + ls + ms]);
     };
-    // staged F^comp_{l+dl, mm}: row |mm| - (m0 - 1); out-of-range rows were staged as 0
+    // staged F^{x,y,z}_{l+dl, mm}: row |mm| - (m0 - 1); out-of-range rows were staged as 0;
+    // combo comp of favest/transforms.py:112 formed on read
     auto f = [&](int comp, int dl, int mm) -> double2 {
-      return cgf_smem[((dl + 1) * ROWS + abs(mm) - (m0 - 1)) * RS + 6 * b + 2 * comp + (mm < 0 ? 1 : 0)];
+      const double2* r = cgf_smem + ((dl + 1) * ROWS + abs(mm) - (m0 - 1)) * RS + 6 * b + (mm < 0 ? 1 : 0);
+      return combo_uvw(comp, r[0], r[2], r[4]);
     };
     const double x1 = tab(0, l - 1, M - 1), x2 = tab(1, l + 1, M - 1);
     const double x3 = tab(2, l - 1, M + 1), x4 = tab(3, l + 1, M + 1);

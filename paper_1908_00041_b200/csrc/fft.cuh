@@ -53,11 +53,12 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 
 // exp(-2 pi i e / R) for the composite radices' internal twiddles, packed by R
 // (offsets below; filled per device by plan.cu).
-constexpr int kCompR[9] = {4, 6, 8, 9, 10, 12, 14, 15, 16};
-__constant__ double kCompCos[4 + 6 + 8 + 9 + 10 + 12 + 14 + 15 + 16];
-__constant__ double kCompSin[4 + 6 + 8 + 9 + 10 + 12 + 14 + 15 + 16];
+constexpr int kCompR[11] = {4, 6, 8, 9, 10, 12, 14, 15, 16, 18, 20};
+__constant__ double kCompCos[4 + 6 + 8 + 9 + 10 + 12 + 14 + 15 + 16 + 18 + 20];
+__constant__ double kCompSin[4 + 6 + 8 + 9 + 10 + 12 + 14 + 15 + 16 + 18 + 20];
 __host__ __device__ constexpr int comp_offset(int R) {
-  return R == 4 ? 0 : R == 6 ? 4 : R == 8 ? 10 : R == 9 ? 18 : R == 10 ? 27 : R == 12 ? 37 : R == 14 ? 49 : R == 15 ? 63 : 78;
+  return R == 4 ? 0 : R == 6 ? 4 : R == 8 ? 10 : R == 9 ? 18 : R == 10 ? 27 : R == 12 ? 37 : R == 14 ? 49
+       : R == 15 ? 63 : R == 16 ? 78 : R == 18 ? 94 : 112;
 }
 __host__ __device__ constexpr int first_factor(int R) {
   return R % 4 == 0 ? 4 : R % 2 == 0 ? 2 : R % 3 == 0 ? 3 : R % 5 == 0 ? 5 : R % 7 == 0 ? 7 : R;

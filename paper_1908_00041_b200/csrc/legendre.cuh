@@ -8,6 +8,8 @@
 //   north = E + O, south = E - O.
 //
 // Columns: col = 12*field + 4*component + 2*sign + re/im (sign 0: +m, 1: -m);
+// forward columns are the Cartesian components x, y, z (the U/V/W combos are
+// formed in the CG stage), adjoint columns the merged g^X, g^Y, g^Z;
 // 8-column n-tiles, NT of them per launch (<= 4 fields per launch).
 //
 // Both kernels are warp specialised.  Four producer warps (one per SMSP) run
@@ -94,7 +96,7 @@ struct __align__(16) StageMeta {
 };
 
 struct FwdArgs {
-  const double* X;          // [m][chunk][par][ks 8][NT][32]
+  const double* X;          // [m][chunk][par][ks 8][NT][k 4][n 8]
   double* F;                // rows tri(l, m) (l-major), 8*NT doubles each
   const int* start_l;       // [m][nPpad] polar start degree (Lt+1: never)
   const double2* start_v;   // [m][nPpad] (P_ls, P_ls+1)
@@ -389,6 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
   const int nh = cw & 1;
   const int nt0 = nh * NTW;
   const int g = lane >> 2, q = lane & 3;
+  const int xq = q * 8 + g;  // B element (k = q, n = g) of an [k 4][n 8] X tile (2 wavefronts, conflict free)
   const int ncolF = 8 * NT;
   double acc[2][NTW][2];
 #pragma unroll
@@ -432,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
           a1[ks] = lds_f64(&Ps[((par * 4 + 2 * mh + 1) * 8 + ks) * 32 + sw]);
 #pragma unroll
           for (int jn = 0; jn < NTW; ++jn)
-            bb[ks][jn] = (nt0 + jn < NT) ? lds_f64(&Xs[((par * 8 + ks) * NT + nt0 + jn) * 32 + lane]) : 0.0;
+            bb[ks][jn] = (nt0 + jn < NT) ? lds_f64(&Xs[((par * 8 + ks) * NT + nt0 + jn) * 32 + xq]) : 0.0;
         }
         const int r0 = l0 + 32 * mh, r1 = r0 + 16;
         int kf0 = 8, kf1 = 8;

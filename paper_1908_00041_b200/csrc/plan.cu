@@ -8,6 +8,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <type_traits>
 #include <map>
 #include <tuple>
 #include <string>
@@ -17,6 +19,7 @@
 #include "../../include/favest_b200.h"
 #include "aux_kernels.cuh"
 #include "fft.cuh"
+#include "fft2.cuh"
 #include "legendre.cuh"
 #include "points.cuh"
 
@@ -121,6 +124,11 @@ struct fvPlan {
   int fft_nst = 0;
   int fft_radix[fv::FFT_MAXST] = {};
   double2* fft_tw = nullptr;
+  // two-ring FFT (fft2.cuh): radix plan, per-stage twiddle tables; fused forward fold
+  bool fft2 = false, fused_fold = false;
+  int f2_nst = 0;
+  int f2_radix[fv::FFT_MAXST] = {};
+  double2* f2_tw = nullptr;
   // profiling
   bool profiling = false;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
@@ -144,7 +152,7 @@ void free_plan(fvPlan* p) {
                   p->seed_e, p->start_l,  p->start_v, p->ab,   p->abofs,  p->gofs,
                   p->dg,     p->dgofs,  p->cgt,     p->cga,     p->ptab_f,  p->mtab_f, p->tofs,   p->ptab_a, p->aofs,
                   p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->G,
-                  p->fft_tw};
+                  p->fft_tw, p->f2_tw};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
@@ -430,6 +438,143 @@ int setup_fft(fvPlan* p) {
   return FV_OK;
 }
 
+// Radix plan of the two-ring kernel (fft2.cuh): radices 2..20, each stage's
+// butterflies (2 n / R of them) spread over F2_T threads with at most f2_kb(R)
+// per thread (they are held in registers across the in-place barrier).  Cost
+// model: per-thread butterfly work  sum_s ceil(2n / (R_s T)) R_s (2 + log2 R_s)
+// plus a fixed cost per stage (barrier, shared-memory pass); minimised by DP over
+// the divisors of n.  Largest radix first (the first stage has no twiddles).
+bool fft2_factor(int n, int* radix, int* nst) {
+  if (n < 2 || 2 * (size_t)n * sizeof(double2) > 110 * 1024) return false;
+  std::map<int, std::pair<double, int>> best;  // remaining length -> (cost, first radix)
+  std::function<double(int)> solve = [&](int m) -> double {
+    if (m == 1) return 0.0;
+    auto it = best.find(m);
+    if (it != best.end()) return it->second.first;
+    double bc = 1e300;
+    int br = 0;
+    for (int R = 2; R <= 20; ++R) {
+      if (m % R) continue;
+      const int kb = (2 * n / R + fv::F2_T - 1) / fv::F2_T;
+      if (kb > fv::f2_kb_rt(R)) continue;
+      const double c = kb * R * (2.0 + std::log2((double)R)) + 40.0 + solve(m / R);
+      if (c < bc) {
+        bc = c;
+        br = R;
+      }
+    }
+    best[m] = {bc, br};
+    return bc;
+  };
+  if (solve(n) >= 1e299) return false;
+  std::vector<int> out;
+  for (int m = n; m > 1; m /= best[m].second) out.push_back(best[m].second);
+  if ((int)out.size() > fv::FFT_MAXST) return false;
+  std::sort(out.begin(), out.end(), std::greater<int>());
+  for (size_t i = 0; i < out.size(); ++i) radix[i] = out[i];
+  *nst = (int)out.size();
+  return true;
+}
+
+bool f2_instantiated(const int* r, int nst) {
+  const int r1 = nst > 1 ? r[1] : 0, r2 = nst > 2 ? r[2] : 0;
+#define FV_F2_HAS(a, b, c) \
+  if (r[0] == a && r1 == b && r2 == c) return true;
+  FV_F2_PLANS(FV_F2_HAS)
+#undef FV_F2_HAS
+  return false;
+}
+
+template <typename F>
+int f2_dispatch(const fvPlan* p, F&& f) {
+  const int r0 = p->f2_radix[0], r1 = p->f2_nst > 1 ? p->f2_radix[1] : 0, r2 = p->f2_nst > 2 ? p->f2_radix[2] : 0;
+#define FV_F2_CALL(a, b, c) \
+  if (r0 == a && r1 == b && r2 == c) return f(std::integral_constant<int, a>{}, std::integral_constant<int, b>{}, std::integral_constant<int, c>{});
+  FV_F2_PLANS(FV_F2_CALL)
+#undef FV_F2_CALL
+  return fail(FV_EINVAL, "no compiled two-ring FFT plan");
+}
+
+int setup_fft2(fvPlan* p) {
+  const char* env = std::getenv("FV_FFT");
+  if (env && (std::string(env) == "cufft" || std::string(env) == "v1")) return FV_OK;
+  if (!fft2_factor(p->n_phi, p->f2_radix, &p->f2_nst) || p->f2_nst > 3 || !f2_instantiated(p->f2_radix, p->f2_nst))
+    return FV_OK;
+  const int n = p->n_phi;
+  // twiddles of stages 1.. (stage 0 has none): entry [k < Ns][r - 1 < R - 1] = w^(r k n / (Ns R))
+  std::vector<double2> tw;
+  int ns = p->f2_radix[0];
+  for (int s = 1; s < p->f2_nst; ++s) {
+    const int R = p->f2_radix[s];
+    const long long ts = n / (ns * R);
+    for (int k = 0; k < ns; ++k)
+      for (int r = 1; r < R; ++r) {
+        const long double a = 2.0L * 3.141592653589793238462643383279502884L * (long double)(r * k * ts) / n;
+        tw.push_back(make_double2((double)cosl(a), -(double)sinl(a)));
+      }
+    ns *= R;
+  }
+  FV_TRY(dalloc(&p->f2_tw, tw.size()));
+  if (!tw.empty())
+    FV_CUDA(cudaMemcpy(p->f2_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  const int smem = (int)(fv::F2_NR * (size_t)n * sizeof(double2));
+  FV_TRY(f2_dispatch(p, [&](auto A, auto B, auto C) -> int {
+    FV_CUDA(cudaFuncSetAttribute(fv::ring_fft2_kernel<false, A, B, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FV_CUDA(cudaFuncSetAttribute(fv::ring_fft2_kernel<true, A, B, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    FV_CUDA(cudaFuncSetAttribute(fv::fft_fold_kernel<A, B, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    return FV_OK;
+  }));
+  p->fft2 = true;
+  const char* ff = std::getenv("FV_FUSED_FOLD");
+  p->fused_fold = !(ff && std::atoi(ff) == 0);
+  return FV_OK;
+}
+
+int ring_fft2_raw(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
+                  double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s) {
+  fv::Fft2Args a{};
+  a.tw = p->f2_tw;
+  a.in = in;
+  a.out = out;
+  a.in_cs = in_cs; a.in_rs = in_rs; a.in_es = (int)in_es;
+  a.out_cs = out_cs; a.out_rs = out_rs; a.out_es = (int)out_es;
+  a.nrings = nrings;
+  const int grid = 3 * ((nrings + fv::F2_NR - 1) / fv::F2_NR);
+  const size_t smem = fv::F2_NR * (size_t)p->n_phi * sizeof(double2);
+  return f2_dispatch(p, [&](auto A, auto B, auto C) -> int {
+    if (inverse) fv::ring_fft2_kernel<true, A, B, C><<<grid, fv::F2_T, smem, s>>>(a, grid);
+    else fv::ring_fft2_kernel<false, A, B, C><<<grid, fv::F2_T, smem, s>>>(a, grid);
+    FV_CUDA(cudaGetLastError());
+    return FV_OK;
+  });
+}
+
+// fused forward FFT + fold of fields b0 .. b0 + nf - 1 of T (B, N, 3) into X (all orders)
+int fft_fold(fvPlan* p, const double2* T, int b0, int nf, cudaStream_t s) {
+  fv::Fft2Args a{};
+  const long long n = p->n_phi;
+  a.tw = p->f2_tw;
+  a.in_rs = 3 * n;
+  a.in_es = 3;
+  a.field_stride = 3 * n * p->n_theta;
+  a.in = T + (long long)b0 * a.field_stride;
+  a.X = p->X;
+  a.pair_n = p->pair_n;
+  a.pair_s = p->pair_s;
+  a.ring_w = p->ring_w;
+  a.nchunks = p->nchunks;
+  a.NT = ntiles_for(nf);
+  a.nfields = nf;
+  a.Lt = p->Lt;
+  const int grid = p->nchunks * fv::FWD_RC * nf * 3;
+  const size_t smem = fv::F2_NR * (size_t)p->n_phi * sizeof(double2);
+  return f2_dispatch(p, [&](auto A, auto B, auto C) -> int {
+    fv::fft_fold_kernel<A, B, C><<<grid, fv::F2_T, smem, s>>>(a, grid);
+    FV_CUDA(cudaGetLastError());
+    return FV_OK;
+  });
+}
+
 // 3 components x nrings ring DFTs with the hand-written kernel; element (c, ring, q) at
 // c * cs + ring * rs + q * es (complex units) on both sides
 int ring_fft_raw(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
@@ -595,7 +740,7 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
     fv::cga_table_kernel<<<grid, 32>>>(Lt, p->gofs, p->cgt, p->cga, 32 * p->g_tiles);
     FV_CUDA(cudaGetLastError());
   }
-  if ((rc = setup_fft(p))) return bail(rc);
+  if ((rc = setup_fft(p)) || (rc = setup_fft2(p))) return bail(rc);
   // workspaces (field groups of <= 4 -> NT <= 6)
   const int gs = std::min(4, max_batch);
   const int NTmax = ntiles_for(gs);
@@ -708,19 +853,22 @@ int check_grid_call(fvPlan* p, int B, const void* x, const void* y, const void* 
 // fold + Legendre over orders [m_lo, m_hi) and CG for orders [c_lo, c_hi), reading the
 // spectra of every ring of the grid in layout `lay` (natural or compact bins)
 int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* a, double* b, int B, int m_lo,
-                   int m_hi, int c_lo, int c_hi, cudaStream_t s) {
+                   int m_hi, int c_lo, int c_hi, cudaStream_t s, const double2* Tfield = nullptr) {
   const int Lt = p->Lt;
   const int mc = m_hi - m_lo;
   for (int b0 = 0; b0 < B; b0 += 4) {
     const int nf = std::min(4, B - b0);
     const int NT = ntiles_for(nf);
-    {
+    if (S) {
       StageMark mk(p, 1, s);
       fv::FoldArgs fa{S, p->X, p->pair_n, p->pair_s, p->ring_w, p->n_phi, p->n_theta, B, b0, nf, NT,
                       p->nchunks * fv::FWD_RC, p->nchunks, m_lo, mc, lay};
-      dim3 grid((p->nchunks * fv::FWD_RC + 127) / 128, mc, nf + 1);
+      dim3 grid((p->nchunks * fv::FWD_RC + 127) / 128, mc, 3 * nf + 1);
       fv::fold_fwd_kernel<<<grid, 128, 0, s>>>(fa);
       FV_CUDA(cudaGetLastError());
+    } else {  // fused FFT + fold straight from the field (fft2.cuh)
+      StageMark mk(p, 0, s);
+      FV_TRY(fft_fold(p, Tfield, b0, nf, s));
     }
     {
       StageMark mk(p, 2, s);
@@ -784,6 +932,7 @@ int adjoint_orders(fvPlan* p, const double* a, const double* b, double2* S, cons
 int ring_ffts(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
               double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s) {
   StageMark mk(p, 0, s);
+  if (p->fft2) return ring_fft2_raw(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   if (p->custom_fft) return ring_fft_raw(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   cufftHandle h;
   FV_TRY(get_fft_strided(p, in_rs, in_es, out_rs, out_es, nrings, &h));
@@ -802,6 +951,9 @@ int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, voi
   FV_TRY(check_grid_call(p, B, T, a, b));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const long long n = p->n_phi;
+  if (p->fft2 && p->fused_fold)
+    return forward_orders(p, nullptr, p->lay_f, a, b, B, 0, p->Lt + 1, 0, p->L + 1, s,
+                          reinterpret_cast<const double2*>(T));
   FV_TRY(ring_ffts(p, false, reinterpret_cast<const double2*>(T), 1, 3 * n, 3, p->Sf, p->lay_f.cs, p->lay_f.rs,
                    p->lay_f.bs, B * p->n_theta, s));
   return forward_orders(p, p->Sf, p->lay_f, a, b, B, 0, p->Lt + 1, 0, p->L + 1, s);
