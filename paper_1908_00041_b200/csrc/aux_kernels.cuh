@@ -167,9 +167,10 @@ __global__ void ab_kernel(int Lt, const long long* __restrict__ abofs, double2* 
 // Forward fold.  Thread per (local order mi, pair p, field b, component c):
 //   E = w_n S_n + w_s S_s, O = w_n S_n - w_s S_s of the Cartesian ring spectra
 //   at bins +m and -m (times sigma_{-m} on the -m bin), written as the four
-//   columns 12 b + 4 c + (2 sign + re/im) of X[mi][chunk][par][ks][nt][k 4][n 8]
-//   (B operand tiles; the consumer lane (k = lane & 3, n = lane >> 2) reads
-//   k * 8 + n), one aligned 32-byte sector per parity.  The U/V/W combos of
+//   columns 12 b + 4 c + (2 sign + re/im) of
+//   X[mi][chunk][par][ks][nt][n_hi 2][k 4][n_lo 4] (B operand tiles; the
+//   consumer lane (k = lane & 3, n = lane >> 2) reads 16 n_hi + 4 k + n_lo),
+//   one aligned 32-byte sector per parity.  The U/V/W combos of
 //   favest/transforms.py:112 are formed after the (linear) scalar transform, in
 //   the CG stage.  blockIdx.z == 3 nfields zeroes the padding columns.  The
 //   grid path fuses this into the ring FFT (fft2.cuh fft_fold_kernel).
@@ -190,11 +191,11 @@ __global__ void fold_fwd_kernel(FoldArgs a) {
   if (p >= a.nPpad) return;
   const int m = a.m_begin + mi;
   const int chunk = p >> 5, ks = (p >> 2) & 7, q = p & 3;
-  double* xt = a.X + ((size_t)mi * a.nchunks + chunk) * (2 * 8 * a.NT * 32) + (size_t)ks * a.NT * 32 + q * 8;
+  double* xt = a.X + ((size_t)mi * a.nchunks + chunk) * (2 * 8 * a.NT * 32) + (size_t)ks * a.NT * 32 + q * 4;
   const size_t par_stride = (size_t)8 * a.NT * 32;
-  auto put4 = [&](int col, double2 v0, double2 v1, double2 o0, double2 o1) {
-    double2* e = reinterpret_cast<double2*>(xt + (col >> 3) * 32 + (col & 7));
-    double2* o = reinterpret_cast<double2*>(xt + par_stride + (col >> 3) * 32 + (col & 7));
+  auto put4 = [&](int col, double2 v0, double2 v1, double2 o0, double2 o1) {  // col % 4 == 0
+    double2* e = reinterpret_cast<double2*>(xt + (col >> 3) * 32 + ((col >> 2) & 1) * 16);
+    double2* o = reinterpret_cast<double2*>(xt + par_stride + (col >> 3) * 32 + ((col >> 2) & 1) * 16);
     e[0] = v0;
     e[1] = v1;
     o[0] = o0;

@@ -246,7 +246,8 @@ __global__ void __launch_bounds__(F2_T, 2) ring_fft2_kernel(Fft2Args a, int nite
 // 3 n, field stride field_stride); X receives, for every order m = 0..Lt and
 // parity,  E/O = sigma * (w_n S_n[+-m] +/- w_s S_s[+-m])  at columns
 // 12 b + 4 c + (2 sign + re/im) (Cartesian component c), rows ordered
-// [m][chunk][par][ks][nt][k 4][n 8] (the Legendre consumers' B fragments).
+// [m][chunk][par][ks][nt][n_hi 2][k 4][n_lo 4] (the Legendre consumers' B
+// fragments; a component's four columns share n_hi, so they are one sector).
 template <int R0, int R1, int R2>
 __global__ void __launch_bounds__(F2_T, 2) fft_fold_kernel(Fft2Args a, int nitems) {
   extern __shared__ __align__(16) double2 f2buf[];
@@ -267,12 +268,12 @@ __global__ void __launch_bounds__(F2_T, 2) fft_fold_kernel(Fft2Args a, int nitem
   const int col = 12 * b + 4 * c;
   const size_t tile = (size_t)2 * 8 * a.NT * 32;
   const size_t par_stride = (size_t)8 * a.NT * 32;
-  const size_t off = ((size_t)ks * a.NT + (col >> 3)) * 32 + kq * 8 + (col & 7);
+  const size_t off = ((size_t)ks * a.NT + (col >> 3)) * 32 + ((col >> 2) & 1) * 16 + kq * 4;
   // padding columns 12 nf .. 8 NT - 1 (when 12 nf is not a multiple of 8): the
   // last (field, component) item zeroes them
   const bool padcols = (b == a.nfields - 1) && c == 2 && ((12 * a.nfields) & 7) == 4;
   const int pcol = 12 * a.nfields;
-  const size_t poff = ((size_t)ks * a.NT + (pcol >> 3)) * 32 + kq * 8 + (pcol & 7);
+  const size_t poff = ((size_t)ks * a.NT + (pcol >> 3)) * 32 + ((pcol >> 2) & 1) * 16 + kq * 4;
   const double wn = rn >= 0 ? a.ring_w[rn] : 0.0;
   const double ws = rs >= 0 ? a.ring_w[rs] : 0.0;
   const double2* Sn = f2buf;

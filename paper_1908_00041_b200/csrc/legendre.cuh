@@ -96,7 +96,7 @@ struct __align__(16) StageMeta {
 };
 
 struct FwdArgs {
-  const double* X;          // [m][chunk][par][ks 8][NT][k 4][n 8]
+  const double* X;          // [m][chunk][par][ks 8][NT][n_hi 2][k 4][n_lo 4]
   double* F;                // rows tri(l, m) (l-major), 8*NT doubles each
   const int* start_l;       // [m][nPpad] polar start degree (Lt+1: never)
   const double2* start_v;   // [m][nPpad] (P_ls, P_ls+1)
@@ -391,7 +391,9 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
   const int nh = cw & 1;
   const int nt0 = nh * NTW;
   const int g = lane >> 2, q = lane & 3;
-  const int xq = q * 8 + g;  // B element (k = q, n = g) of an [k 4][n 8] X tile (2 wavefronts, conflict free)
+  // B element (k = q, n = g) of an [n_hi 2][k 4][n_lo 4] X tile: each half-warp (g < 4, g >= 4) reads 16
+  // consecutive doubles (conflict free; an [k][n] order would be 2-way conflicted per half-warp)
+  const int xq = (g >> 2) * 16 + q * 4 + (g & 3);
   const int ncolF = 8 * NT;
   double acc[2][NTW][2];
 #pragma unroll
