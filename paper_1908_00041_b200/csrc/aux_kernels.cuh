@@ -580,34 +580,17 @@ __global__ void __launch_bounds__(CGA_THREADS) cg_adj_tile_kernel(CgAdjArgs a) {
   }
   __syncthreads();
   if (work) {
-    const double is2 = 0.7071067811865475;
-    const double x1 = cfv[0], x2 = cfv[1], x3 = cfv[2], x4 = cfv[3], x5 = cfv[4], x6 = cfv[5];
-    const double u1 = cfv[6], u2 = cfv[7], u3 = cfv[8];
     const int m = sg ? -am : am;
     double sig = (m < 0 && (am & 1)) ? -1.0 : 1.0;  // favest/legendre.py:101-103
     sig *= gam;                                      // gamma_l (legendre.cuh)
     // staged entries: row r = l - l0 + 1 (+-1), j = 3 sg + (M' - m + 1)
     auto at = [&](const double2* t, int dr, int dm) { return t[(b * 34 + idx + 1 + dr) * 7 + 3 * sg + dm + 1]; };
-    const double2 ap1p = at(As, 1, 1), ap1m = at(As, 1, -1), am1p = at(As, -1, 1), am1m = at(As, -1, -1);
-    const double2 ap10 = at(As, 1, 0), am10 = at(As, -1, 0);
-    const double2 bp = at(Bs, 0, 1), bm = at(Bs, 0, -1), b0 = at(Bs, 0, 0);
-    // nu1..nu6, eta1..eta3 (favest/coupling.py:227-239)
-    const double2 nu1 = make_double2(ap1p.x * x1 - ap1m.x * x3, ap1p.y * x1 - ap1m.y * x3);
-    const double2 nu2 = make_double2(am1p.x * x2 - am1m.x * x4, am1p.y * x2 - am1m.y * x4);
-    const double2 s3 = make_double2(ap1p.x * x1 + ap1m.x * x3, ap1p.y * x1 + ap1m.y * x3);
-    const double2 nu3 = make_double2(-s3.y, s3.x);
-    const double2 s4 = make_double2(am1p.x * x2 + am1m.x * x4, am1p.y * x2 + am1m.y * x4);
-    const double2 nu4 = make_double2(-s4.y, s4.x);
-    const double2 nu5 = make_double2(ap10.x * x5, ap10.y * x5);
-    const double2 nu6 = make_double2(am10.x * x6, am10.y * x6);
-    const double2 d1 = make_double2(bp.x * u1 - bm.x * u3, bp.y * u1 - bm.y * u3);
-    const double2 eta1 = make_double2(-d1.y, d1.x);
-    const double2 eta2 = make_double2(bp.x * u1 + bm.x * u3, bp.y * u1 + bm.y * u3);
-    const double2 eta3 = make_double2(-(b0.y * u2), b0.x * u2);
-    // merge (favest/transforms.py:168-175)
-    const double2 gx = make_double2(-is2 * ((nu1.x + nu2.x) + eta1.x), -is2 * ((nu1.y + nu2.y) + eta1.y));
-    const double2 gy = make_double2(-is2 * ((nu3.x + nu4.x) - eta2.x), -is2 * ((nu3.y + nu4.y) - eta2.y));
-    const double2 gz = make_double2((nu5.x + nu6.x) + eta3.x, (nu5.y + nu6.y) + eta3.y);
+    CgAdjIn v;
+    v.ap1p = at(As, 1, 1); v.ap1m = at(As, 1, -1); v.am1p = at(As, -1, 1); v.am1m = at(As, -1, -1);
+    v.ap10 = at(As, 1, 0); v.am10 = at(As, -1, 0);
+    v.bp = at(Bs, 0, 1); v.bm = at(Bs, 0, -1); v.b0 = at(Bs, 0, 0);
+    double2 gx, gy, gz;
+    cg_adj_merge(cfv, v, gx, gy, gz);
     const int par = idx & 1, kk = idx >> 1, ks = kk >> 2, q = kk & 3;
     double* gb = Gs + (par * KS + ks) * BS + q;
     auto put = [&](int n, double v) { gb[(n >> 3) * 32 + ((n & 7) << 2)] = v; };

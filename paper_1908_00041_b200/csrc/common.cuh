@@ -182,4 +182,35 @@ __device__ __forceinline__ double mu_coef(int i, long long l, long long m) {
   return cg_explicit(0, -1, l, m - 1);
 }
 
+// Adjoint coupling of one (l, M, field): nu1..nu6, eta1..eta3
+// (favest/coupling.py:227-239) and the merge into g^X, g^Y, g^Z
+// (favest/transforms.py:168-175), from the nine factors x = (xi1..6, mu1..3) at
+// (l, M) and the a / b entries at the shifted positions (zero outside range).
+// One definition for every caller, so all paths are bitwise equal.
+struct CgAdjIn {
+  double2 ap1p, ap1m, am1p, am1m, ap10, am10;  // a at (l+1, M+1), (l+1, M-1), (l-1, M+1), (l-1, M-1), (l+1, M), (l-1, M)
+  double2 bp, bm, b0;                          // b at (l, M+1), (l, M-1), (l, M)
+};
+
+__device__ __forceinline__ void cg_adj_merge(const double (&x)[9], const CgAdjIn& v, double2& gx, double2& gy,
+                                             double2& gz) {
+  const double is2 = 0.7071067811865475;  // favest/transforms.py:46 (1/np.sqrt(2.0))
+  const double x1 = x[0], x2 = x[1], x3 = x[2], x4 = x[3], x5 = x[4], x6 = x[5], u1 = x[6], u2 = x[7], u3 = x[8];
+  const double2 nu1 = make_double2(v.ap1p.x * x1 - v.ap1m.x * x3, v.ap1p.y * x1 - v.ap1m.y * x3);
+  const double2 nu2 = make_double2(v.am1p.x * x2 - v.am1m.x * x4, v.am1p.y * x2 - v.am1m.y * x4);
+  const double2 s3 = make_double2(v.ap1p.x * x1 + v.ap1m.x * x3, v.ap1p.y * x1 + v.ap1m.y * x3);
+  const double2 nu3 = make_double2(-s3.y, s3.x);
+  const double2 s4 = make_double2(v.am1p.x * x2 + v.am1m.x * x4, v.am1p.y * x2 + v.am1m.y * x4);
+  const double2 nu4 = make_double2(-s4.y, s4.x);
+  const double2 nu5 = make_double2(v.ap10.x * x5, v.ap10.y * x5);
+  const double2 nu6 = make_double2(v.am10.x * x6, v.am10.y * x6);
+  const double2 d1 = make_double2(v.bp.x * u1 - v.bm.x * u3, v.bp.y * u1 - v.bm.y * u3);
+  const double2 eta1 = make_double2(-d1.y, d1.x);
+  const double2 eta2 = make_double2(v.bp.x * u1 + v.bm.x * u3, v.bp.y * u1 + v.bm.y * u3);
+  const double2 eta3 = make_double2(-(v.b0.y * u2), v.b0.x * u2);
+  gx = make_double2(-is2 * ((nu1.x + nu2.x) + eta1.x), -is2 * ((nu1.y + nu2.y) + eta1.y));
+  gy = make_double2(-is2 * ((nu3.x + nu4.x) - eta2.x), -is2 * ((nu3.y + nu4.y) - eta2.y));
+  gz = make_double2((nu5.x + nu6.x) + eta3.x, (nu5.y + nu6.y) + eta3.y);
+}
+
 }  // namespace fv

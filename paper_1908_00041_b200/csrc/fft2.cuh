@@ -46,6 +46,9 @@ template <int R>
 __host__ __device__ constexpr int f2_kb() {
   return F2_MAXREG / R > 0 ? F2_MAXREG / R : 1;
 }
+// rings / threads per CTA of the plain transform (stage templates take both;
+// one ring per 128-thread CTA, four CTAs per SM, measured 4% slower at n = 2052)
+constexpr int F2P_NR = 2, F2P_T = 256;
 __host__ __device__ constexpr int f2_kb_rt(int R) { return F2_MAXREG / R > 0 ? F2_MAXREG / R : 1; }
 
 // threadIdx.x re-read per stage: an opaque value stops the compiler from
@@ -94,31 +97,31 @@ __device__ __forceinline__ void f2_twiddle(double2 (&v)[R], const double2* __res
 // First stage (Ns = 1): inputs straight from global memory (per-ring base
 // pointers, element stride es), outputs to shared memory or, for a one-stage
 // plan, to global memory (element stride des).
-template <int R, int N, bool INV, bool LAST>
-__device__ __forceinline__ void f2_first(const double2* const (&src)[F2_NR], int es, int nr, double2* buf,
-                                         double2* const (&dst)[F2_NR], int des) {
-  constexpr int KB = f2_kb<R>(), NB = N / R;
+template <int R, int N, bool INV, bool LAST, int NR, int T>
+__device__ __forceinline__ void f2_first(const double2* const (&src)[NR], int es, int nr, double2* buf,
+                                         double2* const (&dst)[NR], int des) {
+  constexpr int KB = f2_kb<R>(), NB = N / R;  // plan.cu fft2_factor: <= KB butterflies per thread at T / NR = 128
   const int tot = nr * NB;
   const int tid = threadIdx.x;
   double2 v[KB][R];
 #pragma unroll
   for (int k = 0; k < KB; ++k) {
-    const int j = tid + k * F2_T;
+    const int j = tid + k * T;
     if (j < tot) {
       const int ring = j / NB, jj = j - ring * NB;
-      const double2* s = ring ? src[1] : src[0];
+      const double2* s = (NR > 1 && ring) ? src[NR - 1] : src[0];
 #pragma unroll
       for (int r = 0; r < R; ++r) v[k][r] = __ldg(s + (long long)(jj + r * NB) * es);
     }
   }
 #pragma unroll
   for (int k = 0; k < KB; ++k) {
-    const int j = tid + k * F2_T;
+    const int j = tid + k * T;
     if (j < tot) {
       const int ring = j / NB, jj = j - ring * NB;
       dft<R, INV>(v[k]);
       if (LAST) {
-        double2* d = ring ? dst[1] : dst[0];
+        double2* d = (NR > 1 && ring) ? dst[NR - 1] : dst[0];
 #pragma unroll
         for (int r = 0; r < R; ++r) d[(long long)(jj + r * NB) * des] = v[k][r];
       } else {
@@ -131,15 +134,15 @@ __device__ __forceinline__ void f2_first(const double2* const (&src)[F2_NR], int
 }
 
 // Middle stage (or the last stage of the fused epilogue): in place in shared memory.
-template <int R, int NS, int N, bool INV>
+template <int R, int NS, int N, bool INV, int T>
 __device__ __forceinline__ void f2_mid(const double2* __restrict__ tw, int nr, double2* buf) {
-  constexpr int KB = f2_kb<R>(), NB = N / R;
+  constexpr int KB = f2_kb<R>(), NB = N / R;  // plan.cu fft2_factor: <= KB butterflies per thread at T / NR = 128
   const int tot = nr * NB;
   const int tid = threadIdx.x;
   double2 v[KB][R];
 #pragma unroll
   for (int k = 0; k < KB; ++k) {
-    const int j = tid + k * F2_T;
+    const int j = tid + k * T;
     if (j < tot) {
       const int ring = j / NB, jj = j - ring * NB;
       const double2* src = buf + ring * N;
@@ -152,7 +155,7 @@ __device__ __forceinline__ void f2_mid(const double2* __restrict__ tw, int nr, d
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < KB; ++k) {
-    const int j = tid + k * F2_T;
+    const int j = tid + k * T;
     if (j < tot) {
       const int ring = j / NB, jj = j - ring * NB;
       double2* d = buf + ring * N + (jj / NS) * NS * R + jj % NS;
@@ -164,15 +167,15 @@ __device__ __forceinline__ void f2_mid(const double2* __restrict__ tw, int nr, d
 }
 
 // Last stage of the plain transform: shared memory -> global (element stride des).
-template <int R, int NS, int N, bool INV>
+template <int R, int NS, int N, bool INV, int NR, int T>
 __device__ __forceinline__ void f2_last(const double2* __restrict__ tw, int nr, const double2* buf,
-                                        double2* const (&dst)[F2_NR], int des) {
-  constexpr int KB = f2_kb<R>(), NB = N / R;
+                                        double2* const (&dst)[NR], int des) {
+  constexpr int KB = f2_kb<R>(), NB = N / R;  // plan.cu fft2_factor: <= KB butterflies per thread at T / NR = 128
   const int tot = nr * NB;
   const int tid = threadIdx.x;
 #pragma unroll
   for (int k = 0; k < KB; ++k) {
-    const int j = tid + k * F2_T;
+    const int j = tid + k * T;
     if (j < tot) {
       const int ring = j / NB, jj = j - ring * NB;
       const double2* src = buf + ring * N;
@@ -182,7 +185,7 @@ __device__ __forceinline__ void f2_last(const double2* __restrict__ tw, int nr, 
       const int kk = jj % NS;
       f2_twiddle<R, INV>(v, tw + kk * (R - 1));
       const int base = (jj / NS) * NS * R + kk;
-      double2* d = ring ? dst[1] : dst[0];
+      double2* d = (NR > 1 && ring) ? dst[NR - 1] : dst[0];
       if constexpr (R >= 11 && first_factor(R) == R) {
         prime_store<R, INV>(v, d, base, NS, des);
       } else {
@@ -196,49 +199,49 @@ __device__ __forceinline__ void f2_last(const double2* __restrict__ tw, int nr, 
 
 // nr rings (<= 2) of length N: global src -> ... -> shared memory (KEEP: the
 // spectrum stays in buf for the fused epilogue) or -> global dst.
-template <int R0, int R1, int R2, bool INV, bool KEEP>
-__device__ __forceinline__ void f2_run(const double2* tw, const double2* const (&src)[F2_NR], int es, int nr,
-                                       double2* buf, double2* const (&dst)[F2_NR], int des) {
+template <int R0, int R1, int R2, bool INV, bool KEEP, int NR, int T>
+__device__ __forceinline__ void f2_run(const double2* tw, const double2* const (&src)[NR], int es, int nr,
+                                       double2* buf, double2* const (&dst)[NR], int des) {
   using P = F2Plan<R0, R1, R2>;
   constexpr int N = P::N;
   if constexpr (P::NST == 1) {
-    f2_first<R0, N, INV, !KEEP>(src, es, nr, buf, dst, des);
+    f2_first<R0, N, INV, !KEEP, NR, T>(src, es, nr, buf, dst, des);
     if (KEEP) __syncthreads();
   } else if constexpr (P::NST == 2) {
-    f2_first<R0, N, INV, false>(src, es, nr, buf, dst, des);
+    f2_first<R0, N, INV, false, NR, T>(src, es, nr, buf, dst, des);
     __syncthreads();
-    if constexpr (KEEP) f2_mid<R1, R0, N, INV>(tw, nr, buf);
-    else f2_last<R1, R0, N, INV>(tw, nr, buf, dst, des);
+    if constexpr (KEEP) f2_mid<R1, R0, N, INV, T>(tw, nr, buf);
+    else f2_last<R1, R0, N, INV, NR, T>(tw, nr, buf, dst, des);
   } else {
-    f2_first<R0, N, INV, false>(src, es, nr, buf, dst, des);
+    f2_first<R0, N, INV, false, NR, T>(src, es, nr, buf, dst, des);
     __syncthreads();
-    f2_mid<R1, R0, N, INV>(tw, nr, buf);
-    if constexpr (KEEP) f2_mid<R2, R0 * R1, N, INV>(tw + P::TW2, nr, buf);
-    else f2_last<R2, R0 * R1, N, INV>(tw + P::TW2, nr, buf, dst, des);
+    f2_mid<R1, R0, N, INV, T>(tw, nr, buf);
+    if constexpr (KEEP) f2_mid<R2, R0 * R1, N, INV, T>(tw + P::TW2, nr, buf);
+    else f2_last<R2, R0 * R1, N, INV, NR, T>(tw + P::TW2, nr, buf, dst, des);
   }
 }
 
-// Plain transform: item = (group of NR consecutive rings, component), component
-// fastest; one CTA per item.  (Persistent CTAs with an L2 prefetch of the next
+// Plain transform: item = (group of F2P_NR consecutive rings, component),
+// component fastest; one CTA per item.  (Persistent CTAs with an L2 prefetch of the next
 // item were measured slower: the item loop made ptxas hoist per-thread index
 // math across stages and spill.)
 template <bool INV, int R0, int R1, int R2>
-__global__ void __launch_bounds__(F2_T, 2) ring_fft2_kernel(Fft2Args a, int nitems) {
+__global__ void __launch_bounds__(F2P_T, 2) ring_fft2_kernel(Fft2Args a, int nitems) {
   extern __shared__ __align__(16) double2 f2buf[];
   const int item = blockIdx.x;
   if (item >= nitems) return;
   const int c = item % 3, g = item / 3;
-  const int r0 = g * F2_NR;
-  const int nr = min(F2_NR, a.nrings - r0);
-  const double2* src[F2_NR];
-  double2* dst[F2_NR];
+  const int r0 = g * F2P_NR;
+  const int nr = min(F2P_NR, a.nrings - r0);
+  const double2* src[F2P_NR];
+  double2* dst[F2P_NR];
 #pragma unroll
-  for (int i = 0; i < F2_NR; ++i) {
+  for (int i = 0; i < F2P_NR; ++i) {
     const int r = min(r0 + i, a.nrings - 1);
     src[i] = a.in + c * a.in_cs + r * a.in_rs;
     dst[i] = a.out + c * a.out_cs + r * a.out_rs;
   }
-  f2_run<R0, R1, R2, INV, false>(a.tw, src, a.in_es, nr, f2buf, dst, a.out_es);
+  f2_run<R0, R1, R2, INV, false, F2P_NR, F2P_T>(a.tw, src, a.in_es, nr, f2buf, dst, a.out_es);
 }
 
 // Fused forward: item = (pair p < nchunks * 32, field b < nfields, component c),
@@ -261,7 +264,7 @@ __global__ void __launch_bounds__(F2_T, 2) fft_fold_kernel(Fft2Args a, int nitem
     const double2* base = a.in + (long long)b * a.field_stride + c;
     const double2* src[F2_NR] = {base + (long long)rn * a.in_rs, base + (long long)(rs >= 0 ? rs : rn) * a.in_rs};
     double2* dst[F2_NR] = {nullptr, nullptr};
-    f2_run<R0, R1, R2, false, true>(a.tw, src, a.in_es, nr, f2buf, dst, 0);
+    f2_run<R0, R1, R2, false, true, F2_NR, F2_T>(a.tw, src, a.in_es, nr, f2buf, dst, 0);
   }
   // epilogue: thread per order m
   const int chunk = p >> 5, ks = (p >> 2) & 7, kq = p & 3;

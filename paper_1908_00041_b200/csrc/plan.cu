@@ -539,11 +539,11 @@ int ring_fft2_raw(fvPlan* p, bool inverse, const double2* in, long long in_cs, l
   a.in_cs = in_cs; a.in_rs = in_rs; a.in_es = (int)in_es;
   a.out_cs = out_cs; a.out_rs = out_rs; a.out_es = (int)out_es;
   a.nrings = nrings;
-  const int grid = 3 * ((nrings + fv::F2_NR - 1) / fv::F2_NR);
-  const size_t smem = fv::F2_NR * (size_t)p->n_phi * sizeof(double2);
+  const int grid = 3 * ((nrings + fv::F2P_NR - 1) / fv::F2P_NR);
+  const size_t smem = fv::F2P_NR * (size_t)p->n_phi * sizeof(double2);
   return f2_dispatch(p, [&](auto A, auto B, auto C) -> int {
-    if (inverse) fv::ring_fft2_kernel<true, A, B, C><<<grid, fv::F2_T, smem, s>>>(a, grid);
-    else fv::ring_fft2_kernel<false, A, B, C><<<grid, fv::F2_T, smem, s>>>(a, grid);
+    if (inverse) fv::ring_fft2_kernel<true, A, B, C><<<grid, fv::F2P_T, smem, s>>>(a, grid);
+    else fv::ring_fft2_kernel<false, A, B, C><<<grid, fv::F2P_T, smem, s>>>(a, grid);
     FV_CUDA(cudaGetLastError());
     return FV_OK;
   });
