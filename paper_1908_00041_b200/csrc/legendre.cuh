@@ -493,7 +493,10 @@ constexpr int ADJ_LC = 32;       // l values per stage (16 per parity, 4 k-steps
 constexpr int ADJ_KS = ADJ_LC / 8;
 constexpr int ADJ_RC = 128;      // ring pairs per CTA (16 M-tiles, one per producer lane)
 constexpr int ADJ_MT = ADJ_RC / 8;
-constexpr int ADJ_STAGES = 4;
+#ifndef FV_ADJ_STAGES
+#define FV_ADJ_STAGES 5
+#endif
+constexpr int ADJ_STAGES = FV_ADJ_STAGES;
 constexpr int ADJ_MTILE = 2 * ADJ_KS * 32;           // doubles per M-tile: [par][ks][lane]
 constexpr int ADJ_PTILE = ADJ_MT * ADJ_MTILE;         // doubles: [Mtile][par][ks][lane] (M-tile major, so
                                                       // any run of M-tiles is one contiguous bulk copy)
@@ -524,9 +527,8 @@ template <int NT>
 struct AdjSmem {
   static constexpr int GTILE = 2 * ADJ_KS * NT * 32;
   static constexpr int STAGE = ADJ_PTILE + GTILE;
-  static constexpr int XCH = 4 * 4 * NT * 32 * 2;  // epilogue parity exchange
   static constexpr size_t bytes() {
-    return (size_t)(ADJ_STAGES * STAGE + XCH) * 8 + 2 * ADJ_STAGES * 8 + kProducerWarps * ADJ_LC * 16;
+    return (size_t)ADJ_STAGES * STAGE * 8 + 2 * ADJ_STAGES * 8 + kProducerWarps * ADJ_LC * 16;
   }
 };
 
@@ -598,37 +600,27 @@ __global__ void __launch_bounds__(32 * kProducerWarps) ptab_adj_kernel(AdjArgs a
   }
 }
 
+// DMMAs of one (k-step, parity) for a consumer warp: M-tiles ii >= I0 of its two
 template <int I0, int NT>
-__device__ __forceinline__ void adj_ks_run(double (&acc)[4][NT][2], const double (&a)[4], const double (&b)[NT]) {
+__device__ __forceinline__ void adj_ks_run(double (&acc)[2][NT][2], const double (&a)[2], const double (&b)[NT]) {
 #pragma unroll
   for (int jn = 0; jn < NT; ++jn)
 #pragma unroll
-    for (int ii = I0; ii < 4; ++ii) dmma_m8n8k4(acc[ii][jn][0], acc[ii][jn][1], a[ii], b[jn]);
-}
-
-template <int NT>
-__device__ __forceinline__ void adj_ks_dmma(int ifirst, double (&acc)[4][NT][2], const double (&a)[4],
-                                            const double (&b)[NT]) {
-  switch (ifirst) {
-    case 0: adj_ks_run<0, NT>(acc, a, b); break;
-    case 1: adj_ks_run<1, NT>(acc, a, b); break;
-    case 2: adj_ks_run<2, NT>(acc, a, b); break;
-    case 3: adj_ks_run<3, NT>(acc, a, b); break;
-    default: break;
-  }
+    for (int ii = I0; ii < 2; ++ii) dmma_m8n8k4(acc[ii][jn][0], acc[ii][jn][1], a[ii], b[jn]);
 }
 
 // Persistent: one CTA per SM walks the (order m, 128-pair chunk) items in
 // descending-work order (item = blockIdx.x + k * gridDim.x; m ascending), with
 // one stage counter across items, so the producers fill the next item's stages
-// while the consumers run the previous item's epilogue.  The parity exchange of
-// the epilogue has its own shared buffer for the same reason.
+// while the consumers run the previous item's epilogue.  Each consumer warp owns
+// both parities of its M-tiles, so the epilogue (north = E + O, south = E - O)
+// is register-local: no exchange buffer and no CTA barrier, and the shared
+// memory goes to a fifth stage.
 template <int NT>
 __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args) {
   extern __shared__ __align__(128) double smem[];
   using SM = AdjSmem<NT>;
-  double* xch = smem + ADJ_STAGES * SM::STAGE;  // [mq][ii][jn][lane][2]
-  uint64_t* full = reinterpret_cast<uint64_t*>(xch + SM::XCH);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ADJ_STAGES * SM::STAGE);
   uint64_t* empty = full + ADJ_STAGES;
   double2* abw_all = reinterpret_cast<double2*>(empty + ADJ_STAGES);
 
@@ -729,13 +721,12 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
   }
 
   // -------------------------------- consumers --------------------------------
-  // warp (par, mq): M-tiles mq, mq+4, mq+8, mq+12 x all NT n-tiles of parity
-  // par.  The interleave gives every SM sub-partition (warp % 4 == mq) the same
-  // mix of polar and equatorial pairs, so the polar skip shortens the stage
-  // instead of idling one sub-partition's DMMA pipe.
+  // warp cw owns M-tiles cw and cw + 8 (pairs 8 cw .. 8 cw + 7 and 64 + 8 cw ..)
+  // for both parities and all NT n-tiles; the SM sub-partition cw % 4 thus sees
+  // M-tiles {s, s + 4, s + 8, s + 12}, the same mix of polar and equatorial
+  // pairs on every sub-partition, so the polar skip shortens the stage instead
+  // of idling one sub-partition's DMMA pipe.
   const int cw = consumer_index(warp);
-  const int par = cw >> 2;
-  const int mq = cw & 3;
   const int g = lane >> 2, q = lane & 3;
   uint32_t sc = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
@@ -743,19 +734,22 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
     const int rc = item % args.nrc;
     const int nlc = (Lt + 1 - m + ADJ_LC - 1) / ADJ_LC;
     // first degree at which each of the warp's M-tiles has a pair above the polar threshold
-    int mt_start[4];
+    int mt_start[2];
     {
-      int v = args.start_l[(size_t)m * args.nPpad + rc * ADJ_RC + 8 * mq + 32 * (lane >> 3) + (lane & 7)];
+      const int l16 = lane & 15;
+      int v = args.start_l[(size_t)m * args.nPpad + rc * ADJ_RC + 8 * cw + 64 * (l16 >> 3) + (l16 & 7)];
 #pragma unroll
       for (int o = 1; o < 8; o <<= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
 #pragma unroll
-      for (int ii = 0; ii < 4; ++ii) mt_start[ii] = __shfl_sync(0xffffffffu, v, 8 * ii);
+      for (int ii = 0; ii < 2; ++ii) mt_start[ii] = __shfl_sync(0xffffffffu, v, 8 * ii);
     }
-    double acc[4][NT][2];
+    double acc[2][2][NT][2];  // [parity][M-tile][n-tile][re/im]
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int b = 0; b < NT; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+      for (int p2 = 0; p2 < 2; ++p2)
+#pragma unroll
+        for (int b = 0; b < NT; ++b) acc[a][p2][b][0] = acc[a][p2][b][1] = 0.0;
 
     for (int lc = 0; lc < nlc; ++lc, ++sc) {
       const int stage = sc % ADJ_STAGES;
@@ -767,15 +761,17 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
       if (tr && cw == 0) args.trace[sc * 8 + 4] = clock64();
       const double* Ps = smem + stage * SM::STAGE;
       const double* Gs = Ps + ADJ_PTILE;
-      const int mts = min(min(mt_start[0], mt_start[1]), min(mt_start[2], mt_start[3]));
+      const int mts = min(mt_start[0], mt_start[1]);
       if (!(args.dbg & 1) && mts <= l0s + ADJ_LC - 1 && l0s <= Lt) {
-        // k-step fragments double-buffered in registers: the loads of step ks+1
-        // are in flight while the DMMAs of step ks issue
-        double a[2][4], b[2][NT];
-        auto load = [&](int ks, int bufi) {
+        // half-steps t = (k-step ks = t / 2, parity t % 2), fragments double-buffered
+        // in registers: the loads of half-step t + 1 are in flight while the DMMAs
+        // of half-step t issue
+        double a[2][2], b[2][NT];
+        auto load = [&](int t, int bufi) {
+          const int ks = t >> 1, par = t & 1;
 #pragma unroll
-          for (int ii = 0; ii < 4; ++ii) {
-            const int i = mq + 4 * ii;
+          for (int ii = 0; ii < 2; ++ii) {
+            const int i = cw + 8 * ii;
             a[bufi][ii] = lds_f64(&Ps[i * ADJ_MTILE + (par * ADJ_KS + ks) * 32 + adj_swz(g, q, i)]);
           }
 #pragma unroll
@@ -783,50 +779,29 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
         };
         load(0, 0);
 #pragma unroll
-        for (int ks = 0; ks < ADJ_KS; ++ks) {
-          if (ks + 1 < ADJ_KS) load(ks + 1, (ks + 1) & 1);
-          // k-step ks holds degrees l0s + 8 ks .. + 7 (one parity).  Active M-tiles
-          // form a suffix (pairs nearer the equator start earlier; padding pairs at
-          // the end never start, their accumulators are discarded): dispatch on the
-          // first active one with a real branch (a predicated-off DMMA still
-          // occupies the pipe); k-steps past Lt hold zero coefficient rows.
+        for (int t = 0; t < 2 * ADJ_KS; ++t) {
+          if (t + 1 < 2 * ADJ_KS) load(t + 1, (t + 1) & 1);
+          // k-step ks holds degrees l0s + 8 ks .. + 7 of both parities.  The active
+          // M-tile set is a suffix of {cw, cw + 8} (pairs nearer the equator start
+          // earlier); k-steps past Lt hold zero coefficient rows.  Real branches:
+          // a predicated-off DMMA still occupies the pipe.
+          const int ks = t >> 1, par = t & 1;
           const int khi = l0s + 8 * ks + 7;
-          int ifirst = 4;
           if (l0s + 8 * ks <= Lt) {
-#pragma unroll
-            for (int ii = 3; ii >= 0; --ii)
-              if (mt_start[ii] <= khi) ifirst = ii;
+            if (mt_start[0] <= khi) adj_ks_run<0, NT>(acc[par], a[t & 1], b[t & 1]);
+            else if (mt_start[1] <= khi) adj_ks_run<1, NT>(acc[par], a[t & 1], b[t & 1]);
           }
-          adj_ks_dmma<NT>(ifirst, acc, a[ks & 1], b[ks & 1]);
         }
       }
       if (tr) args.trace[sc * 8 + (cw == 0 ? 5 : 7)] = clock64();
       mbar_arrive(&empty[stage]);
     }
-    const bool tre = args.trace && blockIdx.x == args.trace_cta && cw == 0 && lane == 0 && sc <= 1024;
-    if (tre) args.trace[4096 * 8 + (sc - 1) * 4] = clock64();
 
-    // epilogue: combine parities through the exchange buffer (odd warps publish,
-    // even warps finish); the first barrier also retires the previous item's reads
-    asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps));
-    if (tre) args.trace[4096 * 8 + (sc - 1) * 4 + 1] = clock64();
-    if (par == 1) {
-#pragma unroll
-      for (int ii = 0; ii < 4; ++ii)
-#pragma unroll
-        for (int jn = 0; jn < NT; ++jn) {
-          double* d = xch + ((size_t)((mq * 4 + ii) * NT + jn) * 32 + lane) * 2;
-          d[0] = acc[ii][jn][0];
-          d[1] = acc[ii][jn][1];
-        }
-    }
-    asm volatile("bar.sync 1, %0;" ::"r"(32 * kConsumerWarps));
-    if (tre) args.trace[4096 * 8 + (sc - 1) * 4 + 2] = clock64();
-    if (par == 0 && rc * ADJ_RC + 8 * mq < args.nP && !(args.dbg & 4)) {
-      // per-lane column targets first (the column -> (field, comp, sign) map and
-      // the bin row depend only on jn and q), ring indices next, then only
-      // stores (bin-major layout: lanes g are 8 consecutive pairs -> 8 consecutive
-      // north (south) rings, i.e. 128-byte runs of one bin row)
+    // epilogue, register-local: north = E + O, south = E - O (bin-major layout:
+    // lanes g are 8 consecutive pairs -> 8 consecutive north (south) rings, i.e.
+    // 128-byte runs of one bin row).  Column -> (field, comp, sign) and the bin
+    // rows depend only on jn and q.
+    if (rc * ADJ_RC + 8 * cw < args.nP && !(args.dbg & 4)) {
       const long long bin0 = spec_bin(args.lay, m, 0, args.n_phi), bin1 = spec_bin(args.lay, m, 1, args.n_phi);
       double2* dst[NT];
       bool ok[NT];
@@ -838,27 +813,21 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
         dst[jn] = args.S + comp * args.lay.cs + (long long)(args.b0 + b) * args.n_theta * args.lay.rs +
                   (sgn ? bin1 : bin0) * args.lay.bs;
       }
-      int rn[4], rs[4];
 #pragma unroll
-      for (int ii = 0; ii < 4; ++ii) {
-        const int p = rc * ADJ_RC + (mq + 4 * ii) * 8 + g;
-        rn[ii] = args.pair_n[p];
-        rs[ii] = args.pair_s[p];
-      }
-#pragma unroll
-      for (int ii = 0; ii < 4; ++ii) {
-        if (rn[ii] < 0) continue;
+      for (int ii = 0; ii < 2; ++ii) {
+        const int p = rc * ADJ_RC + (cw + 8 * ii) * 8 + g;
+        const int rn = args.pair_n[p], rs = args.pair_s[p];
+        if (rn < 0) continue;
 #pragma unroll
         for (int jn = 0; jn < NT; ++jn) {
           if (!ok[jn]) continue;
-          const double2 o = *reinterpret_cast<const double2*>(xch + ((size_t)((mq * 4 + ii) * NT + jn) * 32 + lane) * 2);
-          const double er = acc[ii][jn][0], ei = acc[ii][jn][1];
-          dst[jn][rn[ii] * args.lay.rs] = make_double2(er + o.x, ei + o.y);
-          if (rs[ii] >= 0) dst[jn][rs[ii] * args.lay.rs] = make_double2(er - o.x, ei - o.y);
+          const double er = acc[0][ii][jn][0], ei = acc[0][ii][jn][1];
+          const double orr = acc[1][ii][jn][0], oi = acc[1][ii][jn][1];
+          dst[jn][rn * args.lay.rs] = make_double2(er + orr, ei + oi);
+          if (rs >= 0) dst[jn][rs * args.lay.rs] = make_double2(er - orr, ei - oi);
         }
       }
     }
-    if (tre) args.trace[4096 * 8 + (sc - 1) * 4 + 3] = clock64();
   }
 }
 
