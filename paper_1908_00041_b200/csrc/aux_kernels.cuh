@@ -194,12 +194,9 @@ __global__ void fold_fwd_kernel(FoldArgs a) {
   double* xt = a.X + ((size_t)mi * a.nchunks + chunk) * (2 * 8 * a.NT * 32) + (size_t)ks * a.NT * 32 + q * 4;
   const size_t par_stride = (size_t)8 * a.NT * 32;
   auto put4 = [&](int col, double2 v0, double2 v1, double2 o0, double2 o1) {  // col % 4 == 0
-    double2* e = reinterpret_cast<double2*>(xt + (col >> 3) * 32 + ((col >> 2) & 1) * 16);
-    double2* o = reinterpret_cast<double2*>(xt + par_stride + (col >> 3) * 32 + ((col >> 2) & 1) * 16);
-    e[0] = v0;
-    e[1] = v1;
-    o[0] = o0;
-    o[1] = o1;
+    const int off = (col >> 3) * 32 + ((col >> 2) & 1) * 16;
+    st_global_v4(xt + off, v0, v1);
+    st_global_v4(xt + par_stride + off, o0, o1);
   };
   const double2 zero = make_double2(0.0, 0.0);
   if (z == 3 * a.nfields) {  // padding columns 12 nf .. 8 NT - 1 (at most one group of 4)

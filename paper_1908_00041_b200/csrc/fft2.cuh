@@ -300,16 +300,12 @@ __global__ void __launch_bounds__(F2_T, 2) fft_fold_kernel(Fft2Args a, int nitem
       if (m == 0) Em = Om = make_double2(0.0, 0.0);
     }
     double* xt = a.X + ((size_t)m * a.nchunks + chunk) * tile;
-    double2* e2 = reinterpret_cast<double2*>(xt + off);
-    double2* o2 = reinterpret_cast<double2*>(xt + par_stride + off);
-    e2[0] = Ep;
-    e2[1] = Em;
-    o2[0] = Op;
-    o2[1] = Om;
+    st_global_v4(xt + off, Ep, Em);
+    st_global_v4(xt + par_stride + off, Op, Om);
     if (padcols) {
-      double2* pe = reinterpret_cast<double2*>(xt + poff);
-      double2* po = reinterpret_cast<double2*>(xt + par_stride + poff);
-      pe[0] = pe[1] = po[0] = po[1] = make_double2(0.0, 0.0);
+      const double2 z = make_double2(0.0, 0.0);
+      st_global_v4(xt + poff, z, z);
+      st_global_v4(xt + par_stride + poff, z, z);
     }
   }
 }
