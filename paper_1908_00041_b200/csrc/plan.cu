@@ -1038,12 +1038,23 @@ int fv_adjoint_points(fvPlan* p, const double* xyz, long long M, const double* a
     {
       StageMark mk(p, 2, s);
       fv::PtsArgs pa{xyz, M, p->G, p->rowofs, p->ab, p->abofs, reinterpret_cast<double2*>(T), Lt, B, b0};
-      const unsigned grid = (unsigned)((M + 127) / 128);
-      switch (nf) {
-        case 1: fv::adjoint_points_kernel<1><<<grid, 128, 0, s>>>(pa); break;
-        case 2: fv::adjoint_points_kernel<2><<<grid, 128, 0, s>>>(pa); break;
-        case 3: fv::adjoint_points_kernel<3><<<grid, 128, 0, s>>>(pa); break;
-        default: fv::adjoint_points_kernel<4><<<grid, 128, 0, s>>>(pa); break;
+      const unsigned grid = (unsigned)((M + fv::PTS_THREADS - 1) / fv::PTS_THREADS);
+      const size_t smem = (size_t)2 * (Lt + 1) * 12 * nf * sizeof(double);
+      const bool stage = smem <= 200 * 1024;  // else rows straight from global memory
+      auto launch = [&](auto kern) -> int {
+        if (stage) FV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, fv::PTS_THREADS, stage ? smem : 0, s>>>(pa);
+        return FV_OK;
+      };
+      switch (nf * 2 + (stage ? 1 : 0)) {
+        case 3: FV_TRY(launch(fv::adjoint_points_kernel<1, true>)); break;
+        case 2: FV_TRY(launch(fv::adjoint_points_kernel<1, false>)); break;
+        case 5: FV_TRY(launch(fv::adjoint_points_kernel<2, true>)); break;
+        case 4: FV_TRY(launch(fv::adjoint_points_kernel<2, false>)); break;
+        case 7: FV_TRY(launch(fv::adjoint_points_kernel<3, true>)); break;
+        case 6: FV_TRY(launch(fv::adjoint_points_kernel<3, false>)); break;
+        case 9: FV_TRY(launch(fv::adjoint_points_kernel<4, true>)); break;
+        default: FV_TRY(launch(fv::adjoint_points_kernel<4, false>)); break;
       }
       FV_CUDA(cudaGetLastError());
     }

@@ -3,8 +3,8 @@
 //
 // One thread per point.  Orders are walked in sequence so the diagonal seed is
 // a running product (extended range), the l-recurrence runs in registers, and
-// the merged coefficient rows (sigma applied, m-major) are read as warp-uniform
-// broadcasts.  The per-point recurrence cannot be shared between points, so
+// the merged coefficient rows (sigma applied, m-major) are staged per order in
+// shared memory and read as broadcasts.  The per-point recurrence cannot be shared between points, so
 // this kernel is FP64-pipe bound on the recurrence plus 12*nfields FMA per
 // (l, m, point).
 #pragma once
@@ -23,16 +23,40 @@ struct PtsArgs {
   int Lt, B_total, b0;
 };
 
-template <int NF>
-__global__ void __launch_bounds__(128) adjoint_points_kernel(PtsArgs a) {
+constexpr int PTS_THREADS = 256;
+
+// Coefficient rows of order m (rows rowofs[m] .. + Lt - m, NC doubles each) into
+// shared memory with cp.async (16-byte pieces); one commit group per order.
+template <int NC>
+__device__ __forceinline__ void pts_stage_rows(const PtsArgs& a, int m, double* dst) {
+  if (m <= a.Lt) {
+    const double2* src = reinterpret_cast<const double2*>(a.Grow + (size_t)a.rowofs[m] * NC);
+    const int n2 = (a.Lt + 1 - m) * NC / 2;
+    for (int i = threadIdx.x; i < n2; i += PTS_THREADS)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + 2 * i)), "l"(src + i) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+// The block's points walk the orders together; order m's coefficient rows are
+// staged in shared memory (double-buffered: the rows of m + 1 are in flight
+// while m is consumed) and read as broadcasts, the next row prefetched into
+// registers one degree ahead of its FMAs.  STAGE = false (degrees whose two
+// row buffers exceed shared memory) reads the rows from global memory instead.
+template <int NF, bool STAGE>
+__global__ void __launch_bounds__(PTS_THREADS) adjoint_points_kernel(PtsArgs a) {
+  constexpr int NC = 12 * NF;
+  extern __shared__ __align__(16) double pts_rows[];  // 2 x (Lt + 1) x NC
+  const int Lt = a.Lt;
+  const size_t bufsz = (size_t)(Lt + 1) * NC;
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= a.M) return;
-  const double x = a.xyz[3 * p], y = a.xyz[3 * p + 1], zr = a.xyz[3 * p + 2];
+  const bool live = p < a.M;
+  const long long pc = live ? p : a.M - 1;
+  const double x = a.xyz[3 * pc], y = a.xyz[3 * pc + 1], zr = a.xyz[3 * pc + 2];
   const double t = fmin(1.0, fmax(-1.0, zr));
   const double s = sqrt(fmax(0.0, 1.0 - t * t));
   double phi = atan2(y, x);
   if (phi < 0.0) phi += 6.283185307179586;  // np.mod(atan2, 2*pi) (favest/core.py:82)
-  constexpr int NC = 12 * NF;
   double out[NF][6];
 #pragma unroll
   for (int b = 0; b < NF; ++b)
@@ -40,8 +64,14 @@ __global__ void __launch_bounds__(128) adjoint_points_kernel(PtsArgs a) {
     for (int c = 0; c < 6; ++c) out[b][c] = 0.0;
   double seed = 0.28209479177387814;
   int se = 0;
-  const int Lt = a.Lt;
+  if (STAGE) pts_stage_rows<NC>(a, 0, pts_rows);
   for (int m = 0; m <= Lt; ++m) {
+    const double* rows = STAGE ? pts_rows + (m & 1) * bufsz : a.Grow + (size_t)a.rowofs[m] * NC;
+    if (STAGE) {
+      pts_stage_rows<NC>(a, m + 1, pts_rows + ((m + 1) & 1) * bufsz);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // order m's rows have landed
+      __syncthreads();
+    }
     if (m > 0) {
       const double c = sqrt((2 * m + 1) / (2.0 * m));
       seed = __dmul_rn(__dmul_rn(-c, s), seed);
@@ -55,18 +85,36 @@ __global__ void __launch_bounds__(128) adjoint_points_kernel(PtsArgs a) {
     for (int b = 0; b < NF; ++b)
 #pragma unroll
       for (int c = 0; c < 12; ++c) acc[b][c] = 0.0;
-    const double* rows = a.Grow + (size_t)a.rowofs[m] * NC;
     double p2 = seed, p1 = __dmul_rn(__dmul_rn(sqrt(2 * m + 3.0), t), seed);
     int e = se;
     const double2* abm = a.ab + a.abofs[m];
+    double2 gnext[NF][6];
+#pragma unroll
+    for (int b = 0; b < NF; ++b)
+#pragma unroll
+      for (int c = 0; c < 6; ++c) gnext[b][c] = reinterpret_cast<const double2*>(rows)[6 * b + c];
+    double2 abn = (m + 2 <= Lt) ? __ldg(abm) : make_double2(0.0, 0.0);
     for (int l = m; l <= Lt; ++l) {
+      double2 g[NF][6];
+#pragma unroll
+      for (int b = 0; b < NF; ++b)
+#pragma unroll
+        for (int c = 0; c < 6; ++c) g[b][c] = gnext[b][c];
+      if (l < Lt) {
+        const double2* nrow = reinterpret_cast<const double2*>(rows + (size_t)(l + 1 - m) * NC);
+#pragma unroll
+        for (int b = 0; b < NF; ++b)
+#pragma unroll
+          for (int c = 0; c < 6; ++c) gnext[b][c] = nrow[6 * b + c];
+      }
       double v;
       if (l == m) {
         v = p2;
       } else if (l == m + 1) {
         v = p1;
       } else {
-        const double2 abv = abm[l - m - 2];  // (a_l, a_l * b_l)
+        const double2 abv = abn;  // (a_l, a_l * b_l)
+        if (l + 1 <= Lt) abn = __ldg(abm + (l + 1 - m - 2));
         const double pn = fma(abv.x * t, p1, -(abv.y * p2));
         p2 = p1;
         p1 = pn;
@@ -78,14 +126,12 @@ __global__ void __launch_bounds__(128) adjoint_points_kernel(PtsArgs a) {
         v = p1;
       }
       if (e < 0) v = xr_value(v, e);
-      const double* row = rows + (size_t)(l - m) * NC;
 #pragma unroll
       for (int b = 0; b < NF; ++b)
 #pragma unroll
-        for (int c = 0; c < 12; c += 2) {
-          const double2 g = __ldg(reinterpret_cast<const double2*>(row + 12 * b + c));
-          acc[b][c] = fma(v, g.x, acc[b][c]);
-          acc[b][c + 1] = fma(v, g.y, acc[b][c + 1]);
+        for (int c = 0; c < 6; ++c) {
+          acc[b][2 * c] = fma(v, g[b][c].x, acc[b][2 * c]);
+          acc[b][2 * c + 1] = fma(v, g[b][c].y, acc[b][2 * c + 1]);
         }
     }
     double sn, cs;
@@ -104,7 +150,9 @@ __global__ void __launch_bounds__(128) adjoint_points_kernel(PtsArgs a) {
           out[b][2 * c + 1] += cs * ni - sn * nr;
         }
       }
+    if (STAGE) __syncthreads();  // buffer (m & 1) is refilled with order m + 2 next
   }
+  if (!live) return;
 #pragma unroll
   for (int b = 0; b < NF; ++b)
 #pragma unroll
