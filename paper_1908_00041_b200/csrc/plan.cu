@@ -1039,6 +1039,28 @@ int fv_adjoint_points(fvPlan* p, const double* xyz, long long M, const double* a
       StageMark mk(p, 2, s);
       fv::PtsArgs pa{xyz, M, p->G, p->rowofs, p->ab, p->abofs, reinterpret_cast<double2*>(T), Lt, B, b0};
       const unsigned grid = (unsigned)((M + fv::PTS_THREADS - 1) / fv::PTS_THREADS);
+      // tensor-core kernel when its two row buffers fit shared memory (FV_PTS_DMMA=0: FMA kernel)
+      {
+        const char* e = std::getenv("FV_PTS_DMMA");
+        const int nt = (12 * nf + 7) / 8, rs = ((8 * nt + 11) / 16) * 16 + 4;
+        const size_t sd = (size_t)2 * (((Lt + 1 + 3) & ~3) * rs + 2 * (Lt + 1)) * sizeof(double) +
+                          fv::PTS_THREADS / 32 * 128 * sizeof(double);
+        if (!(e && std::atoi(e) == 0) && sd <= 220 * 1024) {
+          auto launchd = [&](auto kern) -> int {
+            FV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sd));
+            kern<<<grid, fv::PTS_THREADS, sd, s>>>(pa);
+            return FV_OK;
+          };
+          switch (nf) {
+            case 1: FV_TRY(launchd(fv::adjoint_points_dmma_kernel<1>)); break;
+            case 2: FV_TRY(launchd(fv::adjoint_points_dmma_kernel<2>)); break;
+            case 3: FV_TRY(launchd(fv::adjoint_points_dmma_kernel<3>)); break;
+            default: FV_TRY(launchd(fv::adjoint_points_dmma_kernel<4>)); break;
+          }
+          FV_CUDA(cudaGetLastError());
+          continue;
+        }
+      }
       const size_t smem = (size_t)2 * (Lt + 1) * 12 * nf * sizeof(double);
       const bool stage = smem <= 200 * 1024;  // else rows straight from global memory
       auto launch = [&](auto kern) -> int {

@@ -160,4 +160,177 @@ __global__ void __launch_bounds__(PTS_THREADS) adjoint_points_kernel(PtsArgs a) 
       a.T[((size_t)(a.b0 + b) * a.M + p) * 3 + c] = make_double2(out[b][2 * c], out[b][2 * c + 1]);
 }
 
+// ---------------------------------------------------------------------------
+// Tensor-core form of the scattered adjoint.  For each order m the block
+// computes C_m = P_m G_m with P_m[p][l] = Pbar_l^m(z_p) (points x degrees) and
+// G_m[l][col] the merged coefficient rows (degrees x 12 NF columns), on
+// DMMA.8x8x4: a warp owns 32 points = 4 M-tiles, k-steps are 4 degrees.  Each
+// lane runs the recurrence of its own point (extended range as above); the
+// four values of a k-step go through a 1 KB per-warp shared buffer into A
+// fragments (lane (row r, k) reads point 8 i + r, degree k).  The rows of
+// order m are staged in shared memory with a padded stride (RS = 4 mod 16:
+// B-fragment reads are conflict free) and double-buffered across orders.
+// After the last degree of m the accumulators (point, column pair) are rotated
+// by e^{+-i m phi} of their point and added to the output accumulators; the
+// +m / -m column pairs of one (field, component) sit in lanes q and q ^ 1 and
+// are combined once at the end.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int ptsd_nt(int nf) { return (12 * nf + 7) / 8; }
+__host__ __device__ constexpr int ptsd_rs(int nf) { return ((8 * ptsd_nt(nf) + 11) / 16) * 16 + 4; }
+
+template <int NF>
+__device__ __forceinline__ void ptsd_stage_rows(const PtsArgs& a, int m, double* dst, double2* abdst) {
+  constexpr int NC = 12 * NF, RS = ptsd_rs(NF);
+  if (m <= a.Lt) {
+    // recurrence coefficients (a_l, a_l b_l), l = m + 2 .. Lt
+    const double2* abs = a.ab + a.abofs[m];
+    for (int i = threadIdx.x; i < a.Lt - m - 1; i += PTS_THREADS)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(abdst + i)), "l"(abs + i) : "memory");
+    const double2* src = reinterpret_cast<const double2*>(a.Grow + (size_t)a.rowofs[m] * NC);
+    const int nrow = a.Lt + 1 - m;
+    const int n2 = nrow * (NC / 2);
+    for (int i = threadIdx.x; i < n2; i += PTS_THREADS) {
+      const int r = i / (NC / 2), c = i - r * (NC / 2);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + r * RS + 2 * c)), "l"(src + i)
+                   : "memory");
+    }
+    // zero rows up to the next multiple of 4 and the padding columns 12 NF .. 8 NT - 1
+    const int nr4 = (nrow + 3) & ~3;
+    for (int i = threadIdx.x; i < nr4 * (RS - NC); i += PTS_THREADS) {
+      const int r = i / (RS - NC), c = NC + i % (RS - NC);
+      dst[r * RS + c] = 0.0;
+    }
+    for (int i = threadIdx.x; i < (nr4 - nrow) * NC; i += PTS_THREADS) dst[(nrow + i / NC) * RS + i % NC] = 0.0;
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+template <int NF>
+__global__ void __launch_bounds__(PTS_THREADS, NF == 1 ? 2 : 1) adjoint_points_dmma_kernel(PtsArgs a) {
+  constexpr int NT = ptsd_nt(NF), RS = ptsd_rs(NF);
+  extern __shared__ __align__(16) double ptsd_smem[];
+  const int Lt = a.Lt;
+  const int nrows4 = (Lt + 1 + 3) & ~3;
+  const size_t bufsz = (size_t)nrows4 * RS + 2 * (Lt + 1);  // rows, then (a_l, a_l b_l)
+  double* rowbuf = ptsd_smem;                       // 2 x bufsz
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* pbuf = ptsd_smem + 2 * bufsz + warp * 128;  // [32 points][4 degrees]
+  const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = p < a.M;
+  const long long pc = live ? p : a.M - 1;
+  const double x = a.xyz[3 * pc], y = a.xyz[3 * pc + 1], zr = a.xyz[3 * pc + 2];
+  const double t = fmin(1.0, fmax(-1.0, zr));
+  const double s = sqrt(fmax(0.0, 1.0 - t * t));
+  double phi = atan2(y, x);
+  if (phi < 0.0) phi += 6.283185307179586;  // np.mod(atan2, 2*pi) (favest/core.py:82)
+  const int g = lane >> 2, q = lane & 3;
+  // phi of the four points this lane holds accumulators for (M-tile i, row g)
+  double phi_i[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) phi_i[i] = __shfl_sync(0xffffffffu, phi, 8 * i + g);
+  double out[4][NT][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) out[i][j][0] = out[i][j][1] = 0.0;
+  double seed = 0.28209479177387814;
+  int se = 0;
+  auto abuf = [&](int k) { return reinterpret_cast<double2*>(rowbuf + k * bufsz + (size_t)nrows4 * RS); };
+  ptsd_stage_rows<NF>(a, 0, rowbuf, abuf(0));
+  for (int m = 0; m <= Lt; ++m) {
+    const double* rows = rowbuf + (m & 1) * bufsz;
+    const double2* abm = abuf(m & 1);
+    ptsd_stage_rows<NF>(a, m + 1, rowbuf + ((m + 1) & 1) * bufsz, abuf((m + 1) & 1));
+    asm volatile("cp.async.wait_group 1;" ::: "memory");  // order m's rows have landed
+    __syncthreads();
+    if (m > 0) {
+      const double c = sqrt((2 * m + 1) / (2.0 * m));
+      seed = __dmul_rn(__dmul_rn(-c, s), seed);
+      if (fabs(seed) < 0x1p-512 && seed != 0.0) {
+        seed *= 0x1p512;
+        se -= XR_SHIFT;
+      }
+    }
+    double acc[4][NT][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    double p2 = seed, p1 = __dmul_rn(__dmul_rn(sqrt(2 * m + 3.0), t), seed);
+    int e = se;
+    for (int l0 = m; l0 <= Lt; l0 += 4) {
+      double v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int l = l0 + k;
+        double val;
+        if (l > Lt) {
+          val = 0.0;
+        } else if (l == m) {
+          val = p2;
+        } else if (l == m + 1) {
+          val = p1;
+        } else {
+          const double2 abv = abm[l - m - 2];  // (a_l, a_l * b_l), staged
+          const double pn = fma(abv.x * t, p1, -(abv.y * p2));
+          p2 = p1;
+          p1 = pn;
+          if (e < 0 && fabs(p1) >= 0x1p512) {
+            p1 *= 0x1p-512;
+            p2 *= 0x1p-512;
+            e += XR_SHIFT;
+          }
+          val = p1;
+        }
+        v[k] = (e < 0 && l <= Lt) ? xr_value(val, e) : val;
+      }
+      __syncwarp();
+      reinterpret_cast<double2*>(pbuf)[2 * lane] = make_double2(v[0], v[1]);
+      reinterpret_cast<double2*>(pbuf)[2 * lane + 1] = make_double2(v[2], v[3]);
+      __syncwarp();
+      double af[4], bf[NT];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = pbuf[(8 * i + g) * 4 + q];
+      const double* brow = rows + (size_t)(l0 - m + q) * RS + g;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) bf[j] = brow[8 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
+    // rotate by e^{+i m phi} (sign 0 columns) / e^{-i m phi} (sign 1 columns) and accumulate
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      double sn, cs;
+      sincos(phi_i[i] * m, &sn, &cs);
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        const int cp = 4 * j + q;  // column pair: 6 b + 2 c + sign
+        const double sg = (cp & 1) ? -sn : sn;
+        if ((cp & 1) && m == 0) continue;  // the -0 order is not a separate coefficient
+        const double re = acc[i][j][0], im = acc[i][j][1];
+        out[i][j][0] += cs * re - sg * im;
+        out[i][j][1] += cs * im + sg * re;
+      }
+    }
+    __syncthreads();  // buffer (m & 1) is refilled with order m + 2 next
+  }
+  // combine the +m / -m column pairs (lanes q, q ^ 1) and write T
+  const long long pbase = (long long)blockIdx.x * blockDim.x + warp * 32;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const double r = out[i][j][0] + __shfl_xor_sync(0xffffffffu, out[i][j][0], 1);
+      const double im = out[i][j][1] + __shfl_xor_sync(0xffffffffu, out[i][j][1], 1);
+      const int cp = 4 * j + q;
+      const long long pt = pbase + 8 * i + g;
+      if ((q & 1) == 0 && cp < 6 * NF && pt < a.M) {
+        const int b = cp / 6, c = (cp % 6) >> 1;
+        a.T[((size_t)(a.b0 + b) * a.M + pt) * 3 + c] = make_double2(r, im);
+      }
+    }
+}
+
 }  // namespace fv
