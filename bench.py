@@ -22,7 +22,6 @@ import argparse
 import json
 import os
 import sys
-import threading
 import time
 
 import numpy as np
@@ -59,8 +58,12 @@ def hbm_peak():
 # clocks during the timed region
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    """Polls NVML (SM clock, max clock, clock-event reasons) every ~2 ms in a
-    thread while the timed region runs (the B200_PROFILING.md clocks line)."""
+    """NVML SM clock, max clock and clock-event reasons (the B200_PROFILING.md
+    clocks line), read DURING the timed region without touching the launch
+    loop: NVML calls take driver locks that stall kernel launches from another
+    thread, so all steps are enqueued first and ``drain(event)`` then polls
+    every ~2 ms from this thread until the device has executed the timed queue
+    (the end event completes)."""
 
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
@@ -69,7 +72,6 @@ class ClockSampler:
         self.dev = torch_device
         self.samples = []
         self.max_mhz = None
-        self.stop = threading.Event()
         self.ok = False
 
     def __enter__(self):
@@ -88,15 +90,12 @@ class ClockSampler:
             self.nv, self.h = nv, h
             self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
             self.ok = True
-            self.t = threading.Thread(target=self._run, daemon=True)
-            self.t.start()
         except Exception as exc:  # pragma: no cover - NVML missing
             self.err = str(exc)
         return self
 
     def sample(self):
-        """One (SM clock, reasons) reading; also called from the main thread inside
-        the timed region, so short regions still carry samples."""
+        """One (SM clock, reasons) reading."""
         if not self.ok:
             return
         nv, h = self.nv, self.h
@@ -110,15 +109,14 @@ class ClockSampler:
         except Exception:
             pass
 
-    def _run(self):
-        while not self.stop.is_set():
+    def drain(self, end_event):
+        """Sample every ~2 ms while the device still runs the enqueued timed steps."""
+        while not end_event.query():
             self.sample()
             time.sleep(0.002)
 
     def __exit__(self, *a):
-        self.stop.set()
-        if self.ok:
-            self.t.join(timeout=1)
+        pass
 
     def summary(self):
         if not self.samples:
@@ -129,7 +127,7 @@ class ClockSampler:
                 if rs & bit:
                     reasons.add(name)
         return {"sm_mhz": float(np.median([c for c, _ in self.samples])), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(reasons), "samples": len(self.samples), "source": "NVML, 2 ms polling"}
+                "reasons": sorted(reasons), "samples": len(self.samples), "source": "NVML, 2 ms polling while the device drains the enqueued timed steps"}
 
 
 # ---------------------------------------------------------------------------
@@ -293,10 +291,8 @@ def run_ours(args, rank, world, local_rank):
         e0.record(stream)
         for i in range(args.steps):
             step()
-            if i == 1:
-                clocks.sample()  # the device is busy with the queued steps by now
         e1.record(stream)
-        clocks.sample()
+        clocks.drain(e1)  # the device is still executing the queued timed steps
         barrier()
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     stage_ms = plan.stage_ms()
@@ -486,10 +482,8 @@ def run_c4(args, rank, world, local_rank):
         e0.record(stream)
         for i in range(args.steps):
             step()
-            if i == 1:
-                clocks.sample()  # the device is busy with the queued steps by now
         e1.record(stream)
-        clocks.sample()
+        clocks.drain(e1)  # the device is still executing the queued timed steps
         barrier()
     ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
     # parity guard on the timed outputs: adjoint(forward(adjoint(c))) vs adjoint(c) on this rank's rings

@@ -17,6 +17,9 @@
  *   fv_adjoint_points  <- adjoint_favest(coeffs, points) (direct route)
  *                         favest/transforms.py:150-181 with
  *                         _adjoint_direct_values favest/scalar.py:120-128
+ *   fv_forward_points  <- forward_favest(samples, rule, ..., "direct-scalar")
+ *                         favest/transforms.py:79-147 with
+ *                         _forward_direct_values favest/scalar.py:94-105
  *   fv_plan_create_grid <- the per-grid state the reference rebuilds on every
  *                         call: TensorGrid (favest/scalar.py:29-84),
  *                         legendre_table (favest/legendre.py:36-75),
@@ -71,7 +74,7 @@ const char* fv_last_error(void);
 int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const double* ring_theta_host,
                         const double* ring_weight_host, int max_batch, int device);
 
-/* Plan for the scattered-point adjoint at vector degree L. */
+/* Plan for the scattered-point transforms (fv_adjoint_points, fv_forward_points) at vector degree L. */
 int fv_plan_create_points(fvPlan** out, int L, int max_batch, int device);
 
 void fv_plan_destroy(fvPlan* plan);
@@ -88,6 +91,17 @@ int fv_adjoint_grid(fvPlan* plan, const double* a, const double* b, double* T, i
 /* Adjoint VSHT at M scattered unit points: (a, b) -> T [B][M][3]. */
 int fv_adjoint_points(fvPlan* plan, const double* xyz, long long M, const double* a, const double* b,
                       double* T, int B, void* stream);
+
+/*
+ * Forward VSHT at M weighted scattered points (the direct route: a rule without
+ * tensor-grid structure, or path="direct-scalar"): T [B][M][3] -> (a, b).
+ * Replaces forward_favest(..., path="direct-scalar") favest/transforms.py:79-147
+ * with _forward_direct_values favest/scalar.py:94-105.  xyz: float64 [M][3] unit
+ * points, w: float64 [M] weights (QuadratureRule.points / .weights, passed
+ * through verbatim).  M = 0 gives zero coefficients.  Needs a points plan.
+ */
+int fv_forward_points(fvPlan* plan, const double* xyz, const double* w, long long M, const double* T, double* a,
+                      double* b, int B, void* stream);
 
 /*
  * Order-sharded building blocks (ring-sharded fields,

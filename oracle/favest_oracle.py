@@ -32,6 +32,7 @@ __all__ = [
     "FOUR_PI", "INV_SQRT_4PI", "INV_SQRT2", "flat_size", "degrees_orders", "tri_index",
     "gl_grid", "grid_points", "ring_cos_sin", "seed_table", "recurrence_ab", "legendre_m",
     "legendre_table", "sht_forward_grid", "sht_adjoint_grid", "sht_adjoint_points",
+    "sht_forward_points", "vsht_forward_points",
     "cg_explicit_vec", "cg_tables", "shift_read", "vsht_forward_grid", "vsht_adjoint_merged",
     "vsht_adjoint_grid", "vsht_adjoint_points", "coef", "random_points", "tangent_noise",
     "rel_l2", "XR_SHIFT",
@@ -297,6 +298,32 @@ def sht_adjoint_points(g, lt, points):
     return out
 
 
+def sht_forward_points(f, weights, points, lt):
+    """Scalar forward by direct summation over arbitrary weighted points
+    (favest/scalar.py:94-105 with ylm_table, favest/legendre.py:106-123):
+    F_{l,m} = sum_k w_k f_k conj(Y_{l,m}(x_k)),
+    conj(Y_{l,m}) = sigma_m Pbar_l^{|m|}(z) e^{-i m phi}.  ``f`` is (M, C)."""
+    f = np.asarray(f, dtype=np.complex128)
+    w = np.asarray(weights, dtype=np.float64)
+    pts = np.atleast_2d(np.asarray(points, dtype=np.float64))
+    C = f.shape[1]
+    z = np.clip(pts[:, 2], -1.0, 1.0)
+    s = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    phi = np.mod(np.arctan2(pts[:, 1], pts[:, 0]), 2.0 * np.pi)  # favest/core.py:82
+    sx, se = seed_table(lt, s)
+    wf = w[:, None] * f  # scalar.py:96
+    out = np.zeros((flat_size(lt), C), dtype=np.complex128)
+    for m in range(lt + 1):
+        P = legendre_m(m, lt, z, sx[m], se[m])  # (n_l, M)
+        ls = np.arange(m, lt + 1)
+        for sgn in ((1,) if m == 0 else (1, -1)):
+            mm = sgn * m
+            g = np.exp(-1j * mm * phi)[:, None] * wf
+            res = P @ g.real + 1j * (P @ g.imag)
+            out[ls * ls + ls + mm] = _sigma(mm) * res
+    return out
+
+
 # --------------------------------------------------------------------------
 # Clebsch-Gordan stage — favest/coupling.py:25-78, 143-240; transforms.py:109-180
 # --------------------------------------------------------------------------
@@ -403,6 +430,16 @@ def vsht_forward_grid(T, ring_thetas, ring_weights, n_phi, lmax, orders=None):
             need.update({abs(mo) - 1, abs(mo), abs(mo) + 1})
         need = [x for x in need if 0 <= x <= top]
     f = sht_forward_grid(combos, ring_thetas, ring_weights, n_phi, top, orders=need)
+    return cg_forward_assemble(f, lmax)
+
+
+def vsht_forward_points(T, weights, points, lmax):
+    """Forward FaVeST on an arbitrary weighted rule (favest/transforms.py:79-147,
+    direct route favest/scalar.py:94-105).  ``T`` is (M, 3) complex."""
+    T = np.asarray(T, dtype=np.complex128)
+    t1, t2, t3 = T[:, 0], T[:, 1], T[:, 2]
+    combos = np.stack([-t1 + 1j * t2, t1 + 1j * t2, t3], axis=1)  # transforms.py:109-112
+    f = sht_forward_points(combos, weights, points, lmax + 1)
     return cg_forward_assemble(f, lmax)
 
 

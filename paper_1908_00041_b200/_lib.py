@@ -17,7 +17,7 @@ FV_OK, FV_EINVAL, FV_ECUDA, FV_ENCCL, FV_ENOMEM = 0, 1, 2, 3, 4
 EXPORTED = (
     "fv_version", "fv_last_error", "fv_plan_create_grid", "fv_plan_create_points",
     "fv_plan_destroy", "fv_plan_info", "fv_forward_grid", "fv_adjoint_grid",
-    "fv_adjoint_points", "fv_set_profiling", "fv_stage_ms", "fv_stage_count",
+    "fv_adjoint_points", "fv_forward_points", "fv_set_profiling", "fv_stage_ms", "fv_stage_count",
     "fv_ring_fft", "fv_forward_orders", "fv_adjoint_orders",
 )
 
@@ -49,6 +49,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "fv_forward_grid": (i, [vp, vp, vp, vp, i, vp]),
         "fv_adjoint_grid": (i, [vp, vp, vp, vp, i, vp]),
         "fv_adjoint_points": (i, [vp, vp, ll, vp, vp, vp, i, vp]),
+        "fv_forward_points": (i, [vp, vp, vp, ll, vp, vp, vp, i, vp]),
         "fv_set_profiling": (i, [vp, i]),
         "fv_stage_ms": (d, [vp, i]),
         "fv_stage_count": (i, [vp, i]),

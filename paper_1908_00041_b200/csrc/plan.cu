@@ -111,6 +111,12 @@ struct fvPlan {
   size_t ptab_bytes = 0;
   long long* gofs = nullptr;    // tile offsets per order (grid G layout)
   long long* rowofs = nullptr;  // row offsets per order (points G layout)
+  // direct forward at points (points plans, allocated on the first fv_forward_points)
+  double* seedk = nullptr;      // K_m = Pbar_m^m / (-s)^m
+  int2* fitems = nullptr;       // (order, 128-degree window), heaviest first
+  int n_fitems = 0;
+  double* Fpart = nullptr;      // point-range partial rows [R][tri(Lt)][ncol]
+  size_t Fpart_cap = 0, F_cap = 0;
   long long g_tiles = 0;
   // workspaces
   double2* Sf = nullptr;        // ring spectra [comp][bin][ring of all max_batch fields] (ring fastest)
@@ -152,6 +158,7 @@ void free_plan(fvPlan* p) {
                   p->seed_e, p->start_l,  p->start_v, p->ab,   p->abofs,  p->gofs,
                   p->dg,     p->dgofs,  p->cgt,     p->cga,     p->ptab_f,  p->mtab_f, p->tofs,   p->ptab_a, p->aofs,
                   p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->G,
+                  p->seedk,  p->fitems,   p->Fpart,
                   p->fft_tw, p->f2_tw};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -775,6 +782,7 @@ int fv_plan_create_points(fvPlan** out, int L, int max_batch, int device) {
   fvPlan* p = new fvPlan();
   p->kind = 1;
   p->L = L;
+  cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device);
   p->Lt = L + 1;
   p->max_batch = max_batch;
   p->device = device;
@@ -850,6 +858,24 @@ int check_grid_call(fvPlan* p, int B, const void* x, const void* y, const void* 
   return FV_OK;
 }
 
+// CG assembly (favest/transforms.py:120-146) of coefficient orders [c_lo, c_hi) of fields
+// b0 .. b0 + nf - 1 from the forward Legendre rows in p->F (ncol = 8 NT)
+int cg_forward(fvPlan* p, double* a, double* b, int B, int b0, int nf, int NT, int c_lo, int c_hi, cudaStream_t s) {
+  StageMark mk(p, 3, s);
+  fv::CgFwdArgs ca{p->F, reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), p->cgt, p->L, 8 * NT, B, b0,
+                   nf, c_lo, c_hi};
+  dim3 grid((c_hi + fv::CGF_MB - 1) / fv::CGF_MB, p->L + 1);
+  const size_t smem = (size_t)3 * (fv::CGF_MB + 2) * fv::cgf_rs(nf) * sizeof(double2);
+  switch (nf) {
+    case 1: fv::cg_fwd_tile_kernel<1><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
+    case 2: fv::cg_fwd_tile_kernel<2><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
+    case 3: fv::cg_fwd_tile_kernel<3><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
+    default: fv::cg_fwd_tile_kernel<4><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
+  }
+  FV_CUDA(cudaGetLastError());
+  return FV_OK;
+}
+
 // fold + Legendre over orders [m_lo, m_hi) and CG for orders [c_lo, c_hi), reading the
 // spectra of every ring of the grid in layout `lay` (natural or compact bins)
 int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* a, double* b, int B, int m_lo,
@@ -876,20 +902,7 @@ int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* 
                        p->nchunks, m_lo, dbg_mode(), mc, trace_buf(), trace_cta(), p->ptab_f, p->mtab_f, p->tofs};
       FV_TRY(dispatch_fwd(p, NT, args, mc, s));
     }
-    if (c_hi > c_lo) {
-      StageMark mk(p, 3, s);
-      fv::CgFwdArgs ca{p->F, reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), p->cgt, p->L, 8 * NT, B, b0,
-                       nf, c_lo, c_hi};
-      dim3 grid((c_hi + fv::CGF_MB - 1) / fv::CGF_MB, p->L + 1);
-      const size_t smem = (size_t)3 * (fv::CGF_MB + 2) * fv::cgf_rs(nf) * sizeof(double2);
-      switch (nf) {
-        case 1: fv::cg_fwd_tile_kernel<1><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
-        case 2: fv::cg_fwd_tile_kernel<2><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
-        case 3: fv::cg_fwd_tile_kernel<3><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
-        default: fv::cg_fwd_tile_kernel<4><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
-      }
-      FV_CUDA(cudaGetLastError());
-    }
+    if (c_hi > c_lo) FV_TRY(cg_forward(p, a, b, B, b0, nf, NT, c_lo, c_hi, s));
   }
   return FV_OK;
 }
@@ -1085,3 +1098,116 @@ int fv_adjoint_points(fvPlan* p, const double* xyz, long long M, const double* a
 }
 
 }  // extern "C"
+
+// ---- direct forward at weighted points (favest/scalar.py:94-105) ----
+namespace {
+
+// plan-time state of the direct forward: K_m seeds and the (order, window) item list
+int fpts_setup(fvPlan* p) {
+  if (p->seedk) return FV_OK;
+  const int Lt = p->Lt;
+  std::vector<double> km(Lt + 1);
+  double cur = 0.28209479177387814;  // 1/sqrt(4 pi), favest/legendre.py:60
+  km[0] = cur;
+  for (int m = 1; m <= Lt; ++m) {
+    cur *= std::sqrt((2 * m + 1) / (2.0 * m));  // |favest/legendre.py:62-65| without the s factor
+    km[m] = cur;
+  }
+  std::vector<int2> items;
+  for (int m = 0; m <= Lt; ++m)
+    for (int w = 0; m + w * fv::FPD_WIN <= Lt; ++w) items.push_back(make_int2(m, w));
+  // heaviest first: window rows, then the recurrence steps below the window
+  auto work = [&](int2 it) {
+    const int lo = it.x + it.y * fv::FPD_WIN, hi = std::min(Lt + 1, lo + fv::FPD_WIN);
+    return 8.0 * (hi - lo) + (lo - it.x);
+  };
+  std::stable_sort(items.begin(), items.end(), [&](int2 x, int2 y) { return work(x) > work(y); });
+  FV_TRY(dalloc(&p->seedk, Lt + 1));
+  FV_TRY(dalloc(&p->fitems, items.size()));
+  FV_CUDA(cudaMemcpy(p->seedk, km.data(), (Lt + 1) * sizeof(double), cudaMemcpyHostToDevice));
+  FV_CUDA(cudaMemcpy(p->fitems, items.data(), items.size() * sizeof(int2), cudaMemcpyHostToDevice));
+  p->n_fitems = (int)items.size();
+  return FV_OK;
+}
+
+int grow(double** buf, size_t* cap, size_t n) {
+  if (*cap >= n) return FV_OK;
+  if (*buf) {
+    FV_CUDA(cudaDeviceSynchronize());  // earlier calls may still read the old buffer
+    cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+  }
+  FV_TRY(dalloc(buf, n));
+  *cap = n;
+  return FV_OK;
+}
+
+template <int NF>
+int launch_fpts(fvPlan* p, const fv::FptsArgs& fa, unsigned grid, cudaStream_t s) {
+  static unsigned long long attr = 0;
+  const size_t smem = fv::fpd_smem_bytes(NF, p->Lt);
+  if (first_use(&attr, p->device))
+    FV_CUDA(cudaFuncSetAttribute(fv::forward_points_dmma_kernel<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 227 * 1024));
+  fv::forward_points_dmma_kernel<NF><<<grid, fv::FPD_THREADS, smem, s>>>(fa);
+  FV_CUDA(cudaGetLastError());
+  return FV_OK;
+}
+
+}  // namespace
+
+extern "C" int fv_forward_points(fvPlan* p, const double* xyz, const double* w, long long M, const double* T,
+                                 double* a, double* b, int B, void* stream) {
+  FV_TRY(begin_call(p));
+  if (p->kind != 1) return fail(FV_EINVAL, "plan was not created for scattered points");
+  if (B < 1 || B > p->max_batch)
+    return fail(FV_EINVAL, "batch " + std::to_string(B) + " outside 1.." + std::to_string(p->max_batch));
+  if (M < 0) return fail(FV_EINVAL, "negative point count");
+  if (!a || !b || (M > 0 && (!xyz || !w || !T))) return fail(FV_EINVAL, "null data pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const long long K = (long long)(p->L + 1) * (p->L + 1);
+  if (M == 0) {  // empty rule: every coefficient is an empty sum
+    FV_CUDA(cudaMemsetAsync(a, 0, (size_t)B * K * 16, s));
+    FV_CUDA(cudaMemsetAsync(b, 0, (size_t)B * K * 16, s));
+    return FV_OK;
+  }
+  const int Lt = p->Lt;
+  if (fv::fpd_smem_bytes(1, Lt) > 227 * 1024)
+    return fail(FV_EINVAL, "degree " + std::to_string(p->L) + " too large for the direct forward kernel");
+  FV_TRY(fpts_setup(p));
+  const int gs = (fv::fpd_smem_bytes(4, Lt) <= 227 * 1024) ? 4 : 1;  // fields per launch
+  const long long rows = (long long)(Lt + 1) * (Lt + 2) / 2;
+  // point ranges: enough CTAs to balance the uneven items over all SMs, bounded workspace
+  const long long nchunk = (M + fv::FPD_CHUNK - 1) / fv::FPD_CHUNK;
+  const long long want = (16LL * p->num_sms + p->n_fitems - 1) / p->n_fitems;
+  const long long cap_r = std::max(1LL, (long long)(1ull << 30) / (rows * 8 * fv::ptsd_nt(gs) * 8));
+  const int R = (int)std::max(1LL, std::min({want, nchunk, 32LL, cap_r}));
+  const int NTmax = fv::ptsd_nt(gs);
+  FV_TRY(grow(&p->Fpart, &p->Fpart_cap, (size_t)R * rows * 8 * NTmax));
+  FV_TRY(grow(&p->F, &p->F_cap, (size_t)rows * 8 * NTmax));
+  for (int b0 = 0; b0 < B; b0 += gs) {
+    const int nf = std::min(gs, B - b0);
+    const int NT = fv::ptsd_nt(nf);
+    {
+      StageMark mk(p, 2, s);
+      fv::FptsArgs fa{xyz, w, M, reinterpret_cast<const double2*>(T), p->Fpart, rows * 8 * NT, p->ab, p->abofs,
+                      p->seedk, p->fitems, Lt, B, b0, R, 8 * NT};
+      const unsigned grid = (unsigned)((long long)p->n_fitems * R);
+      switch (nf) {
+        case 1: FV_TRY(launch_fpts<1>(p, fa, grid, s)); break;
+        case 2: FV_TRY(launch_fpts<2>(p, fa, grid, s)); break;
+        case 3: FV_TRY(launch_fpts<3>(p, fa, grid, s)); break;
+        default: FV_TRY(launch_fpts<4>(p, fa, grid, s)); break;
+      }
+      const long long n2 = rows * 4 * NT;
+      fv::fpart_reduce_kernel<<<(unsigned)std::min<long long>((n2 + 255) / 256, 8LL * p->num_sms), 256, 0, s>>>(
+          reinterpret_cast<const double2*>(p->Fpart), n2, R, reinterpret_cast<double2*>(p->F));
+      FV_CUDA(cudaGetLastError());
+    }
+    FV_TRY(cg_forward(p, a, b, B, b0, nf, NT, 0, p->L + 1, s));
+  }
+  return FV_OK;
+}
+
+

@@ -333,4 +333,232 @@ __global__ void __launch_bounds__(PTS_THREADS, NF == 1 ? 2 : 1) adjoint_points_d
     }
 }
 
+// ---------------------------------------------------------------------------
+// Forward at weighted scattered points — the direct route of forward_favest
+// (favest/scalar.py:94-105: sum_k w_k f_k conj(Y_lm(x_k)), conj(Y_lm) =
+// sigma_m Pbar_l^|m|(z) e^{-i m phi}, favest/legendre.py:101-123).  Output is
+// the forward Legendre row block F[tri(l, m)][col] (col 12 b + 4 c + 2 s + ri,
+// s = 0: +m, s = 1: -m, Cartesian c) that cg_fwd_tile_kernel consumes, the
+// same rows the grid path produces.
+//
+// Per order m: F_m[l][col] = sum_k Pbar_l^m(z_k) Y_k[col] with
+// Y_k[(b, c, +m)] = w_k T_bc(x_k) e^{-i m phi_k} and
+// Y_k[(b, c, -m)] = (-1)^m w_k T_bc(x_k) e^{+i m phi_k}: a DMMA.8x8x4 product
+// with degrees as M, points as K (the reduction) and columns as N.
+//
+// Work item = (order m, 128-degree window, point range r).  The CTA walks its
+// point range in chunks of 256 (one point per thread): each thread forms its
+// point's Y row in shared memory, seeds Pbar_m^m directly in extended range
+// (K_m (-s)^m by square-and-multiply, no per-order running product) and runs
+// the three-term recurrence across the window, 32 degrees at a time into a
+// shared P block; then warp (mi, h) contracts M-tile mi of the block over the
+// chunk's points h*128 .. h*128+127 into register accumulators that live for
+// the whole item.  At the end the two K halves are summed in a fixed order and
+// the item's rows are written to its range slice of the partial workspace;
+// fpart_reduce_kernel adds the R slices in range order (deterministic).
+// ---------------------------------------------------------------------------
+struct FptsArgs {
+  const double* xyz;      // (M, 3) unit points
+  const double* w;        // (M) weights
+  long long M;
+  const double2* T;       // (B_total, M, 3)
+  double* Fpart;          // [R][tri(Lt)][ncol]
+  long long part_stride;  // doubles per range slice
+  const double2* ab;      // recurrence (a_l, a_l b_l) per order (ab_kernel)
+  const long long* abofs;
+  const double* seedk;    // K_m = Pbar_m^m(t) / (-s)^m
+  const int2* items;      // (m, window), heaviest first
+  int Lt, B_total, b0, R, ncol;
+};
+
+constexpr int FPD_THREADS = 256, FPD_CHUNK = 256, FPD_DB = 32, FPD_PS = FPD_CHUNK + 4, FPD_MT = 4;
+constexpr int FPD_WIN = FPD_MT * FPD_DB;  // degrees per window
+
+__host__ __device__ constexpr size_t fpd_smem_bytes(int nf, int Lt) {
+  return ((size_t)FPD_DB * FPD_PS + (size_t)FPD_CHUNK * ptsd_rs(nf)) * sizeof(double) +
+         (size_t)(Lt > 2 ? Lt - 1 : 1) * sizeof(double2);
+}
+
+// Pbar_m^m(t) = (-1)^m K_m s^m as x * 2^e (e a multiple of 512, e <= 0), with
+// s^m = r 2^E from square-and-multiply on frexp-normalised factors (exact range)
+__device__ __forceinline__ void fpd_seed(int m, double s, double km, double& x, int& e) {
+  e = 0;
+  if (m == 0) {
+    x = km;
+    return;
+  }
+  if (s == 0.0) {
+    x = 0.0;
+    return;
+  }
+  int ks;
+  const double f = frexp(s, &ks);
+  double r = 1.0, bb = f;
+  long long er = 0, eb = 0;
+  for (int n = m;;) {
+    int tt;
+    if (n & 1) {
+      r = frexp(r * bb, &tt);
+      er += eb + tt;
+    }
+    n >>= 1;
+    if (!n) break;
+    bb = frexp(bb * bb, &tt);
+    eb = 2 * eb + tt;
+  }
+  const long long E = er + (long long)ks * m;
+  const double v = (m & 1) ? -km * r : km * r;
+  const long long qq = E > 0 ? 0 : (-E) / XR_SHIFT;
+  e = (int)(-XR_SHIFT * qq);
+  x = ldexp(v, (int)(E + XR_SHIFT * qq));
+}
+
+template <int NF>
+__global__ void __launch_bounds__(FPD_THREADS) forward_points_dmma_kernel(FptsArgs a) {
+  constexpr int NT = ptsd_nt(NF), RS = ptsd_rs(NF), NCOL = 8 * NT;
+  extern __shared__ __align__(16) double fpd_smem[];
+  double* Ps = fpd_smem;                                                    // [FPD_DB][FPD_PS]
+  double* Ys = Ps + FPD_DB * FPD_PS;                                        // [FPD_CHUNK][RS]
+  double2* abs_ = reinterpret_cast<double2*>(Ys + (size_t)FPD_CHUNK * RS);  // (a_l, a_l b_l), l = m+2..Lt
+  const int item = blockIdx.x / a.R, r = blockIdx.x - item * a.R;
+  const int2 it = a.items[item];
+  const int m = it.x, Lt = a.Lt;
+  const int lw0 = m + it.y * FPD_WIN, lw1 = min(Lt + 1, lw0 + FPD_WIN);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int mi = warp & 3, h = warp >> 2;
+  for (int i = threadIdx.x; i < Lt - m - 1; i += FPD_THREADS) abs_[i] = a.ab[a.abofs[m] + i];
+  const long long p_begin = a.M * r / a.R, p_end = a.M * (r + 1) / a.R;
+  const double km = a.seedk[m], c1 = sqrt(2 * m + 3.0);
+  const double sgm = (m & 1) ? -1.0 : 1.0;
+  double acc[FPD_MT][NT][2];
+#pragma unroll
+  for (int j = 0; j < FPD_MT; ++j)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[j][n][0] = acc[j][n][1] = 0.0;
+  __syncthreads();  // recurrence coefficients staged
+  for (long long c0 = p_begin; c0 < p_end; c0 += FPD_CHUNK) {
+    const long long p = c0 + threadIdx.x;
+    const bool live = p < p_end;
+    double t = 0.0, s = 0.0;
+    double* yrow = Ys + threadIdx.x * RS;
+    if (live) {
+      const double x = a.xyz[3 * p], y = a.xyz[3 * p + 1], zr = a.xyz[3 * p + 2];
+      t = fmin(1.0, fmax(-1.0, zr));
+      s = sqrt(fmax(0.0, 1.0 - t * t));
+      double phi = atan2(y, x);
+      if (phi < 0.0) phi += 6.283185307179586;  // np.mod(atan2, 2*pi) (favest/core.py:82)
+      const double wk = a.w[p];
+      double sn, cs;
+      sincos(phi * m, &sn, &cs);  // favest/legendre.py:121: exp(i * (phi * m))
+#pragma unroll
+      for (int b = 0; b < NF; ++b)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double2 v = a.T[((size_t)(a.b0 + b) * a.M + p) * 3 + c];
+          const double vr = wk * v.x, vi = wk * v.y;
+          // +m: e^{-i m phi} (w T);  -m: (-1)^m e^{+i m phi} (w T), absent at m = 0
+          reinterpret_cast<double2*>(yrow)[6 * b + 2 * c] = make_double2(cs * vr + sn * vi, cs * vi - sn * vr);
+          reinterpret_cast<double2*>(yrow)[6 * b + 2 * c + 1] =
+              m == 0 ? make_double2(0.0, 0.0) : make_double2(sgm * (cs * vr - sn * vi), sgm * (cs * vi + sn * vr));
+        }
+#pragma unroll
+      for (int c = 12 * NF; c < NCOL; ++c) yrow[c] = 0.0;
+    } else {
+#pragma unroll
+      for (int c = 0; c < NCOL; ++c) yrow[c] = 0.0;
+    }
+    // recurrence state of this thread's point, seeded at degree m
+    double p2, p1;
+    int e;
+    fpd_seed(m, s, km, p2, e);
+    p1 = __dmul_rn(__dmul_rn(c1, t), p2);  // favest/legendre.py:66-67
+    int l = m;
+    auto produce = [&]() -> double {  // Pbar_l^m(t), then l += 1
+      double v;
+      if (l == m) {
+        v = p2;
+      } else if (l == m + 1) {
+        v = p1;
+      } else {
+        const double2 abv = abs_[l - m - 2];
+        const double pn = fma(abv.x * t, p1, -(abv.y * p2));
+        p2 = p1;
+        p1 = pn;
+        if (e < 0 && fabs(p1) >= 0x1p512) {
+          p1 *= 0x1p-512;
+          p2 *= 0x1p-512;
+          e += XR_SHIFT;
+        }
+        v = p1;
+      }
+      ++l;
+      return e < 0 ? xr_value(v, e) : v;
+    };
+    while (l < lw0) produce();  // degrees below this item's window
+#pragma unroll
+    for (int j = 0; j < FPD_MT; ++j) {
+      const int d0 = lw0 + j * FPD_DB;
+      if (d0 >= lw1) break;
+#pragma unroll 4
+      for (int k = 0; k < FPD_DB; ++k) Ps[k * FPD_PS + threadIdx.x] = (d0 + k < lw1) ? produce() : 0.0;
+      __syncthreads();
+      if (d0 + 8 * mi < lw1) {
+        const double* pa = Ps + (8 * mi + g) * FPD_PS + h * (FPD_CHUNK / 2) + q;
+        const double* pb = Ys + (size_t)(h * (FPD_CHUNK / 2) + q) * RS + g;
+#pragma unroll 8
+        for (int ks = 0; ks < FPD_CHUNK / 8; ++ks) {
+          const double af = pa[4 * ks];
+          double bf[NT];
+#pragma unroll
+          for (int n = 0; n < NT; ++n) bf[n] = pb[(size_t)4 * ks * RS + 8 * n];
+#pragma unroll
+          for (int n = 0; n < NT; ++n) dmma_m8n8k4(acc[j][n][0], acc[j][n][1], af, bf[n]);
+        }
+      }
+      __syncthreads();  // P block (and, after the last block, the Y tile) free again
+    }
+  }
+  // sum the two point halves (h = 0 + h = 1, fixed order) and store the item's rows
+  double* red = Ps;  // [4 M-tile warps][FPD_MT][NT][2][32]
+  if (h == 1) {
+#pragma unroll
+    for (int j = 0; j < FPD_MT; ++j)
+#pragma unroll
+      for (int n = 0; n < NT; ++n) {
+        red[(((mi * FPD_MT + j) * NT + n) * 2 + 0) * 32 + lane] = acc[j][n][0];
+        red[(((mi * FPD_MT + j) * NT + n) * 2 + 1) * 32 + lane] = acc[j][n][1];
+      }
+  }
+  __syncthreads();
+  if (h == 0) {
+    double* out = a.Fpart + (size_t)r * a.part_stride;
+#pragma unroll
+    for (int j = 0; j < FPD_MT; ++j) {
+      const int lr = lw0 + j * FPD_DB + 8 * mi + g;
+      if (lr < lw1) {
+        double* row = out + ((size_t)lr * (lr + 1) / 2 + m) * a.ncol;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const double v0 = acc[j][n][0] + red[(((mi * FPD_MT + j) * NT + n) * 2 + 0) * 32 + lane];
+          const double v1 = acc[j][n][1] + red[(((mi * FPD_MT + j) * NT + n) * 2 + 1) * 32 + lane];
+          *reinterpret_cast<double2*>(row + 8 * n + 2 * q) = make_double2(v0, v1);
+        }
+      }
+    }
+  }
+}
+
+// F = sum over the R point-range slices, in range order (bitwise reproducible)
+__global__ void fpart_reduce_kernel(const double2* __restrict__ part, long long n2, int R, double2* __restrict__ F) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+    double2 s = part[i];
+    for (int r = 1; r < R; ++r) {
+      const double2 v = part[(size_t)r * n2 + i];
+      s.x += v.x;
+      s.y += v.y;
+    }
+    F[i] = s;
+  }
+}
+
 }  // namespace fv

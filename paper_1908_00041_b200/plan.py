@@ -3,7 +3,8 @@
 ``GridPlan`` owns one ``fvPlan`` for a tensor grid (ring tables, Legendre
 seeds, recurrence coefficients, cuFFT plans and workspaces) and runs the
 forward / adjoint VSHT on ``(B, N, 3)`` / ``(B, K)`` complex128 CUDA tensors.
-``PointsPlan`` does the same for the scattered-point adjoint.
+``PointsPlan`` does the same at scattered points: the adjoint, and the
+forward on weighted rules without tensor-grid structure (the direct route).
 
 All tensors stay on the device; calls are asynchronous on the current torch
 stream (``torch.cuda.current_stream``).
@@ -139,7 +140,8 @@ class GridPlan:
 
 
 class PointsPlan:
-    """Adjoint VSHT of vector degree ``lmax`` at scattered unit points."""
+    """Adjoint and forward (direct-route) VSHT of vector degree ``lmax`` at
+    scattered unit points."""
 
     def __init__(self, lmax, max_batch=1, device=None):
         self.lib = _lib.load()
@@ -164,15 +166,45 @@ class PointsPlan:
         except Exception:
             pass
 
-    def adjoint(self, xyz, a, b, T=None):
-        """xyz (M, 3) float64, (a, b) (B, K) complex128 -> T (B, M, 3) complex128."""
+    def _points(self, xyz):
         torch = _torch()
         if not isinstance(xyz, torch.Tensor) or xyz.dtype != torch.float64 or xyz.dim() != 2 \
                 or xyz.shape[1] != 3:
             raise ValueError("xyz must be a (M, 3) float64 tensor")
         if xyz.device != self.device:
             raise ValueError(f"xyz is on {xyz.device}, plan is on {self.device}")
-        xyz = xyz.contiguous()
+        return xyz.contiguous()
+
+    def forward(self, xyz, w, T, a=None, b=None):
+        """Direct-route forward (favest/scalar.py:94-105 + favest/transforms.py:79-147):
+        xyz (M, 3) float64 points, w (M,) float64 weights, T (B, M, 3) complex128
+        -> (a, b), each (B, (lmax+1)**2) complex128."""
+        torch = _torch()
+        xyz = self._points(xyz)
+        M = int(xyz.shape[0])
+        if not isinstance(w, torch.Tensor) or w.dtype != torch.float64 or tuple(w.shape) != (M,):
+            raise ValueError(f"w must be a ({M},) float64 tensor")
+        if w.device != self.device:
+            raise ValueError(f"w is on {w.device}, plan is on {self.device}")
+        w = w.contiguous()
+        B = int(T.shape[0]) if T.dim() == 3 else -1
+        T = _check_tensor(T, (B, M, 3), "T", self.device)
+        if a is None:
+            a = torch.empty((B, self.n_coeffs), dtype=torch.complex128, device=self.device)
+        if b is None:
+            b = torch.empty((B, self.n_coeffs), dtype=torch.complex128, device=self.device)
+        a = _check_tensor(a, (B, self.n_coeffs), "a", self.device)
+        b = _check_tensor(b, (B, self.n_coeffs), "b", self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.fv_forward_points(
+                self._h, xyz.data_ptr(), w.data_ptr(), M, T.data_ptr(), a.data_ptr(), b.data_ptr(), B,
+                _stream_ptr(self.device)))
+        return a, b
+
+    def adjoint(self, xyz, a, b, T=None):
+        """xyz (M, 3) float64, (a, b) (B, K) complex128 -> T (B, M, 3) complex128."""
+        torch = _torch()
+        xyz = self._points(xyz)
         M = int(xyz.shape[0])
         B = int(a.shape[0]) if a.dim() == 2 else -1
         a = _check_tensor(a, (B, self.n_coeffs), "a", self.device)

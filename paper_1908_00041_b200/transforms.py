@@ -11,8 +11,8 @@ Routes (reference: ``_pick_path``, favest/transforms.py:59-76):
   * tensor grid with n_phi >= 2(L+1)+1, path "auto"/"fast-scalar"
       -> ``fv_forward_grid`` / ``fv_adjoint_grid``
   * raw points or "direct-scalar" (adjoint) -> ``fv_adjoint_points``
-  * "direct-scalar" forward on arbitrary rules: not on the GPU path yet
-     -> NotImplementedError, never a CPU fallback.
+  * rules without a usable grid, or "direct-scalar" (forward)
+      -> ``fv_forward_points`` (favest/scalar.py:94-105)
 """
 
 from __future__ import annotations
@@ -125,15 +125,15 @@ def forward_favest(samples, rule, lmax: int, path: str = "auto", tables=None) ->
     grid = getattr(rule, "grid", None)
     use_fast = _pick_path(path, grid, lmax)
     _check_tables(tables, lmax)
-    if not use_fast:
-        raise NotImplementedError(
-            "direct-scalar forward on non-grid rules is not on the B200 path yet "
-            "(SURVEY §8(f) #2); use a tensor-grid rule"
-        )
-    plan = grid_plan(grid, lmax)
-    T = torch.from_numpy(np.ascontiguousarray(samples.values, dtype=np.complex128))
-    T = T.reshape(1, -1, 3).to(plan.device)
-    a, b = plan.forward(T)
+    T = torch.from_numpy(np.ascontiguousarray(samples.values, dtype=np.complex128)).reshape(1, -1, 3)
+    if use_fast:
+        plan = grid_plan(grid, lmax)
+        a, b = plan.forward(T.to(plan.device))
+    else:  # direct route on the rule's own points and weights (favest/scalar.py:94-105)
+        plan = points_plan(lmax)
+        xyz = torch.from_numpy(np.ascontiguousarray(rpts, dtype=np.float64)).to(plan.device)
+        w = torch.from_numpy(np.ascontiguousarray(rule.weights, dtype=np.float64)).to(plan.device)
+        a, b = plan.forward(xyz, w, T.to(plan.device))
     a = a[0].cpu().numpy()
     b = b[0].cpu().numpy()
     return VectorCoefficients(ScalarCoefficients(lmax, a), ScalarCoefficients(lmax, b))

@@ -92,6 +92,41 @@ def main():
             os.path.join(HERE, f"scattered_l{lmax}_m{M}.npz"),
             lmax=lmax, points=pts, a=a, b=b, T=out.values,
         )
+    # 5. direct-route forward on non-grid rules (favest/scalar.py:94-105):
+    #    (a) a GL tensor rule forced onto path="direct-scalar",
+    #    (b) a custom rule: random points, random positive weights summing to 4 pi,
+    #    (c) the bundled 12-point icosahedron design (equal weights 4 pi / 12)
+    from favest.core import QuadratureRule
+    from favest.quadrature import bundled_design
+
+    def tangent(rng, pts, scale=1.0):
+        raw = scale * (rng.standard_normal(pts.shape) + 1j * rng.standard_normal(pts.shape))
+        return raw - np.sum(raw * pts, axis=1)[:, None] * pts
+
+    cases = []
+    grid, rule = gen_gl_tensor(2 * 12 + 3)
+    rng = np.random.default_rng(121)
+    a, b = coef(rng, 12, "inv")
+    T = adjoint_favest(vc(a, b, 12), rule)
+    cases.append(("direct_gl_l12", 12, rule, T.values + tangent(rng, rule.points, 1e-3)))
+    rng = np.random.default_rng(161)
+    M = 400
+    v = rng.standard_normal((M, 3))
+    pts = v / np.linalg.norm(v, axis=1, keepdims=True)
+    w = rng.uniform(0.5, 1.5, M)
+    w *= 4.0 * np.pi / w.sum()
+    rule = QuadratureRule(points=pts, weights=w, exactness=0)
+    cases.append(("direct_custom_l16_m400", 16, rule, tangent(rng, pts)))
+    rule = bundled_design("icosahedron12")
+    rng = np.random.default_rng(12)
+    cases.append(("direct_ico_l3", 3, rule, tangent(rng, rule.points)))
+    for name, lmax, rule, vals in cases:
+        F = forward_favest(TangentFieldSamples(rule.points, vals), rule, lmax, path="direct-scalar")
+        np.savez_compressed(
+            os.path.join(HERE, f"{name}.npz"),
+            lmax=lmax, points=rule.points, weights=rule.weights, T=vals,
+            fa=F.div.values, fb=F.curl.values,
+        )
     print("reference favest", getattr(favest, "__version__", "?"), "numpy", np.__version__)
 
 

@@ -370,3 +370,119 @@ def _lib_check_bad_orders(plan):
 
     buf = ctypes.c_void_p(1)
     _lib.check(plan.lib.fv_forward_orders(plan._h, buf, 1, 1, 1, 0, 0, buf, buf, 1, 5, 3, 0, 0, None))
+
+
+# ---------------------------------------------------------------------------
+# direct-route forward at weighted points (fv_forward_points,
+# favest/scalar.py:94-105 + favest/transforms.py:79-147)
+# ---------------------------------------------------------------------------
+def _pplan(L, B=1):
+    from paper_1908_00041_b200.plan import PointsPlan
+
+    return PointsPlan(L, max_batch=B)
+
+
+def _fwd_pts(pp, pts, w, T):
+    a, b = pp.forward(_t(pts), _t(w), _t(T))
+    return a.cpu().numpy(), b.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["direct_gl_l12", "direct_custom_l16_m400", "direct_ico_l3"])
+def test_golden_direct_forward(golden, name):
+    import paper_1908_00041_b200 as fb
+
+    cuda_or_skip()
+    g = golden(name)
+    L = int(g["lmax"])
+    a, b = _fwd_pts(_pplan(L), g["points"], g["weights"], g["T"][None])
+    ref = np.concatenate([g["fa"], g["fb"]])
+    assert O.rel_l2(np.concatenate([a[0], b[0]]), ref) <= TOL
+    # through the reference-signature entry point with a custom rule object
+    rule = fb.QuadratureRule(points=g["points"], weights=g["weights"], exactness=0)
+    c = fb.forward_favest(fb.TangentFieldSamples(g["points"], g["T"]), rule, L, path="direct-scalar")
+    assert O.rel_l2(np.concatenate([c.div.values, c.curl.values]), ref) <= TOL
+    assert c.div.values[0] == 0 and c.curl.values[0] == 0
+
+
+def test_direct_forward_c5_points_against_oracle():
+    # C5 shapes (L=128, scattered points, seeded) at a size the oracle finishes in seconds;
+    # 130 degrees at m = 0, 1 exceed one 128-degree window
+    cuda_or_skip()
+    L, M = 128, 6000
+    rng = np.random.default_rng(5)
+    pts = O.random_points(rng, M)
+    w = rng.uniform(0.5, 1.5, M)
+    w *= 4 * np.pi / w.sum()
+    T = np.stack([O.tangent_noise(rng, pts, 1.0) for _ in range(2)])
+    a, b = _fwd_pts(_pplan(L, 2), pts, w, T)
+    for f in range(2):
+        ra, rb = O.vsht_forward_points(T[f], w, pts, L)
+        assert O.rel_l2(np.concatenate([a[f], b[f]]), np.concatenate([ra, rb])) <= TOL
+
+
+def test_direct_forward_multi_window_and_poles():
+    # several degree windows per order (L=300), exact poles and an equator point
+    cuda_or_skip()
+    L, M = 300, 700
+    rng = np.random.default_rng(31)
+    pts = O.random_points(rng, M)
+    pts[0] = [0.0, 0.0, 1.0]
+    pts[1] = [0.0, 0.0, -1.0]
+    pts[2] = [1.0, 0.0, 0.0]
+    w = np.full(M, 4 * np.pi / M)
+    T = O.tangent_noise(rng, pts, 1.0)[None]
+    a, b = _fwd_pts(_pplan(L), pts, w, T)
+    ra, rb = O.vsht_forward_points(T[0], w, pts, L)
+    assert O.rel_l2(np.concatenate([a[0], b[0]]), np.concatenate([ra, rb])) <= TOL
+
+
+def test_direct_forward_equals_grid_forward_and_is_adjoint():
+    # on a GL rule the direct and FFT routes agree; <F_w T, c> = <T, S c>_w
+    cuda_or_skip()
+    L = 24
+    th, wr, nphi = O.gl_grid(L)
+    pts = O.grid_points(th, nphi)
+    w = np.repeat(wr, nphi)
+    rng = np.random.default_rng(17)
+    T = O.tangent_noise(rng, pts, 1.0)[None]
+    pp = _pplan(L)
+    a, b = _fwd_pts(pp, pts, w, T)
+    ga, gb = _plan(L, th, wr, nphi).forward(_t(T))
+    got = np.concatenate([a[0], b[0]])
+    assert O.rel_l2(got, np.concatenate([ga[0].cpu().numpy(), gb[0].cpu().numpy()])) <= 1e-12
+    # adjointness at scattered points with arbitrary weights
+    M = 900
+    p2 = O.random_points(rng, M)
+    w2 = rng.uniform(0.1, 2.0, M)
+    T2 = O.tangent_noise(rng, p2, 1.0)[None]
+    ca, cb = O.coef(rng, L, "inv")
+    fa, fb_ = _fwd_pts(pp, p2, w2, T2)
+    S = pp.adjoint(_t(p2), _t(ca[None]), _t(cb[None])).cpu().numpy()[0]
+    lhs = np.vdot(np.concatenate([ca, cb]), np.concatenate([fa[0], fb_[0]]))
+    rhs = np.vdot(S * w2[:, None], T2[0])
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+
+
+def test_direct_forward_batch_determinism_and_edges():
+    torch = cuda_or_skip()
+    L, M = 20, 1000
+    rng = np.random.default_rng(41)
+    pts = O.random_points(rng, M)
+    w = rng.uniform(0.5, 1.5, M)
+    T = np.stack([O.tangent_noise(rng, pts, 1.0) for _ in range(5)])  # groups of 4 + 1
+    pp = _pplan(L, 5)
+    a, b = _fwd_pts(pp, pts, w, T)
+    a2, b2 = _fwd_pts(pp, pts, w, T)
+    assert np.array_equal(a, a2) and np.array_equal(b, b2)  # fixed-order reductions
+    for f in (0, 4):
+        sa, sb = _fwd_pts(pp, pts, w, T[f:f + 1])
+        assert O.rel_l2(np.concatenate([a[f], b[f]]), np.concatenate([sa[0], sb[0]])) <= 1e-14
+    # one point
+    a1, b1 = _fwd_pts(pp, pts[:1], w[:1], T[:1, :1])
+    ra, rb = O.vsht_forward_points(T[0, :1], w[:1], pts[:1], L)
+    assert O.rel_l2(np.concatenate([a1[0], b1[0]]), np.concatenate([ra, rb])) <= TOL
+    # empty rule: zero coefficients, outputs fully written
+    a0 = torch.full((1, (L + 1) ** 2), 7.0, dtype=torch.complex128, device="cuda")
+    b0 = a0.clone()
+    pp.forward(_t(np.zeros((0, 3))), _t(np.zeros(0)), _t(np.zeros((1, 0, 3), complex)), a0, b0)
+    assert float(a0.abs().max()) == 0.0 and float(b0.abs().max()) == 0.0

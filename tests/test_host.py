@@ -53,8 +53,11 @@ def test_forward_argument_errors_before_any_device_work():
 
     with pytest.raises(ValueError, match="cannot serve"):
         fb.forward_favest(samples, rule, 6, tables=Tab())
-    with pytest.raises(NotImplementedError):
-        fb.forward_favest(samples, rule, 6, path="direct-scalar")
+    import torch
+
+    if not torch.cuda.is_available():  # the direct route runs on the GPU only: no CPU fallback
+        with pytest.raises(RuntimeError, match="needs a CUDA device"):
+            fb.forward_favest(samples, rule, 6, path="direct-scalar")
 
 
 def test_adjoint_argument_errors():

@@ -105,3 +105,23 @@ def test_partial_orders_match_full():
     ls, ms = O.degrees_orders(L)
     sel = np.isin(np.abs(ms), [0, 5, 20])
     assert np.array_equal(pa[sel], fa[sel]) and np.array_equal(pb[sel], fb[sel])
+
+
+@pytest.mark.parametrize("name", ["direct_gl_l12", "direct_custom_l16_m400", "direct_ico_l3"])
+def test_direct_forward_against_reference(golden, name):
+    # forward_favest(..., path="direct-scalar") on grid / custom / design rules
+    # (favest/scalar.py:94-105, favest/transforms.py:79-147)
+    g = golden(name)
+    fa, fb = O.vsht_forward_points(g["T"], g["weights"], g["points"], int(g["lmax"]))
+    assert O.rel_l2(np.concatenate([fa, fb]), np.concatenate([g["fa"], g["fb"]])) <= 1e-14
+
+
+def test_direct_forward_matches_grid_forward():
+    # on a GL rule the direct route and the FFT route are the same transform
+    # (pkg/tests/test_scalar.py:96-109 pins fast == direct to 1e-11)
+    g = np.load(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden", "roundtrip_l17.npz"))
+    L = 17
+    th, w, nphi = g["ring_thetas"], g["ring_weights"], int(g["n_phi"])
+    pts = O.grid_points(th, nphi)
+    fa, fb = O.vsht_forward_points(g["Tn"], np.repeat(w, nphi), pts, L)
+    assert O.rel_l2(np.concatenate([fa, fb]), np.concatenate([g["fna"], g["fnb"]])) <= 1e-13

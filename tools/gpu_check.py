@@ -115,3 +115,25 @@ def c5_timing(reps=5):
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "c5":
     c5_timing()
+
+def c5f_timing(reps=5):
+    """Direct-route forward at C5 shapes: M = 200,000 weighted scattered points, L = 128."""
+    L, M = 128, 200_000
+    rng = np.random.default_rng(5)
+    x = O.random_points(rng, M)
+    w = np.full(M, 4 * np.pi / M)
+    for B in (1, 4):
+        T = np.stack([O.tangent_noise(rng, x, 1.0) for _ in range(B)])
+        pp = PointsPlan(L, max_batch=B)
+        X = torch.from_numpy(x).cuda(); W = torch.from_numpy(w).cuda(); Td = torch.from_numpy(T).cuda()
+        pp.forward(X, W, Td); torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps): pp.forward(X, W, Td)
+        e1.record(); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        flops = B * 24 * ((L + 2) * (L + 3) // 2) * M + 4 * ((L + 2) * (L + 3) // 2) * M
+        print(f"C5-forward L={L} M={M} B={B}: {ms:.3f} ms  {B*1e3/ms:.1f} transforms/s  {flops/ms/1e9:.2f} TF/s canonical", flush=True)
+
+if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "c5f":
+    c5f_timing()
