@@ -342,7 +342,9 @@ def run_ours(args, rank, world, local_rank):
 
     # end to end: pinned host buffers through the public API, copies inside the timed region.
     # HostPipeline (paper_1908_00041_b200/pipeline.py) overlaps batch k+1's host->device copy,
-    # batch k's transforms and batch k-1's device->host copy on three streams; every step's
+    # batch k's transforms and batch k-1's device->host copy on three streams (three staging
+    # slots: with two, batch k+2's upload waits on batch k's download, which waits on batch
+    # k's transforms, so the compute was not hidden); every step's
     # (B, N, 3) samples still cross the link in, and its (B, N, 3) result out.
     e2e = None
     if not args.no_e2e:
@@ -351,8 +353,8 @@ def run_ours(args, rank, world, local_rank):
         Th = torch.empty(T.shape, dtype=T.dtype, pin_memory=True)
         Th.copy_(T)
         Toh = torch.empty_like(Th, pin_memory=True)
-        pipe = HostPipeline(plan, depth=2)
-        n_e = max(4, min(args.steps, 8))
+        pipe = HostPipeline(plan, depth=3)
+        n_e = max(8, min(args.steps, 40))
         for _ in range(2):
             pipe.submit_roundtrip(Th, Toh)
         pipe.synchronize()

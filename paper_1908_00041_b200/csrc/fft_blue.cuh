@@ -1,0 +1,289 @@
+// Ring DFTs of lengths with a prime factor P > 19 (C2: n_phi = 516 = 12 * 43,
+// C4: n_phi = 8196 = 12 * 683), replacing the cuFFT Bluestein plans (7.4 ms
+// per direction at C4).  favest/scalar.py:149 (np.fft.fft along a ring) and
+// :178 (np.fft.ifft * n_phi, i.e. the unnormalised inverse).
+//
+// n = R * P.  Decimation in time over the R residues:
+//   X[k + P s] = sum_r w_R^{r s} ( w_n^{r k} Y_r[k] ),   Y_r = DFT_P(x[r + R q], q < P)
+// * blue_p_kernel: one CTA per (component, ring, residue r) computes Y_r by
+//   Bluestein's chirp-z identity q k = (q^2 + k^2 - (k - q)^2) / 2:
+//   Y_r[k] = c_k * sum_q (x_q c_q) conj(c_{k-q}),  c_j = exp(-pi i j^2 / P),
+//   a cyclic convolution of length M >= 2P - 1 (M = 2^a 3^b) done as
+//   FFT_M -> x FFT_M(conj c) / M (plan-time table) -> inverse FFT_M, all in
+//   shared memory with a Stockham radix-{2,3,4,8} loop; then applies w_n^{r k}
+//   and stores Y'_r contiguously in a scratch buffer.
+// * blue_r_kernel: thread per (component, ring, k) forms the R outputs
+//   X[k + P s] from the R scratch values (direct R-point DFT) and writes them
+//   with the caller's strides.
+// The inverse direction is conj(DFT(conj(x))): conjugate on load (K1) and on
+// store (K2).  Tables (chirps, roots, FFT_M of the chirp) are exactly rounded
+// from long double on the host.
+#pragma once
+#include "common.cuh"
+
+namespace fv {
+
+constexpr int BLUE_T = 256;
+constexpr int BLUE_MAXST = 12;
+
+struct BlueArgs {
+  const double2* in;
+  long long in_cs, in_rs, in_es;
+  double2* out;
+  long long out_cs, out_rs, out_es;
+  double2* S1;            // scratch [3 * nrings][R][P]
+  const double2* rootM;   // exp(-2 pi i j / M), j < M
+  const double2* chirp;   // exp(-pi i q^2 / P), q < P
+  const double2* FB;      // FFT_M(b) / M, b_j = conj(chirp_|j|) wrapped cyclically
+  const double2* rootN;   // exp(-2 pi i j / n), j < n
+  const double2* rootR;   // exp(-2 pi i j / R), j < R
+  int n, R, P, M, nrings, inverse;
+  int nst;
+  int radix[BLUE_MAXST];  // M = prod radix (each 2, 3, 4 or 8)
+};
+
+__device__ __forceinline__ double2 bl_mul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 bl_add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 bl_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+// multiply by -i
+__device__ __forceinline__ double2 bl_mi(double2 a) { return make_double2(a.y, -a.x); }
+
+// forward-sign (exp(-2 pi i / R)) DFT codelets
+template <int R>
+__device__ __forceinline__ void bl_dft(double2 (&v)[8]);
+
+template <>
+__device__ __forceinline__ void bl_dft<2>(double2 (&v)[8]) {
+  const double2 a = v[0], b = v[1];
+  v[0] = bl_add(a, b);
+  v[1] = bl_sub(a, b);
+}
+
+template <>
+__device__ __forceinline__ void bl_dft<3>(double2 (&v)[8]) {
+  const double s3 = 0.86602540378443864676;  // sin(2 pi / 3)
+  const double2 t1 = bl_add(v[1], v[2]);
+  const double2 t2 = make_double2(v[0].x - 0.5 * t1.x, v[0].y - 0.5 * t1.y);
+  const double2 d = bl_sub(v[1], v[2]);
+  const double2 t3 = make_double2(s3 * d.y, -s3 * d.x);  // -i sin(2pi/3) (v1 - v2)
+  v[0] = bl_add(v[0], t1);
+  v[1] = bl_add(t2, t3);
+  v[2] = bl_sub(t2, t3);
+}
+
+template <>
+__device__ __forceinline__ void bl_dft<4>(double2 (&v)[8]) {
+  const double2 a = bl_add(v[0], v[2]), b = bl_sub(v[0], v[2]);
+  const double2 c = bl_add(v[1], v[3]), d = bl_mi(bl_sub(v[1], v[3]));
+  v[0] = bl_add(a, c);
+  v[2] = bl_sub(a, c);
+  v[1] = bl_add(b, d);
+  v[3] = bl_sub(b, d);
+}
+
+template <>
+__device__ __forceinline__ void bl_dft<8>(double2 (&v)[8]) {
+  const double h = 0.70710678118654752440;  // sqrt(2) / 2
+  double2 e[8] = {v[0], v[2], v[4], v[6]}, o[8] = {v[1], v[3], v[5], v[7]};
+  bl_dft<4>(e);
+  bl_dft<4>(o);
+  // w8^k o_k, w8 = exp(-i pi / 4)
+  const double2 o1 = make_double2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
+  const double2 o2 = bl_mi(o[2]);
+  const double2 o3 = make_double2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
+  v[0] = bl_add(e[0], o[0]);
+  v[4] = bl_sub(e[0], o[0]);
+  v[1] = bl_add(e[1], o1);
+  v[5] = bl_sub(e[1], o1);
+  v[2] = bl_add(e[2], o2);
+  v[6] = bl_sub(e[2], o2);
+  v[3] = bl_add(e[3], o3);
+  v[7] = bl_sub(e[3], o3);
+}
+
+// One Stockham stage x -> y of the length-M transform with sub-transform span Ns.
+template <int R>
+__device__ __forceinline__ void bl_stage(const double2* x, double2* y, const double2* __restrict__ rootM, int M,
+                                         int Ns) {
+  const int nb = M / R;
+  const int tstep = M / (Ns * R);
+  for (int j = threadIdx.x; j < nb; j += BLUE_T) {
+    const int k = j % Ns;
+    double2 v[8];
+#pragma unroll
+    for (int i = 0; i < R; ++i) v[i] = x[j + i * nb];
+    if (Ns > 1) {
+#pragma unroll
+      for (int i = 1; i < R; ++i) v[i] = bl_mul(v[i], __ldg(&rootM[i * k * tstep]));
+    }
+    bl_dft<R>(v);
+    const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int i = 0; i < R; ++i) y[base + i * Ns] = v[i];
+  }
+}
+
+// forward FFT_M of buf[0..M) (ping-pong with tmp); returns the buffer holding the result
+__device__ __forceinline__ double2* bl_fft(double2* buf, double2* tmp, const BlueArgs& a) {
+  int Ns = 1;
+  for (int s = 0; s < a.nst; ++s) {
+    const int R = a.radix[s];
+    switch (R) {
+      case 2: bl_stage<2>(buf, tmp, a.rootM, a.M, Ns); break;
+      case 3: bl_stage<3>(buf, tmp, a.rootM, a.M, Ns); break;
+      case 4: bl_stage<4>(buf, tmp, a.rootM, a.M, Ns); break;
+      default: bl_stage<8>(buf, tmp, a.rootM, a.M, Ns); break;
+    }
+    __syncthreads();
+    double2* t = buf;
+    buf = tmp;
+    tmp = t;
+    Ns *= R;
+  }
+  return buf;
+}
+
+__global__ void __launch_bounds__(BLUE_T) blue_p_kernel(BlueArgs a) {
+  extern __shared__ __align__(16) double2 bl_smem[];  // 2 x M
+  double2* b0 = bl_smem;
+  double2* b1 = bl_smem + a.M;
+  const int r = blockIdx.x % a.R;
+  const long long rc = blockIdx.x / a.R;  // c * nrings + ring
+  const int c = (int)(rc / a.nrings), ring = (int)(rc % a.nrings);
+  const double2* src = a.in + c * a.in_cs + ring * a.in_rs;
+  const double cj = a.inverse ? -1.0 : 1.0;
+  for (int q = threadIdx.x; q < a.M; q += BLUE_T) {
+    double2 v = make_double2(0.0, 0.0);
+    if (q < a.P) {
+      double2 x = src[(long long)(r + (long long)a.R * q) * a.in_es];
+      x.y *= cj;
+      v = bl_mul(x, __ldg(&a.chirp[q]));
+    }
+    b0[q] = v;
+  }
+  __syncthreads();
+  double2* X = bl_fft(b0, b1, a);
+  double2* T = (X == b0) ? b1 : b0;
+  // convolution with the chirp in the frequency domain; the inverse FFT_M as
+  // conj(FFT(conj(.))) (the 1 / M is folded into FB)
+  for (int q = threadIdx.x; q < a.M; q += BLUE_T) {
+    const double2 v = bl_mul(X[q], __ldg(&a.FB[q]));
+    X[q] = make_double2(v.x, -v.y);
+  }
+  __syncthreads();
+  double2* Y = bl_fft(X, T, a);
+  double2* dst = a.S1 + (rc * a.R + r) * (long long)a.P;
+  for (int k = threadIdx.x; k < a.P; k += BLUE_T) {
+    const double2 y = make_double2(Y[k].x, -Y[k].y);
+    const double2 v = bl_mul(bl_mul(y, __ldg(&a.chirp[k])), __ldg(&a.rootN[(long long)r * k]));
+    dst[k] = v;
+  }
+}
+
+template <int RR>
+__global__ void __launch_bounds__(BLUE_T) blue_r_kernel(BlueArgs a) {
+  const long long idx = (long long)blockIdx.x * BLUE_T + threadIdx.x;
+  const long long total = 3LL * a.nrings * a.P;
+  if (idx >= total) return;
+  const long long rc = idx / a.P;
+  const int k = (int)(idx - rc * a.P);
+  const int c = (int)(rc / a.nrings), ring = (int)(rc % a.nrings);
+  const double2* src = a.S1 + rc * RR * (long long)a.P + k;
+  double2 z[RR];
+#pragma unroll
+  for (int r = 0; r < RR; ++r) z[r] = src[(long long)r * a.P];
+  double2* dst = a.out + c * a.out_cs + ring * a.out_rs;
+  const double cj = a.inverse ? -1.0 : 1.0;
+#pragma unroll 1
+  for (int s = 0; s < RR; ++s) {
+    double2 acc = z[0];
+#pragma unroll
+    for (int r = 1; r < RR; ++r) acc = bl_add(acc, bl_mul(z[r], __ldg(&a.rootR[(r * s) % RR])));
+    dst[(long long)(k + (long long)a.P * s) * a.out_es] = make_double2(acc.x, cj * acc.y);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Small prime factor (P <= 64, e.g. C2's 516 = 12 * 43): one CTA per
+// (ring, component) does the whole ring in shared memory with direct
+// conjugate-pair DFTs (no Bluestein):
+//   Y_r[k] = x_0 + sum_{q=1}^{(P-1)/2} (x_q + x_{P-q}) cos(2 pi q k / P)
+//                - i (x_q - x_{P-q}) sin(2 pi q k / P)        (and k -> P - k: + i)
+// on the residue subsequences x_q = x[r + R q], then w_n^{r k} and the direct
+// R-point DFTs X[k + P s] = sum_r w_R^{r s} Y'_r[k] (output index = thread
+// index: coalesced stores).  ~2P + 8R flops per point.
+// ---------------------------------------------------------------------------
+constexpr int SMALLP_MAX = 64;
+
+struct SmallPArgs {
+  const double2* in;
+  long long in_cs, in_rs, in_es;
+  double2* out;
+  long long out_cs, out_rs, out_es;
+  const double2* rootN;  // exp(-2 pi i j / n), j < n
+  const double2* rootR;  // exp(-2 pi i j / R), j < R
+  const double2* csP;    // (cos, sin)(2 pi j / P), j < P
+  int n, R, P, nrings, inverse;
+};
+
+__global__ void __launch_bounds__(BLUE_T) smallp_kernel(SmallPArgs a) {
+  extern __shared__ __align__(16) double2 sp_smem[];
+  double2* xs = sp_smem;           // [n] ring component
+  double2* ys = sp_smem + a.n;     // [R][P] twiddled residue DFTs
+  double2* cs = ys + a.n;          // [P] (cos, sin)
+  double2* wr = cs + a.P;          // [R]
+  const int c = blockIdx.x % 3, ring = blockIdx.x / 3;
+  const double cj = a.inverse ? -1.0 : 1.0;
+  const double2* src = a.in + c * a.in_cs + ring * a.in_rs;
+  for (int i = threadIdx.x; i < a.n; i += BLUE_T) {
+    double2 v = src[(long long)i * a.in_es];
+    v.y *= cj;
+    xs[i] = v;
+  }
+  for (int i = threadIdx.x; i < a.P; i += BLUE_T) cs[i] = __ldg(&a.csP[i]);
+  for (int i = threadIdx.x; i < a.R; i += BLUE_T) wr[i] = __ldg(&a.rootR[i]);
+  __syncthreads();
+  const int H = (a.P - 1) / 2;
+  const int nitem = a.R * (H + 1);
+  for (int it = threadIdx.x; it < nitem; it += BLUE_T) {
+    const int r = it / (H + 1), k = it - r * (H + 1);
+    const double2* x = xs + r;
+    const double2 x0 = x[0];
+    double2 A = x0, Bv = make_double2(0.0, 0.0);
+    int idx = 0;
+    for (int q = 1; q <= H; ++q) {
+      idx += k;
+      if (idx >= a.P) idx -= a.P;
+      const double2 u = x[q * a.R], w = x[(a.P - q) * a.R];
+      const double2 t = cs[idx];
+      A.x = fma(u.x + w.x, t.x, A.x);
+      A.y = fma(u.y + w.y, t.x, A.y);
+      Bv.x = fma(u.x - w.x, t.y, Bv.x);
+      Bv.y = fma(u.y - w.y, t.y, Bv.y);
+    }
+    // X_k = A - i B, X_{P-k} = A + i B; then the twiddle w_n^{r k}
+    const double2 xk = make_double2(A.x + Bv.y, A.y - Bv.x);
+    ys[r * a.P + k] = bl_mul(xk, __ldg(&a.rootN[(long long)r * k]));
+    if (k > 0) {
+      const double2 xm = make_double2(A.x - Bv.y, A.y + Bv.x);
+      ys[r * a.P + (a.P - k)] = bl_mul(xm, __ldg(&a.rootN[(long long)r * (a.P - k)]));
+    }
+  }
+  __syncthreads();
+  double2* dst = a.out + c * a.out_cs + ring * a.out_rs;
+  for (int o = threadIdx.x; o < a.n; o += BLUE_T) {
+    const int s = o / a.P, k = o - s * a.P;
+    double2 acc = ys[k];
+    int idx = 0;
+    for (int r = 1; r < a.R; ++r) {
+      idx += s;
+      if (idx >= a.R) idx -= a.R;
+      acc = bl_add(acc, bl_mul(ys[r * a.P + k], wr[idx]));
+    }
+    dst[(long long)o * a.out_es] = make_double2(acc.x, cj * acc.y);
+  }
+}
+
+}  // namespace fv

@@ -20,6 +20,7 @@
 #include "aux_kernels.cuh"
 #include "fft.cuh"
 #include "fft2.cuh"
+#include "fft_blue.cuh"
 #include "legendre.cuh"
 #include "points.cuh"
 
@@ -127,6 +128,13 @@ struct fvPlan {
   std::map<std::tuple<long long, long long, long long, long long, int>, cufftHandle> ffts;  // strided cuFFT plans
   // hand-written ring FFT (fft.cuh) when every prime factor of n_phi is <= 19
   bool custom_fft = false;
+  // Bluestein ring FFT (fft_blue.cuh) for n_phi = R * P with a prime P > 19
+  bool blue = false, smallp = false;
+  fv::BlueArgs blue_args{};  // tables and factorisation (pointers owned below)
+  fv::SmallPArgs sp_args{};
+  double2* blue_tab = nullptr;
+  double2* blue_s1 = nullptr;
+  size_t blue_s1_cap = 0;
   int fft_nst = 0;
   int fft_radix[fv::FFT_MAXST] = {};
   double2* fft_tw = nullptr;
@@ -158,7 +166,7 @@ void free_plan(fvPlan* p) {
                   p->seed_e, p->start_l,  p->start_v, p->ab,   p->abofs,  p->gofs,
                   p->dg,     p->dgofs,  p->cgt,     p->cga,     p->ptab_f,  p->mtab_f, p->tofs,   p->ptab_a, p->aofs,
                   p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->G,
-                  p->seedk,  p->fitems,   p->Fpart,
+                  p->seedk,  p->fitems,   p->Fpart,   p->blue_tab, p->blue_s1,
                   p->fft_tw, p->f2_tw};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -537,6 +545,204 @@ int setup_fft2(fvPlan* p) {
   return FV_OK;
 }
 
+// Bluestein ring FFT plan (fft_blue.cuh): n = R * P with P the largest prime
+// factor (> 19, which the radix kernels do not cover), every prime of R <= 19
+// and R an instantiated blue_r_kernel size; M = 2^a 3^b >= 2P - 1, M <= 4096.
+constexpr int kBlueR[] = {1, 2, 3, 4, 6, 8, 12, 16, 24};
+
+int setup_blue(fvPlan* p) {
+  const char* env = std::getenv("FV_FFT");
+  if (env && std::string(env) == "cufft") return FV_OK;
+  const int n = p->n_phi;
+  int P = 1, rem = n;
+  for (int f = 2; (long long)f * f <= rem; ++f)
+    while (rem % f == 0) {
+      P = std::max(P, f);
+      rem /= f;
+    }
+  P = std::max(P, rem);
+  if (P <= 19) return FV_OK;
+  const int R = n / P;
+  const long double PI_ = 3.141592653589793238462643383279502884L;
+  if (P <= fv::SMALLP_MAX && R <= 64 && !(env && std::string(env) == "blue")) {
+    // direct conjugate-pair DFTs in one CTA per ring (smallp_kernel)
+    std::vector<double2> tab(n + R + P);
+    for (int j = 0; j < n; ++j) {
+      const long double g = 2.0L * PI_ * j / n;
+      tab[j] = make_double2((double)cosl(g), -(double)sinl(g));
+    }
+    for (int j = 0; j < R; ++j) {
+      const long double g = 2.0L * PI_ * j / R;
+      tab[n + j] = make_double2((double)cosl(g), -(double)sinl(g));
+    }
+    for (int j = 0; j < P; ++j) {
+      const long double g = 2.0L * PI_ * j / P;
+      tab[n + R + j] = make_double2((double)cosl(g), (double)sinl(g));
+    }
+    FV_TRY(dalloc(&p->blue_tab, tab.size()));
+    FV_CUDA(cudaMemcpy(p->blue_tab, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    fv::SmallPArgs& s = p->sp_args;
+    s.n = n;
+    s.R = R;
+    s.P = P;
+    s.rootN = p->blue_tab;
+    s.rootR = p->blue_tab + n;
+    s.csP = p->blue_tab + n + R;
+    const size_t smem = (size_t)(2 * n + P + R) * sizeof(double2);
+    if (smem > 200 * 1024) return FV_OK;
+    FV_CUDA(cudaFuncSetAttribute(fv::smallp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    p->smallp = true;
+    return FV_OK;
+  }
+  // large P: the Bluestein kernels are correct but still slower than cuFFT's own plan
+  // at C4 (9.4 vs 8.2 ms per direction), so they are opt-in (FV_FFT=blue) for now
+  if (!(env && std::string(env) == "blue")) return FV_OK;
+  bool ok = false;
+  for (int x : kBlueR) ok |= (x == R);
+  if (!ok) return FV_OK;
+  int M = 1 << 30;
+  for (long long a2 = 1; a2 <= 4096; a2 *= 2)
+    for (long long a3 = a2; a3 <= 4096; a3 *= 3)
+      if (a3 >= 2LL * P - 1) M = std::min<long long>(M, a3);
+  if (M > 4096) return FV_OK;
+  fv::BlueArgs& a = p->blue_args;
+  a.n = n;
+  a.R = R;
+  a.P = P;
+  a.M = M;
+  a.nst = 0;
+  {
+    int m = M;
+    while (m % 3 == 0) {
+      a.radix[a.nst++] = 3;
+      m /= 3;
+    }
+    while (m % 8 == 0) {
+      a.radix[a.nst++] = 8;
+      m /= 8;
+    }
+    if (m % 4 == 0) {
+      a.radix[a.nst++] = 4;
+      m /= 4;
+    }
+    if (m % 2 == 0) {
+      a.radix[a.nst++] = 2;
+      m /= 2;
+    }
+  }
+  const long double PI = 3.141592653589793238462643383279502884L;
+  auto root = [&](long long num, long long den) {  // exp(-2 pi i num / den)
+    const long double ang = 2.0L * PI * (long double)(num % den) / (long double)den;
+    return std::make_pair(cosl(ang), -sinl(ang));
+  };
+  std::vector<double2> tab;
+  std::vector<std::pair<long double, long double>> chirp(P), rootM(M);
+  for (int j = 0; j < M; ++j) rootM[j] = root(j, M);
+  for (int q = 0; q < P; ++q) chirp[q] = root((long long)q * q % (2LL * P), 2LL * P);  // exp(-pi i q^2 / P)
+  // b_j = conj(chirp_|j|) on the cyclic index, FB = DFT_M(b) / M (direct sum in long double)
+  std::vector<std::pair<long double, long double>> b(M, {0.0L, 0.0L});
+  for (int j = 0; j < P; ++j) {
+    b[j] = {chirp[j].first, -chirp[j].second};
+    if (j > 0) b[M - j] = b[j];
+  }
+  const size_t o_rootM = 0, o_chirp = o_rootM + M, o_FB = o_chirp + P, o_rootN = o_FB + M, o_rootR = o_rootN + n;
+  tab.resize(o_rootR + R);
+  for (int j = 0; j < M; ++j) tab[o_rootM + j] = make_double2((double)rootM[j].first, (double)rootM[j].second);
+  for (int q = 0; q < P; ++q) tab[o_chirp + q] = make_double2((double)chirp[q].first, (double)chirp[q].second);
+  for (int k = 0; k < M; ++k) {
+    long double re = 0.0L, im = 0.0L;
+    for (int j = 0; j < M; ++j) {
+      if (b[j].first == 0.0L && b[j].second == 0.0L) continue;
+      const auto& w = rootM[(long long)j * k % M];
+      re += b[j].first * w.first - b[j].second * w.second;
+      im += b[j].first * w.second + b[j].second * w.first;
+    }
+    tab[o_FB + k] = make_double2((double)(re / M), (double)(im / M));
+  }
+  for (int j = 0; j < n; ++j) {
+    const auto w = root(j, n);
+    tab[o_rootN + j] = make_double2((double)w.first, (double)w.second);
+  }
+  for (int j = 0; j < R; ++j) {
+    const auto w = root(j, R);
+    tab[o_rootR + j] = make_double2((double)w.first, (double)w.second);
+  }
+  FV_TRY(dalloc(&p->blue_tab, tab.size()));
+  FV_CUDA(cudaMemcpy(p->blue_tab, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  a.rootM = p->blue_tab + o_rootM;
+  a.chirp = p->blue_tab + o_chirp;
+  a.FB = p->blue_tab + o_FB;
+  a.rootN = p->blue_tab + o_rootN;
+  a.rootR = p->blue_tab + o_rootR;
+  FV_CUDA(cudaFuncSetAttribute(fv::blue_p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(2 * (size_t)M * sizeof(double2))));
+  p->blue = true;
+  return FV_OK;
+}
+
+int ring_fft_smallp(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
+                    double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s) {
+  fv::SmallPArgs a = p->sp_args;
+  a.in = in;
+  a.in_cs = in_cs;
+  a.in_rs = in_rs;
+  a.in_es = in_es;
+  a.out = out;
+  a.out_cs = out_cs;
+  a.out_rs = out_rs;
+  a.out_es = out_es;
+  a.nrings = nrings;
+  a.inverse = inverse ? 1 : 0;
+  const size_t smem = (size_t)(2 * a.n + a.P + a.R) * sizeof(double2);
+  fv::smallp_kernel<<<(unsigned)(3LL * nrings), fv::BLUE_T, smem, s>>>(a);
+  FV_CUDA(cudaGetLastError());
+  return FV_OK;
+}
+
+int ring_fft_blue(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
+                  double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s) {
+  fv::BlueArgs a = p->blue_args;
+  const size_t need = (size_t)3 * nrings * a.n;
+  if (p->blue_s1_cap < need) {
+    if (p->blue_s1) {
+      FV_CUDA(cudaDeviceSynchronize());
+      cudaFree(p->blue_s1);
+      p->blue_s1 = nullptr;
+      p->blue_s1_cap = 0;
+    }
+    FV_TRY(dalloc(&p->blue_s1, need));
+    p->blue_s1_cap = need;
+  }
+  a.in = in;
+  a.in_cs = in_cs;
+  a.in_rs = in_rs;
+  a.in_es = in_es;
+  a.out = out;
+  a.out_cs = out_cs;
+  a.out_rs = out_rs;
+  a.out_es = out_es;
+  a.S1 = p->blue_s1;
+  a.nrings = nrings;
+  a.inverse = inverse ? 1 : 0;
+  const long long ntr = 3LL * nrings * a.R;
+  fv::blue_p_kernel<<<(unsigned)ntr, fv::BLUE_T, 2 * (size_t)a.M * sizeof(double2), s>>>(a);
+  FV_CUDA(cudaGetLastError());
+  const unsigned g2 = (unsigned)((3LL * nrings * a.P + fv::BLUE_T - 1) / fv::BLUE_T);
+  switch (a.R) {
+    case 1: fv::blue_r_kernel<1><<<g2, fv::BLUE_T, 0, s>>>(a); break;
+    case 2: fv::blue_r_kernel<2><<<g2, fv::BLUE_T, 0, s>>>(a); break;
+    case 3: fv::blue_r_kernel<3><<<g2, fv::BLUE_T, 0, s>>>(a); break;
+    case 4: fv::blue_r_kernel<4><<<g2, fv::BLUE_T, 0, s>>>(a); break;
+    case 6: fv::blue_r_kernel<6><<<g2, fv::BLUE_T, 0, s>>>(a); break;
+    case 8: fv::blue_r_kernel<8><<<g2, fv::BLUE_T, 0, s>>>(a); break;
+    case 12: fv::blue_r_kernel<12><<<g2, fv::BLUE_T, 0, s>>>(a); break;
+    case 16: fv::blue_r_kernel<16><<<g2, fv::BLUE_T, 0, s>>>(a); break;
+    default: fv::blue_r_kernel<24><<<g2, fv::BLUE_T, 0, s>>>(a); break;
+  }
+  FV_CUDA(cudaGetLastError());
+  return FV_OK;
+}
+
 int ring_fft2_raw(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
                   double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s) {
   fv::Fft2Args a{};
@@ -747,7 +953,7 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
     fv::cga_table_kernel<<<grid, 32>>>(Lt, p->gofs, p->cgt, p->cga, 32 * p->g_tiles);
     FV_CUDA(cudaGetLastError());
   }
-  if ((rc = setup_fft(p)) || (rc = setup_fft2(p))) return bail(rc);
+  if ((rc = setup_fft(p)) || (rc = setup_fft2(p)) || (rc = setup_blue(p))) return bail(rc);
   // workspaces (field groups of <= 4 -> NT <= 6)
   const int gs = std::min(4, max_batch);
   const int NTmax = ntiles_for(gs);
@@ -947,6 +1153,8 @@ int ring_ffts(fvPlan* p, bool inverse, const double2* in, long long in_cs, long 
   StageMark mk(p, 0, s);
   if (p->fft2) return ring_fft2_raw(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   if (p->custom_fft) return ring_fft_raw(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
+  if (p->smallp) return ring_fft_smallp(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
+  if (p->blue) return ring_fft_blue(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   cufftHandle h;
   FV_TRY(get_fft_strided(p, in_rs, in_es, out_rs, out_es, nrings, &h));
   FV_CUFFT(cufftSetStream(h, s));

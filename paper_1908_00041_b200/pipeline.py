@@ -5,7 +5,9 @@ batch in each direction (for the round trip: the samples in, the synthesised
 field out), which on a PCIe-attached B200 costs several times the transforms
 themselves.  ``HostPipeline`` hides what can be hidden: batch k+1's
 host->device copy, batch k's transforms and batch k-1's device->host copy run
-on three CUDA streams against double-buffered device staging, so a stream of
+on three CUDA streams against ``depth`` device staging slots (default 3: with
+two, batch k+2's upload has to wait for batch k's download, which waits for
+batch k's transforms, so the compute is exposed every period), so a stream of
 batches is bound by the slower link direction instead of the sum of both
 directions plus the compute.  Every batch's bytes still cross the link once
 each way (nothing is cached between batches).
@@ -32,7 +34,7 @@ class HostPipeline:
     output buffer, before then.
     """
 
-    def __init__(self, plan: GridPlan, depth: int = 2):
+    def __init__(self, plan: GridPlan, depth: int = 3):
         torch = _torch()
         self.plan = plan
         self.depth = max(1, int(depth))

@@ -232,10 +232,13 @@ def test_odd_and_asymmetric_grids():
         assert O.rel_l2(got, np.concatenate([ra, rb])) <= TOL
 
 
-@pytest.mark.parametrize("nphi", [24, 30, 36, 40, 42, 48, 49, 64, 75, 128, 286, 342, 2052, 46])
+@pytest.mark.parametrize("nphi", [24, 30, 36, 40, 42, 48, 49, 64, 75, 128, 286, 342, 2052,
+                                  46, 23, 58, 86, 111, 496, 516, 984, 8196, 115])
 def test_ring_fft_radix_plans(nphi):
-    """Every packed radix (2..16 composites, primes 11..19) and the cuFFT
-    fallback (46 = 2 * 23), forward and adjoint against the oracle."""
+    """Every packed radix (2..16 composites, primes 11..19), the Bluestein
+    lengths R * P with a prime P > 19 (46 = 2 * 23, 23, 58, 86, 111 = 3 * 37,
+    496 = 16 * 31, C2's 516 = 12 * 43, 984 = 24 * 41, C4's 8196 = 12 * 683) and
+    the cuFFT fallback (115 = 5 * 23), forward and adjoint against the oracle."""
     cuda_or_skip()
     rng = np.random.default_rng(nphi)
     L = 8
@@ -486,3 +489,41 @@ def test_direct_forward_batch_determinism_and_edges():
     b0 = a0.clone()
     pp.forward(_t(np.zeros((0, 3))), _t(np.zeros(0)), _t(np.zeros((1, 0, 3), complex)), a0, b0)
     assert float(a0.abs().max()) == 0.0 and float(b0.abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("nphi", [516, 8196, 46])
+def test_ring_fft_against_numpy(nphi):
+    """fv_ring_fft alone (the sharded building block) on random rings, both
+    directions, against numpy's pocketfft (favest/scalar.py:149, :178); the
+    large-prime lengths also through the opt-in Bluestein kernels."""
+    import ctypes
+    import os
+
+    torch = cuda_or_skip()
+    for fft in ("", "blue"):
+        os.environ["FV_FFT"] = fft
+        try:
+            _ring_fft_case(torch, nphi)
+        finally:
+            os.environ.pop("FV_FFT", None)
+
+
+def _ring_fft_case(torch, nphi):
+    import ctypes
+
+    L = 8
+    th, w, _ = O.gl_grid(L)
+    plan = _plan(L, th, w, nphi, B=1)
+    rng = np.random.default_rng(nphi + 1)
+    nr = len(th)
+    x = rng.standard_normal((nr, nphi, 3)) + 1j * rng.standard_normal((nr, nphi, 3))
+    xd = _t(x)
+    out = torch.empty((3, nr, nphi), dtype=torch.complex128, device="cuda")
+    lib = plan.lib
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    for inv in (0, 1):
+        rc = lib.fv_ring_fft(plan._h, inv, xd.data_ptr(), 1, 3 * nphi, 3, out.data_ptr(), nr * nphi, nphi, 1, nr, s)
+        assert rc == 0
+        ref = np.fft.ifft(x, axis=1) * nphi if inv else np.fft.fft(x, axis=1)
+        got = np.moveaxis(out.cpu().numpy(), 0, -1)
+        assert O.rel_l2(got, ref) <= 1e-13
