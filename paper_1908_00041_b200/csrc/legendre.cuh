@@ -328,7 +328,17 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       if (item >= args.m_count) break;
       const int m = args.m_begin + item;
       const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
-      // this warp's chunks only: no other warp touches these state entries
+      // Tile ownership.  A producer waits for its slot with a parity wait, which
+      // aliases once the slot is two rounds behind, so each warp's consecutive
+      // tiles must be at most FWD_STAGES apart: with nchunks >= 4 the warps take
+      // the order's tiles round robin (every 4th tile; a chunk's recurrence state
+      // then moves between warps from one l-block to the next, ordered by the
+      // full -> consumer -> empty barrier chain because nchunks >= FWD_STAGES
+      // puts the chunk's previous tile at least one stage round earlier); with
+      // fewer chunks each warp keeps chunk pw (tiles nchunks <= 3 apart).
+      const bool rr = nchunks >= kProducerWarps;
+      static_assert(FWD_STAGES >= kProducerWarps + 1, "round-robin tiles need nchunks >= FWD_STAGES handoff");
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kProducerWarps) : "memory");  // previous order's tiles done
       for (int c = pw; c < nchunks; c += kProducerWarps) {
         const int p = c * FWD_RC + lane;
         st_t[p] = args.pair_t[p];
@@ -336,12 +346,15 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
         st_p1[p] = 0.0;
         st_p2[p] = 0.0;
       }
-      __syncwarp();
-      for (int j = 0; j < nlb; ++j) {
+      asm volatile("bar.sync 1, %0;" ::"n"(32 * kProducerWarps) : "memory");
+      const int ntl = nlb * nchunks;
+      int jprev = -1;
+      for (int tl = pw; tl < ntl && (rr || pw < nchunks); tl += rr ? kProducerWarps : nchunks) {
+        const int j = tl / nchunks, c = tl - j * nchunks;
         const int l0 = m + FWD_LB * j;
-        if (!table) fwd_stage_coefs(abw, args, m, l0, lane);
-        for (int c = pw; c < nchunks; c += kProducerWarps) {
-          const int tl = j * nchunks + c;
+        if (!table && j != jprev) fwd_stage_coefs(abw, args, m, l0, lane);
+        jprev = j;
+        {
           const uint32_t t = tbase + tl;
           const int stage = t % FWD_STAGES;
           const uint32_t round = t / FWD_STAGES;

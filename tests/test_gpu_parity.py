@@ -527,3 +527,41 @@ def _ring_fft_case(torch, nphi):
         ref = np.fft.ifft(x, axis=1) * nphi if inv else np.fft.fft(x, axis=1)
         got = np.moveaxis(out.cpu().numpy(), 0, -1)
         assert O.rel_l2(got, ref) <= 1e-13
+
+
+@pytest.mark.parametrize("L,B", [(100, 5), (300, 1), (400, 2), (450, 1), (700, 1)])
+def test_on_the_fly_legendre_matches_table_mode(L, B):
+    """FV_PTAB=0 (the on-the-fly recurrence producer; what large L uses when the
+    plan tables do not fit) against the oracle and the table-mode plan, at
+    forward chunk counts 2, 5, 7, 8 and 11 (32 ring pairs per chunk): every
+    residue of the producer warps' tile ownership modulo 4."""
+    import os
+
+    cuda_or_skip()
+    th, w, nphi = O.gl_grid(L)
+    rng = np.random.default_rng(L + B)
+    A, Bc = [], []
+    for _ in range(B):
+        a, b = O.coef(rng, L, "inv")
+        A.append(a)
+        Bc.append(b)
+    A, Bc = np.stack(A), np.stack(Bc)
+    res = {}
+    for mode in ("1", "0"):
+        os.environ["FV_PTAB"] = mode
+        try:
+            plan = _plan(L, th, w, nphi, B=B)
+        finally:
+            os.environ.pop("FV_PTAB", None)
+        T = plan.adjoint(_t(A), _t(Bc))
+        fa, fb_ = plan.forward(T)
+        res[mode] = (T.cpu().numpy(), fa.cpu().numpy(), fb_.cpu().numpy())
+        del plan
+    for x, y in zip(res["0"], res["1"]):
+        assert O.rel_l2(x, y) <= 1e-13
+    T0 = res["0"][0]
+    for f in (0, B - 1):
+        assert O.rel_l2(T0[f], O.vsht_adjoint_grid(A[f], Bc[f], L, th, nphi)) <= TOL
+        ra, rb = O.vsht_forward_grid(T0[f], th, w, nphi, L)
+        got = np.concatenate([res["0"][1][f], res["0"][2][f]])
+        assert O.rel_l2(got, np.concatenate([ra, rb])) <= TOL
