@@ -120,9 +120,11 @@ template <int NT>
 struct FwdSmem {
   static constexpr int XTILE = 2 * 8 * NT * 32;
   static constexpr int STAGE = FWD_PTILE + XTILE;
+  // K-split consumers (NT <= 2): partial sums of k-quarters 1..3 [par][3][Mtile 4][NT][2][lane]
+  static constexpr int KRED = NT <= 2 ? 2 * 3 * 4 * NT * 2 * 32 : 0;
   static constexpr size_t bytes(int nPx) {
     return (size_t)FWD_STAGES * STAGE * 8 + 2 * FWD_STAGES * 8 + FWD_STAGES * sizeof(StageMeta) +
-           kProducerWarps * FWD_LB * 16 + (size_t)nPx * 28;
+           kProducerWarps * FWD_LB * 16 + (size_t)nPx * 28 + (size_t)KRED * 8;
   }
 };
 
@@ -397,6 +399,118 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
   }
 
   // -------------------------------- consumers --------------------------------
+  if constexpr (NT <= 2) {
+    // Single-field launches (NT <= 2: 12 columns): with the (parity, row half,
+    // column half) split below every warp would hold one n-tile, 1.5 fragment
+    // loads per DMMA, and the consumers become shared-memory-issue bound (C4:
+    // 30.7 of 32.7 ms with the recurrence switched off).  K-split instead: warp
+    // (par, kq) takes all four M-tiles x NT n-tiles of its parity over k-steps
+    // 2 kq, 2 kq + 1 (0.75 loads per DMMA); the four k-quarter partial sums are
+    // added in a fixed order (kq 0, 1, 2, 3) at each l-block's epilogue.
+    const int cw = consumer_index(warp);
+    const int par = cw >> 2, kq = cw & 3;
+    const int g = lane >> 2, q = lane & 3;
+    const int xq = (g >> 2) * 16 + q * 4 + (g & 3);
+    const int ncolF = 8 * NT;
+    double* red = reinterpret_cast<double*>(st_ls + nPx);
+    double acc[4][NT][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int jn = 0; jn < NT; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
+    uint32_t tbase = 0;
+    for (int k = 0;; ++k) {
+      const int item = fwd_item(k, blockIdx.x, gridDim.x);
+      if (item >= args.m_count) break;
+      const int m = args.m_begin + item;
+      const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
+      for (int j = 0; j < nlb; ++j) {
+        const int l0 = m + FWD_LB * j;
+        for (int c = 0; c < nchunks; ++c) {
+          const uint32_t t = tbase + j * nchunks + c;
+          const int stage = t % FWD_STAGES;
+          mbar_wait(&full[stage], (t / FWD_STAGES) & 1);
+          const double* Ps = smem + stage * SM::STAGE;
+          const double* Xs = Ps + FWD_PTILE;
+          const int km0 = meta[stage].kmin[2 * kq], km1 = meta[stage].kmin[2 * kq + 1];
+          if (!meta[stage].zero && !(args.dbg & 1)) {
+            double a[2][4], bb[2][NT];
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+              const int ks = 2 * kq + kk;
+              const int sw = ((g ^ (ks & 3)) << 2) + q;
+#pragma unroll
+              for (int i = 0; i < 4; ++i) a[kk][i] = lds_f64(&Ps[((par * 4 + i) * 8 + ks) * 32 + sw]);
+#pragma unroll
+              for (int jn = 0; jn < NT; ++jn) bb[kk][jn] = lds_f64(&Xs[((par * 8 + ks) * NT + jn) * 32 + xq]);
+            }
+            // M-tile i (rows l0 + 16 i .. + 15) runs k-step ks once some pair of it has
+            // started (kmin[ks] <= last row) and it is not padding past Lt; real branches
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const int r0 = l0 + 16 * i;
+              if (r0 > Lt) continue;
+              if (km0 <= r0 + 15) {
+#pragma unroll
+                for (int jn = 0; jn < NT; ++jn) dmma_m8n8k4(acc[i][jn][0], acc[i][jn][1], a[0][i], bb[0][jn]);
+              }
+              if (km1 <= r0 + 15) {
+#pragma unroll
+                for (int jn = 0; jn < NT; ++jn) dmma_m8n8k4(acc[i][jn][0], acc[i][jn][1], a[1][i], bb[1][jn]);
+              }
+            }
+          }
+          mbar_arrive(&empty[stage]);
+        }
+        // epilogue of the l-block: k-quarters 1..3 park their partial sums, quarter 0
+        // adds them in order and writes rows l = l0 + 2 (8 i + g) + par
+        double* rp = red + (size_t)(par * 3) * 4 * NT * 64;
+        if (kq > 0) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int jn = 0; jn < NT; ++jn) {
+              double* r = rp + (((kq - 1) * 4 + i) * NT + jn) * 64;
+              r[lane] = acc[i][jn][0];
+              r[32 + lane] = acc[i][jn][1];
+            }
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * kConsumerWarps) : "memory");
+        if (kq == 0) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int l = l0 + 2 * (8 * i + g) + par;
+            double v[NT][2];
+#pragma unroll
+            for (int jn = 0; jn < NT; ++jn) {
+              v[jn][0] = acc[i][jn][0];
+              v[jn][1] = acc[i][jn][1];
+#pragma unroll
+              for (int w = 0; w < 3; ++w) {
+                const double* r = rp + ((w * 4 + i) * NT + jn) * 64;
+                v[jn][0] += r[lane];
+                v[jn][1] += r[32 + lane];
+              }
+            }
+            if (l <= Lt) {
+              double* row = args.F + ((size_t)l * (l + 1) / 2 + m) * ncolF;
+              const double gam = args.dg[args.dgofs[m] + (l - m)].y;  // P_l = gamma_l R_l
+#pragma unroll
+              for (int jn = 0; jn < NT; ++jn)
+                *reinterpret_cast<double2*>(row + jn * 8 + 2 * q) = make_double2(gam * v[jn][0], gam * v[jn][1]);
+            }
+          }
+        }
+        asm volatile("bar.sync 2, %0;" ::"n"(32 * kConsumerWarps) : "memory");
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int jn = 0; jn < NT; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
+      }
+      tbase += nlb * nchunks;
+    }
+    return;
+  }
   constexpr int NTW = (NT + 1) / 2;
   const int cw = consumer_index(warp);
   const int par = cw >> 2;
@@ -676,6 +790,13 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
       double p1 = 0.0, p2 = 0.0;
       const double2* dgm = args.dg + args.dgofs[m];
       const double* Gm = args.G + (size_t)args.gofs[m] * SM::GTILE;
+      // (d, gamma) of the stage's 32 degrees, one per lane, loaded one stage ahead
+      // (an L2 round trip on the recurrence's critical path otherwise)
+      auto dg_at = [&](int lcx) {
+        const int l = m + ADJ_LC * lcx + lane;
+        return (l <= Lt) ? __ldg(&dgm[l - m]) : make_double2(0.0, 1.0);
+      };
+      double2 dg_next = table ? make_double2(0.0, 1.0) : dg_at(0);
       for (int lc = 0; lc < nlc; ++lc, ++sc) {
         const int stage = sc % ADJ_STAGES;
         const uint32_t round = sc / ADJ_STAGES;
@@ -683,11 +804,14 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
         const bool before = in.ls > l0 + ADJ_LC - 1;
         const bool zero = __all_sync(0xffffffffu, before);
         const bool mixed = __any_sync(0xffffffffu, !before && in.ls + 1 >= l0);
-        if (!zero && !table) {
-          __syncwarp();
-          const int l = l0 + lane;
-          abw[lane] = (l <= Lt) ? dgm[l - m] : make_double2(0.0, 1.0);
-          __syncwarp();
+        if (!table) {
+          const double2 dg_cur = dg_next;
+          if (lc + 1 < nlc) dg_next = dg_at(lc + 1);
+          if (!zero) {
+            __syncwarp();
+            abw[lane] = dg_cur;
+            __syncwarp();
+          }
         }
         // table mode: each producer warp copies the run of its four M-tiles that
         // holds a started pair in this stage (polar start, padding pairs) -- the
