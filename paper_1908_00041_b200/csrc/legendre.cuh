@@ -131,7 +131,7 @@ struct FwdSmem {
 // rows idx = 0..63 of one (l-block, chunk) tile; lane = ring pair 4s+q of the chunk.
 // (d, gamma) for the 64 rows are staged in shared memory and pulled 8 at a time;
 // rows 31 and 63 end a 32-degree block: the state goes back to P units there.
-template <bool MIXED>
+template <bool MIXED, bool SCALE = false>
 __device__ __forceinline__ void fwd_produce(double* Ps, const double2* dgw, double tt, double& p1, double& p2,
                                             int lane, int l0, const Inject& in) {
   const int s = lane >> 2, q = lane & 3, sx = s & 3;
@@ -148,7 +148,7 @@ __device__ __forceinline__ void fwd_produce(double* Ps, const double2* dgw, doub
       const int idx = b0 + k;
       const double v = rec_step<MIXED>(p1, p2, tt, dd[k], l0 + idx, in);
       const int par = idx & 1, rp = idx >> 1, i = rp >> 3, g = rp & 7;
-      bp[g][(par * 4 + i) * 8 * 32] = v;
+      bp[g][(par * 4 + i) * 8 * 32] = SCALE ? v * dgw[idx].y : v;  // SCALE: Pbar itself (plan tables)
       if ((idx & 31) == 31) {
         p1 *= dgw[idx].y;
         p2 *= dgw[idx - 1].y;
@@ -171,9 +171,8 @@ struct TileClass {
   int km;  // smallest polar start of the lane's k-step
 };
 
-__device__ __forceinline__ TileClass fwd_classify(const FwdState& st, int p, int l0, int lane) {
+__device__ __forceinline__ TileClass fwd_classify_ls(int ls, int l0) {
   TileClass tc;
-  const int ls = st.ls[p];
   const bool before = ls > l0 + FWD_LB - 1;          // tile entirely below start
   const bool inject = !before && ls + 1 >= l0;        // start value(s) land in this tile
   tc.zero = __all_sync(0xffffffffu, before);
@@ -183,7 +182,12 @@ __device__ __forceinline__ TileClass fwd_classify(const FwdState& st, int p, int
   return tc;
 }
 
+__device__ __forceinline__ TileClass fwd_classify(const FwdState& st, int p, int l0, int lane) {
+  return fwd_classify_ls(st.ls[p], l0);
+}
+
 // rows of one (l-block j, chunk c) tile into Ps (shared or global), state update
+template <bool SCALE = false>
 __device__ __forceinline__ void fwd_compute(const FwdArgs& args, const FwdState& st, const TileClass& tc, double* Ps,
                                             const double2* abw, int m, int j, int nlb, int p, int l0, int lane) {
   Inject in;
@@ -196,8 +200,8 @@ __device__ __forceinline__ void fwd_compute(const FwdArgs& args, const FwdState&
   }
   double p1 = st.p1[p], p2 = st.p2[p];
   const double tt = st.t[p];
-  if (tc.mixed) fwd_produce<true>(Ps, abw, tt, p1, p2, lane, l0, in);
-  else fwd_produce<false>(Ps, abw, tt, p1, p2, lane, l0, in);
+  if (tc.mixed) fwd_produce<true, SCALE>(Ps, abw, tt, p1, p2, lane, l0, in);
+  else fwd_produce<false, SCALE>(Ps, abw, tt, p1, p2, lane, l0, in);
   if (j + 1 < nlb) {
     st.p1[p] = p1;
     st.p2[p] = p2;
@@ -251,7 +255,8 @@ __global__ void __launch_bounds__(32 * kProducerWarps) ptab_fwd_kernel(FwdArgs a
       const TileClass tc = fwd_classify(st, p, l0, lane);
       if (lane == 0) mtab[tile].zero = tc.zero;
       if ((lane & 3) == 0) mtab[tile].kmin[lane >> 2] = tc.km;
-      if (!tc.zero) fwd_compute(args, st, tc, ptab + tile * FWD_PTILE, abw, m, j, nlb, p, l0, lane);
+      // table tiles hold Pbar = gamma_l R_l itself: the table-mode epilogue needs no gamma
+      if (!tc.zero) fwd_compute<true>(args, st, tc, ptab + tile * FWD_PTILE, abw, m, j, nlb, p, l0, lane);
     }
   }
 }
@@ -340,15 +345,18 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       // fewer chunks each warp keeps chunk pw (tiles nchunks <= 3 apart).
       const bool rr = nchunks >= kProducerWarps;
       static_assert(FWD_STAGES >= kProducerWarps + 1, "round-robin tiles need nchunks >= FWD_STAGES handoff");
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * kProducerWarps) : "memory");  // previous order's tiles done
-      for (int c = pw; c < nchunks; c += kProducerWarps) {
-        const int p = c * FWD_RC + lane;
-        st_t[p] = args.pair_t[p];
-        st_ls[p] = args.start_l[(size_t)m * args.nPpad + p];
-        st_p1[p] = 0.0;
-        st_p2[p] = 0.0;
+      // (table mode reads the polar starts from global memory: no state to set up)
+      if (!table) {
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kProducerWarps) : "memory");  // previous order's tiles done
+        for (int c = pw; c < nchunks; c += kProducerWarps) {
+          const int p = c * FWD_RC + lane;
+          st_t[p] = args.pair_t[p];
+          st_ls[p] = args.start_l[(size_t)m * args.nPpad + p];
+          st_p1[p] = 0.0;
+          st_p2[p] = 0.0;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * kProducerWarps) : "memory");
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(32 * kProducerWarps) : "memory");
       const int ntl = nlb * nchunks;
       int jprev = -1;
       for (int tl = pw; tl < ntl && (rr || pw < nchunks); tl += rr ? kProducerWarps : nchunks) {
@@ -361,7 +369,8 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
           const int stage = t % FWD_STAGES;
           const uint32_t round = t / FWD_STAGES;
           const int p = c * FWD_RC + lane;
-          const TileClass tc = fwd_classify(st, p, l0, lane);
+          const TileClass tc =
+              fwd_classify_ls(table ? __ldg(&args.start_l[(size_t)m * args.nPpad + p]) : st_ls[p], l0);
           const bool tr = args.trace && blockIdx.x == args.trace_cta && lane == 0 && t < 4096;
           if (tr) args.trace[t * 8 + 0] = clock64();
           mbar_wait(&empty[stage], (round & 1) ^ 1);
@@ -494,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
             }
             if (l <= Lt) {
               double* row = args.F + ((size_t)l * (l + 1) / 2 + m) * ncolF;
-              const double gam = args.dg[args.dgofs[m] + (l - m)].y;  // P_l = gamma_l R_l
+              const double gam = args.ptab ? 1.0 : args.dg[args.dgofs[m] + (l - m)].y;  // P_l = gamma_l R_l
 #pragma unroll
               for (int jn = 0; jn < NT; ++jn)
                 *reinterpret_cast<double2*>(row + jn * 8 + 2 * q) = make_double2(gam * v[jn][0], gam * v[jn][1]);
@@ -586,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       const int l = l0 + 2 * (8 * i + g) + par;
       if (l <= Lt) {
         double* row = args.F + ((size_t)l * (l + 1) / 2 + m) * ncolF;
-        const double gam = args.dg[args.dgofs[m] + (l - m)].y;  // P_l = gamma_l R_l
+        const double gam = args.ptab ? 1.0 : args.dg[args.dgofs[m] + (l - m)].y;  // P_l = gamma_l R_l
 #pragma unroll
         for (int jn = 0; jn < NTW; ++jn) {
           if (nt0 + jn < NT) {
@@ -880,6 +889,15 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
 #pragma unroll
       for (int ii = 0; ii < 2; ++ii) mt_start[ii] = __shfl_sync(0xffffffffu, v, 8 * ii);
     }
+    // the epilogue's ring indices, loaded now (their latency hides behind the item's
+    // stages instead of sitting between the last DMMA and the stores)
+    int ring_n[2], ring_s[2];
+#pragma unroll
+    for (int ii = 0; ii < 2; ++ii) {
+      const int p = rc * ADJ_RC + (cw + 8 * ii) * 8 + g;
+      ring_n[ii] = __ldg(&args.pair_n[p]);
+      ring_s[ii] = __ldg(&args.pair_s[p]);
+    }
     double acc[2][2][NT][2];  // [parity][M-tile][n-tile][re/im]
 #pragma unroll
     for (int a = 0; a < 2; ++a)
@@ -952,8 +970,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
       }
 #pragma unroll
       for (int ii = 0; ii < 2; ++ii) {
-        const int p = rc * ADJ_RC + (cw + 8 * ii) * 8 + g;
-        const int rn = args.pair_n[p], rs = args.pair_s[p];
+        const int rn = ring_n[ii], rs = ring_s[ii];
         if (rn < 0) continue;
 #pragma unroll
         for (int jn = 0; jn < NT; ++jn) {
