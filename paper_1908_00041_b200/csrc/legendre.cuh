@@ -433,8 +433,16 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       if (item >= args.m_count) break;
       const int m = args.m_begin + item;
       const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
+      const double2* dgm = args.dg + args.dgofs[m];
       for (int j = 0; j < nlb; ++j) {
         const int l0 = m + FWD_LB * j;
+        // gamma of this warp's epilogue rows, loaded before the tiles (not after them)
+        double gam4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int l = l0 + 2 * (8 * i + g) + par;
+          gam4[i] = (args.ptab || l > Lt) ? 1.0 : __ldg(&dgm[l - m].y);
+        }
         for (int c = 0; c < nchunks; ++c) {
           const uint32_t t = tbase + j * nchunks + c;
           const int stage = t % FWD_STAGES;
@@ -503,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
             }
             if (l <= Lt) {
               double* row = args.F + ((size_t)l * (l + 1) / 2 + m) * ncolF;
-              const double gam = args.ptab ? 1.0 : args.dg[args.dgofs[m] + (l - m)].y;  // P_l = gamma_l R_l
+              const double gam = gam4[i];  // P_l = gamma_l R_l
 #pragma unroll
               for (int jn = 0; jn < NT; ++jn)
                 *reinterpret_cast<double2*>(row + jn * 8 + 2 * q) = make_double2(gam * v[jn][0], gam * v[jn][1]);
