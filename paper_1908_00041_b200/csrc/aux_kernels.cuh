@@ -341,6 +341,25 @@ __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
   extern __shared__ __align__(16) double2 cgf_smem[];  // [3][ROWS][RS]
   constexpr int NE = 3 * ROWS * NV, PER = (NE + CGF_THREADS - 1) / CGF_THREADS;
   const int Lt = a.L + 1;
+  const int K = (a.L + 1) * (a.L + 1), Kt = (Lt + 1) * (Lt + 1);
+  // this thread's output (order m0 + mi, field b, sign sg); its nine factors are
+  // loaded together with the staging loads (one memory round trip, not one more
+  // after the barrier)
+  constexpr int NW = CGF_MB * NF * 2;
+  static_assert(NW <= CGF_THREADS, "one (order, field, sign) output per thread");
+  const int w = threadIdx.x;
+  const int mi = w % CGF_MB, b = (w / CGF_MB) % NF, sg = w / (CGF_MB * NF);
+  const int am = m0 + mi;
+  const bool work = w < NW && am <= l && !(sg == 1 && am == 0) && am >= a.c_lo && am < a.c_hi;
+  const int M = sg ? -am : am;
+  auto tab = [&](int i, int ls, int ms) -> double {
+    if (!work || ls < 0 || ls > Lt || abs(ms) > ls) return 0.0;
+    return __ldg(&a.cgt[i * Kt + ls * ls + ls + ms]);
+  };
+  const double x1 = tab(0, l - 1, M - 1), x2 = tab(1, l + 1, M - 1);
+  const double x3 = tab(2, l - 1, M + 1), x4 = tab(3, l + 1, M + 1);
+  const double x5 = tab(4, l - 1, M), x6 = tab(5, l + 1, M);
+  const double u1 = tab(6, l, M - 1), u2 = tab(7, l, M), u3 = tab(8, l, M + 1);
   double2 x[PER];
 #pragma unroll
   for (int u = 0; u < PER; ++u) {  // all loads of the thread in flight before the stores
@@ -359,44 +378,28 @@ __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
     if (e < NE) cgf_smem[e / NV * RS + e % NV] = x[u];
   }
   __syncthreads();
+  if (!work) return;
   const double is2 = 0.7071067811865475;  // favest/transforms.py:46 (1/np.sqrt(2.0))
-  const int K = (a.L + 1) * (a.L + 1), Kt = (Lt + 1) * (Lt + 1);
-  constexpr int NW = CGF_MB * NF * 2;
-#pragma unroll 1
-  for (int w = threadIdx.x; w < NW; w += CGF_THREADS) {
-    const int mi = w % CGF_MB, b = (w / CGF_MB) % NF, sg = w / (CGF_MB * NF);
-    const int am = m0 + mi;
-    if (am > l || (sg == 1 && am == 0) || am < a.c_lo || am >= a.c_hi) continue;
-    const int M = sg ? -am : am;
-    auto tab = [&](int i, int ls, int ms) -> double {
-      if (ls < 0 || ls > Lt || abs(ms) > ls) return 0.0;
-      return __ldg(&a.cgt[i * Kt + ls * ls + ls + ms]);
-    };
-    // staged F^{x,y,z}_{l+dl, mm}: row |mm| - (m0 - 1); out-of-range rows were staged as 0;
-    // combo comp of favest/transforms.py:112 formed on read
-    auto f = [&](int comp, int dl, int mm) -> double2 {
-      const double2* r = cgf_smem + ((dl + 1) * ROWS + abs(mm) - (m0 - 1)) * RS + 6 * b + (mm < 0 ? 1 : 0);
-      return combo_uvw(comp, r[0], r[2], r[4]);
-    };
-    const double x1 = tab(0, l - 1, M - 1), x2 = tab(1, l + 1, M - 1);
-    const double x3 = tab(2, l - 1, M + 1), x4 = tab(3, l + 1, M + 1);
-    const double x5 = tab(4, l - 1, M), x6 = tab(5, l + 1, M);
-    const double u1 = tab(6, l, M - 1), u2 = tab(7, l, M), u3 = tab(8, l, M + 1);
-    const double2 fu_a = f(0, -1, M - 1), fu_b = f(0, 1, M - 1);
-    const double2 fv_a = f(1, -1, M + 1), fv_b = f(1, 1, M + 1);
-    const double2 fw_a = f(2, -1, M), fw_b = f(2, 1, M);
-    const double2 fu_c = f(0, 0, M - 1), fv_c = f(1, 0, M + 1);
-    const double2 fw_c = f(2, 0, M);
-    double ar = is2 * (((x1 * fu_a.x + x2 * fu_b.x) + x3 * fv_a.x) + x4 * fv_b.x) + x5 * fw_a.x + x6 * fw_b.x;
-    double ai = is2 * (((x1 * fu_a.y + x2 * fu_b.y) + x3 * fv_a.y) + x4 * fv_b.y) + x5 * fw_a.y + x6 * fw_b.y;
-    const double sr = u1 * fu_c.x + u3 * fv_c.x, si = u1 * fu_c.y + u3 * fv_c.y;
-    double br = is2 * si + u2 * fw_c.y;
-    double bi = -is2 * sr - u2 * fw_c.x;
-    if (l == 0) ar = ai = br = bi = 0.0;  // favest/transforms.py:145-146
-    const size_t o = (size_t)(a.b0 + b) * K + (l * l + l + M);
-    a.A[o] = make_double2(ar, ai);
-    a.Bc[o] = make_double2(br, bi);
-  }
+  // staged F^{x,y,z}_{l+dl, mm}: row |mm| - (m0 - 1); out-of-range rows were staged as 0;
+  // combo comp of favest/transforms.py:112 formed on read
+  auto f = [&](int comp, int dl, int mm) -> double2 {
+    const double2* r = cgf_smem + ((dl + 1) * ROWS + abs(mm) - (m0 - 1)) * RS + 6 * b + (mm < 0 ? 1 : 0);
+    return combo_uvw(comp, r[0], r[2], r[4]);
+  };
+  const double2 fu_a = f(0, -1, M - 1), fu_b = f(0, 1, M - 1);
+  const double2 fv_a = f(1, -1, M + 1), fv_b = f(1, 1, M + 1);
+  const double2 fw_a = f(2, -1, M), fw_b = f(2, 1, M);
+  const double2 fu_c = f(0, 0, M - 1), fv_c = f(1, 0, M + 1);
+  const double2 fw_c = f(2, 0, M);
+  double ar = is2 * (((x1 * fu_a.x + x2 * fu_b.x) + x3 * fv_a.x) + x4 * fv_b.x) + x5 * fw_a.x + x6 * fw_b.x;
+  double ai = is2 * (((x1 * fu_a.y + x2 * fu_b.y) + x3 * fv_a.y) + x4 * fv_b.y) + x5 * fw_a.y + x6 * fw_b.y;
+  const double sr = u1 * fu_c.x + u3 * fv_c.x, si = u1 * fu_c.y + u3 * fv_c.y;
+  double br = is2 * si + u2 * fw_c.y;
+  double bi = -is2 * sr - u2 * fw_c.x;
+  if (l == 0) ar = ai = br = bi = 0.0;  // favest/transforms.py:145-146
+  const size_t o = (size_t)(a.b0 + b) * K + (l * l + l + M);
+  a.A[o] = make_double2(ar, ai);
+  a.Bc[o] = make_double2(br, bi);
 }
 
 // ---------------------------------------------------------------------------
