@@ -993,4 +993,278 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Single-field on-the-fly adjoint (NT <= 2: C4, and any one-field call whose
+// plan tables do not fit).  With one field the DMMA work per stage is a third
+// of C3's, and the producers' recurrence (one dependent chain per lane, ~30
+// cycles per step while DMMAs hold the SM sub-partition's FP64 datapath) was
+// the critical path: C4 adjoint Legendre 25.6 ms against 18.4 ms for the
+// consumers alone.  Here a work item is a PAIR of 128-pair chunks (A, B) of
+// one order: every producer lane runs two independent chains (its pair in A
+// and in B), and the stage slots alternate A, B, A, B ... (all producer warps
+// still touch every slot, so the parity slot waits stay exact); consumers keep
+// an accumulator set per chunk and write both epilogues at the item's end.
+// ---------------------------------------------------------------------------
+template <bool MIXED>
+__device__ __forceinline__ void adj_produce2(double* PsA, double* PsB, const double2* dgw, double ttA, double ttB,
+                                             double& p1A, double& p2A, double& p1B, double& p2B, int i, int g, int l0,
+                                             const Inject& inA, const Inject& inB) {
+  const int cx = (g >> 2) | ((i & 1) << 1);
+  double* bA[4];
+  double* bB[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    bA[q] = PsA + i * ADJ_MTILE + (g << 2) + (q ^ cx);
+    bB[q] = PsB + i * ADJ_MTILE + (g << 2) + (q ^ cx);
+  }
+#pragma unroll
+  for (int b0 = 0; b0 < ADJ_LC; b0 += 8) {
+    double dd[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dd[k] = dgw[b0 + k].x;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int idx = b0 + k;
+      const double vA = rec_step<MIXED>(p1A, p2A, ttA, dd[k], l0 + idx, inA);
+      const double vB = rec_step<MIXED>(p1B, p2B, ttB, dd[k], l0 + idx, inB);
+      const int par = idx & 1, kk = idx >> 1, ks = kk >> 2, q = kk & 3;
+      bA[q][(par * ADJ_KS + ks) * 32] = vA;
+      bB[q][(par * ADJ_KS + ks) * 32] = vB;
+    }
+  }
+  const double g1 = dgw[ADJ_LC - 1].y, g2 = dgw[ADJ_LC - 2].y;
+  p1A *= g1;
+  p2A *= g2;
+  p1B *= g1;
+  p2B *= g2;
+}
+
+// one consumer stage (the warp's M-tiles {cw, cw + 8}, both parities), as in legendre_adj_kernel
+template <int NT>
+__device__ __forceinline__ void adj_consume(const double* Ps, const double* Gs, double (&acc)[2][2][NT][2],
+                                            const int (&mt_start)[2], int l0s, int Lt, int cw, int g, int q,
+                                            int lane) {
+  const int mts = min(mt_start[0], mt_start[1]);
+  if (!(mts <= l0s + ADJ_LC - 1 && l0s <= Lt)) return;
+  double a[2][2], b[2][NT];
+  auto load = [&](int t, int bufi) {
+    const int ks = t >> 1, par = t & 1;
+#pragma unroll
+    for (int ii = 0; ii < 2; ++ii) {
+      const int i = cw + 8 * ii;
+      a[bufi][ii] = lds_f64(&Ps[i * ADJ_MTILE + (par * ADJ_KS + ks) * 32 + adj_swz(g, q, i)]);
+    }
+#pragma unroll
+    for (int jn = 0; jn < NT; ++jn) b[bufi][jn] = lds_f64(&Gs[((par * ADJ_KS + ks) * NT + jn) * 32 + lane]);
+  };
+  load(0, 0);
+#pragma unroll
+  for (int t = 0; t < 2 * ADJ_KS; ++t) {
+    if (t + 1 < 2 * ADJ_KS) load(t + 1, (t + 1) & 1);
+    const int ks = t >> 1, par = t & 1;
+    const int khi = l0s + 8 * ks + 7;
+    if (l0s + 8 * ks <= Lt) {
+      if (mt_start[0] <= khi) adj_ks_run<0, NT>(acc[par], a[t & 1], b[t & 1]);
+      else if (mt_start[1] <= khi) adj_ks_run<1, NT>(acc[par], a[t & 1], b[t & 1]);
+    }
+  }
+}
+
+// epilogue of one chunk: north = E + O, south = E - O into the spectrum (as in legendre_adj_kernel)
+template <int NT>
+__device__ __forceinline__ void adj_store(const AdjArgs& args, const double (&acc)[2][2][NT][2], const int (&ring_n)[2],
+                                          const int (&ring_s)[2], int m, int q) {
+  const long long bin0 = spec_bin(args.lay, m, 0, args.n_phi), bin1 = spec_bin(args.lay, m, 1, args.n_phi);
+#pragma unroll
+  for (int jn = 0; jn < NT; ++jn) {
+    const int ser = 4 * jn + q;  // 6*field + 2*comp + sign
+    const int b = ser / 6, comp = (ser % 6) >> 1, sgn = ser & 1;
+    if (!(b < args.nfields && !(sgn == 1 && m == 0))) continue;
+    double2* dst = args.S + comp * args.lay.cs + (long long)(args.b0 + b) * args.n_theta * args.lay.rs +
+                   (sgn ? bin1 : bin0) * args.lay.bs;
+#pragma unroll
+    for (int ii = 0; ii < 2; ++ii) {
+      const int rn = ring_n[ii], rs = ring_s[ii];
+      if (rn < 0) continue;
+      const double er = acc[0][ii][jn][0], ei = acc[0][ii][jn][1];
+      const double orr = acc[1][ii][jn][0], oi = acc[1][ii][jn][1];
+      dst[rn * args.lay.rs] = make_double2(er + orr, ei + oi);
+      if (rs >= 0) dst[rs * args.lay.rs] = make_double2(er - orr, ei - oi);
+    }
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kThreads, 1) legendre_adj_dual_kernel(AdjArgs args) {
+  static_assert(NT <= 2, "dual-chunk items are for single-field launches");
+  extern __shared__ __align__(128) double smem[];
+  using SM = AdjSmem<NT>;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ADJ_STAGES * SM::STAGE);
+  uint64_t* empty = full + ADJ_STAGES;
+  double2* abw_all = reinterpret_cast<double2*>(empty + ADJ_STAGES);
+  const int Lt = args.Lt;
+  const int nrcp = (args.nrc + 1) / 2;  // chunk pairs per order
+  const int nitems = args.m_count * nrcp;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ADJ_STAGES; ++s) {
+      mbar_init(&full[s], 32 * kProducerWarps);
+      mbar_init(&empty[s], 32 * kConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (is_producer(warp)) {
+    const int pw = producer_index(warp);
+    double2* abw = abw_all + pw * ADJ_LC;
+    const int rho = 32 * pw + lane;
+    const int i = rho >> 3, g = rho & 7;
+    const uint64_t pol_last = l2_evict_last();
+    uint32_t sc = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+      const int m = args.m_begin + item / nrcp;
+      const int rcA = 2 * (item % nrcp);
+      const bool hasB = rcA + 1 < args.nrc;
+      const int nlc = (Lt + 1 - m + ADJ_LC - 1) / ADJ_LC;
+      const int pA = rcA * ADJ_RC + rho, pB = hasB ? pA + ADJ_RC : pA;
+      const double ttA = args.pair_t[pA], ttB = args.pair_t[pB];
+      Inject inA, inB;
+      inA.ls = args.start_l[(size_t)m * args.nPpad + pA];
+      inB.ls = hasB ? args.start_l[(size_t)m * args.nPpad + pB] : Lt + ADJ_LC + 1;  // absent: never starts
+      {
+        const double2 vA = args.start_v[(size_t)m * args.nPpad + pA];
+        const double2 vB = args.start_v[(size_t)m * args.nPpad + pB];
+        inA.A = vA.x;
+        inA.B = vA.y;
+        inB.A = vB.x;
+        inB.B = vB.y;
+      }
+      double p1A = 0.0, p2A = 0.0, p1B = 0.0, p2B = 0.0;
+      const double2* dgm = args.dg + args.dgofs[m];
+      const double* Gm = args.G + (size_t)args.gofs[m] * SM::GTILE;
+      auto dg_at = [&](int lcx) {
+        const int l = m + ADJ_LC * lcx + lane;
+        return (l <= Lt) ? __ldg(&dgm[l - m]) : make_double2(0.0, 1.0);
+      };
+      double2 dg_next = dg_at(0);
+      for (int lc = 0; lc < nlc; ++lc) {
+        const int l0 = m + ADJ_LC * lc;
+        const bool beforeA = inA.ls > l0 + ADJ_LC - 1, beforeB = inB.ls > l0 + ADJ_LC - 1;
+        const bool zeroA = __all_sync(0xffffffffu, beforeA), zeroB = __all_sync(0xffffffffu, beforeB);
+        const bool mixed = __any_sync(0xffffffffu, (!beforeA && inA.ls + 1 >= l0) || (!beforeB && inB.ls + 1 >= l0));
+        const double2 dg_cur = dg_next;
+        if (lc + 1 < nlc) dg_next = dg_at(lc + 1);
+        if (!zeroA || !zeroB) {
+          __syncwarp();
+          abw[lane] = dg_cur;
+          __syncwarp();
+        }
+        const int sA = sc % ADJ_STAGES;
+        mbar_wait(&empty[sA], ((sc / ADJ_STAGES) & 1) ^ 1);
+        const uint32_t scB = sc + 1;
+        const int sB = scB % ADJ_STAGES;
+        if (hasB) mbar_wait(&empty[sB], ((scB / ADJ_STAGES) & 1) ^ 1);
+        double* PsA = smem + sA * SM::STAGE;
+        double* PsB = smem + sB * SM::STAGE;
+        if (lane == 0 && pw == 0) {
+          // the order's coefficient tile of this degree block, once per chunk slot
+          asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[sA])),
+                       "r"((uint32_t)(SM::GTILE * 8))
+                       : "memory");
+          bulk_g2s_hint(PsA + ADJ_PTILE, Gm + (size_t)lc * SM::GTILE, SM::GTILE * 8, &full[sA], pol_last);
+          if (hasB) {
+            asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[sB])),
+                         "r"((uint32_t)(SM::GTILE * 8))
+                         : "memory");
+            bulk_g2s_hint(PsB + ADJ_PTILE, Gm + (size_t)lc * SM::GTILE, SM::GTILE * 8, &full[sB], pol_last);
+          }
+        }
+        if (!(args.dbg & 2)) {
+          if (!zeroA && !zeroB) {
+            if (mixed) adj_produce2<true>(PsA, PsB, abw, ttA, ttB, p1A, p2A, p1B, p2B, i, g, l0, inA, inB);
+            else adj_produce2<false>(PsA, PsB, abw, ttA, ttB, p1A, p2A, p1B, p2B, i, g, l0, inA, inB);
+          } else if (!zeroA) {
+            if (mixed) adj_produce<true>(PsA, abw, ttA, p1A, p2A, i, g, l0, inA);
+            else adj_produce<false>(PsA, abw, ttA, p1A, p2A, i, g, l0, inA);
+          } else if (!zeroB) {
+            if (mixed) adj_produce<true>(PsB, abw, ttB, p1B, p2B, i, g, l0, inB);
+            else adj_produce<false>(PsB, abw, ttB, p1B, p2B, i, g, l0, inB);
+          }
+        }
+        mbar_arrive(&full[sA]);
+        if (hasB) mbar_arrive(&full[sB]);
+        sc += hasB ? 2 : 1;
+      }
+    }
+    return;
+  }
+
+  const int cw = consumer_index(warp);
+  const int g = lane >> 2, q = lane & 3;
+  uint32_t sc = 0;
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    const int m = args.m_begin + item / nrcp;
+    const int rcA = 2 * (item % nrcp);
+    const bool hasB = rcA + 1 < args.nrc;
+    const int nlc = (Lt + 1 - m + ADJ_LC - 1) / ADJ_LC;
+    int mtA[2], mtB[2], rnA[2], rsA[2], rnB[2], rsB[2];
+    {
+      const int l16 = lane & 15;
+      const int off = 8 * cw + 64 * (l16 >> 3) + (l16 & 7);
+      int vA = args.start_l[(size_t)m * args.nPpad + rcA * ADJ_RC + off];
+      int vB = hasB ? args.start_l[(size_t)m * args.nPpad + (rcA + 1) * ADJ_RC + off] : Lt + ADJ_LC + 1;
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        vA = min(vA, __shfl_xor_sync(0xffffffffu, vA, o));
+        vB = min(vB, __shfl_xor_sync(0xffffffffu, vB, o));
+      }
+#pragma unroll
+      for (int ii = 0; ii < 2; ++ii) {
+        mtA[ii] = __shfl_sync(0xffffffffu, vA, 8 * ii);
+        mtB[ii] = __shfl_sync(0xffffffffu, vB, 8 * ii);
+      }
+    }
+#pragma unroll
+    for (int ii = 0; ii < 2; ++ii) {
+      const int p = rcA * ADJ_RC + (cw + 8 * ii) * 8 + g;
+      rnA[ii] = __ldg(&args.pair_n[p]);
+      rsA[ii] = __ldg(&args.pair_s[p]);
+      rnB[ii] = hasB ? __ldg(&args.pair_n[p + ADJ_RC]) : -1;
+      rsB[ii] = hasB ? __ldg(&args.pair_s[p + ADJ_RC]) : -1;
+    }
+    double accA[2][2][NT][2], accB[2][2][NT][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int p2 = 0; p2 < 2; ++p2)
+#pragma unroll
+        for (int b = 0; b < NT; ++b) accA[a][p2][b][0] = accA[a][p2][b][1] = accB[a][p2][b][0] = accB[a][p2][b][1] = 0.0;
+    for (int lc = 0; lc < nlc; ++lc) {
+      const int l0s = m + ADJ_LC * lc;
+      {
+        const int stage = sc % ADJ_STAGES;
+        mbar_wait(&full[stage], (sc / ADJ_STAGES) & 1);
+        const double* Ps = smem + stage * SM::STAGE;
+        if (!(args.dbg & 1)) adj_consume<NT>(Ps, Ps + ADJ_PTILE, accA, mtA, l0s, Lt, cw, g, q, lane);
+        mbar_arrive(&empty[stage]);
+        ++sc;
+      }
+      if (hasB) {
+        const int stage = sc % ADJ_STAGES;
+        mbar_wait(&full[stage], (sc / ADJ_STAGES) & 1);
+        const double* Ps = smem + stage * SM::STAGE;
+        if (!(args.dbg & 1)) adj_consume<NT>(Ps, Ps + ADJ_PTILE, accB, mtB, l0s, Lt, cw, g, q, lane);
+        mbar_arrive(&empty[stage]);
+        ++sc;
+      }
+    }
+    if (!(args.dbg & 4)) {
+      if (rcA * ADJ_RC + 8 * cw < args.nP) adj_store<NT>(args, accA, rnA, rsA, m, q);
+      if (hasB && (rcA + 1) * ADJ_RC + 8 * cw < args.nP) adj_store<NT>(args, accB, rnB, rsB, m, q);
+    }
+  }
+}
+
 }  // namespace fv

@@ -351,6 +351,21 @@ int launch_adj(fvPlan* p, const fv::AdjArgs& args, int m_count, cudaStream_t s) 
   if (bytes > 227 * 1024) return fail(FV_EINVAL, "adjoint kernel shared memory exceeds 227 KB");
   fv::AdjArgs a2 = args;
   a2.m_count = m_count;
+  if constexpr (NT <= 2) {
+    // single field on the fly: items of two ring chunks, two recurrence chains per producer lane
+    // (FV_ADJ_DUAL=0 keeps one chunk per item)
+    static const bool dual = [] { const char* e = std::getenv("FV_ADJ_DUAL"); return !(e && std::atoi(e) == 0); }();
+    if (dual && !args.ptab) {
+      static unsigned long long attr2 = 0;
+      if (first_use(&attr2, p->device))
+        FV_CUDA(cudaFuncSetAttribute(fv::legendre_adj_dual_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024));
+      const int items2 = m_count * ((p->nrc + 1) / 2);
+      fv::legendre_adj_dual_kernel<NT><<<std::min(items2, p->num_sms), fv::kThreads, bytes, s>>>(a2);
+      FV_CUDA(cudaGetLastError());
+      return FV_OK;
+    }
+  }
   const int items = m_count * p->nrc;
   fv::legendre_adj_kernel<NT><<<std::min(items, p->num_sms), fv::kThreads, bytes, s>>>(a2);
   FV_CUDA(cudaGetLastError());
