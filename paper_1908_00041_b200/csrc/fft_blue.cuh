@@ -223,17 +223,18 @@ struct SmallPArgs {
   double2* out;
   long long out_cs, out_rs, out_es;
   const double2* rootN;  // exp(-2 pi i j / n), j < n
-  const double2* rootR;  // exp(-2 pi i j / R), j < R
-  const double2* csP;    // (cos, sin)(2 pi j / P), j < P
+  const double2* WR;     // [r][s] = exp(-2 pi i (r s mod R) / R), R x R
+  const double2* WP;     // [q - 1][k] = (cos, sin)(2 pi (q k mod P) / P), q = 1..H, k = 0..H, H = (P - 1) / 2
   int n, R, P, nrings, inverse;
 };
 
 __global__ void __launch_bounds__(BLUE_T) smallp_kernel(SmallPArgs a) {
   extern __shared__ __align__(16) double2 sp_smem[];
-  double2* xs = sp_smem;           // [n] ring component
-  double2* ys = sp_smem + a.n;     // [R][P] twiddled residue DFTs
-  double2* cs = ys + a.n;          // [P] (cos, sin)
-  double2* wr = cs + a.P;          // [R]
+  const int H = (a.P - 1) / 2;
+  double2* xs = sp_smem;                  // [n] ring component
+  double2* ys = sp_smem + a.n;            // [R][P] twiddled residue DFTs
+  double2* wp = ys + a.n;                 // [H][H + 1] (cos, sin): lane k reads [q][k], conflict free
+  double2* wr = wp + H * (H + 1);         // [R][R]
   const int c = blockIdx.x % 3, ring = blockIdx.x / 3;
   const double cj = a.inverse ? -1.0 : 1.0;
   const double2* src = a.in + c * a.in_cs + ring * a.in_rs;
@@ -242,26 +243,24 @@ __global__ void __launch_bounds__(BLUE_T) smallp_kernel(SmallPArgs a) {
     v.y *= cj;
     xs[i] = v;
   }
-  for (int i = threadIdx.x; i < a.P; i += BLUE_T) cs[i] = __ldg(&a.csP[i]);
-  for (int i = threadIdx.x; i < a.R; i += BLUE_T) wr[i] = __ldg(&a.rootR[i]);
+  for (int i = threadIdx.x; i < H * (H + 1); i += BLUE_T) wp[i] = __ldg(&a.WP[i]);
+  for (int i = threadIdx.x; i < a.R * a.R; i += BLUE_T) wr[i] = __ldg(&a.WR[i]);
   __syncthreads();
-  const int H = (a.P - 1) / 2;
   const int nitem = a.R * (H + 1);
   for (int it = threadIdx.x; it < nitem; it += BLUE_T) {
     const int r = it / (H + 1), k = it - r * (H + 1);
     const double2* x = xs + r;
     const double2 x0 = x[0];
     double2 A = x0, Bv = make_double2(0.0, 0.0);
-    int idx = 0;
+    const double2* w = wp + k;
+#pragma unroll 4
     for (int q = 1; q <= H; ++q) {
-      idx += k;
-      if (idx >= a.P) idx -= a.P;
-      const double2 u = x[q * a.R], w = x[(a.P - q) * a.R];
-      const double2 t = cs[idx];
-      A.x = fma(u.x + w.x, t.x, A.x);
-      A.y = fma(u.y + w.y, t.x, A.y);
-      Bv.x = fma(u.x - w.x, t.y, Bv.x);
-      Bv.y = fma(u.y - w.y, t.y, Bv.y);
+      const double2 u = x[q * a.R], v = x[(a.P - q) * a.R];
+      const double2 t = w[(q - 1) * (H + 1)];
+      A.x = fma(u.x + v.x, t.x, A.x);
+      A.y = fma(u.y + v.y, t.x, A.y);
+      Bv.x = fma(u.x - v.x, t.y, Bv.x);
+      Bv.y = fma(u.y - v.y, t.y, Bv.y);
     }
     // X_k = A - i B, X_{P-k} = A + i B; then the twiddle w_n^{r k}
     const double2 xk = make_double2(A.x + Bv.y, A.y - Bv.x);
@@ -276,12 +275,8 @@ __global__ void __launch_bounds__(BLUE_T) smallp_kernel(SmallPArgs a) {
   for (int o = threadIdx.x; o < a.n; o += BLUE_T) {
     const int s = o / a.P, k = o - s * a.P;
     double2 acc = ys[k];
-    int idx = 0;
-    for (int r = 1; r < a.R; ++r) {
-      idx += s;
-      if (idx >= a.R) idx -= a.R;
-      acc = bl_add(acc, bl_mul(ys[r * a.P + k], wr[idx]));
-    }
+    const double2* w = wr + s;
+    for (int r = 1; r < a.R; ++r) acc = bl_add(acc, bl_mul(ys[r * a.P + k], w[r * a.R]));
     dst[(long long)o * a.out_es] = make_double2(acc.x, cj * acc.y);
   }
 }

@@ -581,19 +581,22 @@ int setup_blue(fvPlan* p) {
   const long double PI_ = 3.141592653589793238462643383279502884L;
   if (P <= fv::SMALLP_MAX && R <= 64 && !(env && std::string(env) == "blue")) {
     // direct conjugate-pair DFTs in one CTA per ring (smallp_kernel)
-    std::vector<double2> tab(n + R + P);
+    const int H = (P - 1) / 2;
+    std::vector<double2> tab((size_t)n + R * R + H * (H + 1));
     for (int j = 0; j < n; ++j) {
       const long double g = 2.0L * PI_ * j / n;
       tab[j] = make_double2((double)cosl(g), -(double)sinl(g));
     }
-    for (int j = 0; j < R; ++j) {
-      const long double g = 2.0L * PI_ * j / R;
-      tab[n + j] = make_double2((double)cosl(g), -(double)sinl(g));
-    }
-    for (int j = 0; j < P; ++j) {
-      const long double g = 2.0L * PI_ * j / P;
-      tab[n + R + j] = make_double2((double)cosl(g), (double)sinl(g));
-    }
+    for (int r = 0; r < R; ++r)
+      for (int s2 = 0; s2 < R; ++s2) {
+        const long double g = 2.0L * PI_ * ((r * s2) % R) / R;
+        tab[n + r * R + s2] = make_double2((double)cosl(g), -(double)sinl(g));
+      }
+    for (int q = 1; q <= H; ++q)
+      for (int k = 0; k <= H; ++k) {
+        const long double g = 2.0L * PI_ * ((q * k) % P) / P;
+        tab[n + R * R + (q - 1) * (H + 1) + k] = make_double2((double)cosl(g), (double)sinl(g));
+      }
     FV_TRY(dalloc(&p->blue_tab, tab.size()));
     FV_CUDA(cudaMemcpy(p->blue_tab, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice));
     fv::SmallPArgs& s = p->sp_args;
@@ -601,9 +604,9 @@ int setup_blue(fvPlan* p) {
     s.R = R;
     s.P = P;
     s.rootN = p->blue_tab;
-    s.rootR = p->blue_tab + n;
-    s.csP = p->blue_tab + n + R;
-    const size_t smem = (size_t)(2 * n + P + R) * sizeof(double2);
+    s.WR = p->blue_tab + n;
+    s.WP = p->blue_tab + n + R * R;
+    const size_t smem = (size_t)(2 * n + R * R + H * (H + 1)) * sizeof(double2);
     if (smem > 200 * 1024) return FV_OK;
     FV_CUDA(cudaFuncSetAttribute(fv::smallp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     p->smallp = true;
@@ -708,7 +711,8 @@ int ring_fft_smallp(fvPlan* p, bool inverse, const double2* in, long long in_cs,
   a.out_es = out_es;
   a.nrings = nrings;
   a.inverse = inverse ? 1 : 0;
-  const size_t smem = (size_t)(2 * a.n + a.P + a.R) * sizeof(double2);
+  const int H = (a.P - 1) / 2;
+  const size_t smem = (size_t)(2 * a.n + a.R * a.R + H * (H + 1)) * sizeof(double2);
   fv::smallp_kernel<<<(unsigned)(3LL * nrings), fv::BLUE_T, smem, s>>>(a);
   FV_CUDA(cudaGetLastError());
   return FV_OK;
