@@ -19,7 +19,7 @@
 // store (K2).  Tables (chirps, roots, FFT_M of the chirp) are exactly rounded
 // from long double on the host.
 #pragma once
-#include "common.cuh"
+#include "fft2.cuh"
 
 namespace fv {
 
@@ -228,6 +228,42 @@ struct SmallPArgs {
   int n, R, P, nrings, inverse;
 };
 
+// residue DFTs of nr rings: xs[ring][n] -> ys[ring][R][P] (twiddled by w_n^{r k})
+__device__ __forceinline__ void smallp_stage1(const SmallPArgs& a, const double2* xs, double2* ys,
+                                              const double2* wp, int nr) {
+  const int H = (a.P - 1) / 2;
+  const int per = a.R * (H + 1);
+  for (int it = threadIdx.x; it < nr * per; it += BLUE_T) {
+    const int ring = it / per, j = it - ring * per;
+    const int r = j / (H + 1), k = j - r * (H + 1);
+    const double2* x = xs + ring * a.n + r;
+    double2* y = ys + ring * a.n + r * a.P;
+    double2 A = x[0], Bv = make_double2(0.0, 0.0);
+    const double2* w = wp + k;
+#pragma unroll 4
+    for (int q = 1; q <= H; ++q) {
+      const double2 u = x[q * a.R], v = x[(a.P - q) * a.R];
+      const double2 t = w[(q - 1) * (H + 1)];
+      A.x = fma(u.x + v.x, t.x, A.x);
+      A.y = fma(u.y + v.y, t.x, A.y);
+      Bv.x = fma(u.x - v.x, t.y, Bv.x);
+      Bv.y = fma(u.y - v.y, t.y, Bv.y);
+    }
+    // X_k = A - i B, X_{P-k} = A + i B; then the twiddle w_n^{r k}
+    y[k] = bl_mul(make_double2(A.x + Bv.y, A.y - Bv.x), __ldg(&a.rootN[(long long)r * k]));
+    if (k > 0) y[a.P - k] = bl_mul(make_double2(A.x - Bv.y, A.y + Bv.x), __ldg(&a.rootN[(long long)r * (a.P - k)]));
+  }
+}
+
+// R-point DFT of output o = s P + k of one ring's residue spectra
+__device__ __forceinline__ double2 smallp_out(const SmallPArgs& a, const double2* ys, const double2* wr, int o) {
+  const int s = o / a.P, k = o - s * a.P;
+  double2 acc = ys[k];
+  const double2* w = wr + s;
+  for (int r = 1; r < a.R; ++r) acc = bl_add(acc, bl_mul(ys[r * a.P + k], w[r * a.R]));
+  return acc;
+}
+
 __global__ void __launch_bounds__(BLUE_T) smallp_kernel(SmallPArgs a) {
   extern __shared__ __align__(16) double2 sp_smem[];
   const int H = (a.P - 1) / 2;
@@ -246,38 +282,87 @@ __global__ void __launch_bounds__(BLUE_T) smallp_kernel(SmallPArgs a) {
   for (int i = threadIdx.x; i < H * (H + 1); i += BLUE_T) wp[i] = __ldg(&a.WP[i]);
   for (int i = threadIdx.x; i < a.R * a.R; i += BLUE_T) wr[i] = __ldg(&a.WR[i]);
   __syncthreads();
-  const int nitem = a.R * (H + 1);
-  for (int it = threadIdx.x; it < nitem; it += BLUE_T) {
-    const int r = it / (H + 1), k = it - r * (H + 1);
-    const double2* x = xs + r;
-    const double2 x0 = x[0];
-    double2 A = x0, Bv = make_double2(0.0, 0.0);
-    const double2* w = wp + k;
-#pragma unroll 4
-    for (int q = 1; q <= H; ++q) {
-      const double2 u = x[q * a.R], v = x[(a.P - q) * a.R];
-      const double2 t = w[(q - 1) * (H + 1)];
-      A.x = fma(u.x + v.x, t.x, A.x);
-      A.y = fma(u.y + v.y, t.x, A.y);
-      Bv.x = fma(u.x - v.x, t.y, Bv.x);
-      Bv.y = fma(u.y - v.y, t.y, Bv.y);
-    }
-    // X_k = A - i B, X_{P-k} = A + i B; then the twiddle w_n^{r k}
-    const double2 xk = make_double2(A.x + Bv.y, A.y - Bv.x);
-    ys[r * a.P + k] = bl_mul(xk, __ldg(&a.rootN[(long long)r * k]));
-    if (k > 0) {
-      const double2 xm = make_double2(A.x - Bv.y, A.y + Bv.x);
-      ys[r * a.P + (a.P - k)] = bl_mul(xm, __ldg(&a.rootN[(long long)r * (a.P - k)]));
-    }
-  }
+  smallp_stage1(a, xs, ys, wp, 1);
   __syncthreads();
   double2* dst = a.out + c * a.out_cs + ring * a.out_rs;
   for (int o = threadIdx.x; o < a.n; o += BLUE_T) {
-    const int s = o / a.P, k = o - s * a.P;
-    double2 acc = ys[k];
-    const double2* w = wr + s;
-    for (int r = 1; r < a.R; ++r) acc = bl_add(acc, bl_mul(ys[r * a.P + k], w[r * a.R]));
-    dst[(long long)o * a.out_es] = make_double2(acc.x, cj * acc.y);
+    const double2 v = smallp_out(a, ys, wr, o);  // output index = thread index: coalesced
+    dst[(long long)o * a.out_es] = make_double2(v.x, cj * v.y);
+  }
+}
+
+// Forward with the equatorial fold fused (C2: n_phi = 516), the small-prime
+// counterpart of fft2.cuh fft_fold_kernel: CTA per (ring pair, field,
+// component), both rings' spectra kept in shared memory, epilogue writes the
+// Legendre B operand X exactly as fft_fold_kernel does.
+__global__ void __launch_bounds__(BLUE_T) smallp_fold_kernel(SmallPArgs a, Fft2Args f) {
+  extern __shared__ __align__(16) double2 sp_smem[];
+  const int H = (a.P - 1) / 2;
+  const int n = a.n;
+  double2* xs = sp_smem;                  // [2][n] rings, then their spectra
+  double2* ys = sp_smem + 2 * n;          // [2][R][P]
+  double2* wp = ys + 2 * n;
+  double2* wr = wp + H * (H + 1);
+  const int item = blockIdx.x;
+  const int c = item % 3, b = (item / 3) % f.nfields, p = item / (3 * f.nfields);
+  const int rn = f.pair_n[p], rs = f.pair_s[p];
+  const int nr = (rn >= 0) + (rs >= 0);
+  if (nr > 0) {
+    const double2* base = f.in + (long long)b * f.field_stride + c;
+    for (int i = threadIdx.x; i < nr * n; i += BLUE_T) {
+      const int ring = i / n, j = i - ring * n;
+      xs[i] = base[(long long)(ring ? rs : rn) * f.in_rs + (long long)j * f.in_es];
+    }
+    for (int i = threadIdx.x; i < H * (H + 1); i += BLUE_T) wp[i] = __ldg(&a.WP[i]);
+    for (int i = threadIdx.x; i < a.R * a.R; i += BLUE_T) wr[i] = __ldg(&a.WR[i]);
+    __syncthreads();
+    smallp_stage1(a, xs, ys, wp, nr);
+    __syncthreads();
+    for (int i = threadIdx.x; i < nr * n; i += BLUE_T) {
+      const int ring = i / n, o = i - ring * n;
+      xs[i] = smallp_out(a, ys + ring * n, wr, o);
+    }
+    __syncthreads();
+  }
+  // epilogue (fft2.cuh fft_fold_kernel): thread per order m
+  const int chunk = p >> 5, ks = (p >> 2) & 7, kq = p & 3;
+  const int col = 12 * b + 4 * c;
+  const size_t tile = (size_t)2 * 8 * f.NT * 32;
+  const size_t par_stride = (size_t)8 * f.NT * 32;
+  const size_t off = ((size_t)ks * f.NT + (col >> 3)) * 32 + ((col >> 2) & 1) * 16 + kq * 4;
+  const bool padcols = (b == f.nfields - 1) && c == 2 && ((12 * f.nfields) & 7) == 4;
+  const int pcol = 12 * f.nfields;
+  const size_t poff = ((size_t)ks * f.NT + (pcol >> 3)) * 32 + ((pcol >> 2) & 1) * 16 + kq * 4;
+  const double wn = rn >= 0 ? f.ring_w[rn] : 0.0;
+  const double ws = rs >= 0 ? f.ring_w[rs] : 0.0;
+  const double2* Sn = xs;
+  const double2* Ss = xs + n;
+  for (int m = threadIdx.x; m <= f.Lt; m += BLUE_T) {
+    double2 Ep = make_double2(0.0, 0.0), Em = Ep, Op = Ep, Om = Ep;
+    if (nr > 0) {
+      const int bm = m ? n - m : 0;
+      const double2 np = Sn[m], nm = Sn[bm];
+      const double sg = (m & 1) ? -1.0 : 1.0;  // sigma_{-m} on the -m bin
+      if (rs >= 0) {
+        const double2 sp = Ss[m], sm = Ss[bm];
+        Ep = make_double2(wn * np.x + ws * sp.x, wn * np.y + ws * sp.y);
+        Op = make_double2(wn * np.x - ws * sp.x, wn * np.y - ws * sp.y);
+        Em = make_double2(sg * (wn * nm.x + ws * sm.x), sg * (wn * nm.y + ws * sm.y));
+        Om = make_double2(sg * (wn * nm.x - ws * sm.x), sg * (wn * nm.y - ws * sm.y));
+      } else {  // unpaired ring: both parities see the ring itself
+        Ep = Op = make_double2(wn * np.x, wn * np.y);
+        Em = Om = make_double2(sg * (wn * nm.x), sg * (wn * nm.y));
+      }
+      if (m == 0) Em = Om = make_double2(0.0, 0.0);
+    }
+    double* xt = f.X + ((size_t)m * f.nchunks + chunk) * tile;
+    st_global_v4(xt + off, Ep, Em);
+    st_global_v4(xt + par_stride + off, Op, Om);
+    if (padcols) {
+      const double2 z = make_double2(0.0, 0.0);
+      st_global_v4(xt + poff, z, z);
+      st_global_v4(xt + par_stride + poff, z, z);
+    }
   }
 }
 

@@ -607,8 +607,12 @@ int setup_blue(fvPlan* p) {
     s.WR = p->blue_tab + n;
     s.WP = p->blue_tab + n + R * R;
     const size_t smem = (size_t)(2 * n + R * R + H * (H + 1)) * sizeof(double2);
-    if (smem > 200 * 1024) return FV_OK;
+    const size_t smem_f = (size_t)(4 * n + R * R + H * (H + 1)) * sizeof(double2);  // two rings, fused fold
+    if (smem_f > 200 * 1024) return FV_OK;
     FV_CUDA(cudaFuncSetAttribute(fv::smallp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FV_CUDA(cudaFuncSetAttribute(fv::smallp_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
+    const char* ff = std::getenv("FV_FUSED_FOLD");
+    p->fused_fold = !(ff && std::atoi(ff) == 0);
     p->smallp = true;
     return FV_OK;
   }
@@ -784,6 +788,27 @@ int ring_fft2_raw(fvPlan* p, bool inverse, const double2* in, long long in_cs, l
 // fused forward FFT + fold of fields b0 .. b0 + nf - 1 of T (B, N, 3) into X (all orders)
 int fft_fold(fvPlan* p, const double2* T, int b0, int nf, cudaStream_t s) {
   fv::Fft2Args a{};
+  if (p->smallp) {  // small-prime ring DFT (fft_blue.cuh smallp_fold_kernel)
+    const long long n = p->n_phi;
+    a.in_rs = 3 * n;
+    a.in_es = 3;
+    a.field_stride = 3 * n * p->n_theta;
+    a.in = T + (long long)b0 * a.field_stride;
+    a.X = p->X;
+    a.pair_n = p->pair_n;
+    a.pair_s = p->pair_s;
+    a.ring_w = p->ring_w;
+    a.nchunks = p->nchunks;
+    a.NT = ntiles_for(nf);
+    a.nfields = nf;
+    a.Lt = p->Lt;
+    const fv::SmallPArgs& sp = p->sp_args;
+    const int H = (sp.P - 1) / 2;
+    const size_t smem = (size_t)(4 * sp.n + sp.R * sp.R + H * (H + 1)) * sizeof(double2);
+    fv::smallp_fold_kernel<<<p->nchunks * fv::FWD_RC * nf * 3, fv::BLUE_T, smem, s>>>(sp, a);
+    FV_CUDA(cudaGetLastError());
+    return FV_OK;
+  }
   const long long n = p->n_phi;
   a.tw = p->f2_tw;
   a.in_rs = 3 * n;
@@ -1191,7 +1216,7 @@ int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, voi
   FV_TRY(check_grid_call(p, B, T, a, b));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const long long n = p->n_phi;
-  if (p->fft2 && p->fused_fold)
+  if ((p->fft2 || p->smallp) && p->fused_fold)
     return forward_orders(p, nullptr, p->lay_f, a, b, B, 0, p->Lt + 1, 0, p->L + 1, s,
                           reinterpret_cast<const double2*>(T));
   FV_TRY(ring_ffts(p, false, reinterpret_cast<const double2*>(T), 1, 3 * n, 3, p->Sf, p->lay_f.cs, p->lay_f.rs,
