@@ -21,10 +21,21 @@ namespace fv {
 // Compact bins (order-sharded spectra, nbins > 0): only the orders
 // bin_lo .. bin_lo + nbins - 1 are held, +m at bin m - bin_lo, -m at
 // nbins + m - bin_lo.  nbins == 0: natural DFT bins (m, (n_phi - m) % n_phi).
+// Blocked (rblk = 2, the grid adjoint's default when its inverse ring DFT is a
+// hand-written kernel): rings in pairs, [comp][ring / 2][bin][ring % 2] -- the
+// two rings a ring-DFT CTA transforms are one contiguous 32-byte-per-bin
+// stream (coalesced stage-0 loads), and the adjoint epilogue still writes
+// whole 32-byte sectors (rs = pair stride 2 * bins, bs = 2).
 struct SLayout {
   long long cs, rs, bs;
   int bin_lo, nbins;
+  int rblk;  // 0: ring R at R * rs; 2^k: ring R at (R >> k) * rs + (R & (2^k - 1))
+  int rbsh;  // k
 };
+
+__host__ __device__ __forceinline__ long long spec_ring(const SLayout& l, long long R) {
+  return l.rblk ? (R >> l.rbsh) * l.rs + (R & (l.rblk - 1)) : R * l.rs;
+}
 
 __device__ __forceinline__ long long spec_bin(const SLayout& l, int m, int sgn, int n_phi) {
   if (l.nbins == 0) return sgn ? (n_phi - m) % n_phi : m;

@@ -65,6 +65,7 @@ struct Fft2Args {
   double2* out;                      // plain epilogue
   long long in_cs, in_rs, out_cs, out_rs;  // component / ring strides (complex units)
   int in_es, out_es;                 // element strides
+  int in_rblk;                       // plain: blocked input rings (common.cuh SLayout rblk), 0 = in_rs apart
   const double2* tw;                 // twiddle tables (forward sign): stage 1 then stage 2, entry [k][r - 1]
   int nrings;                        // plain: rings per component
   // fused forward fold
@@ -238,7 +239,8 @@ __global__ void __launch_bounds__(F2P_T, 2) ring_fft2_kernel(Fft2Args a, int nit
 #pragma unroll
   for (int i = 0; i < F2P_NR; ++i) {
     const int r = min(r0 + i, a.nrings - 1);
-    src[i] = a.in + c * a.in_cs + r * a.in_rs;
+    src[i] = a.in + c * a.in_cs +
+             (a.in_rblk ? (long long)(r >> (31 - __clz(a.in_rblk))) * a.in_rs + (r & (a.in_rblk - 1)) : r * a.in_rs);
     dst[i] = a.out + c * a.out_cs + r * a.out_rs;
   }
   f2_run<R0, R1, R2, INV, false, F2P_NR, F2P_T>(a.tw, src, a.in_es, nr, f2buf, dst, a.out_es);

@@ -226,6 +226,7 @@ struct SmallPArgs {
   const double2* WR;     // [r][s] = exp(-2 pi i (r s mod R) / R), R x R
   const double2* WP;     // [q - 1][k] = (cos, sin)(2 pi (q k mod P) / P), q = 1..H, k = 0..H, H = (P - 1) / 2
   int n, R, P, nrings, inverse;
+  int in_rblk;           // blocked input rings (common.cuh SLayout rblk), 0: in_rs apart
 };
 
 // residue DFTs of nr rings: xs[ring][n] -> ys[ring][R][P] (twiddled by w_n^{r k})
@@ -273,7 +274,10 @@ __global__ void __launch_bounds__(BLUE_T) smallp_kernel(SmallPArgs a) {
   double2* wr = wp + H * (H + 1);         // [R][R]
   const int c = blockIdx.x % 3, ring = blockIdx.x / 3;
   const double cj = a.inverse ? -1.0 : 1.0;
-  const double2* src = a.in + c * a.in_cs + ring * a.in_rs;
+  const double2* src =
+      a.in + c * a.in_cs +
+      (a.in_rblk ? (long long)(ring >> (31 - __clz(a.in_rblk))) * a.in_rs + (ring & (a.in_rblk - 1))
+                 : (long long)ring * a.in_rs);
   for (int i = threadIdx.x; i < a.n; i += BLUE_T) {
     double2 v = src[(long long)i * a.in_es];
     v.y *= cj;

@@ -967,14 +967,15 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
     if (rc * ADJ_RC + 8 * cw < args.nP && !(args.dbg & 4)) {
       const long long bin0 = spec_bin(args.lay, m, 0, args.n_phi), bin1 = spec_bin(args.lay, m, 1, args.n_phi);
       double2* dst[NT];
+      long long rbase[NT];
       bool ok[NT];
 #pragma unroll
       for (int jn = 0; jn < NT; ++jn) {
         const int ser = 4 * jn + q;  // 6*field + 2*comp + sign
         const int b = ser / 6, comp = (ser % 6) >> 1, sgn = ser & 1;
         ok[jn] = b < args.nfields && !(sgn == 1 && m == 0);
-        dst[jn] = args.S + comp * args.lay.cs + (long long)(args.b0 + b) * args.n_theta * args.lay.rs +
-                  (sgn ? bin1 : bin0) * args.lay.bs;
+        dst[jn] = args.S + comp * args.lay.cs + (sgn ? bin1 : bin0) * args.lay.bs;
+        rbase[jn] = (long long)(args.b0 + b) * args.n_theta;
       }
 #pragma unroll
       for (int ii = 0; ii < 2; ++ii) {
@@ -985,8 +986,8 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
           if (!ok[jn]) continue;
           const double er = acc[0][ii][jn][0], ei = acc[0][ii][jn][1];
           const double orr = acc[1][ii][jn][0], oi = acc[1][ii][jn][1];
-          dst[jn][rn * args.lay.rs] = make_double2(er + orr, ei + oi);
-          if (rs >= 0) dst[jn][rs * args.lay.rs] = make_double2(er - orr, ei - oi);
+          dst[jn][spec_ring(args.lay, rbase[jn] + rn)] = make_double2(er + orr, ei + oi);
+          if (rs >= 0) dst[jn][spec_ring(args.lay, rbase[jn] + rs)] = make_double2(er - orr, ei - oi);
         }
       }
     }
@@ -1080,16 +1081,16 @@ __device__ __forceinline__ void adj_store(const AdjArgs& args, const double (&ac
     const int ser = 4 * jn + q;  // 6*field + 2*comp + sign
     const int b = ser / 6, comp = (ser % 6) >> 1, sgn = ser & 1;
     if (!(b < args.nfields && !(sgn == 1 && m == 0))) continue;
-    double2* dst = args.S + comp * args.lay.cs + (long long)(args.b0 + b) * args.n_theta * args.lay.rs +
-                   (sgn ? bin1 : bin0) * args.lay.bs;
+    double2* dst = args.S + comp * args.lay.cs + (sgn ? bin1 : bin0) * args.lay.bs;
+    const long long rbase = (long long)(args.b0 + b) * args.n_theta;
 #pragma unroll
     for (int ii = 0; ii < 2; ++ii) {
       const int rn = ring_n[ii], rs = ring_s[ii];
       if (rn < 0) continue;
       const double er = acc[0][ii][jn][0], ei = acc[0][ii][jn][1];
       const double orr = acc[1][ii][jn][0], oi = acc[1][ii][jn][1];
-      dst[rn * args.lay.rs] = make_double2(er + orr, ei + oi);
-      if (rs >= 0) dst[rs * args.lay.rs] = make_double2(er - orr, ei - oi);
+      dst[spec_ring(args.lay, rbase + rn)] = make_double2(er + orr, ei + oi);
+      if (rs >= 0) dst[spec_ring(args.lay, rbase + rs)] = make_double2(er - orr, ei - oi);
     }
   }
 }

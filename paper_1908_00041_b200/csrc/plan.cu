@@ -703,8 +703,10 @@ int setup_blue(fvPlan* p) {
 }
 
 int ring_fft_smallp(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
-                    double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s) {
+                    double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s,
+                    int in_rblk = 0) {
   fv::SmallPArgs a = p->sp_args;
+  a.in_rblk = in_rblk;
   a.in = in;
   a.in_cs = in_cs;
   a.in_rs = in_rs;
@@ -767,8 +769,10 @@ int ring_fft_blue(fvPlan* p, bool inverse, const double2* in, long long in_cs, l
 }
 
 int ring_fft2_raw(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
-                  double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s) {
+                  double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s,
+                  int in_rblk = 0) {
   fv::Fft2Args a{};
+  a.in_rblk = in_rblk;
   a.tw = p->f2_tw;
   a.in = in;
   a.out = out;
@@ -1002,16 +1006,25 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
   const int gs = std::min(4, max_batch);
   const int NTmax = ntiles_for(gs);
   {
-    // FV_SLAYOUT=<fwd><adj> digits, 0 ring-major / 1 bin-major (default 01: the
-    // forward FFT writes contiguous rings, the adjoint epilogue writes bin rows)
+    // FV_SLAYOUT=<fwd><adj> digits, 0 ring-major / 1 bin-major / 2 ring pairs (default
+    // 02 when the inverse ring DFT is hand-written, else 01: the forward FFT writes
+    // contiguous rings, the adjoint epilogue writes 128-byte runs of one bin)
     const char* sl = std::getenv("FV_SLAYOUT");
-    const bool fbin = sl && sl[0] == '1', abin = !(sl && sl[0] && sl[1] == '0');
-    const long long rings = (long long)max_batch * n_theta;
-    const fv::SLayout ringmajor{rings * n_phi, n_phi, 1}, binmajor{rings * n_phi, 1, rings};
-    p->lay_f = fbin ? binmajor : ringmajor;
-    p->lay_a = abin ? binmajor : ringmajor;
+    const bool own_fft = p->fft2 || p->smallp;
+    const char fdig = (sl && sl[0]) ? sl[0] : '0';
+    char adig = (sl && sl[0] && sl[1]) ? sl[1] : (own_fft ? '2' : '1');
+    if (adig == '2' && !own_fft) adig = '1';
+    const char* rb = std::getenv("FV_SLAYOUT_RBLK");  // experiments: ring block of the blocked layout
+    int rbsh = 1;  // ring pairs
+    if (rb) rbsh = std::atoi(rb) >= 8 ? 3 : std::atoi(rb) >= 4 ? 2 : 1;
+    const int rblk = 1 << rbsh;
+    const long long rings = (long long)max_batch * n_theta, rings8 = (rings + 7) / 8 * 8;
+    const fv::SLayout ringmajor{rings8 * n_phi, n_phi, 1, 0, 0, 0}, binmajor{rings8 * n_phi, 1, rings, 0, 0, 0},
+        blocked{rings8 * n_phi, (long long)rblk * n_phi, rblk, 0, 0, rblk, rbsh};
+    p->lay_f = fdig == '1' ? binmajor : ringmajor;
+    p->lay_a = adig == '2' ? blocked : adig == '0' ? ringmajor : binmajor;
   }
-  const size_t spec = (size_t)3 * max_batch * n_theta * n_phi;
+  const size_t spec = (size_t)3 * ((max_batch * (size_t)n_theta + 7) / 8 * 8) * n_phi;
   if ((rc = dalloc(&p->Sf, spec)) || (rc = dalloc(&p->Sa, spec)) ||
       (rc = dalloc(&p->X, (size_t)(Lt + 1) * p->nchunks * (2 * 8 * NTmax * 32))) ||
       (rc = dalloc(&p->F, (size_t)(Lt + 1) * (Lt + 2) / 2 * 8 * NTmax)) ||
@@ -1193,8 +1206,16 @@ int adjoint_orders(fvPlan* p, const double* a, const double* b, double2* S, cons
 
 // three components x nrings ring DFTs of length n_phi, arbitrary strides (complex units)
 int ring_ffts(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
-              double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s) {
+              double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s,
+              int in_rblk = 0) {
   StageMark mk(p, 0, s);
+  if (in_rblk) {  // blocked rings: only the hand-written two-ring / small-prime kernels read them
+    if (p->fft2)
+      return ring_fft2_raw(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s, in_rblk);
+    if (p->smallp)
+      return ring_fft_smallp(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s, in_rblk);
+    return fail(FV_EINVAL, "blocked spectrum layout without a hand-written ring DFT");
+  }
   if (p->fft2) return ring_fft2_raw(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   if (p->custom_fft) return ring_fft_raw(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   if (p->smallp) return ring_fft_smallp(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
@@ -1230,7 +1251,7 @@ int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int 
   FV_TRY(adjoint_orders(p, a, b, p->Sa, p->lay_a, B, 0, p->Lt + 1, s));
   const long long n = p->n_phi;
   return ring_ffts(p, true, p->Sa, p->lay_a.cs, p->lay_a.rs, p->lay_a.bs, reinterpret_cast<double2*>(T), 1, 3 * n, 3,
-                   B * p->n_theta, s);
+                   B * p->n_theta, s, p->lay_a.rblk);
 }
 
 // ---- order-sharded building blocks (paper_1908_00041_b200/dist.py) ----
