@@ -258,31 +258,36 @@ __global__ void __launch_bounds__(PTS_THREADS, NF == 1 ? 2 : 1) adjoint_points_d
       for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     double p2 = seed, p1 = __dmul_rn(__dmul_rn(sqrt(2 * m + 3.0), t), seed);
     int e = se;
-    for (int l0 = m; l0 <= Lt; l0 += 4) {
+    // one recurrence step (degree m + 2 + number of steps so far), value in P units
+    const double2* abp = abm;  // (a_l, a_l b_l), l = m + 2 .., staged
+    auto step = [&]() -> double {
+      const double2 abv = *abp++;
+      const double pn = fma(abv.x * t, p1, -(abv.y * p2));
+      p2 = p1;
+      p1 = pn;
+      if (e < 0 && fabs(p1) >= 0x1p512) {
+        p1 *= 0x1p-512;
+        p2 *= 0x1p-512;
+        e += XR_SHIFT;
+      }
+      return e < 0 ? xr_value(p1, e) : p1;
+    };
+    const double* brow = rows + (size_t)q * RS + g;  // B fragment row q of the k-step's four degrees
+    for (int l0 = m; l0 <= Lt; l0 += 4, brow += 4 * RS) {
+      // warp-uniform cases: the order's first k-step starts from the seeds, the
+      // last may run past Lt; every other k-step is four plain recurrence steps
       double v[4];
+      if (l0 == m) {
+        v[0] = e < 0 ? xr_value(p2, e) : p2;
+        v[1] = m + 1 <= Lt ? (e < 0 ? xr_value(p1, e) : p1) : 0.0;
+        v[2] = m + 2 <= Lt ? step() : 0.0;
+        v[3] = m + 3 <= Lt ? step() : 0.0;
+      } else if (l0 + 3 <= Lt) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int l = l0 + k;
-        double val;
-        if (l > Lt) {
-          val = 0.0;
-        } else if (l == m) {
-          val = p2;
-        } else if (l == m + 1) {
-          val = p1;
-        } else {
-          const double2 abv = abm[l - m - 2];  // (a_l, a_l * b_l), staged
-          const double pn = fma(abv.x * t, p1, -(abv.y * p2));
-          p2 = p1;
-          p1 = pn;
-          if (e < 0 && fabs(p1) >= 0x1p512) {
-            p1 *= 0x1p-512;
-            p2 *= 0x1p-512;
-            e += XR_SHIFT;
-          }
-          val = p1;
-        }
-        v[k] = (e < 0 && l <= Lt) ? xr_value(val, e) : val;
+        for (int k = 0; k < 4; ++k) v[k] = step();
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = l0 + k <= Lt ? step() : 0.0;
       }
       __syncwarp();
       reinterpret_cast<double2*>(pbuf)[2 * lane] = make_double2(v[0], v[1]);
@@ -291,7 +296,6 @@ __global__ void __launch_bounds__(PTS_THREADS, NF == 1 ? 2 : 1) adjoint_points_d
       double af[4], bf[NT];
 #pragma unroll
       for (int i = 0; i < 4; ++i) af[i] = pbuf[(8 * i + g) * 4 + q];
-      const double* brow = rows + (size_t)(l0 - m + q) * RS + g;
 #pragma unroll
       for (int j = 0; j < NT; ++j) bf[j] = brow[8 * j];
 #pragma unroll
