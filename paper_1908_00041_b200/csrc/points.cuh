@@ -476,35 +476,40 @@ __global__ void __launch_bounds__(FPD_THREADS) forward_points_dmma_kernel(FptsAr
     int e;
     fpd_seed(m, s, km, p2, e);
     p1 = __dmul_rn(__dmul_rn(c1, t), p2);  // favest/legendre.py:66-67
-    int l = m;
-    auto produce = [&]() -> double {  // Pbar_l^m(t), then l += 1
-      double v;
-      if (l == m) {
-        v = p2;
-      } else if (l == m + 1) {
-        v = p1;
-      } else {
-        const double2 abv = abs_[l - m - 2];
-        const double pn = fma(abv.x * t, p1, -(abv.y * p2));
-        p2 = p1;
-        p1 = pn;
-        if (e < 0 && fabs(p1) >= 0x1p512) {
-          p1 *= 0x1p-512;
-          p2 *= 0x1p-512;
-          e += XR_SHIFT;
-        }
-        v = p1;
+    // plain recurrence step: the next degree m + 2 + (steps so far), in P units
+    const double2* abp = abs_;
+    auto step = [&]() -> double {
+      const double2 abv = *abp++;
+      const double pn = fma(abv.x * t, p1, -(abv.y * p2));
+      p2 = p1;
+      p1 = pn;
+      if (e < 0 && fabs(p1) >= 0x1p512) {
+        p1 *= 0x1p-512;
+        p2 *= 0x1p-512;
+        e += XR_SHIFT;
       }
-      ++l;
-      return e < 0 ? xr_value(v, e) : v;
+      return e < 0 ? xr_value(p1, e) : p1;
     };
-    while (l < lw0) produce();  // degrees below this item's window
+    for (int l = m + 2; l < lw0; ++l) step();  // degrees below this item's window
 #pragma unroll
     for (int j = 0; j < FPD_MT; ++j) {
       const int d0 = lw0 + j * FPD_DB;
       if (d0 >= lw1) break;
+      // warp-uniform cases: the order's first block starts from the seeds, the
+      // window's last block may end early; otherwise 32 plain steps
+      double* pcol = Ps + threadIdx.x;
+      int k0 = 0;
+      if (d0 == m) {
+        pcol[0] = e < 0 ? xr_value(p2, e) : p2;
+        pcol[FPD_PS] = m + 1 < lw1 ? (e < 0 ? xr_value(p1, e) : p1) : 0.0;
+        k0 = 2;
+      }
+      if (d0 + FPD_DB <= lw1) {
 #pragma unroll 4
-      for (int k = 0; k < FPD_DB; ++k) Ps[k * FPD_PS + threadIdx.x] = (d0 + k < lw1) ? produce() : 0.0;
+        for (int k = k0; k < FPD_DB; ++k) pcol[k * FPD_PS] = step();
+      } else {
+        for (int k = k0; k < FPD_DB; ++k) pcol[k * FPD_PS] = d0 + k < lw1 ? step() : 0.0;
+      }
       __syncthreads();
       if (d0 + 8 * mi < lw1) {
         const double* pa = Ps + (8 * mi + g) * FPD_PS + h * (FPD_CHUNK / 2) + q;
