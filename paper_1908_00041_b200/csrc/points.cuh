@@ -258,10 +258,11 @@ __global__ void __launch_bounds__(PTS_THREADS, NF == 1 ? 2 : 1) adjoint_points_d
       for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     double p2 = seed, p1 = __dmul_rn(__dmul_rn(sqrt(2 * m + 3.0), t), seed);
     int e = se;
-    // one recurrence step (degree m + 2 + number of steps so far), value in P units
+    // one recurrence step (degree m + 2 + number of steps so far), value in P units;
+    // the k-step's four coefficient pairs are loaded one k-step ahead (the shared
+    // memory latency otherwise sits on every step of the dependent chain)
     const double2* abp = abm;  // (a_l, a_l b_l), l = m + 2 .., staged
-    auto step = [&]() -> double {
-      const double2 abv = *abp++;
+    auto step = [&](double2 abv) -> double {
       const double pn = fma(abv.x * t, p1, -(abv.y * p2));
       p2 = p1;
       p1 = pn;
@@ -272,22 +273,36 @@ __global__ void __launch_bounds__(PTS_THREADS, NF == 1 ? 2 : 1) adjoint_points_d
       }
       return e < 0 ? xr_value(p1, e) : p1;
     };
+    double2 abn[4];  // coefficients of the next k-step's plain steps
+#pragma unroll
+    for (int k = 0; k < 4; ++k) abn[k] = abp[k];  // (past the order's end: stale rows, never used)
     const double* brow = rows + (size_t)q * RS + g;  // B fragment row q of the k-step's four degrees
     for (int l0 = m; l0 <= Lt; l0 += 4, brow += 4 * RS) {
       // warp-uniform cases: the order's first k-step starts from the seeds, the
       // last may run past Lt; every other k-step is four plain recurrence steps
       double v[4];
+      double2 ab[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ab[k] = abn[k];
       if (l0 == m) {
         v[0] = e < 0 ? xr_value(p2, e) : p2;
         v[1] = m + 1 <= Lt ? (e < 0 ? xr_value(p1, e) : p1) : 0.0;
-        v[2] = m + 2 <= Lt ? step() : 0.0;
-        v[3] = m + 3 <= Lt ? step() : 0.0;
-      } else if (l0 + 3 <= Lt) {
+        abp += 2;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = step();
+        for (int k = 0; k < 4; ++k) abn[k] = abp[k];
+        v[2] = m + 2 <= Lt ? step(ab[0]) : 0.0;
+        v[3] = m + 3 <= Lt ? step(ab[1]) : 0.0;
       } else {
+        abp += 4;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = l0 + k <= Lt ? step() : 0.0;
+        for (int k = 0; k < 4; ++k) abn[k] = abp[k];
+        if (l0 + 3 <= Lt) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) v[k] = step(ab[k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) v[k] = l0 + k <= Lt ? step(ab[k]) : 0.0;
+        }
       }
       __syncwarp();
       reinterpret_cast<double2*>(pbuf)[2 * lane] = make_double2(v[0], v[1]);
