@@ -395,7 +395,7 @@ constexpr int FPD_WIN = FPD_MT * FPD_DB;  // degrees per window
 
 __host__ __device__ constexpr size_t fpd_smem_bytes(int nf, int Lt) {
   return ((size_t)FPD_DB * FPD_PS + (size_t)FPD_CHUNK * ptsd_rs(nf)) * sizeof(double) +
-         (size_t)(Lt > 2 ? Lt - 1 : 1) * sizeof(double2);
+         (size_t)(Lt + 3) * sizeof(double2);  // l = m+2..Lt, plus the two-ahead prefetch
 }
 
 // Pbar_m^m(t) = (-1)^m K_m s^m as x * 2^e (e a multiple of 512, e <= 0), with
@@ -491,10 +491,15 @@ __global__ void __launch_bounds__(FPD_THREADS) forward_points_dmma_kernel(FptsAr
     int e;
     fpd_seed(m, s, km, p2, e);
     p1 = __dmul_rn(__dmul_rn(c1, t), p2);  // favest/legendre.py:66-67
-    // plain recurrence step: the next degree m + 2 + (steps so far), in P units
-    const double2* abp = abs_;
+    // plain recurrence step: the next degree m + 2 + (steps so far), in P units; the
+    // coefficients are read two steps ahead (shared-memory latency off the chain;
+    // the two reads past the order's last degree are padding, never used)
+    const double2* abp = abs_ + 2;
+    double2 ab0 = abs_[0], ab1 = abs_[1];
     auto step = [&]() -> double {
-      const double2 abv = *abp++;
+      const double2 abv = ab0;
+      ab0 = ab1;
+      ab1 = *abp++;
       const double pn = fma(abv.x * t, p1, -(abv.y * p2));
       p2 = p1;
       p1 = pn;
