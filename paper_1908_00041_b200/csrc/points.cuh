@@ -433,7 +433,7 @@ __device__ __forceinline__ void fpd_seed(int m, double s, double km, double& x, 
 }
 
 template <int NF>
-__global__ void __launch_bounds__(FPD_THREADS) forward_points_dmma_kernel(FptsArgs a) {
+__global__ void __launch_bounds__(FPD_THREADS, NF == 1 ? 2 : 1) forward_points_dmma_kernel(FptsArgs a) {
   constexpr int NT = ptsd_nt(NF), RS = ptsd_rs(NF), NCOL = 8 * NT;
   extern __shared__ __align__(16) double fpd_smem[];
   double* Ps = fpd_smem;                                                    // [FPD_DB][FPD_PS]
