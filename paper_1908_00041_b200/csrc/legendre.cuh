@@ -883,6 +883,16 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
   const int cw = consumer_index(warp);
   const int g = lane >> 2, q = lane & 3;
   uint32_t sc = 0;
+  const int l16 = lane & 15;
+  const int soff = 8 * cw + 64 * (l16 >> 3) + (l16 & 7);
+  // polar starts of the warp's pairs, loaded one item ahead (a global-memory round
+  // trip at every item start otherwise, with the stages already filled)
+  auto start_of = [&](int it) {
+    return it < nitems ? __ldg(&args.start_l[(size_t)(args.m_begin + it / args.nrc) * args.nPpad +
+                                             (it % args.nrc) * ADJ_RC + soff])
+                       : 0;
+  };
+  int v_next = start_of(blockIdx.x);
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
     const int m = args.m_begin + item / args.nrc;
     const int rc = item % args.nrc;
@@ -890,8 +900,8 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
     // first degree at which each of the warp's M-tiles has a pair above the polar threshold
     int mt_start[2];
     {
-      const int l16 = lane & 15;
-      int v = args.start_l[(size_t)m * args.nPpad + rc * ADJ_RC + 8 * cw + 64 * (l16 >> 3) + (l16 & 7)];
+      int v = v_next;
+      v_next = start_of(item + gridDim.x);
 #pragma unroll
       for (int o = 1; o < 8; o <<= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
 #pragma unroll
