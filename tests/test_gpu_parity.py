@@ -287,6 +287,30 @@ def test_api_errors_on_device():
     with pytest.raises(ValueError):
         plan.adjoint(torch.zeros((1, 80), dtype=torch.complex128, device="cuda"),
                      torch.zeros((1, 81), dtype=torch.complex128, device="cuda"))
+    # scattered-point plans: batch above max_batch, mismatched weights, wrong dtypes
+    from paper_1908_00041_b200.plan import PointsPlan
+
+    pp = PointsPlan(L, max_batch=1)
+    pts = _t(O.random_points(np.random.default_rng(0), 10))
+    w = torch.ones(10, dtype=torch.float64, device="cuda")
+    T2 = torch.zeros((2, 10, 3), dtype=torch.complex128, device="cuda")
+    with pytest.raises(ValueError, match="batch"):
+        pp.forward(pts, w, T2)
+    with pytest.raises(ValueError):
+        pp.forward(pts, w[:9], T2[:1])
+    with pytest.raises(ValueError):
+        pp.forward(pts, w.float(), T2[:1])
+    with pytest.raises(ValueError):
+        pp.forward(pts.float(), w, T2[:1])
+    # a points plan is not a grid plan and vice versa (C ABI kind checks)
+    import ctypes
+
+    lib = plan.lib
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert lib.fv_forward_points(plan._h, pts.data_ptr(), w.data_ptr(), 10, T2.data_ptr(), T2.data_ptr(),
+                                 T2.data_ptr(), 1, s) == 1
+    assert b"scattered" in lib.fv_last_error()
+    assert lib.fv_forward_grid(pp._h, T2.data_ptr(), T2.data_ptr(), T2.data_ptr(), 1, s) == 1
 
 
 def test_host_pipeline_matches_device_path():
