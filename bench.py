@@ -46,6 +46,10 @@ def canonical_flops(L: int, B: int) -> dict:
     return {"legendre": leg, "fft": fft, "total": leg + fft}
 
 
+# DMMA.8x8x4 instructions x 512 flops per C3 launch (ncu --set full, r01c capture)
+EXEC_GFLOP_C3 = {"forward": 42543048 * 512 / 1e9, "adjoint": 41064672 * 512 / 1e9}
+
+
 def hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -337,6 +341,12 @@ def run_ours(args, rank, world, local_rank):
                 "peak_source": "DMMA microbenchmark on this pool (profiles/r01_fp64_microbench.txt); "
                                "datasheet 40 TFLOP/s; MEASURED_PEAKS.json has no FP64 entry",
                 "avg_launch_ms": leg_ms, "share_of_step": stage_ms["legendre"] / ms_total}
+    if L == 1024 and B == 4:
+        # executed DMMA work (the polar skip leaves out whole M-tile k-steps): ncu DMMA
+        # instruction counts x 512 flops of the C3 launches, profiles/r01c_ncu_c3_kernels.md
+        ex = (EXEC_GFLOP_C3["forward"] + EXEC_GFLOP_C3["adjoint"]) / 2
+        roofline["executed_gflop_per_launch"] = dict(EXEC_GFLOP_C3, source="ncu DMMA count x 512")
+        roofline["executed_frac"] = ex / (leg_ms / 1e3) / 1e3 / FP64_PEAK_MEASURED
     hbm, hbm_src = hbm_peak()
     step_frac = (2 * fl["total"] / (ms_step / 1e3)) / (FP64_PEAK_DATASHEET * 1e12)
 
