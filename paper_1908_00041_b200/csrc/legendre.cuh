@@ -112,7 +112,40 @@ struct FwdArgs {
   const double* ptab;         // [tile][FWD_PTILE], tile = tofs[m] + j * nchunks + c
   const StageMeta* mtab;
   const long long* tofs;
+  // per (order, chunk): smallest polar start of the chunk's 32 pairs (plan-time);
+  // the leading chunks of an l-block whose start lies past the block are skipped
+  // by producers and consumers alike (no pipeline stage for an all-zero tile)
+  const int* cmin;
 };
+
+// chunk starts of one order held across the warp (chunk 32 g + lane in v[g])
+struct ChunkStarts {
+  int v[4];
+  int ng;  // 0: no skipping (more than 128 chunks)
+};
+
+__device__ __forceinline__ ChunkStarts load_chunk_starts(const int* cmin_m, int nchunks, int lane) {
+  ChunkStarts cs;
+  cs.ng = nchunks <= 128 ? (nchunks + 31) / 32 : 0;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const int c = 32 * g + lane;
+    cs.v[g] = (g < cs.ng && c < nchunks) ? __ldg(&cmin_m[c]) : 0x7fffffff;
+  }
+  return cs;
+}
+
+// first chunk of the l-block [l0, l0 + FWD_LB) with a started pair (chunks before it are all-zero tiles)
+__device__ __forceinline__ int first_live_chunk(const ChunkStarts& cs, int l0, int nchunks) {
+  if (cs.ng == 0) return 0;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    if (g >= cs.ng) break;
+    const unsigned b = __ballot_sync(0xffffffffu, cs.v[g] <= l0 + FWD_LB - 1);
+    if (b) return min(32 * g + __ffs(b) - 1, nchunks);
+  }
+  return nchunks;
+}
 
 
 
@@ -123,7 +156,7 @@ struct FwdSmem {
   // K-split consumers (NT <= 2): partial sums of k-quarters 1..3 [par][3][Mtile 4][NT][2][lane]
   static constexpr int KRED = NT <= 2 ? 2 * 3 * 4 * NT * 2 * 32 : 0;
   static constexpr size_t bytes(int nPx) {
-    return (size_t)FWD_STAGES * STAGE * 8 + 2 * FWD_STAGES * 8 + FWD_STAGES * sizeof(StageMeta) +
+    return (size_t)FWD_STAGES * STAGE * 8 + 2 * FWD_STAGES * 8 + 16 + FWD_STAGES * sizeof(StageMeta) +
            kProducerWarps * FWD_LB * 16 + (size_t)nPx * 28 + (size_t)KRED * 8;
   }
 };
@@ -299,7 +332,9 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
   const int nPx = args.nchunks * FWD_RC;  // pairs covered by the forward chunks
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + FWD_STAGES * SM::STAGE);
   uint64_t* empty = full + FWD_STAGES;
-  StageMeta* meta = reinterpret_cast<StageMeta*>(empty + FWD_STAGES);
+  // consumer warp 0's count of finished tiles (the producers' aliasing guard)
+  volatile int* cons0 = reinterpret_cast<volatile int*>(empty + FWD_STAGES);
+  StageMeta* meta = reinterpret_cast<StageMeta*>(empty + FWD_STAGES + 2);
   double2* abw_all = reinterpret_cast<double2*>(meta + FWD_STAGES);
   double* st_p1 = reinterpret_cast<double*>(abw_all + kProducerWarps * FWD_LB);
   double* st_p2 = st_p1 + nPx;
@@ -316,6 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       mbar_init(&full[s], 32);
       mbar_init(&empty[s], 32 * kConsumerWarps);
     }
+    *cons0 = 0;
     fence_barrier_init();
   }
   unsigned long long gt0 = 0;
@@ -335,19 +371,15 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       if (item >= args.m_count) break;
       const int m = args.m_begin + item;
       const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
-      // Tile ownership.  A producer waits for its slot with a parity wait, which
-      // aliases once the slot is two rounds behind, so each warp's consecutive
-      // tiles must be at most FWD_STAGES apart: with nchunks >= 4 the warps take
-      // the order's tiles round robin (every 4th tile; a chunk's recurrence state
-      // then moves between warps from one l-block to the next, ordered by the
-      // full -> consumer -> empty barrier chain because nchunks >= FWD_STAGES
-      // puts the chunk's previous tile at least one stage round earlier); with
-      // fewer chunks each warp keeps chunk pw (tiles nchunks <= 3 apart).
-      const bool rr = nchunks >= kProducerWarps;
-      static_assert(FWD_STAGES >= kProducerWarps + 1, "round-robin tiles need nchunks >= FWD_STAGES handoff");
-      // (table mode reads the polar starts from global memory: no state to set up)
+      // Tile ownership.  Warp pw owns the chunks c = pw (mod 4) (their recurrence
+      // state never changes hands).  Each l-block's leading all-zero chunks
+      // (polar start past the block) are skipped by producers and consumers
+      // alike, so tile t of the pipeline is the t-th live tile.  A producer
+      // waits for its slot with a parity wait, which aliases once the slot is
+      // two rounds behind; a warp's consecutive tiles can be up to ~2 rounds
+      // apart here, so it first waits until consumer warp 0 has finished tile
+      // t - 5 (which implies every consumer has finished tile t - 10).
       if (!table) {
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kProducerWarps) : "memory");  // previous order's tiles done
         for (int c = pw; c < nchunks; c += kProducerWarps) {
           const int p = c * FWD_RC + lane;
           st_t[p] = args.pair_t[p];
@@ -355,17 +387,21 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
           st_p1[p] = 0.0;
           st_p2[p] = 0.0;
         }
-        asm volatile("bar.sync 1, %0;" ::"n"(32 * kProducerWarps) : "memory");
+        __syncwarp();
       }
-      const int ntl = nlb * nchunks;
-      int jprev = -1;
-      for (int tl = pw; tl < ntl && (rr || pw < nchunks); tl += rr ? kProducerWarps : nchunks) {
-        const int j = tl / nchunks, c = tl - j * nchunks;
+      const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane);
+      uint32_t tb = tbase;
+      for (int j = 0; j < nlb; ++j) {
         const int l0 = m + FWD_LB * j;
-        if (!table && j != jprev) fwd_stage_coefs(abw, args, m, l0, lane);
-        jprev = j;
+        const int c0 = first_live_chunk(cst, l0, nchunks);
+        const int cfirst = c0 + ((pw - c0) & (kProducerWarps - 1));
+        if (!table && cfirst < nchunks) fwd_stage_coefs(abw, args, m, l0, lane);
+        for (int c = cfirst; c < nchunks; c += kProducerWarps) {
+          const int tl = j * nchunks + c;  // table tile index (all chunks)
+          const uint32_t t = tb + (c - c0);
+          if (t >= 2 * FWD_STAGES)
+            while (*cons0 < (int)t - (FWD_STAGES - 1)) __nanosleep(32);
         {
-          const uint32_t t = tbase + tl;
           const int stage = t % FWD_STAGES;
           const uint32_t round = t / FWD_STAGES;
           const int p = c * FWD_RC + lane;
@@ -401,8 +437,10 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
           if (tr) args.trace[t * 8 + 2] = clock64() | ((long long)tc.zero << 62) | ((long long)tc.mixed << 61);
           mbar_arrive(&full[stage]);
         }
+        }
+        tb += nchunks - c0;
       }
-      tbase += nlb * nchunks;
+      tbase = tb;
     }
     return;
   }
@@ -434,8 +472,10 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       const int m = args.m_begin + item;
       const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
       const double2* dgm = args.dg + args.dgofs[m];
+      const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane);
       for (int j = 0; j < nlb; ++j) {
         const int l0 = m + FWD_LB * j;
+        const int c0 = first_live_chunk(cst, l0, nchunks);
         // gamma of this warp's epilogue rows, loaded before the tiles (not after them)
         double gam4[4];
 #pragma unroll
@@ -443,8 +483,8 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
           const int l = l0 + 2 * (8 * i + g) + par;
           gam4[i] = (args.ptab || l > Lt) ? 1.0 : __ldg(&dgm[l - m].y);
         }
-        for (int c = 0; c < nchunks; ++c) {
-          const uint32_t t = tbase + j * nchunks + c;
+        for (int c = c0; c < nchunks; ++c) {
+          const uint32_t t = tbase + (c - c0);
           const int stage = t % FWD_STAGES;
           mbar_wait(&full[stage], (t / FWD_STAGES) & 1);
           const double* Ps = smem + stage * SM::STAGE;
@@ -478,7 +518,9 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
             }
           }
           mbar_arrive(&empty[stage]);
+          if (cw == 0 && lane == 0) *cons0 = (int)t + 1;
         }
+        tbase += nchunks - c0;
         // epilogue of the l-block: k-quarters 1..3 park their partial sums, quarter 0
         // adds them in order and writes rows l = l0 + 2 (8 i + g) + par
         double* rp = red + (size_t)(par * 3) * 4 * NT * 64;
@@ -524,7 +566,6 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
 #pragma unroll
           for (int jn = 0; jn < NT; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
       }
-      tbase += nlb * nchunks;
     }
     return;
   }
@@ -551,10 +592,12 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
   if (item >= args.m_count) break;
   const int m = args.m_begin + item;
   const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
+  const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane);
   for (int j = 0; j < nlb; ++j) {
     const int l0 = m + FWD_LB * j;
-    for (int c = 0; c < nchunks; ++c) {
-      const uint32_t t = tbase + j * nchunks + c;
+    const int c0 = first_live_chunk(cst, l0, nchunks);
+    for (int c = c0; c < nchunks; ++c) {
+      const uint32_t t = tbase + (c - c0);
       const int stage = t % FWD_STAGES;
       const uint32_t round = t / FWD_STAGES;
       const bool tr = args.trace && blockIdx.x == args.trace_cta && lane == 0 && cw == 0 && t < 4096;
@@ -595,7 +638,9 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       }
       if (tr) args.trace[t * 8 + 5] = clock64();
       mbar_arrive(&empty[stage]);
+      if (cw == 0 && lane == 0) *cons0 = (int)t + 1;
     }
+    tbase += nchunks - c0;
     // epilogue for this l-block: rows l = l0 + 2*(8*i + g) + par
 #pragma unroll
     for (int ii = 0; ii < 2; ++ii) {
@@ -616,7 +661,6 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       for (int jn = 0; jn < NTW; ++jn) acc[ii][jn][0] = acc[ii][jn][1] = 0.0;
     }
   }
-  tbase += nlb * nchunks;
   }
   if (args.trace && cw == 0 && lane == 0 && blockIdx.x < 4096) {
     unsigned long long gt1;

@@ -96,6 +96,7 @@ struct fvPlan {
   double* seed_x = nullptr;  // plan-time only (freed after the polar-start tables)
   int* seed_e = nullptr;
   int* start_l = nullptr;
+  int* cmin = nullptr;          // [m][forward chunk] smallest polar start of the chunk's pairs
   double2* start_v = nullptr;
   double2* ab = nullptr;
   long long* abofs = nullptr;
@@ -166,7 +167,7 @@ void free_plan(fvPlan* p) {
                   p->seed_e, p->start_l,  p->start_v, p->ab,   p->abofs,  p->gofs,
                   p->dg,     p->dgofs,  p->cgt,     p->cga,     p->ptab_f,  p->mtab_f, p->tofs,   p->ptab_a, p->aofs,
                   p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->G,
-                  p->seedk,  p->fitems,   p->Fpart,   p->blue_tab, p->blue_s1,
+                  p->seedk,  p->fitems,   p->Fpart,   p->blue_tab, p->blue_s1, p->cmin,
                   p->fft_tw, p->f2_tw};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -987,6 +988,10 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
     cudaFree(p->seed_e);
     p->seed_x = nullptr;
     p->seed_e = nullptr;
+    if ((rc = dalloc(&p->cmin, (size_t)(Lt + 1) * p->nchunks))) return bail(rc);
+    dim3 cg((p->nchunks + 127) / 128, Lt + 1);
+    fv::chunk_start_kernel<<<cg, 128>>>(p->start_l, p->nPpad, p->nchunks, Lt, p->cmin);
+    if (cudaGetLastError() != cudaSuccess) return bail(fail(FV_ECUDA, "chunk-start kernel launch failed"));
   }
   if ((rc = ptab_tables(p))) return bail(rc);
   // G layout tile offsets: nlc(m) = ceil((Lt+1-m)/ADJ_LC) tiles per order
@@ -1162,7 +1167,7 @@ int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* 
     {
       StageMark mk(p, 2, s);
       fv::FwdArgs args{p->X, p->F, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, Lt, p->nP, p->nPpad,
-                       p->nchunks, m_lo, dbg_mode(), mc, trace_buf(), trace_cta(), p->ptab_f, p->mtab_f, p->tofs};
+                       p->nchunks, m_lo, dbg_mode(), mc, trace_buf(), trace_cta(), p->ptab_f, p->mtab_f, p->tofs, p->cmin};
       FV_TRY(dispatch_fwd(p, NT, args, mc, s));
     }
     if (c_hi > c_lo) FV_TRY(cg_forward(p, a, b, B, b0, nf, NT, c_lo, c_hi, s));
