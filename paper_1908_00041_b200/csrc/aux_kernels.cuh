@@ -174,14 +174,15 @@ __global__ void ab_kernel(int Lt, const long long* __restrict__ abofs, double2* 
 //   favest/transforms.py:112 are formed after the (linear) scalar transform, in
 //   the CG stage.  blockIdx.z == 3 nfields zeroes the padding columns.  The
 //   grid path fuses this into the ring FFT (fft2.cuh fft_fold_kernel).
-// per (order m, forward chunk c): the smallest polar start among the chunk's
-// 32 pairs (legendre.cuh first_live_chunk skips the all-zero leading chunks)
-__global__ void chunk_start_kernel(const int* __restrict__ start_l, int nPpad, int nchunks, int Lt, int* cmin) {
+// per (order m, chunk c of `width` pairs): the smallest polar start among the
+// chunk's pairs (legendre.cuh: the forward skips all-zero leading chunk tiles
+// of each l-block, the adjoint all-zero leading stages of each item)
+__global__ void chunk_start_kernel(const int* __restrict__ start_l, int nPpad, int nchunks, int width, int* cmin) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x, m = blockIdx.y;
   if (c >= nchunks) return;
-  const int* s = start_l + (size_t)m * nPpad + c * 32;
+  const int* s = start_l + (size_t)m * nPpad + (size_t)c * width;
   int v = s[0];
-  for (int i = 1; i < 32; ++i) v = min(v, s[i]);
+  for (int i = 1; i < width; ++i) v = min(v, s[i]);
   cmin[(size_t)m * nchunks + c] = v;
 }
 

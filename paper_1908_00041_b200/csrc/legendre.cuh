@@ -709,7 +709,17 @@ struct AdjArgs {
   long long* trace;  // optional pipeline timeline of CTA trace_cta (clock64 stamps), normally null
   int trace_cta;
   SLayout lay;
+  const int* cmin;   // per (order, 128-pair chunk): smallest polar start (the leading all-zero stages are skipped)
 };
+
+// first 32-degree stage of item (m, rc) in which some pair of the chunk has started
+__device__ __forceinline__ int adj_first_stage(const AdjArgs& a, int m, int rc) {
+  const int cm = __ldg(&a.cmin[(size_t)m * a.nrc + rc]);
+  const int nlc = (a.Lt + 1 - m + ADJ_LC - 1) / ADJ_LC;
+  if (cm > a.Lt) return nlc;
+  const int x = cm - m - (ADJ_LC - 1);
+  return x > 0 ? (x + ADJ_LC - 1) / ADJ_LC : 0;
+}
 
 template <int NT>
 struct AdjSmem {
@@ -857,8 +867,9 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
         const int l = m + ADJ_LC * lcx + lane;
         return (l <= Lt) ? __ldg(&dgm[l - m]) : make_double2(0.0, 1.0);
       };
-      double2 dg_next = table ? make_double2(0.0, 1.0) : dg_at(0);
-      for (int lc = 0; lc < nlc; ++lc, ++sc) {
+      const int lc0 = adj_first_stage(args, m, rc);  // leading all-zero stages are skipped
+      double2 dg_next = table ? make_double2(0.0, 1.0) : dg_at(lc0);
+      for (int lc = lc0; lc < nlc; ++lc, ++sc) {
         const int stage = sc % ADJ_STAGES;
         const uint32_t round = sc / ADJ_STAGES;
         const int l0 = m + ADJ_LC * lc;
@@ -968,7 +979,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
 #pragma unroll
         for (int b = 0; b < NT; ++b) acc[a][p2][b][0] = acc[a][p2][b][1] = 0.0;
 
-    for (int lc = 0; lc < nlc; ++lc, ++sc) {
+    for (int lc = adj_first_stage(args, m, rc); lc < nlc; ++lc, ++sc) {
       const int stage = sc % ADJ_STAGES;
       const uint32_t round = sc / ADJ_STAGES;
       const int l0s = m + ADJ_LC * lc;
@@ -1203,8 +1214,10 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_dual_kernel(AdjArgs 
         const int l = m + ADJ_LC * lcx + lane;
         return (l <= Lt) ? __ldg(&dgm[l - m]) : make_double2(0.0, 1.0);
       };
-      double2 dg_next = dg_at(0);
-      for (int lc = 0; lc < nlc; ++lc) {
+      const int lc0 = hasB ? min(adj_first_stage(args, m, rcA), adj_first_stage(args, m, rcA + 1))
+                           : adj_first_stage(args, m, rcA);
+      double2 dg_next = dg_at(lc0);
+      for (int lc = lc0; lc < nlc; ++lc) {
         const int l0 = m + ADJ_LC * lc;
         const bool beforeA = inA.ls > l0 + ADJ_LC - 1, beforeB = inB.ls > l0 + ADJ_LC - 1;
         const bool zeroA = __all_sync(0xffffffffu, beforeA), zeroB = __all_sync(0xffffffffu, beforeB);
@@ -1296,7 +1309,9 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_dual_kernel(AdjArgs 
       for (int p2 = 0; p2 < 2; ++p2)
 #pragma unroll
         for (int b = 0; b < NT; ++b) accA[a][p2][b][0] = accA[a][p2][b][1] = accB[a][p2][b][0] = accB[a][p2][b][1] = 0.0;
-    for (int lc = 0; lc < nlc; ++lc) {
+    const int lc0 = hasB ? min(adj_first_stage(args, m, rcA), adj_first_stage(args, m, rcA + 1))
+                         : adj_first_stage(args, m, rcA);
+    for (int lc = lc0; lc < nlc; ++lc) {
       const int l0s = m + ADJ_LC * lc;
       {
         const int stage = sc % ADJ_STAGES;

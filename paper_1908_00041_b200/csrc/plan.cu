@@ -97,6 +97,7 @@ struct fvPlan {
   int* seed_e = nullptr;
   int* start_l = nullptr;
   int* cmin = nullptr;          // [m][forward chunk] smallest polar start of the chunk's pairs
+  int* cmin_a = nullptr;        // [m][adjoint 128-pair chunk]
   double2* start_v = nullptr;
   double2* ab = nullptr;
   long long* abofs = nullptr;
@@ -167,7 +168,7 @@ void free_plan(fvPlan* p) {
                   p->seed_e, p->start_l,  p->start_v, p->ab,   p->abofs,  p->gofs,
                   p->dg,     p->dgofs,  p->cgt,     p->cga,     p->ptab_f,  p->mtab_f, p->tofs,   p->ptab_a, p->aofs,
                   p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->G,
-                  p->seedk,  p->fitems,   p->Fpart,   p->blue_tab, p->blue_s1, p->cmin,
+                  p->seedk,  p->fitems,   p->Fpart,   p->blue_tab, p->blue_s1, p->cmin, p->cmin_a,
                   p->fft_tw, p->f2_tw};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -990,7 +991,10 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
     p->seed_e = nullptr;
     if ((rc = dalloc(&p->cmin, (size_t)(Lt + 1) * p->nchunks))) return bail(rc);
     dim3 cg((p->nchunks + 127) / 128, Lt + 1);
-    fv::chunk_start_kernel<<<cg, 128>>>(p->start_l, p->nPpad, p->nchunks, Lt, p->cmin);
+    fv::chunk_start_kernel<<<cg, 128>>>(p->start_l, p->nPpad, p->nchunks, fv::FWD_RC, p->cmin);
+    if ((rc = dalloc(&p->cmin_a, (size_t)(Lt + 1) * p->nrc))) return bail(rc);
+    dim3 ca((p->nrc + 127) / 128, Lt + 1);
+    fv::chunk_start_kernel<<<ca, 128>>>(p->start_l, p->nPpad, p->nrc, fv::ADJ_RC, p->cmin_a);
     if (cudaGetLastError() != cudaSuccess) return bail(fail(FV_ECUDA, "chunk-start kernel launch failed"));
   }
   if ((rc = ptab_tables(p))) return bail(rc);
@@ -1202,7 +1206,7 @@ int adjoint_orders(fvPlan* p, const double* a, const double* b, double2* S, cons
       StageMark mk(p, 2, s);
       fv::AdjArgs args{p->G, p->gofs, S, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, p->pair_n,
                        p->pair_s, Lt, p->nP, p->nPpad, p->nrc, p->n_phi, p->n_theta, B, b0, nf, m_lo, dbg_mode(),
-                       mc, p->ptab_a, p->aofs, trace_buf(), trace_cta(), lay};
+                       mc, p->ptab_a, p->aofs, trace_buf(), trace_cta(), lay, p->cmin_a};
       FV_TRY(dispatch_adj(p, NT, args, mc, s));
     }
   }
