@@ -131,7 +131,8 @@ struct fvPlan {
   // hand-written ring FFT (fft.cuh) when every prime factor of n_phi is <= 19
   bool custom_fft = false;
   // Bluestein ring FFT (fft_blue.cuh) for n_phi = R * P with a prime P > 19
-  bool blue = false, smallp = false;
+  bool blue = false, smallp = false, rpfft = false;
+  std::map<std::tuple<long long, long long, int>, cufftHandle> subffts;  // length-P sub-DFT plans (rpfft)
   fv::BlueArgs blue_args{};  // tables and factorisation (pointers owned below)
   fv::SmallPArgs sp_args{};
   double2* blue_tab = nullptr;
@@ -173,6 +174,7 @@ void free_plan(fvPlan* p) {
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (auto& kv : p->ffts) cufftDestroy(kv.second);
+  for (auto& kv : p->subffts) cufftDestroy(kv.second);
   for (auto e : p->ev_pool) cudaEventDestroy(e);
   delete p;
 }
@@ -618,12 +620,33 @@ int setup_blue(fvPlan* p) {
     p->smallp = true;
     return FV_OK;
   }
-  // large P: the Bluestein kernels are correct but still slower than cuFFT's own plan
-  // at C4 (9.4 vs 8.2 ms per direction), so they are opt-in (FV_FFT=blue) for now
-  if (!(env && std::string(env) == "blue")) return FV_OK;
   bool ok = false;
   for (int x : kBlueR) ok |= (x == R);
   if (!ok) return FV_OK;
+  // large P: batched cuFFT sub-DFTs of length P + the combine kernel (rp_combine_kernel);
+  // the Bluestein kernels are correct but slower (9.4 vs 8.2 ms per direction at C4),
+  // opt-in with FV_FFT=blue
+  if (!(env && std::string(env) == "blue")) {
+    if (R == 1) return FV_OK;  // a prime length: cuFFT's own plan
+    std::vector<double2> tab(n + R);
+    for (int j = 0; j < n; ++j) {
+      const long double g = 2.0L * PI_ * j / n;
+      tab[j] = make_double2((double)cosl(g), -(double)sinl(g));
+    }
+    for (int j = 0; j < R; ++j) {
+      const long double g = 2.0L * PI_ * j / R;
+      tab[n + j] = make_double2((double)cosl(g), -(double)sinl(g));
+    }
+    FV_TRY(dalloc(&p->blue_tab, tab.size()));
+    FV_CUDA(cudaMemcpy(p->blue_tab, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    p->blue_args.n = n;
+    p->blue_args.R = R;
+    p->blue_args.P = P;
+    p->blue_args.rootN = p->blue_tab;
+    p->blue_args.rootR = p->blue_tab + n;
+    p->rpfft = true;
+    return FV_OK;
+  }
   int M = 1 << 30;
   for (long long a2 = 1; a2 <= 4096; a2 *= 2)
     for (long long a3 = a2; a3 <= 4096; a3 *= 3)
@@ -722,6 +745,55 @@ int ring_fft_smallp(fvPlan* p, bool inverse, const double2* in, long long in_cs,
   const int H = (a.P - 1) / 2;
   const size_t smem = (size_t)(2 * a.n + a.R * a.R + H * (H + 1)) * sizeof(double2);
   fv::smallp_kernel<<<(unsigned)(3LL * nrings), fv::BLUE_T, smem, s>>>(a);
+  FV_CUDA(cudaGetLastError());
+  return FV_OK;
+}
+
+int ring_fft_rp(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
+                double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s) {
+  const fv::BlueArgs& ba = p->blue_args;
+  const int R = ba.R, P = ba.P;
+  const size_t need = (size_t)3 * nrings * ba.n;
+  if (p->blue_s1_cap < need) {
+    if (p->blue_s1) {
+      FV_CUDA(cudaDeviceSynchronize());
+      cudaFree(p->blue_s1);
+      p->blue_s1 = nullptr;
+      p->blue_s1_cap = 0;
+    }
+    FV_TRY(dalloc(&p->blue_s1, need));
+    p->blue_s1_cap = need;
+  }
+  // sub-DFT plan: element q of residue r at in + r * es + q * (R es), transform b at + b * rs
+  const long long istride = (long long)R * in_es;
+  const auto key = std::make_tuple(istride, in_rs, nrings);
+  auto it = p->subffts.find(key);
+  if (it == p->subffts.end()) {
+    if (istride > INT32_MAX || in_rs > INT32_MAX) return fail(FV_EINVAL, "ring stride too large for cuFFT");
+    int nP = P;
+    cufftHandle hh;
+    FV_CUFFT(cufftPlanMany(&hh, 1, &nP, &nP, (int)istride, (int)in_rs, &nP, 1, P, CUFFT_Z2Z, nrings));
+    it = p->subffts.emplace(key, hh).first;
+  }
+  FV_CUFFT(cufftSetStream(it->second, s));
+  for (int c = 0; c < 3; ++c)
+    for (int r = 0; r < R; ++r) {
+      auto* ip = reinterpret_cast<cufftDoubleComplex*>(const_cast<double2*>(in + c * in_cs + r * in_es));
+      auto* op = reinterpret_cast<cufftDoubleComplex*>(p->blue_s1 + ((size_t)(c * R + r) * nrings) * P);
+      FV_CUFFT(cufftExecZ2Z(it->second, ip, op, inverse ? CUFFT_INVERSE : CUFFT_FORWARD));
+    }
+  fv::RpArgs a{p->blue_s1, out, out_cs, out_rs, out_es, ba.rootN, ba.rootR, ba.n, P, nrings, inverse ? 1 : 0};
+  const unsigned g = (unsigned)((3LL * nrings * P + fv::BLUE_T - 1) / fv::BLUE_T);
+  switch (R) {
+    case 2: fv::rp_combine_kernel<2><<<g, fv::BLUE_T, 0, s>>>(a); break;
+    case 3: fv::rp_combine_kernel<3><<<g, fv::BLUE_T, 0, s>>>(a); break;
+    case 4: fv::rp_combine_kernel<4><<<g, fv::BLUE_T, 0, s>>>(a); break;
+    case 6: fv::rp_combine_kernel<6><<<g, fv::BLUE_T, 0, s>>>(a); break;
+    case 8: fv::rp_combine_kernel<8><<<g, fv::BLUE_T, 0, s>>>(a); break;
+    case 12: fv::rp_combine_kernel<12><<<g, fv::BLUE_T, 0, s>>>(a); break;
+    case 16: fv::rp_combine_kernel<16><<<g, fv::BLUE_T, 0, s>>>(a); break;
+    default: fv::rp_combine_kernel<24><<<g, fv::BLUE_T, 0, s>>>(a); break;
+  }
   FV_CUDA(cudaGetLastError());
   return FV_OK;
 }
@@ -1228,6 +1300,7 @@ int ring_ffts(fvPlan* p, bool inverse, const double2* in, long long in_cs, long 
   if (p->fft2) return ring_fft2_raw(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   if (p->custom_fft) return ring_fft_raw(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   if (p->smallp) return ring_fft_smallp(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
+  if (p->rpfft) return ring_fft_rp(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   if (p->blue) return ring_fft_blue(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   cufftHandle h;
   FV_TRY(get_fft_strided(p, in_rs, in_es, out_rs, out_es, nrings, &h));

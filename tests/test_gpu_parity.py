@@ -233,12 +233,14 @@ def test_odd_and_asymmetric_grids():
 
 
 @pytest.mark.parametrize("nphi", [24, 30, 36, 40, 42, 48, 49, 64, 75, 128, 286, 342, 2052,
-                                  46, 23, 58, 86, 111, 496, 516, 984, 8196, 115])
+                                  46, 23, 58, 86, 111, 496, 516, 984, 8196, 115, 134, 303, 1668])
 def test_ring_fft_radix_plans(nphi):
     """Every packed radix (2..16 composites, primes 11..19), the Bluestein
     lengths R * P with a prime P > 19 (46 = 2 * 23, 23, 58, 86, 111 = 3 * 37,
     496 = 16 * 31, C2's 516 = 12 * 43, 984 = 24 * 41, C4's 8196 = 12 * 683) and
-    the cuFFT fallback (115 = 5 * 23), forward and adjoint against the oracle."""
+    the cuFFT sub-DFT + combine path for P > 64 (134 = 2 * 67, 303 = 3 * 101,
+    1668 = 12 * 139, 8196) and the cuFFT fallback (115 = 5 * 23), forward and
+    adjoint against the oracle."""
     cuda_or_skip()
     rng = np.random.default_rng(nphi)
     L = 8
@@ -515,7 +517,7 @@ def test_direct_forward_batch_determinism_and_edges():
     assert float(a0.abs().max()) == 0.0 and float(b0.abs().max()) == 0.0
 
 
-@pytest.mark.parametrize("nphi", [516, 8196, 46])
+@pytest.mark.parametrize("nphi", [516, 8196, 46, 134, 303])
 def test_ring_fft_against_numpy(nphi):
     """fv_ring_fft alone (the sharded building block) on random rings, both
     directions, against numpy's pocketfft (favest/scalar.py:149, :178); the
