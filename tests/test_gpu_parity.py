@@ -591,3 +591,39 @@ def test_on_the_fly_legendre_matches_table_mode(L, B):
         ra, rb = O.vsht_forward_grid(T0[f], th, w, nphi, L)
         got = np.concatenate([res["0"][1][f], res["0"][2][f]])
         assert O.rel_l2(got, np.concatenate([ra, rb])) <= TOL
+
+
+def test_cuda_graph_capture_replays_bitwise():
+    """The C-ABI calls run on torch's current stream with no host synchronisation or
+    allocation in steady state, so a round trip can be captured in a CUDA graph
+    (C1 latency 56 -> 25 us, tools/c1_latency.py) and replays bitwise."""
+    torch = cuda_or_skip()
+    L = 32
+    th, w, nphi = O.gl_grid(L)
+    plan = _plan(L, th, w, nphi)
+    rng = np.random.default_rng(77)
+    a0, b0 = O.coef(rng, L, "inv")
+    A, B = _t(a0[None]), _t(b0[None])
+    T = torch.empty((1, len(th) * nphi, 3), dtype=torch.complex128, device="cuda")
+    a, b = torch.empty_like(A), torch.empty_like(B)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(2):
+            plan.adjoint(A, B, T)
+            plan.forward(T, a, b)
+    torch.cuda.synchronize()
+    eager = (T.clone(), a.clone(), b.clone())
+    T.zero_(); a.zero_(); b.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        plan.adjoint(A, B, T)
+        plan.forward(T, a, b)
+    g.replay()
+    torch.cuda.synchronize()
+    for x, y in zip((T, a, b), eager):
+        assert torch.equal(x, y)
+    A.copy_(_t(2.0 * a0[None]))  # new inputs in the captured buffers (the transform is linear)
+    B.copy_(_t(2.0 * b0[None]))
+    g.replay()
+    torch.cuda.synchronize()
+    assert O.rel_l2(T[0].cpu().numpy(), 2.0 * eager[0][0].cpu().numpy()) <= TOL
