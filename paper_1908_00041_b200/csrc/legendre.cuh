@@ -116,6 +116,10 @@ struct FwdArgs {
   // the leading chunks of an l-block whose start lies past the block are skipped
   // by producers and consumers alike (no pipeline stage for an all-zero tile)
   const int* cmin;
+  // several 4-field groups in one launch (small problems: more CTAs per launch):
+  // CTA b works on group b % ngroups, X / F of group g at + g * x_gstride / f_gstride
+  int ngroups;
+  long long x_gstride, f_gstride;
 };
 
 // chunk starts of one order held across the warp (chunk 32 g + lane in v[g])
@@ -345,6 +349,14 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
   const int nchunks = args.nchunks;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  {  // field group of this CTA (blocks interleave the groups: heavy orders of every group first)
+    const int ng = args.ngroups > 0 ? args.ngroups : 1;
+    const int gi = blockIdx.x % ng;
+    args.X += gi * args.x_gstride;
+    args.F += gi * args.f_gstride;
+  }
+  const int bxg = blockIdx.x / (args.ngroups > 0 ? args.ngroups : 1);
+  const int gdg = gridDim.x / (args.ngroups > 0 ? args.ngroups : 1);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < FWD_STAGES; ++s) {
@@ -367,7 +379,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
     const uint64_t pol_first = l2_evict_first(), pol_last = l2_evict_last();
     uint32_t tbase = 0;  // tile counter across this CTA's orders
     for (int k = 0;; ++k) {
-      const int item = fwd_item(k, blockIdx.x, gridDim.x);
+      const int item = fwd_item(k, bxg, gdg);
       if (item >= args.m_count) break;
       const int m = args.m_begin + item;
       const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
@@ -467,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       for (int jn = 0; jn < NT; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
     uint32_t tbase = 0;
     for (int k = 0;; ++k) {
-      const int item = fwd_item(k, blockIdx.x, gridDim.x);
+      const int item = fwd_item(k, bxg, gdg);
       if (item >= args.m_count) break;
       const int m = args.m_begin + item;
       const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
@@ -588,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
 
   uint32_t tbase = 0;
   for (int k = 0;; ++k) {
-  const int item = fwd_item(k, blockIdx.x, gridDim.x);
+  const int item = fwd_item(k, bxg, gdg);
   if (item >= args.m_count) break;
   const int m = args.m_begin + item;
   const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
@@ -710,6 +722,10 @@ struct AdjArgs {
   int trace_cta;
   SLayout lay;
   const int* cmin;   // per (order, 128-pair chunk): smallest polar start (the leading all-zero stages are skipped)
+  // several 4-field groups in one launch: item i works on group i % ngroups (G of group g
+  // at + g * g_gstride, its fields from b0 + 4 g)
+  int ngroups;
+  long long g_gstride;
 };
 
 // first 32-degree stage of item (m, rc) in which some pair of the chunk has started
@@ -823,7 +839,8 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
   double2* abw_all = reinterpret_cast<double2*>(empty + ADJ_STAGES);
 
   const int Lt = args.Lt;
-  const int nitems = args.m_count * args.nrc;
+  const int ngr = args.ngroups > 0 ? args.ngroups : 1;
+  const int nitems = args.m_count * args.nrc * ngr;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
@@ -845,7 +862,8 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
     const bool table = args.ptab != nullptr;
     const uint64_t pol_first = l2_evict_first(), pol_last = l2_evict_last();
     uint32_t sc = 0;                           // stage counter across items
-    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    for (int itg = blockIdx.x; itg < nitems; itg += gridDim.x) {
+      const int gi = itg % ngr, item = itg / ngr;
       const int m = args.m_begin + item / args.nrc;
       const int rc = item % args.nrc;
       const int nlc = (Lt + 1 - m + ADJ_LC - 1) / ADJ_LC;
@@ -860,7 +878,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
       }
       double p1 = 0.0, p2 = 0.0;
       const double2* dgm = args.dg + args.dgofs[m];
-      const double* Gm = args.G + (size_t)args.gofs[m] * SM::GTILE;
+      const double* Gm = args.G + gi * args.g_gstride + (size_t)args.gofs[m] * SM::GTILE;
       // (d, gamma) of the stage's 32 degrees, one per lane, loaded one stage ahead
       // (an L2 round trip on the recurrence's critical path otherwise)
       auto dg_at = [&](int lcx) {
@@ -942,21 +960,24 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
   const int soff = 8 * cw + 64 * (l16 >> 3) + (l16 & 7);
   // polar starts of the warp's pairs, loaded one item ahead (a global-memory round
   // trip at every item start otherwise, with the stages already filled)
-  auto start_of = [&](int it) {
-    return it < nitems ? __ldg(&args.start_l[(size_t)(args.m_begin + it / args.nrc) * args.nPpad +
-                                             (it % args.nrc) * ADJ_RC + soff])
-                       : 0;
+  auto start_of = [&](int itg) {
+    const int it = itg / ngr;
+    return itg < nitems ? __ldg(&args.start_l[(size_t)(args.m_begin + it / args.nrc) * args.nPpad +
+                                              (it % args.nrc) * ADJ_RC + soff])
+                        : 0;
   };
   int v_next = start_of(blockIdx.x);
-  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+  for (int itg = blockIdx.x; itg < nitems; itg += gridDim.x) {
+    const int gi = itg % ngr, item = itg / ngr;
     const int m = args.m_begin + item / args.nrc;
     const int rc = item % args.nrc;
+    const int fb0 = args.b0 + 4 * gi;  // first field of this item's group
     const int nlc = (Lt + 1 - m + ADJ_LC - 1) / ADJ_LC;
     // first degree at which each of the warp's M-tiles has a pair above the polar threshold
     int mt_start[2];
     {
       int v = v_next;
-      v_next = start_of(item + gridDim.x);
+      v_next = start_of(itg + gridDim.x);
 #pragma unroll
       for (int o = 1; o < 8; o <<= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
 #pragma unroll
@@ -1040,7 +1061,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
         const int b = ser / 6, comp = (ser % 6) >> 1, sgn = ser & 1;
         ok[jn] = b < args.nfields && !(sgn == 1 && m == 0);
         dst[jn] = args.S + comp * args.lay.cs + (sgn ? bin1 : bin0) * args.lay.bs;
-        rbase[jn] = (long long)(args.b0 + b) * args.n_theta;
+        rbase[jn] = (long long)(fb0 + b) * args.n_theta;
       }
 #pragma unroll
       for (int ii = 0; ii < 2; ++ii) {

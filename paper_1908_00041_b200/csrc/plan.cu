@@ -127,6 +127,8 @@ struct fvPlan {
   double* X = nullptr;
   double* F = nullptr;
   double* G = nullptr;
+  int ngroups_buf = 1;                            // 4-field groups whose X / F / G fit side by side
+  size_t x_gstride = 0, f_gstride = 0, g_gstride = 0;  // doubles per group
   std::map<std::tuple<long long, long long, long long, long long, int>, cufftHandle> ffts;  // strided cuFFT plans
   // hand-written ring FFT (fft.cuh) when every prime factor of n_phi is <= 19
   bool custom_fft = false;
@@ -339,7 +341,7 @@ int launch_fwd(fvPlan* p, const fv::FwdArgs& args, int m_count, cudaStream_t s) 
   a2.m_count = m_count;
   // one CTA per order: the hardware block scheduler hands out orders in ascending m
   // (descending work) dynamically, which balances better than a static persistent split
-  fv::legendre_fwd_kernel<NT><<<m_count, fv::kThreads, bytes, s>>>(a2);
+  fv::legendre_fwd_kernel<NT><<<m_count * std::max(1, a2.ngroups), fv::kThreads, bytes, s>>>(a2);
   FV_CUDA(cudaGetLastError());
   return FV_OK;
 }
@@ -370,7 +372,7 @@ int launch_adj(fvPlan* p, const fv::AdjArgs& args, int m_count, cudaStream_t s) 
       return FV_OK;
     }
   }
-  const int items = m_count * p->nrc;
+  const int items = m_count * p->nrc * std::max(1, a2.ngroups);
   fv::legendre_adj_kernel<NT><<<std::min(items, p->num_sms), fv::kThreads, bytes, s>>>(a2);
   FV_CUDA(cudaGetLastError());
   return FV_OK;
@@ -864,7 +866,7 @@ int ring_fft2_raw(fvPlan* p, bool inverse, const double2* in, long long in_cs, l
 }
 
 // fused forward FFT + fold of fields b0 .. b0 + nf - 1 of T (B, N, 3) into X (all orders)
-int fft_fold(fvPlan* p, const double2* T, int b0, int nf, cudaStream_t s) {
+int fft_fold(fvPlan* p, const double2* T, int b0, int nf, cudaStream_t s, double* X) {
   fv::Fft2Args a{};
   if (p->smallp) {  // small-prime ring DFT (fft_blue.cuh smallp_fold_kernel)
     const long long n = p->n_phi;
@@ -872,7 +874,7 @@ int fft_fold(fvPlan* p, const double2* T, int b0, int nf, cudaStream_t s) {
     a.in_es = 3;
     a.field_stride = 3 * n * p->n_theta;
     a.in = T + (long long)b0 * a.field_stride;
-    a.X = p->X;
+    a.X = X;
     a.pair_n = p->pair_n;
     a.pair_s = p->pair_s;
     a.ring_w = p->ring_w;
@@ -893,7 +895,7 @@ int fft_fold(fvPlan* p, const double2* T, int b0, int nf, cudaStream_t s) {
   a.in_es = 3;
   a.field_stride = 3 * n * p->n_theta;
   a.in = T + (long long)b0 * a.field_stride;
-  a.X = p->X;
+  a.X = X;
   a.pair_n = p->pair_n;
   a.pair_s = p->pair_s;
   a.ring_w = p->ring_w;
@@ -1106,10 +1108,18 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
     p->lay_a = adig == '2' ? blocked : adig == '0' ? ringmajor : binmajor;
   }
   const size_t spec = (size_t)3 * ((max_batch * (size_t)n_theta + 7) / 8 * 8) * n_phi;
-  if ((rc = dalloc(&p->Sf, spec)) || (rc = dalloc(&p->Sa, spec)) ||
-      (rc = dalloc(&p->X, (size_t)(Lt + 1) * p->nchunks * (2 * 8 * NTmax * 32))) ||
-      (rc = dalloc(&p->F, (size_t)(Lt + 1) * (Lt + 2) / 2 * 8 * NTmax)) ||
-      (rc = dalloc(&p->G, (size_t)p->g_tiles * (2 * fv::ADJ_KS * NTmax * 32))))
+  p->x_gstride = (size_t)(Lt + 1) * p->nchunks * (2 * 8 * NTmax * 32);
+  p->f_gstride = (size_t)(Lt + 1) * (Lt + 2) / 2 * 8 * NTmax;
+  p->g_gstride = (size_t)p->g_tiles * (2 * fv::ADJ_KS * NTmax * 32);
+  {
+    // several full field groups per Legendre launch when their buffers stay small (<= 2 GB)
+    const size_t per = (p->x_gstride + p->f_gstride + p->g_gstride) * sizeof(double);
+    const int want = (max_batch + 3) / 4;
+    p->ngroups_buf = std::max(1, std::min(want, (int)std::min<size_t>(16, (2ull << 30) / std::max<size_t>(per, 1))));
+  }
+  const size_t ngb = (size_t)p->ngroups_buf;
+  if ((rc = dalloc(&p->Sf, spec)) || (rc = dalloc(&p->Sa, spec)) || (rc = dalloc(&p->X, ngb * p->x_gstride)) ||
+      (rc = dalloc(&p->F, ngb * p->f_gstride)) || (rc = dalloc(&p->G, ngb * p->g_gstride)))
     return bail(rc);
   if (cudaMemset(p->Sa, 0, spec * sizeof(double2)) != cudaSuccess) return bail(fail(FV_ECUDA, "memset failed"));
   cudaError_t e = cudaDeviceSynchronize();
@@ -1204,9 +1214,10 @@ int check_grid_call(fvPlan* p, int B, const void* x, const void* y, const void* 
 
 // CG assembly (favest/transforms.py:120-146) of coefficient orders [c_lo, c_hi) of fields
 // b0 .. b0 + nf - 1 from the forward Legendre rows in p->F (ncol = 8 NT)
-int cg_forward(fvPlan* p, double* a, double* b, int B, int b0, int nf, int NT, int c_lo, int c_hi, cudaStream_t s) {
+int cg_forward(fvPlan* p, double* a, double* b, int B, int b0, int nf, int NT, int c_lo, int c_hi, cudaStream_t s,
+               const double* F = nullptr) {
   StageMark mk(p, 3, s);
-  fv::CgFwdArgs ca{p->F, reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), p->cgt, p->L, 8 * NT, B, b0,
+  fv::CgFwdArgs ca{F ? F : p->F, reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), p->cgt, p->L, 8 * NT, B, b0,
                    nf, c_lo, c_hi};
   dim3 grid((c_hi + fv::CGF_MB - 1) / fv::CGF_MB, p->L + 1);
   const size_t smem = (size_t)3 * (fv::CGF_MB + 2) * fv::cgf_rs(nf) * sizeof(double2);
@@ -1226,27 +1237,37 @@ int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* 
                    int m_hi, int c_lo, int c_hi, cudaStream_t s, const double2* Tfield = nullptr) {
   const int Lt = p->Lt;
   const int mc = m_hi - m_lo;
-  for (int b0 = 0; b0 < B; b0 += 4) {
-    const int nf = std::min(4, B - b0);
+  for (int b0 = 0; b0 < B;) {
+    // up to ngroups_buf full 4-field groups go through one Legendre launch
+    const int ng = std::max(1, std::min((B - b0) / 4, p->ngroups_buf));
+    const int nf = ng > 1 ? 4 : std::min(4, B - b0);
     const int NT = ntiles_for(nf);
-    if (S) {
-      StageMark mk(p, 1, s);
-      fv::FoldArgs fa{S, p->X, p->pair_n, p->pair_s, p->ring_w, p->n_phi, p->n_theta, B, b0, nf, NT,
-                      p->nchunks * fv::FWD_RC, p->nchunks, m_lo, mc, lay};
-      dim3 grid((p->nchunks * fv::FWD_RC + 127) / 128, mc, 3 * nf + 1);
-      fv::fold_fwd_kernel<<<grid, 128, 0, s>>>(fa);
-      FV_CUDA(cudaGetLastError());
-    } else {  // fused FFT + fold straight from the field (fft2.cuh)
-      StageMark mk(p, 0, s);
-      FV_TRY(fft_fold(p, Tfield, b0, nf, s));
+    for (int g = 0; g < ng; ++g) {
+      double* Xg = p->X + (size_t)g * p->x_gstride;
+      const int bg = b0 + 4 * g;
+      if (S) {
+        StageMark mk(p, 1, s);
+        fv::FoldArgs fa{S, Xg, p->pair_n, p->pair_s, p->ring_w, p->n_phi, p->n_theta, B, bg, nf, NT,
+                        p->nchunks * fv::FWD_RC, p->nchunks, m_lo, mc, lay};
+        dim3 grid((p->nchunks * fv::FWD_RC + 127) / 128, mc, 3 * nf + 1);
+        fv::fold_fwd_kernel<<<grid, 128, 0, s>>>(fa);
+        FV_CUDA(cudaGetLastError());
+      } else {  // fused FFT + fold straight from the field (fft2.cuh / fft_blue.cuh)
+        StageMark mk(p, 0, s);
+        FV_TRY(fft_fold(p, Tfield, bg, nf, s, Xg));
+      }
     }
     {
       StageMark mk(p, 2, s);
       fv::FwdArgs args{p->X, p->F, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, Lt, p->nP, p->nPpad,
-                       p->nchunks, m_lo, dbg_mode(), mc, trace_buf(), trace_cta(), p->ptab_f, p->mtab_f, p->tofs, p->cmin};
+                       p->nchunks, m_lo, dbg_mode(), mc, trace_buf(), trace_cta(), p->ptab_f, p->mtab_f, p->tofs, p->cmin,
+                       ng, (long long)p->x_gstride, (long long)p->f_gstride};
       FV_TRY(dispatch_fwd(p, NT, args, mc, s));
     }
-    if (c_hi > c_lo) FV_TRY(cg_forward(p, a, b, B, b0, nf, NT, c_lo, c_hi, s));
+    if (c_hi > c_lo)
+      for (int g = 0; g < ng; ++g)
+        FV_TRY(cg_forward(p, a, b, B, b0 + 4 * g, nf, NT, c_lo, c_hi, s, p->F + (size_t)g * p->f_gstride));
+    b0 += ng > 1 ? 4 * ng : nf;
   }
   return FV_OK;
 }
@@ -1256,13 +1277,16 @@ int adjoint_orders(fvPlan* p, const double* a, const double* b, double2* S, cons
                    int m_hi, cudaStream_t s) {
   const int Lt = p->Lt;
   const int mc = m_hi - m_lo;
-  for (int b0 = 0; b0 < B; b0 += 4) {
-    const int nf = std::min(4, B - b0);
+  for (int b0 = 0; b0 < B;) {
+    // up to ngroups_buf full 4-field groups go through one Legendre launch
+    const int ng = std::max(1, std::min((B - b0) / 4, p->ngroups_buf));
+    const int nf = ng > 1 ? 4 : std::min(4, B - b0);
     const int NT = ntiles_for(nf);
-    {
+    for (int g = 0; g < ng; ++g) {
       StageMark mk(p, 3, s);
       fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), p->dg, p->dgofs,
-                       p->cgt, p->G, p->gofs, nullptr, p->L, NT, B, b0, nf, m_lo, 0, p->cga, 32 * p->g_tiles};
+                       p->cgt, p->G + (size_t)g * p->g_gstride, p->gofs, nullptr, p->L, NT, B, b0 + 4 * g, nf, m_lo,
+                       0, p->cga, 32 * p->g_tiles};
       dim3 grid((Lt + 1 - m_lo + fv::ADJ_LC - 1) / fv::ADJ_LC, mc);
       const size_t smem = (size_t)2 * fv::ADJ_KS * fv::cga_bstride(nf) * sizeof(double) +
                           2 * (size_t)nf * 34 * 7 * sizeof(double2);
@@ -1278,9 +1302,10 @@ int adjoint_orders(fvPlan* p, const double* a, const double* b, double2* S, cons
       StageMark mk(p, 2, s);
       fv::AdjArgs args{p->G, p->gofs, S, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, p->pair_n,
                        p->pair_s, Lt, p->nP, p->nPpad, p->nrc, p->n_phi, p->n_theta, B, b0, nf, m_lo, dbg_mode(),
-                       mc, p->ptab_a, p->aofs, trace_buf(), trace_cta(), lay, p->cmin_a};
+                       mc, p->ptab_a, p->aofs, trace_buf(), trace_cta(), lay, p->cmin_a, ng, (long long)p->g_gstride};
       FV_TRY(dispatch_adj(p, NT, args, mc, s));
     }
+    b0 += ng > 1 ? 4 * ng : nf;
   }
   return FV_OK;
 }
