@@ -265,33 +265,41 @@ __device__ __forceinline__ double2 smallp_out(const SmallPArgs& a, const double2
   return acc;
 }
 
+// Plain transform: CTA per (component, ring pair) -- both rings' items keep all
+// 256 threads busy through both stages, and in the adjoint's ring-pair spectrum
+// layout the two rings' bins are one contiguous stream.
 __global__ void __launch_bounds__(BLUE_T) smallp_kernel(SmallPArgs a) {
   extern __shared__ __align__(16) double2 sp_smem[];
   const int H = (a.P - 1) / 2;
-  double2* xs = sp_smem;                  // [n] ring component
-  double2* ys = sp_smem + a.n;            // [R][P] twiddled residue DFTs
-  double2* wp = ys + a.n;                 // [H][H + 1] (cos, sin): lane k reads [q][k], conflict free
+  const int n = a.n;
+  double2* xs = sp_smem;                  // [2][n] rings
+  double2* ys = sp_smem + 2 * n;          // [2][R][P] twiddled residue DFTs
+  double2* wp = ys + 2 * n;               // [H][H + 1] (cos, sin): lane k reads [q][k], conflict free
   double2* wr = wp + H * (H + 1);         // [R][R]
-  const int c = blockIdx.x % 3, ring = blockIdx.x / 3;
+  const int c = blockIdx.x % 3, r0 = 2 * (blockIdx.x / 3);
+  const int nr = min(2, a.nrings - r0);
   const double cj = a.inverse ? -1.0 : 1.0;
-  const double2* src =
-      a.in + c * a.in_cs +
-      (a.in_rblk ? (long long)(ring >> (31 - __clz(a.in_rblk))) * a.in_rs + (ring & (a.in_rblk - 1))
-                 : (long long)ring * a.in_rs);
-  for (int i = threadIdx.x; i < a.n; i += BLUE_T) {
-    double2 v = src[(long long)i * a.in_es];
+  auto ring_base = [&](int ring) {
+    return a.in_rblk ? (long long)(ring >> (31 - __clz(a.in_rblk))) * a.in_rs + (ring & (a.in_rblk - 1))
+                     : (long long)ring * a.in_rs;
+  };
+  const double2* src0 = a.in + c * a.in_cs + ring_base(r0);
+  const double2* src1 = a.in + c * a.in_cs + ring_base(r0 + nr - 1);
+  for (int i = threadIdx.x; i < nr * n; i += BLUE_T) {
+    const int ring = i / n, j = i - ring * n;
+    double2 v = (ring ? src1 : src0)[(long long)j * a.in_es];
     v.y *= cj;
     xs[i] = v;
   }
   for (int i = threadIdx.x; i < H * (H + 1); i += BLUE_T) wp[i] = __ldg(&a.WP[i]);
   for (int i = threadIdx.x; i < a.R * a.R; i += BLUE_T) wr[i] = __ldg(&a.WR[i]);
   __syncthreads();
-  smallp_stage1(a, xs, ys, wp, 1);
+  smallp_stage1(a, xs, ys, wp, nr);
   __syncthreads();
-  double2* dst = a.out + c * a.out_cs + ring * a.out_rs;
-  for (int o = threadIdx.x; o < a.n; o += BLUE_T) {
-    const double2 v = smallp_out(a, ys, wr, o);  // output index = thread index: coalesced
-    dst[(long long)o * a.out_es] = make_double2(v.x, cj * v.y);
+  for (int i = threadIdx.x; i < nr * n; i += BLUE_T) {
+    const int ring = i / n, o = i - ring * n;
+    const double2 v = smallp_out(a, ys + ring * n, wr, o);  // output index = thread index: coalesced
+    a.out[c * a.out_cs + (long long)(r0 + ring) * a.out_rs + (long long)o * a.out_es] = make_double2(v.x, cj * v.y);
   }
 }
 

@@ -612,10 +612,9 @@ int setup_blue(fvPlan* p) {
     s.rootN = p->blue_tab;
     s.WR = p->blue_tab + n;
     s.WP = p->blue_tab + n + R * R;
-    const size_t smem = (size_t)(2 * n + R * R + H * (H + 1)) * sizeof(double2);
-    const size_t smem_f = (size_t)(4 * n + R * R + H * (H + 1)) * sizeof(double2);  // two rings, fused fold
+    const size_t smem_f = (size_t)(4 * n + R * R + H * (H + 1)) * sizeof(double2);  // two rings per CTA
     if (smem_f > 200 * 1024) return FV_OK;
-    FV_CUDA(cudaFuncSetAttribute(fv::smallp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    FV_CUDA(cudaFuncSetAttribute(fv::smallp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
     FV_CUDA(cudaFuncSetAttribute(fv::smallp_fold_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_f));
     const char* ff = std::getenv("FV_FUSED_FOLD");
     p->fused_fold = !(ff && std::atoi(ff) == 0);
@@ -745,8 +744,8 @@ int ring_fft_smallp(fvPlan* p, bool inverse, const double2* in, long long in_cs,
   a.nrings = nrings;
   a.inverse = inverse ? 1 : 0;
   const int H = (a.P - 1) / 2;
-  const size_t smem = (size_t)(2 * a.n + a.R * a.R + H * (H + 1)) * sizeof(double2);
-  fv::smallp_kernel<<<(unsigned)(3LL * nrings), fv::BLUE_T, smem, s>>>(a);
+  const size_t smem = (size_t)(4 * a.n + a.R * a.R + H * (H + 1)) * sizeof(double2);  // two rings per CTA
+  fv::smallp_kernel<<<(unsigned)(3LL * ((nrings + 1) / 2)), fv::BLUE_T, smem, s>>>(a);
   FV_CUDA(cudaGetLastError());
   return FV_OK;
 }
