@@ -200,7 +200,11 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     L = args.L
-    for _ in range(args.warmup):
+    # wall-clock budget: each step is a ~4 s sample of the host computation, so a long
+    # --steps run stops early (the median of the completed steps is the value)
+    budget = float(os.environ.get("FV_REF_BUDGET_S", "240"))
+    t_start = time.perf_counter()
+    for _ in range(min(args.warmup, 3)):
         cpu_port_rate(L, args.ref_every * 4)
     rates, secs = [], []
     desc = ""
@@ -208,7 +212,11 @@ def run_reference(args, rank, world):
         r, dt, desc = cpu_port_rate(L, args.ref_every)
         rates.append(r)
         secs.append(dt)
+        if time.perf_counter() - t_start > budget:
+            break
     rate = float(np.median(rates))
+    if len(rates) < args.steps:
+        desc += f"; {len(rates)} of {args.steps} steps within the {budget:.0f} s wall budget"
     cores = os.cpu_count()
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps,
