@@ -495,42 +495,71 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
           const int l = l0 + 2 * (8 * i + g) + par;
           gam4[i] = (args.ptab || l > Lt) ? 1.0 : __ldg(&dgm[l - m].y);
         }
-        for (int c = c0; c < nchunks; ++c) {
-          const uint32_t t = tbase + (c - c0);
+        // Tiles of the l-block software-pipelined by one: the DMMAs of tile t are
+        // issued, tile t is released, then tile t + 1 is awaited and its fragments
+        // loaded while those DMMAs execute (without this both consumer warps of an
+        // SMSP woke on the same barrier and loaded together, leaving the DMMA pipe
+        // idle for the load latency of every tile).
+        struct Frag {
+          double a[2][4], bb[2][NT];
+          int km0, km1;
+          bool live;
+        };
+        auto fetch = [&](uint32_t t, Frag& f) {
           const int stage = t % FWD_STAGES;
           mbar_wait(&full[stage], (t / FWD_STAGES) & 1);
           const double* Ps = smem + stage * SM::STAGE;
           const double* Xs = Ps + FWD_PTILE;
-          const int km0 = meta[stage].kmin[2 * kq], km1 = meta[stage].kmin[2 * kq + 1];
-          if (!meta[stage].zero && !(args.dbg & 1)) {
-            double a[2][4], bb[2][NT];
+          f.km0 = meta[stage].kmin[2 * kq];
+          f.km1 = meta[stage].kmin[2 * kq + 1];
+          f.live = !meta[stage].zero && !(args.dbg & 1);
+          if (f.live) {
 #pragma unroll
             for (int kk = 0; kk < 2; ++kk) {
               const int ks = 2 * kq + kk;
               const int sw = ((g ^ (ks & 3)) << 2) + q;
 #pragma unroll
-              for (int i = 0; i < 4; ++i) a[kk][i] = lds_f64(&Ps[((par * 4 + i) * 8 + ks) * 32 + sw]);
+              for (int i = 0; i < 4; ++i) f.a[kk][i] = lds_f64(&Ps[((par * 4 + i) * 8 + ks) * 32 + sw]);
 #pragma unroll
-              for (int jn = 0; jn < NT; ++jn) bb[kk][jn] = lds_f64(&Xs[((par * 8 + ks) * NT + jn) * 32 + xq]);
-            }
-            // M-tile i (rows l0 + 16 i .. + 15) runs k-step ks once some pair of it has
-            // started (kmin[ks] <= last row) and it is not padding past Lt; real branches
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const int r0 = l0 + 16 * i;
-              if (r0 > Lt) continue;
-              if (km0 <= r0 + 15) {
-#pragma unroll
-                for (int jn = 0; jn < NT; ++jn) dmma_m8n8k4(acc[i][jn][0], acc[i][jn][1], a[0][i], bb[0][jn]);
-              }
-              if (km1 <= r0 + 15) {
-#pragma unroll
-                for (int jn = 0; jn < NT; ++jn) dmma_m8n8k4(acc[i][jn][0], acc[i][jn][1], a[1][i], bb[1][jn]);
-              }
+              for (int jn = 0; jn < NT; ++jn) f.bb[kk][jn] = lds_f64(&Xs[((par * 8 + ks) * NT + jn) * 32 + xq]);
             }
           }
-          mbar_arrive(&empty[stage]);
+        };
+        // M-tile i (rows l0 + 16 i .. + 15) runs k-step ks once some pair of it has
+        // started (kmin[ks] <= last row) and it is not padding past Lt; real branches
+        auto mma = [&](const Frag& f) {
+          if (!f.live) return;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int r0 = l0 + 16 * i;
+            if (r0 > Lt) continue;
+            if (f.km0 <= r0 + 15) {
+#pragma unroll
+              for (int jn = 0; jn < NT; ++jn) dmma_m8n8k4(acc[i][jn][0], acc[i][jn][1], f.a[0][i], f.bb[0][jn]);
+            }
+            if (f.km1 <= r0 + 15) {
+#pragma unroll
+              for (int jn = 0; jn < NT; ++jn) dmma_m8n8k4(acc[i][jn][0], acc[i][jn][1], f.a[1][i], f.bb[1][jn]);
+            }
+          }
+        };
+        auto release = [&](uint32_t t) {
+          mbar_arrive(&empty[t % FWD_STAGES]);  // the fragments are in registers
           if (cw == 0 && lane == 0) *cons0 = (int)t + 1;
+        };
+        // two register sets alternate: tile t + 1 is awaited and loaded into the
+        // other set while tile t's DMMAs execute
+        Frag f0, f1;
+        const uint32_t tend = tbase + (uint32_t)(nchunks - c0);
+        if (tbase < tend) fetch(tbase, f0);
+        for (uint32_t t = tbase; t < tend; t += 2) {
+          mma(f0);
+          release(t);
+          if (t + 1 >= tend) break;
+          fetch(t + 1, f1);
+          mma(f1);
+          release(t + 1);
+          if (t + 2 < tend) fetch(t + 2, f0);
         }
         tbase += nchunks - c0;
         // epilogue of the l-block: k-quarters 1..3 park their partial sums, quarter 0
