@@ -95,14 +95,15 @@ def c4_timing(reps=3):
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "c4":
     c4_timing()
 
-def c5_timing(reps=5):
-    """C5: adjoint at M = 200,000 scattered points, L = 128 (one field)."""
+def c5_timing(reps=5, B=1):
+    """C5: adjoint at M = 200,000 scattered points, L = 128 (B fields)."""
     L, M = 128, 200_000
     rng = np.random.default_rng(5)
     v = rng.standard_normal((M, 3)); x = v / np.linalg.norm(v, axis=1, keepdims=True)
-    a, b = O.coef(rng, L, "inv")
-    pp = PointsPlan(L)
-    X = torch.from_numpy(x).cuda(); A = torch.from_numpy(a[None]).cuda(); Bc = torch.from_numpy(b[None]).cuda()
+    cs = [O.coef(rng, L, "inv") for _ in range(B)]
+    a = np.stack([c[0] for c in cs]); b = np.stack([c[1] for c in cs])
+    pp = PointsPlan(L, max_batch=B)
+    X = torch.from_numpy(x).cuda(); A = torch.from_numpy(a).cuda(); Bc = torch.from_numpy(b).cuda()
     T = pp.adjoint(X, A, Bc); torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -110,11 +111,12 @@ def c5_timing(reps=5):
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     Kt = (L + 2) ** 2
-    flops = 24 * ((L + 2) * (L + 3) // 2) * M + 4 * ((L + 2) * (L + 3) // 2) * M
-    print(f"C5 L={L} M={M}: {ms:.3f} ms  {1e3/ms:.1f} transforms/s  {flops/ms/1e9:.2f} TF/s (SURVEY canonical 47.37 GFLOP)", flush=True)
+    flops = B * 24 * ((L + 2) * (L + 3) // 2) * M + 4 * ((L + 2) * (L + 3) // 2) * M
+    print(f"C5 L={L} M={M} B={B}: {ms:.3f} ms  {B*1e3/ms:.1f} transforms/s  {flops/ms/1e9:.2f} TF/s (SURVEY canonical 47.37 GFLOP per field)", flush=True)
 
 if __name__ == "__main__" and len(sys.argv) > 1 and sys.argv[1] == "c5":
     c5_timing()
+    c5_timing(B=4)
 
 def c5f_timing(reps=5):
     """Direct-route forward at C5 shapes: M = 200,000 weighted scattered points, L = 128."""
