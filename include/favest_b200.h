@@ -20,6 +20,10 @@
  *   fv_forward_points  <- forward_favest(samples, rule, ..., "direct-scalar")
  *                         favest/transforms.py:79-147 with
  *                         _forward_direct_values favest/scalar.py:94-105
+ *   fv_forward_scalar_grid / fv_adjoint_scalar_grid
+ *                      <- forward_sht_fast / adjoint_sht_fast favest/scalar.py:146-184
+ *   fv_forward_scalar_points / fv_adjoint_scalar_points
+ *                      <- forward_sht_direct / adjoint_sht_direct favest/scalar.py:94-128
  *   fv_plan_create_grid <- the per-grid state the reference rebuilds on every
  *                         call: TensorGrid (favest/scalar.py:29-84),
  *                         legendre_table (favest/legendre.py:36-75),
@@ -102,6 +106,21 @@ int fv_adjoint_points(fvPlan* plan, const double* xyz, long long M, const double
  */
 int fv_forward_points(fvPlan* plan, const double* xyz, const double* w, long long M, const double* T, double* a,
                       double* b, int B, void* stream);
+
+/*
+ * Scalar spherical harmonic transforms of degree lmax <= the plan's L + 1
+ * (favest/scalar.py:94-128, 146-184: forward_sht_fast, adjoint_sht_fast,
+ * forward_sht_direct, adjoint_sht_direct).  B <= 3 * max_batch scalar fields
+ * f [B][N] (grid) or [B][M] (points), coefficients [B][(lmax+1)^2] at
+ * l*l + l + m.  They run through the vector kernels with the scalar fields as
+ * the Cartesian components of pseudo fields (no Clebsch-Gordan stage).
+ */
+int fv_forward_scalar_grid(fvPlan* plan, const double* f, double* out, int lmax, int B, void* stream);
+int fv_adjoint_scalar_grid(fvPlan* plan, const double* g, double* f, int lmax, int B, void* stream);
+int fv_forward_scalar_points(fvPlan* plan, const double* xyz, const double* w, long long M, const double* f,
+                             double* out, int lmax, int B, void* stream);
+int fv_adjoint_scalar_points(fvPlan* plan, const double* xyz, long long M, const double* g, double* f, int lmax,
+                             int B, void* stream);
 
 /*
  * Order-sharded building blocks (ring-sharded fields,

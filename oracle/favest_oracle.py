@@ -32,7 +32,7 @@ __all__ = [
     "FOUR_PI", "INV_SQRT_4PI", "INV_SQRT2", "flat_size", "degrees_orders", "tri_index",
     "gl_grid", "grid_points", "ring_cos_sin", "seed_table", "recurrence_ab", "legendre_m",
     "legendre_table", "sht_forward_grid", "sht_adjoint_grid", "sht_adjoint_points",
-    "sht_forward_points", "vsht_forward_points",
+    "sht_forward_points", "vsht_forward_points", "verify_exactness",
     "cg_explicit_vec", "cg_tables", "shift_read", "vsht_forward_grid", "vsht_adjoint_merged",
     "vsht_adjoint_grid", "vsht_adjoint_points", "coef", "random_points", "tangent_noise",
     "rel_l2", "XR_SHIFT",
@@ -322,6 +322,22 @@ def sht_forward_points(f, weights, points, lt):
             res = P @ g.real + 1j * (P @ g.imag)
             out[ls * ls + ls + mm] = _sigma(mm) * res
     return out
+
+
+def verify_exactness(points, weights, t):
+    """Rule certification (favest/quadrature.py:51-76): the largest
+    |sum_i w_i Y(l, m, x_i) - sqrt(4 pi) [l = 0]| over l <= t, 0 <= m <= l, and
+    whether it is <= 1e-8.  Real weights: |sum w conj(Y)| = |sum w Y|, so the
+    sums are the direct forward of the constant 1."""
+    if t < 0:
+        raise ValueError(f"certification degree must be non-negative, got {t}")
+    n = np.asarray(points).shape[0]
+    c = sht_forward_points(np.ones((n, 1)), weights, points, t)[:, 0]
+    _, ms = degrees_orders(t)
+    sums = c[ms >= 0].copy()
+    sums[0] -= np.sqrt(4.0 * np.pi)
+    d = float(np.max(np.abs(sums)))
+    return d, d <= 1e-8
 
 
 # --------------------------------------------------------------------------

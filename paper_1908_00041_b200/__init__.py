@@ -17,6 +17,7 @@ from .core import (
 from .grid import TensorGrid, gen_gl_tensor, gl_grid_for
 from .transforms import PATHS, adjoint_favest, forward_favest, grid_plan, points_plan
 from .pipeline import HostPipeline
+from .scalar import adjoint_sht_direct, adjoint_sht_fast, forward_sht_direct, forward_sht_fast, verify_exactness
 
 __version__ = "0.1.0"
 
@@ -24,4 +25,5 @@ __all__ = [
     "QuadratureRule", "ScalarCoefficients", "TangentFieldSamples", "VectorCoefficients",
     "degrees_orders", "flat_index", "flat_size", "TensorGrid", "gen_gl_tensor", "gl_grid_for",
     "PATHS", "adjoint_favest", "forward_favest", "grid_plan", "points_plan", "HostPipeline",
+    "forward_sht_fast", "adjoint_sht_fast", "forward_sht_direct", "adjoint_sht_direct", "verify_exactness",
 ]

@@ -23,6 +23,7 @@
 #include "fft_blue.cuh"
 #include "legendre.cuh"
 #include "points.cuh"
+#include "scalar.cuh"
 
 namespace {
 
@@ -119,6 +120,8 @@ struct fvPlan {
   int2* fitems = nullptr;       // (order, 128-degree window), heaviest first
   int n_fitems = 0;
   double* Fpart = nullptr;      // point-range partial rows [R][tri(Lt)][ncol]
+  double* Tp = nullptr;         // scalar transforms: pseudo fields [K][n][3]
+  size_t Tp_cap = 0;
   size_t Fpart_cap = 0, F_cap = 0;
   long long g_tiles = 0;
   // workspaces
@@ -171,7 +174,7 @@ void free_plan(fvPlan* p) {
                   p->seed_e, p->start_l,  p->start_v, p->ab,   p->abofs,  p->gofs,
                   p->dg,     p->dgofs,  p->cgt,     p->cga,     p->ptab_f,  p->mtab_f, p->tofs,   p->ptab_a, p->aofs,
                   p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->G,
-                  p->seedk,  p->fitems,   p->Fpart,   p->blue_tab, p->blue_s1, p->cmin, p->cmin_a,
+                  p->seedk,  p->fitems,   p->Fpart,   p->blue_tab, p->blue_s1, p->cmin, p->cmin_a, p->Tp,
                   p->fft_tw, p->f2_tw};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -1232,8 +1235,25 @@ int cg_forward(fvPlan* p, double* a, double* b, int B, int b0, int nf, int NT, i
 
 // fold + Legendre over orders [m_lo, m_hi) and CG for orders [c_lo, c_hi), reading the
 // spectra of every ring of the grid in layout `lay` (natural or compact bins)
+// Scalar mode of the vector pipeline (scalar.cuh): the fields are pseudo fields
+// whose components are scalar fields; the CG stages become unpack / pack.
+struct ScalarIO {
+  double2* out = nullptr;       // forward: flat scalar coefficients [B][(lmax + 1)^2]
+  const double2* in = nullptr;  // adjoint: flat scalar coefficients
+  int lmax = 0, B = 0;          // scalar degree and scalar field count
+};
+
+int scalar_unpack(const ScalarIO& io, const double* F, int NT, int pf0, int nfp, int Lt_rows, cudaStream_t s) {
+  const int lm = std::min(io.lmax, Lt_rows);
+  dim3 grid((lm + 1 + 127) / 128, lm + 1);
+  fv::scalar_unpack_kernel<<<grid, 128, 0, s>>>(F, 8 * NT, io.lmax, pf0, nfp, io.B, io.out);
+  FV_CUDA(cudaGetLastError());
+  return FV_OK;
+}
+
 int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* a, double* b, int B, int m_lo,
-                   int m_hi, int c_lo, int c_hi, cudaStream_t s, const double2* Tfield = nullptr) {
+                   int m_hi, int c_lo, int c_hi, cudaStream_t s, const double2* Tfield = nullptr,
+                   const ScalarIO* sio = nullptr) {
   const int Lt = p->Lt;
   const int mc = m_hi - m_lo;
   for (int b0 = 0; b0 < B;) {
@@ -1263,7 +1283,12 @@ int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* 
                        ng, (long long)p->x_gstride, (long long)p->f_gstride};
       FV_TRY(dispatch_fwd(p, NT, args, mc, s));
     }
-    if (c_hi > c_lo)
+    if (sio)
+      for (int g = 0; g < ng; ++g) {
+        StageMark mk(p, 3, s);
+        FV_TRY(scalar_unpack(*sio, p->F + (size_t)g * p->f_gstride, NT, b0 + 4 * g, nf, Lt, s));
+      }
+    else if (c_hi > c_lo)
       for (int g = 0; g < ng; ++g)
         FV_TRY(cg_forward(p, a, b, B, b0 + 4 * g, nf, NT, c_lo, c_hi, s, p->F + (size_t)g * p->f_gstride));
     b0 += ng > 1 ? 4 * ng : nf;
@@ -1273,7 +1298,7 @@ int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* 
 
 // CG + Legendre synthesis for orders [m_lo, m_hi) into spectra of every ring (layout `lay`)
 int adjoint_orders(fvPlan* p, const double* a, const double* b, double2* S, const fv::SLayout& lay, int B, int m_lo,
-                   int m_hi, cudaStream_t s) {
+                   int m_hi, cudaStream_t s, const ScalarIO* sio = nullptr) {
   const int Lt = p->Lt;
   const int mc = m_hi - m_lo;
   for (int b0 = 0; b0 < B;) {
@@ -1281,7 +1306,15 @@ int adjoint_orders(fvPlan* p, const double* a, const double* b, double2* S, cons
     const int ng = std::max(1, std::min((B - b0) / 4, p->ngroups_buf));
     const int nf = ng > 1 ? 4 : std::min(4, B - b0);
     const int NT = ntiles_for(nf);
-    for (int g = 0; g < ng; ++g) {
+    for (int g = 0; g < ng && sio; ++g) {  // scalar mode: pack the coefficients instead of coupling them
+      StageMark mk(p, 3, s);
+      fv::ScalarPackArgs sa{sio->in, sio->lmax, sio->B, b0 + 4 * g, nf, p->G + (size_t)g * p->g_gstride, p->gofs,
+                            nullptr, p->dg, p->dgofs, Lt, NT, 0, m_lo};
+      dim3 grid((Lt + 1 - m_lo + fv::ADJ_LC - 1) / fv::ADJ_LC * fv::ADJ_LC / 32, mc);
+      fv::scalar_pack_kernel<<<grid, 32, 0, s>>>(sa);
+      FV_CUDA(cudaGetLastError());
+    }
+    for (int g = 0; g < ng && !sio; ++g) {
       StageMark mk(p, 3, s);
       fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), p->dg, p->dgofs,
                        p->cgt, p->G + (size_t)g * p->g_gstride, p->gofs, nullptr, p->L, NT, B, b0 + 4 * g, nf, m_lo,
@@ -1339,25 +1372,98 @@ int ring_ffts(fvPlan* p, bool inverse, const double2* in, long long in_cs, long 
 
 }  // namespace
 
-int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, void* stream) {
-  FV_TRY(check_grid_call(p, B, T, a, b));
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+namespace {
+int forward_grid_impl(fvPlan* p, const double2* T, double* a, double* b, int B, cudaStream_t s,
+                      const ScalarIO* sio = nullptr) {
   const long long n = p->n_phi;
   if ((p->fft2 || p->smallp) && p->fused_fold)
-    return forward_orders(p, nullptr, p->lay_f, a, b, B, 0, p->Lt + 1, 0, p->L + 1, s,
-                          reinterpret_cast<const double2*>(T));
-  FV_TRY(ring_ffts(p, false, reinterpret_cast<const double2*>(T), 1, 3 * n, 3, p->Sf, p->lay_f.cs, p->lay_f.rs,
-                   p->lay_f.bs, B * p->n_theta, s));
-  return forward_orders(p, p->Sf, p->lay_f, a, b, B, 0, p->Lt + 1, 0, p->L + 1, s);
+    return forward_orders(p, nullptr, p->lay_f, a, b, B, 0, p->Lt + 1, 0, p->L + 1, s, T, sio);
+  FV_TRY(ring_ffts(p, false, T, 1, 3 * n, 3, p->Sf, p->lay_f.cs, p->lay_f.rs, p->lay_f.bs, B * p->n_theta, s));
+  return forward_orders(p, p->Sf, p->lay_f, a, b, B, 0, p->Lt + 1, 0, p->L + 1, s, nullptr, sio);
+}
+
+int adjoint_grid_impl(fvPlan* p, const double* a, const double* b, double2* T, int B, cudaStream_t s,
+                      const ScalarIO* sio = nullptr) {
+  FV_TRY(adjoint_orders(p, a, b, p->Sa, p->lay_a, B, 0, p->Lt + 1, s, sio));
+  const long long n = p->n_phi;
+  return ring_ffts(p, true, p->Sa, p->lay_a.cs, p->lay_a.rs, p->lay_a.bs, T, 1, 3 * n, 3, B * p->n_theta, s,
+                   p->lay_a.rblk);
+}
+
+// pseudo-field scratch for B scalar fields of n points: ceil(B / 3) x n x 3
+int scalar_scratch(fvPlan* p, int B, long long n) {
+  const size_t need = (size_t)((B + 2) / 3) * n * 3 * 2;  // doubles
+  if (p->Tp_cap >= need) return FV_OK;
+  if (p->Tp) {
+    FV_CUDA(cudaDeviceSynchronize());
+    cudaFree(p->Tp);
+    p->Tp = nullptr;
+    p->Tp_cap = 0;
+  }
+  FV_TRY(dalloc(&p->Tp, need));
+  p->Tp_cap = need;
+  return FV_OK;
+}
+
+int check_scalar_call(fvPlan* p, int B, int lmax, const void* x, const void* y) {
+  if (B < 1 || B > 3 * p->max_batch)
+    return fail(FV_EINVAL, "scalar batch " + std::to_string(B) + " outside 1.." + std::to_string(3 * p->max_batch));
+  if (lmax < 0) return fail(FV_EINVAL, "lmax must be non-negative, got " + std::to_string(lmax));
+  if (lmax > p->Lt)
+    return fail(FV_EINVAL, "scalar degree " + std::to_string(lmax) + " exceeds the plan's " + std::to_string(p->Lt));
+  if (!x || !y) return fail(FV_EINVAL, "null data pointer");
+  return FV_OK;
+}
+
+unsigned grid_for(long long n) { return (unsigned)std::min<long long>((n + 255) / 256, 148LL * 16); }
+}  // namespace
+
+int fv_forward_grid(fvPlan* p, const double* T, double* a, double* b, int B, void* stream) {
+  FV_TRY(check_grid_call(p, B, T, a, b));
+  return forward_grid_impl(p, reinterpret_cast<const double2*>(T), a, b, B, reinterpret_cast<cudaStream_t>(stream));
 }
 
 int fv_adjoint_grid(fvPlan* p, const double* a, const double* b, double* T, int B, void* stream) {
   FV_TRY(check_grid_call(p, B, T, a, b));
+  return adjoint_grid_impl(p, a, b, reinterpret_cast<double2*>(T), B, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int fv_forward_scalar_grid(fvPlan* p, const double* f, double* out, int lmax, int B, void* stream) {
+  FV_TRY(begin_call(p));
+  if (p->kind != 0) return fail(FV_EINVAL, "fast-scalar path requires a rule with tensor-grid structure");
+  FV_TRY(check_scalar_call(p, B, lmax, f, out));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  FV_TRY(adjoint_orders(p, a, b, p->Sa, p->lay_a, B, 0, p->Lt + 1, s));
-  const long long n = p->n_phi;
-  return ring_ffts(p, true, p->Sa, p->lay_a.cs, p->lay_a.rs, p->lay_a.bs, reinterpret_cast<double2*>(T), 1, 3 * n, 3,
-                   B * p->n_theta, s, p->lay_a.rblk);
+  const long long n = (long long)p->n_theta * p->n_phi;
+  FV_TRY(scalar_scratch(p, B, n));
+  const int K = (B + 2) / 3;
+  const long long tot = (long long)K * n * 3;
+  fv::scalar_to_pseudo_kernel<<<grid_for(tot), 256, 0, s>>>(reinterpret_cast<const double2*>(f), n, B,
+                                                            reinterpret_cast<double2*>(p->Tp), tot);
+  FV_CUDA(cudaGetLastError());
+  ScalarIO io;
+  io.out = reinterpret_cast<double2*>(out);
+  io.lmax = lmax;
+  io.B = B;
+  return forward_grid_impl(p, reinterpret_cast<const double2*>(p->Tp), nullptr, nullptr, K, s, &io);
+}
+
+int fv_adjoint_scalar_grid(fvPlan* p, const double* g, double* f, int lmax, int B, void* stream) {
+  FV_TRY(begin_call(p));
+  if (p->kind != 0) return fail(FV_EINVAL, "fast-scalar path requires a rule with tensor-grid structure");
+  FV_TRY(check_scalar_call(p, B, lmax, g, f));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const long long n = (long long)p->n_theta * p->n_phi;
+  FV_TRY(scalar_scratch(p, B, n));
+  const int K = (B + 2) / 3;
+  ScalarIO io;
+  io.in = reinterpret_cast<const double2*>(g);
+  io.lmax = lmax;
+  io.B = B;
+  FV_TRY(adjoint_grid_impl(p, nullptr, nullptr, reinterpret_cast<double2*>(p->Tp), K, s, &io));
+  fv::pseudo_to_scalar_kernel<<<grid_for((long long)B * n), 256, 0, s>>>(reinterpret_cast<const double2*>(p->Tp), n,
+                                                                         B, reinterpret_cast<double2*>(f));
+  FV_CUDA(cudaGetLastError());
+  return FV_OK;
 }
 
 // ---- order-sharded building blocks (paper_1908_00041_b200/dist.py) ----
@@ -1406,6 +1512,11 @@ int fv_adjoint_orders(fvPlan* p, const double* a, const double* b, int B, int m_
                         reinterpret_cast<cudaStream_t>(stream));
 }
 
+namespace {
+int adjoint_points_impl(fvPlan* p, const double* xyz, long long M, const double* a, const double* b, double* T, int B,
+                        cudaStream_t s, const ScalarIO* sio = nullptr);
+}  // namespace
+
 int fv_adjoint_points(fvPlan* p, const double* xyz, long long M, const double* a, const double* b, double* T,
                       int B, void* stream) {
   FV_TRY(begin_call(p));
@@ -1415,11 +1526,23 @@ int fv_adjoint_points(fvPlan* p, const double* xyz, long long M, const double* a
   if (M < 0) return fail(FV_EINVAL, "negative point count");
   if (M == 0) return FV_OK;
   if (!xyz || !T || !a || !b) return fail(FV_EINVAL, "null data pointer");
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  return adjoint_points_impl(p, xyz, M, a, b, T, B, reinterpret_cast<cudaStream_t>(stream));
+}
+
+namespace {
+int adjoint_points_impl(fvPlan* p, const double* xyz, long long M, const double* a, const double* b, double* T, int B,
+                        cudaStream_t s, const ScalarIO* sio) {
   const int Lt = p->Lt;
   for (int b0 = 0; b0 < B; b0 += 4) {
     const int nf = std::min(4, B - b0);
-    {
+    if (sio) {  // scalar mode: the coefficients packed into the merged rows
+      StageMark mk(p, 3, s);
+      fv::ScalarPackArgs sa{sio->in, sio->lmax, sio->B, b0, nf, p->G, nullptr, p->rowofs, nullptr, nullptr,
+                            Lt, 0, 1, 0};
+      dim3 grid((Lt + 1 + 127) / 128, Lt + 1);
+      fv::scalar_pack_kernel<<<grid, 128, 0, s>>>(sa);
+      FV_CUDA(cudaGetLastError());
+    } else {
       StageMark mk(p, 3, s);
       fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), nullptr, nullptr,
                        p->cgt, p->G, nullptr, p->rowofs, p->L, 0, B, b0, nf, 0, 1};
@@ -1475,6 +1598,7 @@ int fv_adjoint_points(fvPlan* p, const double* xyz, long long M, const double* a
   }
   return FV_OK;
 }
+}  // namespace
 
 }  // extern "C"
 
@@ -1536,6 +1660,11 @@ int launch_fpts(fvPlan* p, const fv::FptsArgs& fa, unsigned grid, cudaStream_t s
 
 }  // namespace
 
+namespace {
+int forward_points_impl(fvPlan* p, const double* xyz, const double* w, long long M, const double* T, double* a,
+                        double* b, int B, cudaStream_t s, const ScalarIO* sio);
+}  // namespace
+
 extern "C" int fv_forward_points(fvPlan* p, const double* xyz, const double* w, long long M, const double* T,
                                  double* a, double* b, int B, void* stream) {
   FV_TRY(begin_call(p));
@@ -1551,6 +1680,12 @@ extern "C" int fv_forward_points(fvPlan* p, const double* xyz, const double* w, 
     FV_CUDA(cudaMemsetAsync(b, 0, (size_t)B * K * 16, s));
     return FV_OK;
   }
+  return forward_points_impl(p, xyz, w, M, T, a, b, B, s, nullptr);
+}
+
+namespace {
+int forward_points_impl(fvPlan* p, const double* xyz, const double* w, long long M, const double* T, double* a,
+                        double* b, int B, cudaStream_t s, const ScalarIO* sio) {
   const int Lt = p->Lt;
   if (fv::fpd_smem_bytes(1, Lt) > 227 * 1024)
     return fail(FV_EINVAL, "degree " + std::to_string(p->L) + " too large for the direct forward kernel");
@@ -1584,8 +1719,61 @@ extern "C" int fv_forward_points(fvPlan* p, const double* xyz, const double* w, 
           reinterpret_cast<const double2*>(p->Fpart), n2, R, reinterpret_cast<double2*>(p->F));
       FV_CUDA(cudaGetLastError());
     }
-    FV_TRY(cg_forward(p, a, b, B, b0, nf, NT, 0, p->L + 1, s));
+    if (sio) {
+      StageMark mk(p, 3, s);
+      FV_TRY(scalar_unpack(*sio, p->F, NT, b0, nf, Lt, s));
+    } else {
+      FV_TRY(cg_forward(p, a, b, B, b0, nf, NT, 0, p->L + 1, s));
+    }
   }
+  return FV_OK;
+}
+}  // namespace
+
+extern "C" int fv_forward_scalar_points(fvPlan* p, const double* xyz, const double* w, long long M, const double* f,
+                                        double* out, int lmax, int B, void* stream) {
+  FV_TRY(begin_call(p));
+  if (p->kind != 1) return fail(FV_EINVAL, "plan was not created for scattered points");
+  FV_TRY(check_scalar_call(p, B, lmax, out, out));
+  if (M < 0) return fail(FV_EINVAL, "negative point count");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (M == 0) {
+    FV_CUDA(cudaMemsetAsync(out, 0, (size_t)B * (lmax + 1) * (lmax + 1) * 16, s));
+    return FV_OK;
+  }
+  if (!xyz || !w || !f) return fail(FV_EINVAL, "null data pointer");
+  FV_TRY(scalar_scratch(p, B, M));
+  const int K = (B + 2) / 3;
+  const long long tot = (long long)K * M * 3;
+  fv::scalar_to_pseudo_kernel<<<grid_for(tot), 256, 0, s>>>(reinterpret_cast<const double2*>(f), M, B,
+                                                            reinterpret_cast<double2*>(p->Tp), tot);
+  FV_CUDA(cudaGetLastError());
+  ScalarIO io;
+  io.out = reinterpret_cast<double2*>(out);
+  io.lmax = lmax;
+  io.B = B;
+  return forward_points_impl(p, xyz, w, M, p->Tp, nullptr, nullptr, K, s, &io);
+}
+
+extern "C" int fv_adjoint_scalar_points(fvPlan* p, const double* xyz, long long M, const double* g, double* f,
+                                        int lmax, int B, void* stream) {
+  FV_TRY(begin_call(p));
+  if (p->kind != 1) return fail(FV_EINVAL, "plan was not created for scattered points");
+  FV_TRY(check_scalar_call(p, B, lmax, g, g));
+  if (M < 0) return fail(FV_EINVAL, "negative point count");
+  if (M == 0) return FV_OK;
+  if (!xyz || !f) return fail(FV_EINVAL, "null data pointer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  FV_TRY(scalar_scratch(p, B, M));
+  const int K = (B + 2) / 3;
+  ScalarIO io;
+  io.in = reinterpret_cast<const double2*>(g);
+  io.lmax = lmax;
+  io.B = B;
+  FV_TRY(adjoint_points_impl(p, xyz, M, nullptr, nullptr, p->Tp, K, s, &io));
+  fv::pseudo_to_scalar_kernel<<<grid_for((long long)B * M), 256, 0, s>>>(reinterpret_cast<const double2*>(p->Tp), M,
+                                                                         B, reinterpret_cast<double2*>(f));
+  FV_CUDA(cudaGetLastError());
   return FV_OK;
 }
 

@@ -138,6 +138,29 @@ class GridPlan:
                 self._h, a.data_ptr(), b.data_ptr(), T.data_ptr(), B, _stream_ptr(self.device)))
         return T
 
+    # scalar transforms of degree lmax <= self.lmax + 1 (favest/scalar.py:146-184)
+    def forward_scalar(self, f, lmax):
+        """f (B, N) complex128 -> (B, (lmax+1)**2) complex128 (forward_sht_fast)."""
+        torch = _torch()
+        B = int(f.shape[0]) if f.dim() == 2 else -1
+        f = _check_tensor(f, (B, self.n_points), "f", self.device)
+        out = torch.empty((B, (lmax + 1) ** 2), dtype=torch.complex128, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.fv_forward_scalar_grid(
+                self._h, f.data_ptr(), out.data_ptr(), int(lmax), B, _stream_ptr(self.device)))
+        return out
+
+    def adjoint_scalar(self, g, lmax):
+        """g (B, (lmax+1)**2) complex128 -> f (B, N) complex128 (adjoint_sht_fast)."""
+        torch = _torch()
+        B = int(g.shape[0]) if g.dim() == 2 else -1
+        g = _check_tensor(g, (B, (lmax + 1) ** 2), "g", self.device)
+        f = torch.empty((B, self.n_points), dtype=torch.complex128, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.fv_adjoint_scalar_grid(
+                self._h, g.data_ptr(), f.data_ptr(), int(lmax), B, _stream_ptr(self.device)))
+        return f
+
 
 class PointsPlan:
     """Adjoint and forward (direct-route) VSHT of vector degree ``lmax`` at
@@ -200,6 +223,37 @@ class PointsPlan:
                 self._h, xyz.data_ptr(), w.data_ptr(), M, T.data_ptr(), a.data_ptr(), b.data_ptr(), B,
                 _stream_ptr(self.device)))
         return a, b
+
+    def forward_scalar(self, xyz, w, f, lmax):
+        """Direct scalar forward (forward_sht_direct, favest/scalar.py:94-112): xyz (M, 3)
+        float64, w (M,) float64, f (B, M) complex128 -> (B, (lmax+1)**2) complex128."""
+        torch = _torch()
+        xyz = self._points(xyz)
+        M = int(xyz.shape[0])
+        if not isinstance(w, torch.Tensor) or w.dtype != torch.float64 or tuple(w.shape) != (M,):
+            raise ValueError(f"w must be a ({M},) float64 tensor")
+        B = int(f.shape[0]) if f.dim() == 2 else -1
+        f = _check_tensor(f, (B, M), "f", self.device)
+        out = torch.empty((B, (lmax + 1) ** 2), dtype=torch.complex128, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.fv_forward_scalar_points(
+                self._h, xyz.data_ptr(), w.contiguous().data_ptr(), M, f.data_ptr(), out.data_ptr(), int(lmax), B,
+                _stream_ptr(self.device)))
+        return out
+
+    def adjoint_scalar(self, xyz, g, lmax):
+        """Direct scalar synthesis (adjoint_sht_direct, favest/scalar.py:115-128):
+        xyz (M, 3) float64, g (B, (lmax+1)**2) complex128 -> (B, M) complex128."""
+        torch = _torch()
+        xyz = self._points(xyz)
+        M = int(xyz.shape[0])
+        B = int(g.shape[0]) if g.dim() == 2 else -1
+        g = _check_tensor(g, (B, (lmax + 1) ** 2), "g", self.device)
+        f = torch.empty((B, M), dtype=torch.complex128, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.check(self.lib.fv_adjoint_scalar_points(
+                self._h, xyz.data_ptr(), M, g.data_ptr(), f.data_ptr(), int(lmax), B, _stream_ptr(self.device)))
+        return f
 
     def adjoint(self, xyz, a, b, T=None):
         """xyz (M, 3) float64, (a, b) (B, K) complex128 -> T (B, M, 3) complex128."""

@@ -127,6 +127,73 @@ def main():
             lmax=lmax, points=rule.points, weights=rule.weights, T=vals,
             fa=F.div.values, fb=F.curl.values,
         )
+    # 6. scalar transforms (favest/scalar.py:108-184) and rule certification
+    #    (favest/quadrature.py:51-76).  ScalarCoefficients holds one column
+    #    (favest/core.py:104-112), so the public calls take one field each;
+    #    f2's three columns are transformed one by one (the plan-level batch
+    #    is checked against them).
+    from favest.scalar import TensorGrid, adjoint_sht_direct, adjoint_sht_fast, forward_sht_direct, forward_sht_fast
+    from favest.quadrature import verify_exactness
+
+    def scoef(rng, lmax, c=None):
+        K = (lmax + 1) ** 2
+        shape = (K,) if c is None else (K, c)
+        ls, _ = degrees_orders(lmax)
+        scale = (1.0 + ls.astype(np.float64)) ** -1.5
+        if c is not None:
+            scale = scale[:, None]
+        return (rng.standard_normal(shape) + 1j * rng.standard_normal(shape)) * scale
+
+    rng = np.random.default_rng(2024)
+    for lmax, t in ((20, 41), (37, 80)):
+        grid, rule = gen_gl_tensor(t)
+        g = scoef(rng, lmax)
+        f = adjoint_sht_fast(ScalarCoefficients(lmax, g), grid)
+        f2 = np.stack([f + 1e-3 * (rng.standard_normal(f.shape) + 1j * rng.standard_normal(f.shape)),
+                       rng.standard_normal(f.shape) + 0j, f.conj()], axis=1)
+        F = np.stack([forward_sht_fast(f2[:, c], grid, lmax).values for c in range(3)], axis=1)
+        np.savez_compressed(
+            os.path.join(HERE, f"scalar_fast_l{lmax}.npz"),
+            lmax=lmax, thetas=grid.ring_thetas, weights=grid.ring_weights, n_phi=grid.n_phi,
+            g=g, f=f, f2=f2, F=F,
+        )
+    # tiny rings: n_phi = 3 with lmax = 1, n_phi = 1 with lmax = 0
+    for lmax, n_phi in ((1, 3), (0, 1)):
+        grid = TensorGrid(ring_thetas=np.array([0.4, 1.3, 2.2]), ring_weights=np.array([0.7, 1.9, 0.8]) / n_phi,
+                          n_phi=n_phi)
+        g = scoef(rng, lmax)
+        f = adjoint_sht_fast(ScalarCoefficients(lmax, g), grid)
+        fr = rng.standard_normal(f.shape) + 1j * rng.standard_normal(f.shape)
+        F = forward_sht_fast(fr, grid, lmax).values
+        np.savez_compressed(
+            os.path.join(HERE, f"scalar_fast_l{lmax}_nphi{n_phi}.npz"),
+            lmax=lmax, thetas=grid.ring_thetas, weights=grid.ring_weights, n_phi=n_phi, g=g, f=f, fr=fr, F=F,
+        )
+    rng = np.random.default_rng(4001)
+    M, lmax = 400, 16
+    v = rng.standard_normal((M, 3))
+    pts = v / np.linalg.norm(v, axis=1, keepdims=True)
+    w = rng.uniform(0.5, 1.5, M)
+    w *= 4.0 * np.pi / w.sum()
+    rule = QuadratureRule(points=pts, weights=w, exactness=0)
+    fr = rng.standard_normal(M) + 1j * rng.standard_normal(M)
+    F = forward_sht_direct(fr, rule, lmax).values
+    g = scoef(rng, lmax)
+    f = adjoint_sht_direct(ScalarCoefficients(lmax, g), pts)
+    np.savez_compressed(os.path.join(HERE, "scalar_direct_l16_m400.npz"),
+                        lmax=lmax, points=pts, weights=w, fr=fr, F=F, g=g, f=f)
+    ico = bundled_design("icosahedron12")
+    _, glr = gen_gl_tensor(30)
+    rows = []
+    for name, r, t in (("ico", ico, 5), ("ico", ico, 6), ("ico", ico, 0), ("gl30", glr, 30), ("gl30", glr, 31),
+                       ("custom", rule, 4)):
+        d, ok = verify_exactness(r, t)
+        rows.append((name, t, d, ok))
+    np.savez_compressed(os.path.join(HERE, "exactness.npz"),
+                        names=np.array([r[0] for r in rows]), t=np.array([r[1] for r in rows]),
+                        defect=np.array([r[2] for r in rows]), passed=np.array([r[3] for r in rows]),
+                        ico_points=ico.points, ico_weights=ico.weights, gl30_points=glr.points,
+                        gl30_weights=glr.weights, custom_points=pts, custom_weights=w)
     print("reference favest", getattr(favest, "__version__", "?"), "numpy", np.__version__)
 
 

@@ -125,3 +125,35 @@ def test_direct_forward_matches_grid_forward():
     pts = O.grid_points(th, nphi)
     fa, fb = O.vsht_forward_points(g["Tn"], np.repeat(w, nphi), pts, L)
     assert O.rel_l2(np.concatenate([fa, fb]), np.concatenate([g["fna"], g["fnb"]])) <= 1e-13
+
+
+@pytest.mark.parametrize("name", ["scalar_fast_l20", "scalar_fast_l37", "scalar_fast_l1_nphi3", "scalar_fast_l0_nphi1"])
+def test_scalar_grid_against_reference(golden, name):
+    # forward_sht_fast / adjoint_sht_fast (favest/scalar.py:157-184)
+    g = golden(name)
+    L, th, w, nphi = int(g["lmax"]), g["thetas"], g["weights"], int(g["n_phi"])
+    f = O.sht_adjoint_grid(g["g"][:, None], L, th, nphi)[:, 0]
+    assert O.rel_l2(f, g["f"]) <= 1e-13
+    fin = g["f2"] if "f2" in g else g["fr"][:, None]
+    F = O.sht_forward_grid(fin, th, w, nphi, L)
+    assert O.rel_l2(F, g["F"].reshape(F.shape)) <= 1e-13
+
+
+def test_scalar_direct_against_reference(golden):
+    # forward_sht_direct / adjoint_sht_direct (favest/scalar.py:108-128)
+    g = golden("scalar_direct_l16_m400")
+    L = int(g["lmax"])
+    F = O.sht_forward_points(g["fr"][:, None], g["weights"], g["points"], L)[:, 0]
+    assert O.rel_l2(F, g["F"]) <= 1e-13
+    f = O.sht_adjoint_points(g["g"][:, None], L, g["points"])[:, 0]
+    assert O.rel_l2(f, g["f"]) <= 1e-13
+
+
+def test_verify_exactness_against_reference(golden):
+    # favest/quadrature.py:51-76 on the icosahedron design (exact to 5), a GL
+    # tensor rule (exact to 30) and a random rule, each just below and above
+    g = golden("exactness")
+    for name, t, d, ok in zip(g["names"], g["t"], g["defect"], g["passed"]):
+        dd, okk = O.verify_exactness(g[f"{name}_points"], g[f"{name}_weights"], int(t))
+        assert okk == bool(ok)
+        assert abs(dd - d) <= 1e-13 + 1e-12 * d
