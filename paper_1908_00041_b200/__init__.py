@@ -18,6 +18,8 @@ from .grid import TensorGrid, gen_gl_tensor, gl_grid_for
 from .transforms import PATHS, adjoint_favest, forward_favest, grid_plan, points_plan
 from .pipeline import HostPipeline
 from .scalar import adjoint_sht_direct, adjoint_sht_fast, forward_sht_direct, forward_sht_fast, verify_exactness
+from .quadrature import bundled_design, load_design
+from . import io
 
 __version__ = "0.1.0"
 
@@ -26,4 +28,5 @@ __all__ = [
     "degrees_orders", "flat_index", "flat_size", "TensorGrid", "gen_gl_tensor", "gl_grid_for",
     "PATHS", "adjoint_favest", "forward_favest", "grid_plan", "points_plan", "HostPipeline",
     "forward_sht_fast", "adjoint_sht_fast", "forward_sht_direct", "adjoint_sht_direct", "verify_exactness",
+    "bundled_design", "load_design", "io",
 ]

@@ -11,7 +11,7 @@ import os
 
 from .build import LIBPATH
 
-FV_OK, FV_EINVAL, FV_ECUDA, FV_ENCCL, FV_ENOMEM = 0, 1, 2, 3, 4
+FV_OK, FV_EINVAL, FV_ECUDA, FV_ENCCL, FV_ENOMEM, FV_ETYPE = 0, 1, 2, 3, 4, 6
 
 #: every symbol include/favest_b200.h declares
 EXPORTED = (
@@ -20,6 +20,12 @@ EXPORTED = (
     "fv_adjoint_points", "fv_forward_points", "fv_set_profiling", "fv_stage_ms", "fv_stage_count",
     "fv_ring_fft", "fv_forward_orders", "fv_adjoint_orders",
     "fv_forward_scalar_grid", "fv_adjoint_scalar_grid", "fv_forward_scalar_points", "fv_adjoint_scalar_points",
+)
+
+#: every symbol include/favest_io.h declares (host-only file codecs)
+EXPORTED_IO = (
+    "fv_io_free", "fv_io_format_table", "fv_io_format_coefficients", "fv_io_parse_columns",
+    "fv_io_parse_coefficients",
 )
 
 _lib = None
@@ -61,6 +67,11 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "fv_adjoint_scalar_grid": (i, [vp, vp, vp, i, i, vp]),
         "fv_forward_scalar_points": (i, [vp, vp, vp, ll, vp, vp, i, i, vp]),
         "fv_adjoint_scalar_points": (i, [vp, vp, ll, vp, vp, i, i, vp]),
+        "fv_io_free": (None, [vp]),
+        "fv_io_format_table": (i, [vp, ll, i, i, i, ctypes.POINTER(vp), ctypes.POINTER(ll)]),
+        "fv_io_format_coefficients": (i, [i, vp, vp, ctypes.POINTER(vp), ctypes.POINTER(ll)]),
+        "fv_io_parse_columns": (i, [ctypes.c_char_p, ll, i, ctypes.POINTER(vp), ctypes.POINTER(ll), ip]),
+        "fv_io_parse_coefficients": (i, [ctypes.c_char_p, ll, ip, ctypes.POINTER(vp), ctypes.POINTER(vp)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -71,13 +82,18 @@ def load(path: str | None = None) -> ctypes.CDLL:
     return lib
 
 
-def check(rc: int) -> None:
-    """Map a C status code to the reference's exception types."""
+def check(rc: int, path=None) -> None:
+    """Map a C status code to the reference's exception types ("{path}" in a
+    file codec's message becomes the file name)."""
     if rc == FV_OK:
         return
     msg = load().fv_last_error().decode() or f"favest_b200 error {rc}"
+    if path is not None:
+        msg = msg.replace("{path}", str(path))
     if rc == FV_EINVAL:
         raise ValueError(msg)
+    if rc == FV_ETYPE:
+        raise TypeError(msg)
     if rc == FV_ENOMEM:
         raise MemoryError(msg)
     raise RuntimeError(msg)

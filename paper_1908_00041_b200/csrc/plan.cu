@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/favest_b200.h"
+#include "../../include/favest_io.h"
 #include "aux_kernels.cuh"
 #include "fft.cuh"
 #include "fft2.cuh"
@@ -1777,4 +1778,4 @@ extern "C" int fv_adjoint_scalar_points(fvPlan* p, const double* xyz, long long 
   return FV_OK;
 }
 
-
+#include "fileio.cuh"

@@ -194,6 +194,102 @@ def main():
                         defect=np.array([r[2] for r in rows]), passed=np.array([r[3] for r in rows]),
                         ico_points=ico.points, ico_weights=ico.weights, gl30_points=glr.points,
                         gl30_weights=glr.weights, custom_points=pts, custom_weights=w)
+    # 7. file formats (favest/io.py, favest/quadrature.py:79-139): files the
+    #    reference writers produce, and malformed inputs with the exception
+    #    type and message the reference readers raise ("{path}" for the name)
+    import json
+    import tempfile
+
+    from favest import io as rio
+    from favest.quadrature import load_design
+
+    iodir = os.path.join(HERE, "io")
+    os.makedirs(iodir, exist_ok=True)
+    rng = np.random.default_rng(7007)
+    L = 12
+    a, b = coef(rng, L, "inv")
+    b[3] = 1e16 + 0.5j
+    b[4] = complex(-0.0, 5e-324)
+    b[5] = complex(1.7976931348623157e308, -2.2250738585072014e-308)
+    rio.write_coefficients(os.path.join(iodir, "coef_l12.json"), vc(a, b, L))
+    grid, rule = gen_gl_tensor(13)
+    rio.write_rule_file(os.path.join(iodir, "gl13.rule"), rule)
+    vals = tangent(rng, rule.points)
+    rio.write_samples(os.path.join(iodir, "samples_gl13.csv"), TangentFieldSamples(rule.points, vals))
+    rio.write_csv(os.path.join(iodir, "table.csv"), ("l", "err", "name"),
+                  [(1, 0.1, "x"), (2, 1e-300, "y")])
+    rio.write_csv(os.path.join(iodir, "table_f.csv"), ("x", "y"), [(0.1, 2.5), (1e-300, -3.0)])
+    np.savez_compressed(os.path.join(iodir, "values.npz"), a=a, b=b, points=rule.points,
+                        weights=rule.weights, vals=vals)
+
+    good_pair = "[[0, 0], [1, 2], [3, 4], [5, 6]]"
+    cases = [
+        ("coef", "not json", "{"),
+        ("coef", "extra data", '{"L_max": 1, "a": [], "b": []} x'),
+        ("coef", "missing b", '{"L_max": 1, "a": ' + good_pair + "}"),
+        ("coef", "top list", "[1, 2]"),
+        ("coef", "wrong len", '{"L_max": 1, "a": [[0, 0]], "b": ' + good_pair + "}"),
+        ("coef", "lmax float", '{"L_max": 1.9, "a": ' + good_pair + ', "b": ' + good_pair + "}"),
+        ("coef", "lmax string", '{"L_max": "1", "a": ' + good_pair + ', "b": ' + good_pair + "}"),
+        ("coef", "lmax bad string", '{"L_max": "x", "a": [], "b": []}'),
+        ("coef", "lmax negative", '{"L_max": -2, "a": [], "b": []}'),
+        ("coef", "string values", '{"L_max": 1, "a": [[0, 0], ["1_0.5", " -2e3 "], [0, 0], [0, 0]], '
+                              '"b": [[0, 0], ["inf", "-NaN"], [" +.5", "5."], ["1E-2", "-Infinity"]]}'),
+        ("coef", "bad string value", '{"L_max": 0, "a": [["1..5", 0]], "b": [[0, 0]]}'),
+        ("coef", "null value", '{"L_max": 0, "a": [[null, 0]], "b": [[0, 0]]}'),
+        ("coef", "triple", '{"L_max": 0, "a": [[1, 2, 3]], "b": [[0, 0]]}'),
+        ("coef", "single", '{"L_max": 0, "a": [[1]], "b": [[0, 0]]}'),
+        ("coef", "number pair", '{"L_max": 0, "a": [5], "b": [[0, 0]]}'),
+        ("coef", "json literals", '{"L_max": 1, "a": [[0, 0], [NaN, Infinity], [0, 0], [0, 0]], '
+                              '"b": [[0, 0], [-Infinity, true], [false, 0], [0, 0]]}'),
+        ("coef", "duplicate key", '{"L_max": 3, "L_max": 1, "a": [[1, 2]], "b": ' + good_pair
+         + ', "a": ' + good_pair.replace("1", "7") + "}"),
+        ("coef", "python nan", '{"L_max": 0, "a": [[nan, 0]], "b": [[0, 0]]}'),
+        ("coef", "big ints", '{"L_max": 1, "a": [[0, 0], [12345678901234567890123, -0], [0, 0], [0, 0]], '
+                         '"b": [[0, 0], [1e400, 1e-400], [-0.0, 4.9e-324], [0, 0]]}'),
+        ("rule", "ragged", "0 0 1 1\n1 0 0\n"),
+        ("rule", "two cols", "0 0\n1 0\n"),
+        ("rule", "bad float", "0 0 1\n1 0 x\n"),
+        ("rule", "empty", "# nothing\n\n"),
+        ("rule", "off sphere", "0 0 1.1\n1 0 0\n"),
+        ("rule", "commas and crlf", "# c\r\n0, 0, 1 # x\r\n1,0,0\r\n0 1 0\r0 0 -1\n1e0 0 0\n0 -1 0\n"),
+        ("rule", "underscores", "0 0 1_0\n1 0 0\n"),
+        ("samples", "seven cols", "theta,phi,a,b,c,d,e,f\n1,2,3,4,5,6,7\n"),
+        ("samples", "bad float", "1,2,3,4,5,6,7,zz\n"),
+        ("samples", "empty", "theta,phi,t1_re,t1_im,t2_re,t2_im,t3_re,t3_im\n"),
+        ("samples", "comments quoted", '# hi\n"1.0",2,3,4,5,6,7,8\n\n 0.5 ,1,0,0,0,0,0,0\r\n'),
+        ("samples", "header later", "1,2,3,4,5,6,7,8\ntheta,phi,a,b,c,d,e,f\n"),
+    ]
+    results = []
+    tmpd = tempfile.mkdtemp()
+    for kind, name, text in cases:
+        path = os.path.join(tmpd, "case.txt")
+        with open(path, "w", newline="") as fh:
+            fh.write(text)
+        try:
+            if kind == "coef":
+                c = rio.read_coefficients(path)
+                out = {"ok": True, "lmax": c.lmax,
+                       "a": [[float(v.real), float(v.imag)] for v in c.div.values],
+                       "b": [[float(v.real), float(v.imag)] for v in c.curl.values]}
+            elif kind == "rule":
+                r = rio.read_rule_file(path, 1)
+                out = {"ok": True, "points": r.points.tolist(), "weights": r.weights.tolist(), "kind": r.kind}
+            else:
+                s = rio.read_samples(path)
+                out = {"ok": True, "points": s.points.tolist(),
+                       "values": [[[float(v.real), float(v.imag)] for v in row] for row in s.values]}
+        except Exception as exc:  # noqa: BLE001 - the fixture records the reference's exception
+            out = {"ok": False, "type": type(exc).__name__, "msg": str(exc).replace(path, "{path}")}
+        results.append({"kind": kind, "name": name, "text": text, "out": out})
+    design = os.path.join(tmpd, "design.txt")
+    with open(design, "w") as fh:
+        fh.write("# octahedron\n1 0 0\n-1 0 0\n0 1 0\n0 -1 0\n0 0 1\n0 0 -1.0000000001\n")
+    d = load_design(design, 3)
+    results.append({"kind": "design", "name": "octahedron", "text": open(design).read(),
+                    "out": {"ok": True, "points": d.points.tolist(), "weights": d.weights.tolist(), "kind": d.kind}})
+    with open(os.path.join(iodir, "cases.json"), "w") as fh:
+        json.dump(results, fh, indent=1, allow_nan=True)
     print("reference favest", getattr(favest, "__version__", "?"), "numpy", np.__version__)
 
 

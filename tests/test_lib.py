@@ -13,10 +13,11 @@ import pytest
 from paper_1908_00041_b200 import _lib, build
 
 HEADER = os.path.join(build.ROOT, "include", "favest_b200.h")
+HEADER_IO = os.path.join(build.ROOT, "include", "favest_io.h")
 
 
-def header_symbols():
-    txt = open(HEADER).read()
+def header_symbols(path=HEADER):
+    txt = open(path).read()
     return sorted(set(re.findall(r"\b(fv_[a-z_]+)\s*\(", txt)))
 
 
@@ -29,8 +30,9 @@ def test_library_built_and_loads():
 
 def test_exports_every_header_symbol():
     lib = _lib.load()
-    syms = header_symbols()
-    assert set(syms) == set(_lib.EXPORTED)
+    assert set(header_symbols(HEADER_IO)) == set(_lib.EXPORTED_IO)
+    syms = header_symbols() + header_symbols(HEADER_IO)
+    assert set(syms) == set(_lib.EXPORTED) | set(_lib.EXPORTED_IO)
     for s in syms:
         assert hasattr(lib, s), s
     nm = subprocess.run(["nm", "-D", "--defined-only", build.LIBPATH], capture_output=True, text=True).stdout
