@@ -17,7 +17,7 @@ from __future__ import annotations
 import numpy as np
 
 from .core import FOUR_PI, ScalarCoefficients, check_unit
-from .transforms import grid_plan, points_plan
+from .transforms import _to_host, grid_plan, points_plan
 
 
 def _plan_degree(lmax: int) -> int:
@@ -82,7 +82,7 @@ def adjoint_sht_fast(coeffs: ScalarCoefficients, grid) -> np.ndarray:
     import torch
 
     g = torch.from_numpy(np.ascontiguousarray(np.asarray(coeffs.values, dtype=np.complex128)[None]))
-    return plan.adjoint_scalar(g.to(plan.device), lmax)[0].cpu().numpy()
+    return _to_host(plan.adjoint_scalar(g.to(plan.device), lmax)[0])
 
 
 def forward_sht_direct(f, rule, lmax: int) -> ScalarCoefficients:
@@ -113,7 +113,7 @@ def adjoint_sht_direct(coeffs: ScalarCoefficients, points) -> np.ndarray:
     plan = points_plan(_plan_degree(lmax))
     xyz = torch.from_numpy(np.ascontiguousarray(pts)).to(plan.device)
     g = torch.from_numpy(np.ascontiguousarray(np.asarray(coeffs.values, dtype=np.complex128)[None]))
-    return plan.adjoint_scalar(xyz, g.to(plan.device), lmax)[0].cpu().numpy()
+    return _to_host(plan.adjoint_scalar(xyz, g.to(plan.device), lmax)[0])
 
 
 def verify_exactness(rule, t: int) -> tuple[float, bool]:
