@@ -266,52 +266,56 @@ inline bool ascii_only(const char* s, long long n) {
 
 }  // namespace fio
 
-// Column files.  mode 0: rule / design files (favest/quadrature.py:112-131):
-// '#' starts a comment, ',' is a separator, fields split on whitespace, every
-// data line has the first line's width.  mode 1: sample CSV (io.py:111-133):
-// csv records, '#' rows and the "theta" header skipped, 8 fields per row.
-extern "C" int fv_io_parse_columns(const char* text, long long n, int mode, double** data, long long* nrows,
-                                   int* ncols) {
-  if (!data || !nrows || !ncols || n < 0 || (n && !text)) return fail(FV_EINVAL, "invalid parse arguments");
-  *data = nullptr;
-  *nrows = 0;
-  *ncols = 0;
-  if (!fio::ascii_only(text, n)) return fail(FV_EINVAL, "{path}: non-ASCII content");
-  fio::Buf out;
-  long long rows = 0;
-  int width = -1;
-  fio::Lines ln{text, text + n};
+namespace fio {
+
+// One chunk of whole lines of a column file, parsed independently; the chunks'
+// results are stitched in file order (global line numbers, the first data
+// line's width, the first error).
+struct ColChunk {
+  Buf out;                   // doubles, rows x width
+  long long rows = 0, lines = 0;
+  int width = -1;            // width of the chunk's first data line
+  long long first_data = -1; // local line of the first data line
+  long long err_line = -1;   // local line of the first error
+  int err_kind = 0;          // 1 width mismatch (err_got), 2 float (err_text), 3 out of memory
+  long long err_got = 0;
+  std::string err_text;
+};
+
+inline void parse_chunk(const char* s0, const char* e0, int mode, bool file_start, ColChunk& r) {
+  Lines ln{s0, e0};
   const char *s, *t;
-  long long lineno = 0;
   std::vector<std::pair<const char*, long long>> fields;
-  auto bad = [&](const std::string& m) {
-    std::free(out.p);
-    return fail(FV_EINVAL, m);
-  };
+  std::vector<std::string> owned;
   while (ln.next(s, t)) {
-    ++lineno;
+    const long long lineno = ++r.lines;
     fields.clear();
+    owned.clear();
     if (mode == 0) {
       const char* h = static_cast<const char*>(std::memchr(s, '#', (size_t)(t - s)));
       const char* q = h ? h : t;
       const char* p = s;
       while (p < q) {
-        while (p < q && (fio::py_space((unsigned char)*p) || *p == ',')) ++p;
+        while (p < q && (py_space((unsigned char)*p) || *p == ',')) ++p;
         if (p >= q) break;
         const char* f = p;
-        while (p < q && !(fio::py_space((unsigned char)*p) || *p == ',')) ++p;
+        while (p < q && !(py_space((unsigned char)*p) || *p == ',')) ++p;
         fields.emplace_back(f, p - f);
       }
       if (fields.empty()) continue;
-      if (width < 0) width = (int)fields.size();
-      else if ((int)fields.size() != width)
-        return bad("{path}:" + std::to_string(lineno) + ": expected " + std::to_string(width) + " columns, got " +
-                   std::to_string(fields.size()));
+      if (r.width < 0) {
+        r.width = (int)fields.size();
+        r.first_data = lineno;
+      } else if ((int)fields.size() != r.width) {
+        r.err_line = lineno;
+        r.err_kind = 1;
+        r.err_got = (long long)fields.size();
+        return;
+      }
     } else {
       if (s == t) continue;  // csv yields [] for a blank line
       const char* p = s;
-      std::vector<std::string> owned;
-      while (true) {  // minimal csv field splitter with "..." quoting
+      while (true) {  // csv field splitter with "..." quoting
         if (p < t && *p == '"') {
           std::string v;
           ++p;
@@ -342,37 +346,126 @@ extern "C" int fv_io_parse_columns(const char* text, long long n, int mode, doub
           fd = {v.data(), (long long)v.size()};
         }
       const char* f0 = fields[0].first;
-      long long k0 = fields[0].second, i0 = 0;
-      while (i0 < k0 && fio::py_space((unsigned char)f0[i0])) ++i0;
-      if (i0 < k0 && f0[i0] == '#') continue;
-      if (lineno == 1) {
-        long long a = 0, b = k0;
-        while (a < b && fio::py_space((unsigned char)f0[a])) ++a;
-        while (b > a && fio::py_space((unsigned char)f0[b - 1])) --b;
-        if (fio::ieq(f0 + a, b - a, "theta")) continue;
+      const long long k0 = fields[0].second;
+      long long a = 0, b = k0;
+      while (a < b && py_space((unsigned char)f0[a])) ++a;
+      if (a < b && f0[a] == '#') continue;
+      if (file_start && lineno == 1) {
+        while (b > a && py_space((unsigned char)f0[b - 1])) --b;
+        if (ieq(f0 + a, b - a, "theta")) continue;
       }
-      if (fields.size() != 8)
-        return bad("{path}:" + std::to_string(lineno) + ": expected 8 columns, got " + std::to_string(fields.size()));
-      width = 8;
-      if (!out.reserve((rows + 1) * 8 * 8)) return bad("out of host memory");
-      double* d = reinterpret_cast<double*>(out.p) + rows * 8;
-      for (int c = 0; c < 8; ++c)
-        if (!fio::py_float(fields[c].first, fields[c].second, d[c]))
-          return bad("{path}:" + std::to_string(lineno) + ": " + fio::float_err(fields[c].first, fields[c].second));
-      ++rows;
-      continue;
+      if (fields.size() != 8) {
+        r.err_line = lineno;
+        r.err_kind = 1;
+        r.err_got = (long long)fields.size();
+        r.width = 8;
+        return;
+      }
+      if (r.width < 0) {
+        r.width = 8;
+        r.first_data = lineno;
+      }
     }
-    if (!out.reserve((rows + 1) * width * 8)) return bad("out of host memory");
-    double* d = reinterpret_cast<double*>(out.p) + rows * width;
-    for (int c = 0; c < width; ++c)
-      if (!fio::py_float(fields[c].first, fields[c].second, d[c]))
-        return bad("{path}:" + std::to_string(lineno) + ": " + fio::float_err(fields[c].first, fields[c].second));
-    ++rows;
+    if (!r.out.reserve((r.rows + 1) * r.width * 8)) {
+      r.err_line = lineno;
+      r.err_kind = 3;
+      return;
+    }
+    double* d = reinterpret_cast<double*>(r.out.p) + r.rows * r.width;
+    for (int c = 0; c < r.width; ++c)
+      if (!py_float(fields[c].first, fields[c].second, d[c])) {
+        r.err_line = lineno;
+        r.err_kind = 2;
+        r.err_text = float_err(fields[c].first, fields[c].second);
+        return;
+      }
+    ++r.rows;
   }
-  if (rows == 0) return bad(mode == 0 ? "no data rows in {path}" : "{path}: no sample rows");
-  *data = reinterpret_cast<double*>(out.p);
+}
+
+}  // namespace fio
+
+// Column files.  mode 0: rule / design files (favest/quadrature.py:112-131):
+// '#' starts a comment, ',' is a separator, fields split on whitespace, every
+// data line has the first line's width.  mode 1: sample CSV (io.py:111-133):
+// csv records, '#' rows and the "theta" header skipped, 8 fields per row.
+// The text is cut at line boundaries into one chunk per host thread.
+extern "C" int fv_io_parse_columns(const char* text, long long n, int mode, double** data, long long* nrows,
+                                   int* ncols) {
+  if (!data || !nrows || !ncols || n < 0 || (n && !text)) return fail(FV_EINVAL, "invalid parse arguments");
+  *data = nullptr;
+  *nrows = 0;
+  *ncols = 0;
+  if (!fio::ascii_only(text, n)) return fail(FV_EINVAL, "{path}: non-ASCII content");
+  const int T = fio::host_threads(n / 64);
+  std::vector<const char*> cut(T + 1);
+  cut[0] = text;
+  cut[T] = text + n;
+  for (int k = 1; k < T; ++k) {  // after the next line break at or past k n / T
+    const char* p = std::max(cut[k - 1], text + n * k / T);
+    while (p < text + n && *p != '\n' && *p != '\r') ++p;
+    if (p < text + n && *p == '\r') ++p;
+    if (p < text + n && *p == '\n') ++p;
+    cut[k] = p;
+  }
+  std::vector<fio::ColChunk> ch(T);
+  {
+    std::vector<std::thread> th;
+    for (int k = 1; k < T; ++k) th.emplace_back([&, k] { fio::parse_chunk(cut[k], cut[k + 1], mode, false, ch[k]); });
+    fio::parse_chunk(cut[0], cut[1], mode, true, ch[0]);
+    for (auto& x : th) x.join();
+  }
+  auto release = [&] {
+    for (auto& c : ch) std::free(c.out.p);
+  };
+  int W = -1;
+  long long before = 0, rows = 0;
+  for (int k = 0; k < T; ++k) {
+    fio::ColChunk& c = ch[k];
+    if (W < 0 && c.width >= 0) W = c.width;
+    std::string msg;
+    if (mode == 0 && c.first_data >= 0 && c.width != W) {
+      msg = "{path}:" + std::to_string(before + c.first_data) + ": expected " + std::to_string(W) + " columns, got " +
+            std::to_string(c.width);
+    } else if (c.err_kind == 1) {
+      msg = "{path}:" + std::to_string(before + c.err_line) + ": expected " + std::to_string(mode ? 8 : W) +
+            " columns, got " + std::to_string(c.err_got);
+    } else if (c.err_kind == 2) {
+      msg = "{path}:" + std::to_string(before + c.err_line) + ": " + c.err_text;
+    } else if (c.err_kind == 3) {
+      release();
+      return fail(FV_ENOMEM, "out of host memory parsing columns");
+    }
+    if (!msg.empty()) {
+      release();
+      return fail(FV_EINVAL, msg);
+    }
+    before += c.lines;
+    rows += c.rows;
+  }
+  if (rows == 0) {
+    release();
+    return fail(FV_EINVAL, mode == 0 ? "no data rows in {path}" : "{path}: no sample rows");
+  }
+  double* out = static_cast<double*>(std::malloc((size_t)rows * W * 8));
+  if (!out) {
+    release();
+    return fail(FV_ENOMEM, "out of host memory parsing columns");
+  }
+  {
+    std::vector<std::thread> th;
+    long long off = 0;
+    for (int k = 0; k < T; ++k) {
+      const long long nb = ch[k].rows * W * 8;
+      if (nb) th.emplace_back([&, k, off, nb] { std::memcpy(reinterpret_cast<char*>(out) + off, ch[k].out.p, (size_t)nb); });
+      off += nb;
+    }
+    for (auto& x : th) x.join();
+  }
+  release();
+  *data = out;
   *nrows = rows;
-  *ncols = width;
+  *ncols = W;
   return FV_OK;
 }
 

@@ -136,3 +136,55 @@ def test_missing_file_raises_oserror(tmp_path):
         fio.read_coefficients(tmp_path / "nope.json")
     with pytest.raises(FileNotFoundError):
         fio.read_samples(tmp_path / "nope.csv")
+
+
+def _py_read_columns(text):
+    """favest/quadrature.py:112-131 restated (test-local checker for large files)."""
+    rows, width = [], None
+    for lineno, line in enumerate(text.splitlines(), start=1):
+        t = line.split("#", 1)[0].strip()
+        if not t:
+            continue
+        fields = t.replace(",", " ").split()
+        if width is None:
+            width = len(fields)
+        elif len(fields) != width:
+            raise ValueError(f"{lineno}: expected {width} columns, got {len(fields)}")
+        try:
+            rows.append([float(v) for v in fields])
+        except ValueError as exc:
+            raise ValueError(f"{lineno}: {exc}") from None
+    return np.asarray(rows)
+
+
+@pytest.mark.parametrize("inject", [None, ("width", 150_001), ("float", 199_998), ("float", 3), ("width", 40_000)])
+def test_parallel_column_parser_line_numbers(tmp_path, inject):
+    """The column parser cuts the text into one chunk per host thread; line
+    numbers, widths and the first error must be those of a sequential read."""
+    rng = np.random.default_rng(11)
+    n = 200_000
+    v = rng.standard_normal((n, 3))
+    pts = v / np.linalg.norm(v, axis=1, keepdims=True)
+    lines = [" ".join(fio.format_float(x) for x in p) for p in pts]
+    for k in range(0, n, 997):
+        lines[k] = "# comment " + lines[k]
+    for k in range(5, n, 1733):
+        lines[k] = lines[k] + "   # trailing"
+    if inject:
+        kind, at = inject
+        lines[at - 1] = "0 0" if kind == "width" else "0 0 1e"
+    text = "\r\n".join(lines) + "\n"
+    path = tmp_path / "big.rule"
+    path.write_bytes(text.encode())
+    try:
+        ref = _py_read_columns(text)
+        ref_err = None
+    except ValueError as exc:
+        ref_err = str(exc)
+    if ref_err is None:
+        got = fio.read_columns(path)
+        assert np.array_equal(got, ref)
+    else:
+        with pytest.raises(ValueError) as info:
+            fio.read_columns(path)
+        assert str(info.value) == f"{path}:{ref_err}"
