@@ -20,6 +20,24 @@ from .grid import gen_gl_tensor
 from .transforms import adjoint_favest, forward_favest
 
 
+def error_metrics(reference: TangentFieldSamples, reconstruction: TangentFieldSamples,
+                  weights: np.ndarray) -> tuple[float, float]:
+    """(relative quadrature-weighted L2 error, max pointwise Euclidean error)
+    (favest/diagnostics.py:41-60); host arrays, the reference's arithmetic."""
+    if reference.values.shape != reconstruction.values.shape:
+        raise ValueError("sample sets have different shapes")
+    w = np.asarray(weights, dtype=np.float64)
+    diff = reference.values - reconstruction.values
+    sq = np.sum(np.abs(diff) ** 2, axis=1)
+    ref_sq = np.sum(np.abs(reference.values) ** 2, axis=1)
+    num = float(np.sqrt(np.sum(w * sq)))
+    den = float(np.sqrt(np.sum(w * ref_sq)))
+    if den == 0.0:
+        raise ValueError("reference field has zero norm")
+    max_abs = float(np.max(np.sqrt(sq))) if sq.size else 0.0
+    return num / den, max_abs
+
+
 @dataclass
 class BenchRecord:
     """Median transform timings at one degree on a tensor-grid rule."""
@@ -74,4 +92,4 @@ def bench(degrees, repetitions: int = 5, path: str = "fast-scalar", seed: int = 
     return records
 
 
-__all__ = ["BenchRecord", "bench"]
+__all__ = ["BenchRecord", "bench", "error_metrics"]

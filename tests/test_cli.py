@@ -62,3 +62,19 @@ def test_bench_records():
     recs = bench([4, 12], repetitions=3, seed=5)
     assert [r.lmax for r in recs] == [4, 12]
     assert math.isclose(recs[1].forward_ratio, recs[1].forward_seconds / recs[0].forward_seconds)
+
+
+def test_error_metrics_matches_reference_definition():
+    import numpy as np
+
+    from paper_1908_00041_b200.core import TangentFieldSamples
+    from paper_1908_00041_b200.diagnostics import error_metrics
+
+    pts = np.array([[0, 0, 1.0], [1.0, 0, 0], [0, 1.0, 0]])
+    a = TangentFieldSamples(pts, np.array([[1, 0, 0], [0, 1j, 0], [0, 0, 2]], dtype=complex))
+    b = TangentFieldSamples(pts, a.values + np.array([[0, 1e-3, 0], [0, 0, 0], [0, 0, 0]]))
+    w = np.array([1.0, 2.0, 3.0])
+    rel, mx = error_metrics(a, b, w)
+    assert abs(rel - np.sqrt(1e-6 / (1 + 2 + 12))) <= 1e-18 and mx == 1e-3
+    with pytest.raises(ValueError, match="zero norm"):
+        error_metrics(TangentFieldSamples(pts, np.zeros((3, 3))), b, w)

@@ -91,8 +91,17 @@ def test_c2_batch_l256_against_oracle():
     T = plan.adjoint(_t(A), _t(Bc))
     fa, fb_ = plan.forward(T)
     Tn, fa, fb_ = T.cpu().numpy(), fa.cpu().numpy(), fb_.cpu().numpy()
+    from paper_1908_00041_b200.core import TangentFieldSamples
+    from paper_1908_00041_b200.diagnostics import error_metrics
+
+    pts = O.grid_points(th, nphi)
     for k in (0, 5, 15):
-        assert O.rel_l2(Tn[k], O.vsht_adjoint_grid(A[k], Bc[k], L, th, nphi)) <= TOL
+        Tref = O.vsht_adjoint_grid(A[k], Bc[k], L, th, nphi)
+        assert O.rel_l2(Tn[k], Tref) <= TOL
+        # the quadrature-weighted variant (favest/diagnostics.py:41-60) alongside
+        werr, maxabs = error_metrics(TangentFieldSamples(pts, Tref), TangentFieldSamples(pts, Tn[k]),
+                                     np.repeat(w, nphi))
+        assert werr <= TOL and maxabs <= TOL * np.max(np.abs(Tref))
         ra, rb = O.vsht_forward_grid(Tn[k], th, w, nphi, L)
         assert O.rel_l2(np.concatenate([fa[k], fb_[k]]), np.concatenate([ra, rb])) <= TOL
     # whole batch: round trip limited by the reference's scipy GL weights
