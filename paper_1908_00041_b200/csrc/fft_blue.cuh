@@ -216,6 +216,9 @@ __global__ void __launch_bounds__(BLUE_T) blue_r_kernel(BlueArgs a) {
 // index: coalesced stores).  ~2P + 8R flops per point.
 // ---------------------------------------------------------------------------
 constexpr int SMALLP_MAX = 64;
+// 8 warps (288 threads -- one stage-1 pass fewer and a one-pass fold epilogue at
+// C2 -- measured 6 % slower: 72 registers, one CTA per SM fewer)
+constexpr int SMALLP_T = 256;
 
 struct SmallPArgs {
   const double2* in;
@@ -234,7 +237,7 @@ __device__ __forceinline__ void smallp_stage1(const SmallPArgs& a, const double2
                                               const double2* wp, int nr) {
   const int H = (a.P - 1) / 2;
   const int per = a.R * (H + 1);
-  for (int it = threadIdx.x; it < nr * per; it += BLUE_T) {
+  for (int it = threadIdx.x; it < nr * per; it += SMALLP_T) {
     const int ring = it / per, j = it - ring * per;
     const int r = j / (H + 1), k = j - r * (H + 1);
     const double2* x = xs + ring * a.n + r;
@@ -256,6 +259,46 @@ __device__ __forceinline__ void smallp_stage1(const SmallPArgs& a, const double2
   }
 }
 
+// Stage 2, thread per (ring, bin k, group of SG consecutive outputs s): each
+// residue value of bin k is read once and feeds the group's SG accumulators
+// (the generic per-output loop re-read all R of them per output).  Per output
+// the sum still runs over r = 0, 1, ..., R-1 in order: same arithmetic.
+constexpr int SP_SGMAX = 8;
+__host__ __device__ inline int smallp_sg(int P, int R) {  // outputs per thread of stage 2 (two rings)
+  int sg = (2 * P * R + SMALLP_T - 1) / SMALLP_T;
+  while (2 * P * ((R + sg - 1) / sg) > SMALLP_T) ++sg;
+  return sg;
+}
+template <class Store>
+__device__ __forceinline__ void smallp_stage2(const SmallPArgs& a, const double2* ys, const double2* wr, int nr,
+                                              Store st) {
+  const int P = a.P, R = a.R;
+  const int per = nr * P;
+  int SG = (per * R + SMALLP_T - 1) / SMALLP_T;  // outputs per thread: the fewest that give one pass
+  while (per * ((R + SG - 1) / SG) > SMALLP_T) ++SG;
+  const int ngr = (R + SG - 1) / SG;
+  for (int it = threadIdx.x; it < per * ngr; it += SMALLP_T) {
+    const int sgi = it / per, rk = it - sgi * per;
+    const int ring = rk / P, k = rk - ring * P;
+    const double2* yr = ys + ring * a.n + k;
+    const int s0 = sgi * SG, ns = min(R, s0 + SG) - s0;
+    double2 acc[SP_SGMAX];
+    const double2 z0 = yr[0];
+#pragma unroll
+    for (int u = 0; u < SP_SGMAX; ++u) acc[u] = z0;
+    for (int r = 1; r < R; ++r) {
+      const double2 z = yr[r * P];
+      const double2* w = wr + r * R + s0;
+#pragma unroll
+      for (int u = 0; u < SP_SGMAX; ++u)
+        if (u < ns) acc[u] = bl_add(acc[u], bl_mul(z, w[u]));
+    }
+#pragma unroll
+    for (int u = 0; u < SP_SGMAX; ++u)
+      if (u < ns) st(ring, (s0 + u) * P + k, acc[u]);
+  }
+}
+
 // R-point DFT of output o = s P + k of one ring's residue spectra
 __device__ __forceinline__ double2 smallp_out(const SmallPArgs& a, const double2* ys, const double2* wr, int o) {
   const int s = o / a.P, k = o - s * a.P;
@@ -268,7 +311,7 @@ __device__ __forceinline__ double2 smallp_out(const SmallPArgs& a, const double2
 // Plain transform: CTA per (component, ring pair) -- both rings' items keep all
 // 256 threads busy through both stages, and in the adjoint's ring-pair spectrum
 // layout the two rings' bins are one contiguous stream.
-__global__ void __launch_bounds__(BLUE_T) smallp_kernel(SmallPArgs a) {
+__global__ void __launch_bounds__(SMALLP_T) smallp_kernel(SmallPArgs a) {
   extern __shared__ __align__(16) double2 sp_smem[];
   const int H = (a.P - 1) / 2;
   const int n = a.n;
@@ -285,18 +328,24 @@ __global__ void __launch_bounds__(BLUE_T) smallp_kernel(SmallPArgs a) {
   };
   const double2* src0 = a.in + c * a.in_cs + ring_base(r0);
   const double2* src1 = a.in + c * a.in_cs + ring_base(r0 + nr - 1);
-  for (int i = threadIdx.x; i < nr * n; i += BLUE_T) {
+  for (int i = threadIdx.x; i < nr * n; i += SMALLP_T) {
     const int ring = i / n, j = i - ring * n;
     double2 v = (ring ? src1 : src0)[(long long)j * a.in_es];
     v.y *= cj;
     xs[i] = v;
   }
-  for (int i = threadIdx.x; i < H * (H + 1); i += BLUE_T) wp[i] = __ldg(&a.WP[i]);
-  for (int i = threadIdx.x; i < a.R * a.R; i += BLUE_T) wr[i] = __ldg(&a.WR[i]);
+  for (int i = threadIdx.x; i < H * (H + 1); i += SMALLP_T) wp[i] = __ldg(&a.WP[i]);
+  for (int i = threadIdx.x; i < a.R * a.R; i += SMALLP_T) wr[i] = __ldg(&a.WR[i]);
   __syncthreads();
   smallp_stage1(a, xs, ys, wp, nr);
   __syncthreads();
-  for (int i = threadIdx.x; i < nr * n; i += BLUE_T) {
+  if (smallp_sg(a.P, a.R) <= SP_SGMAX) {
+    smallp_stage2(a, ys, wr, nr, [&](int ring, int o, double2 v) {  // consecutive k: coalesced
+      a.out[c * a.out_cs + (long long)(r0 + ring) * a.out_rs + (long long)o * a.out_es] = make_double2(v.x, cj * v.y);
+    });
+    return;
+  }
+  for (int i = threadIdx.x; i < nr * n; i += SMALLP_T) {
     const int ring = i / n, o = i - ring * n;
     const double2 v = smallp_out(a, ys + ring * n, wr, o);  // output index = thread index: coalesced
     a.out[c * a.out_cs + (long long)(r0 + ring) * a.out_rs + (long long)o * a.out_es] = make_double2(v.x, cj * v.y);
@@ -307,7 +356,7 @@ __global__ void __launch_bounds__(BLUE_T) smallp_kernel(SmallPArgs a) {
 // counterpart of fft2.cuh fft_fold_kernel: CTA per (ring pair, field,
 // component), both rings' spectra kept in shared memory, epilogue writes the
 // Legendre B operand X exactly as fft_fold_kernel does.
-__global__ void __launch_bounds__(BLUE_T) smallp_fold_kernel(SmallPArgs a, Fft2Args f) {
+__global__ void __launch_bounds__(SMALLP_T) smallp_fold_kernel(SmallPArgs a, Fft2Args f) {
   extern __shared__ __align__(16) double2 sp_smem[];
   const int H = (a.P - 1) / 2;
   const int n = a.n;
@@ -321,18 +370,22 @@ __global__ void __launch_bounds__(BLUE_T) smallp_fold_kernel(SmallPArgs a, Fft2A
   const int nr = (rn >= 0) + (rs >= 0);
   if (nr > 0) {
     const double2* base = f.in + (long long)b * f.field_stride + c;
-    for (int i = threadIdx.x; i < nr * n; i += BLUE_T) {
+    for (int i = threadIdx.x; i < nr * n; i += SMALLP_T) {
       const int ring = i / n, j = i - ring * n;
       xs[i] = base[(long long)(ring ? rs : rn) * f.in_rs + (long long)j * f.in_es];
     }
-    for (int i = threadIdx.x; i < H * (H + 1); i += BLUE_T) wp[i] = __ldg(&a.WP[i]);
-    for (int i = threadIdx.x; i < a.R * a.R; i += BLUE_T) wr[i] = __ldg(&a.WR[i]);
+    for (int i = threadIdx.x; i < H * (H + 1); i += SMALLP_T) wp[i] = __ldg(&a.WP[i]);
+    for (int i = threadIdx.x; i < a.R * a.R; i += SMALLP_T) wr[i] = __ldg(&a.WR[i]);
     __syncthreads();
     smallp_stage1(a, xs, ys, wp, nr);
     __syncthreads();
-    for (int i = threadIdx.x; i < nr * n; i += BLUE_T) {
-      const int ring = i / n, o = i - ring * n;
-      xs[i] = smallp_out(a, ys + ring * n, wr, o);
+    if (smallp_sg(a.P, a.R) <= SP_SGMAX) {
+      smallp_stage2(a, ys, wr, nr, [&](int ring, int o, double2 v) { xs[ring * n + o] = v; });
+    } else {
+      for (int i = threadIdx.x; i < nr * n; i += SMALLP_T) {
+        const int ring = i / n, o = i - ring * n;
+        xs[i] = smallp_out(a, ys + ring * n, wr, o);
+      }
     }
     __syncthreads();
   }
@@ -349,7 +402,7 @@ __global__ void __launch_bounds__(BLUE_T) smallp_fold_kernel(SmallPArgs a, Fft2A
   const double ws = rs >= 0 ? f.ring_w[rs] : 0.0;
   const double2* Sn = xs;
   const double2* Ss = xs + n;
-  for (int m = threadIdx.x; m <= f.Lt; m += BLUE_T) {
+  for (int m = threadIdx.x; m <= f.Lt; m += SMALLP_T) {
     double2 Ep = make_double2(0.0, 0.0), Em = Ep, Op = Ep, Om = Ep;
     if (nr > 0) {
       const int bm = m ? n - m : 0;

@@ -749,7 +749,7 @@ int ring_fft_smallp(fvPlan* p, bool inverse, const double2* in, long long in_cs,
   a.inverse = inverse ? 1 : 0;
   const int H = (a.P - 1) / 2;
   const size_t smem = (size_t)(4 * a.n + a.R * a.R + H * (H + 1)) * sizeof(double2);  // two rings per CTA
-  fv::smallp_kernel<<<(unsigned)(3LL * ((nrings + 1) / 2)), fv::BLUE_T, smem, s>>>(a);
+  fv::smallp_kernel<<<(unsigned)(3LL * ((nrings + 1) / 2)), fv::SMALLP_T, smem, s>>>(a);
   FV_CUDA(cudaGetLastError());
   return FV_OK;
 }
@@ -888,7 +888,7 @@ int fft_fold(fvPlan* p, const double2* T, int b0, int nf, cudaStream_t s, double
     const fv::SmallPArgs& sp = p->sp_args;
     const int H = (sp.P - 1) / 2;
     const size_t smem = (size_t)(4 * sp.n + sp.R * sp.R + H * (H + 1)) * sizeof(double2);
-    fv::smallp_fold_kernel<<<p->nchunks * fv::FWD_RC * nf * 3, fv::BLUE_T, smem, s>>>(sp, a);
+    fv::smallp_fold_kernel<<<p->nchunks * fv::FWD_RC * nf * 3, fv::SMALLP_T, smem, s>>>(sp, a);
     FV_CUDA(cudaGetLastError());
     return FV_OK;
   }
