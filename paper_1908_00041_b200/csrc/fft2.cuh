@@ -75,7 +75,14 @@ struct Fft2Args {
   const double* ring_w;
   long long field_stride;            // complex units between fields of the input
   int nchunks, NT, nfields, Lt;
+  int ahead;                         // L2 prefetch of the input of item blockIdx.x + ahead (0: off)
 };
+
+// cp.async.bulk.prefetch.L2: one instruction per contiguous block (16-byte
+// aligned address and size); no completion, no register or shared state
+__device__ __forceinline__ void f2_prefetch_l2(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 
 // compile-time plan: up to three stages R0 x R1 x R2 (0 = absent), largest first
 template <int R0, int R1, int R2>
@@ -233,6 +240,14 @@ __global__ void __launch_bounds__(F2P_T, 2) ring_fft2_kernel(Fft2Args a, int nit
   if (item >= nitems) return;
   const int c = item % 3, g = item / 3;
   const int r0 = g * F2P_NR;
+  if (a.ahead && a.in_rblk == F2P_NR && threadIdx.x == 0 && item + a.ahead < nitems) {
+    // the item one wave ahead: its two rings of one component are one
+    // contiguous block of the ring-pair spectrum layout
+    const int it2 = item + a.ahead, c2 = it2 % 3, q0 = (it2 / 3) * F2P_NR;
+    if (a.nrings - q0 >= F2P_NR)
+      f2_prefetch_l2(a.in + c2 * a.in_cs + (long long)(q0 / F2P_NR) * a.in_rs,
+                     (unsigned)(F2P_NR * F2Plan<R0, R1, R2>::N * sizeof(double2)));
+  }
   const int nr = min(F2P_NR, a.nrings - r0);
   const double2* src[F2P_NR];
   double2* dst[F2P_NR];
@@ -260,6 +275,16 @@ __global__ void __launch_bounds__(F2_T, 2) fft_fold_kernel(Fft2Args a, int nitem
   const int item = blockIdx.x;
   if (item >= nitems) return;
   const int c = item % 3, b = (item / 3) % a.nfields, p = item / (3 * a.nfields);
+  if (a.ahead && c == 0 && threadIdx.x == 0 && item + a.ahead < nitems) {
+    // the ring pair of the item one wave ahead (whole rings: all three
+    // components are interleaved), once per (pair, field)
+    const int it2 = item + a.ahead, b2 = (it2 / 3) % a.nfields, p2 = it2 / (3 * a.nfields);
+    const int rn2 = a.pair_n[p2], rs2 = a.pair_s[p2];
+    const double2* base2 = a.in + (long long)b2 * a.field_stride;
+    constexpr unsigned ring_bytes = 3u * n * sizeof(double2);
+    if (rn2 >= 0) f2_prefetch_l2(base2 + (long long)rn2 * a.in_rs, ring_bytes);
+    if (rs2 >= 0) f2_prefetch_l2(base2 + (long long)rs2 * a.in_rs, ring_bytes);
+  }
   const int rn = a.pair_n[p], rs = a.pair_s[p];
   const int nr = (rn >= 0) + (rs >= 0);
   if (nr > 0) {

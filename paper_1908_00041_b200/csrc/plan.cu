@@ -847,6 +847,21 @@ int ring_fft_blue(fvPlan* p, bool inverse, const double2* in, long long in_cs, l
   return FV_OK;
 }
 
+// FFT input prefetch distance in items (FV_FFT_PREFETCH; 0 disables).  C3
+// sweep (fft stage per step, 4 fields): off 0.527 ms, 74 / 110 / 148 / 200 /
+// 296 / 444 items ahead 0.509 / 0.508 / 0.510 / 0.512 / 0.520 / 0.535 ms:
+// default one item per SM
+int fft_prefetch_ahead() {
+  static const int v = [] {
+    const char* e = std::getenv("FV_FFT_PREFETCH");
+    if (e) return std::max(0, std::atoi(e));
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+  }();
+  return v;
+}
+
 int ring_fft2_raw(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
                   double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s,
                   int in_rblk = 0) {
@@ -858,6 +873,7 @@ int ring_fft2_raw(fvPlan* p, bool inverse, const double2* in, long long in_cs, l
   a.in_cs = in_cs; a.in_rs = in_rs; a.in_es = (int)in_es;
   a.out_cs = out_cs; a.out_rs = out_rs; a.out_es = (int)out_es;
   a.nrings = nrings;
+  a.ahead = fft_prefetch_ahead();
   const int grid = 3 * ((nrings + fv::F2P_NR - 1) / fv::F2P_NR);
   const size_t smem = fv::F2P_NR * (size_t)p->n_phi * sizeof(double2);
   return f2_dispatch(p, [&](auto A, auto B, auto C) -> int {
@@ -906,6 +922,7 @@ int fft_fold(fvPlan* p, const double2* T, int b0, int nf, cudaStream_t s, double
   a.NT = ntiles_for(nf);
   a.nfields = nf;
   a.Lt = p->Lt;
+  a.ahead = fft_prefetch_ahead();
   const int grid = p->nchunks * fv::FWD_RC * nf * 3;
   const size_t smem = fv::F2_NR * (size_t)p->n_phi * sizeof(double2);
   return f2_dispatch(p, [&](auto A, auto B, auto C) -> int {
