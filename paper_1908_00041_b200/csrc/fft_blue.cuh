@@ -230,6 +230,7 @@ struct SmallPArgs {
   const double2* WP;     // [q - 1][k] = (cos, sin)(2 pi (q k mod P) / P), q = 1..H, k = 0..H, H = (P - 1) / 2
   int n, R, P, nrings, inverse;
   int in_rblk;           // blocked input rings (common.cuh SLayout rblk), 0: in_rs apart
+  int ahead;             // L2 prefetch of the input of item blockIdx.x + ahead (fft2.cuh), 0: off
 };
 
 // residue DFTs of nr rings: xs[ring][n] -> ys[ring][R][P] (twiddled by w_n^{r k})
@@ -326,6 +327,10 @@ __global__ void __launch_bounds__(SMALLP_T) smallp_kernel(SmallPArgs a) {
     return a.in_rblk ? (long long)(ring >> (31 - __clz(a.in_rblk))) * a.in_rs + (ring & (a.in_rblk - 1))
                      : (long long)ring * a.in_rs;
   };
+  if (a.ahead && a.in_rblk == 2 && threadIdx.x == 0 && blockIdx.x + a.ahead < gridDim.x) {
+    const int it2 = blockIdx.x + a.ahead, c2 = it2 % 3, q0 = 2 * (it2 / 3);
+    if (a.nrings - q0 >= 2) f2_prefetch_l2(a.in + c2 * a.in_cs + ring_base(q0), (unsigned)(2 * n * sizeof(double2)));
+  }
   const double2* src0 = a.in + c * a.in_cs + ring_base(r0);
   const double2* src1 = a.in + c * a.in_cs + ring_base(r0 + nr - 1);
   for (int i = threadIdx.x; i < nr * n; i += SMALLP_T) {
@@ -366,6 +371,14 @@ __global__ void __launch_bounds__(SMALLP_T) smallp_fold_kernel(SmallPArgs a, Fft
   double2* wr = wp + H * (H + 1);
   const int item = blockIdx.x;
   const int c = item % 3, b = (item / 3) % f.nfields, p = item / (3 * f.nfields);
+  if (f.ahead && c == 0 && threadIdx.x == 0 && item + f.ahead < (int)gridDim.x) {
+    const int it2 = item + f.ahead, b2 = (it2 / 3) % f.nfields, p2 = it2 / (3 * f.nfields);
+    const int rn2 = f.pair_n[p2], rs2 = f.pair_s[p2];
+    const double2* base2 = f.in + (long long)b2 * f.field_stride;
+    const unsigned ring_bytes = (unsigned)(3 * n * sizeof(double2));
+    if (rn2 >= 0) f2_prefetch_l2(base2 + (long long)rn2 * f.in_rs, ring_bytes);
+    if (rs2 >= 0) f2_prefetch_l2(base2 + (long long)rs2 * f.in_rs, ring_bytes);
+  }
   const int rn = f.pair_n[p], rs = f.pair_s[p];
   const int nr = (rn >= 0) + (rs >= 0);
   if (nr > 0) {

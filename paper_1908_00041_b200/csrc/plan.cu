@@ -732,6 +732,21 @@ int setup_blue(fvPlan* p) {
   return FV_OK;
 }
 
+// FFT input prefetch distance in items (FV_FFT_PREFETCH; 0 disables).  C3
+// sweep (fft stage per step, 4 fields): off 0.527 ms, 74 / 110 / 148 / 200 /
+// 296 / 444 items ahead 0.509 / 0.508 / 0.510 / 0.512 / 0.520 / 0.535 ms:
+// default one item per SM
+int fft_prefetch_ahead() {
+  static const int v = [] {
+    const char* e = std::getenv("FV_FFT_PREFETCH");
+    if (e) return std::max(0, std::atoi(e));
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+  }();
+  return v;
+}
+
 int ring_fft_smallp(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
                     double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s,
                     int in_rblk = 0) {
@@ -747,6 +762,7 @@ int ring_fft_smallp(fvPlan* p, bool inverse, const double2* in, long long in_cs,
   a.out_es = out_es;
   a.nrings = nrings;
   a.inverse = inverse ? 1 : 0;
+  a.ahead = fft_prefetch_ahead();
   const int H = (a.P - 1) / 2;
   const size_t smem = (size_t)(4 * a.n + a.R * a.R + H * (H + 1)) * sizeof(double2);  // two rings per CTA
   fv::smallp_kernel<<<(unsigned)(3LL * ((nrings + 1) / 2)), fv::SMALLP_T, smem, s>>>(a);
@@ -847,21 +863,6 @@ int ring_fft_blue(fvPlan* p, bool inverse, const double2* in, long long in_cs, l
   return FV_OK;
 }
 
-// FFT input prefetch distance in items (FV_FFT_PREFETCH; 0 disables).  C3
-// sweep (fft stage per step, 4 fields): off 0.527 ms, 74 / 110 / 148 / 200 /
-// 296 / 444 items ahead 0.509 / 0.508 / 0.510 / 0.512 / 0.520 / 0.535 ms:
-// default one item per SM
-int fft_prefetch_ahead() {
-  static const int v = [] {
-    const char* e = std::getenv("FV_FFT_PREFETCH");
-    if (e) return std::max(0, std::atoi(e));
-    int dev = 0, sms = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return sms;
-  }();
-  return v;
-}
-
 int ring_fft2_raw(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
                   double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s,
                   int in_rblk = 0) {
@@ -901,6 +902,7 @@ int fft_fold(fvPlan* p, const double2* T, int b0, int nf, cudaStream_t s, double
     a.NT = ntiles_for(nf);
     a.nfields = nf;
     a.Lt = p->Lt;
+    a.ahead = fft_prefetch_ahead();
     const fv::SmallPArgs& sp = p->sp_args;
     const int H = (sp.P - 1) / 2;
     const size_t smem = (size_t)(4 * sp.n + sp.R * sp.R + H * (H + 1)) * sizeof(double2);
