@@ -766,8 +766,46 @@ extern "C" int fv_io_parse_coefficients(const char* text, long long n, int* lmax
       s.ws();
       const char c = *s.p;
       if (c != '[') {
-        if (c == '"' || c == '{')
-          return bail(FV_EINVAL, "not enough values to unpack (expected 2)");
+        if (c == '"' || c == '{') {
+          // re, im = pair iterates a str's characters / a dict's keys
+          std::vector<std::string> items;
+          fio::Json q{text, s.p, e, {}};
+          if (c == '"') {
+            std::string v;
+            q.string(&v);
+            for (char ch : v) items.push_back(std::string(1, ch));
+          } else {
+            ++q.p;
+            q.ws();
+            while (q.p < e && *q.p == '"') {
+              std::string key;
+              q.string(&key);
+              q.ws();
+              ++q.p;  // ':'
+              q.value(0);
+              q.ws();
+              bool dup = false;
+              for (auto& it : items) dup |= it == key;
+              if (!dup) items.push_back(key);
+              if (*q.p == ',') { ++q.p; q.ws(); }
+            }
+            ++q.p;  // '}'
+          }
+          if (items.size() != 2)
+            return bail(FV_EINVAL, items.size() > 2 ? "too many values to unpack (expected 2)"
+                                                    : "not enough values to unpack (expected 2, got " +
+                                                          std::to_string(items.size()) + ")");
+          double v2[2];
+          for (int c2 = 0; c2 < 2; ++c2)
+            if (!fio::py_float(items[c2].data(), (long long)items[c2].size(), v2[c2]))
+              return bail(FV_EINVAL, fio::float_err(items[c2].data(), (long long)items[c2].size()));
+          outs[w][2 * k] = v2[0];
+          outs[w][2 * k + 1] = v2[1];
+          s.p = q.p;
+          s.ws();
+          if (s.p < e && *s.p == ',') ++s.p;
+          continue;
+        }
         const char* vs = s.p;
         s.value(0);
         bool isint = true;

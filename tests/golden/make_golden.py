@@ -240,6 +240,9 @@ def main():
         ("coef", "triple", '{"L_max": 0, "a": [[1, 2, 3]], "b": [[0, 0]]}'),
         ("coef", "single", '{"L_max": 0, "a": [[1]], "b": [[0, 0]]}'),
         ("coef", "number pair", '{"L_max": 0, "a": [5], "b": [[0, 0]]}'),
+        ("coef", "string pairs", '{"L_max": 1, "a": [[0, 0], "12", "00", [1, 1]], "b": [[0, 0], "12", "00", "7"]}'),
+        ("coef", "dict pair", '{"L_max": 1, "a": [[0, 0], {"1": 0, "2": 0}, [0, 0], [1, 1]], "b": ' + good_pair + "}"),
+        ("coef", "string pair ok", '{"L_max": 1, "a": [[0, 0], "12", {"3": 0, "4": 0}, [1, 1]], "b": ' + good_pair + "}"),
         ("coef", "json literals", '{"L_max": 1, "a": [[0, 0], [NaN, Infinity], [0, 0], [0, 0]], '
                               '"b": [[0, 0], [-Infinity, true], [false, 0], [0, 0]]}'),
         ("coef", "duplicate key", '{"L_max": 3, "L_max": 1, "a": [[1, 2]], "b": ' + good_pair
