@@ -741,13 +741,18 @@ extern "C" int fv_io_parse_coefficients(const char* text, long long n, int* lmax
         return bail(FV_EINVAL, std::string("{path}: array '") + labels[w] + "' is not a list of [re, im] pairs");
       return bail(FV_ETYPE, "object of type '" + std::string(*p == 'n' ? "NoneType" : "float") + "' has no len()");
     }
-    // count entries (top level of this array)
+    // count entries (top level of this array), remembering where every
+    // CH-th one starts: the conversion runs in one chunk per host thread
     long long cnt = 0;
+    const int T = fio::host_threads(size / 8);
+    const long long CH = std::max<long long>(1, (size + T - 1) / T);
+    std::vector<const char*> starts;
     {
       fio::Json s{text, p + 1, e, {}};
       s.ws();
       if (s.p < e && *s.p != ']') {
         while (true) {
+          if (cnt % CH == 0) starts.push_back(s.p);
           s.value(0);
           ++cnt;
           s.ws();
@@ -761,8 +766,18 @@ extern "C" int fv_io_parse_coefficients(const char* text, long long n, int* lmax
                                  " entries, expected " + std::to_string(size) + " for L_max=" + std::to_string(L));
     outs[w] = static_cast<double*>(std::malloc((size_t)std::max<long long>(size, 1) * 16));
     if (!outs[w]) return bail(FV_ENOMEM, "out of host memory");
-    fio::Json s{text, p + 1, e, {}};
-    for (long long k = 0; k < size; ++k) {
+    double* ow = outs[w];
+    // convert elements [k0, k1) from their first character; returns the index
+    // of the first failing element (code / msg set) or -1
+    auto conv = [&](long long k0, long long k1, const char* from, int& code, std::string& msg) -> long long {
+#define FV_FAILK(c_, m_) \
+  do {                   \
+    code = (c_);         \
+    msg = (m_);          \
+    return k;            \
+  } while (0)
+      fio::Json s{text, from, e, {}};
+      for (long long k = k0; k < k1; ++k) {
       s.ws();
       const char c = *s.p;
       if (c != '[') {
@@ -792,15 +807,15 @@ extern "C" int fv_io_parse_coefficients(const char* text, long long n, int* lmax
             ++q.p;  // '}'
           }
           if (items.size() != 2)
-            return bail(FV_EINVAL, items.size() > 2 ? "too many values to unpack (expected 2)"
+            FV_FAILK(FV_EINVAL, items.size() > 2 ? "too many values to unpack (expected 2)"
                                                     : "not enough values to unpack (expected 2, got " +
                                                           std::to_string(items.size()) + ")");
           double v2[2];
           for (int c2 = 0; c2 < 2; ++c2)
             if (!fio::py_float(items[c2].data(), (long long)items[c2].size(), v2[c2]))
-              return bail(FV_EINVAL, fio::float_err(items[c2].data(), (long long)items[c2].size()));
-          outs[w][2 * k] = v2[0];
-          outs[w][2 * k + 1] = v2[1];
+              FV_FAILK(FV_EINVAL, fio::float_err(items[c2].data(), (long long)items[c2].size()));
+          ow[2 * k] = v2[0];
+          ow[2 * k + 1] = v2[1];
           s.p = q.p;
           s.ws();
           if (s.p < e && *s.p == ',') ++s.p;
@@ -810,7 +825,7 @@ extern "C" int fv_io_parse_coefficients(const char* text, long long n, int* lmax
         s.value(0);
         bool isint = true;
         for (const char* q = vs; q < s.p; ++q) isint &= !(*q == '.' || *q == 'e' || *q == 'E' || *q == 'N' || *q == 'I');
-        return bail(FV_ETYPE, std::string("cannot unpack non-iterable ") +
+        FV_FAILK(FV_ETYPE, std::string("cannot unpack non-iterable ") +
                                   (c == 'n' ? "NoneType" : (c == 't' || c == 'f') ? "bool" : isint ? "int" : "float") +
                                   " object");
       }
@@ -833,20 +848,36 @@ extern "C" int fv_io_parse_coefficients(const char* text, long long n, int* lmax
       }
       ++s.p;  // ']'
       if (got != 2)  // re, im = pair (io.py:91)
-        return bail(FV_EINVAL, got > 2 ? "too many values to unpack (expected 2)"
+        FV_FAILK(FV_EINVAL, got > 2 ? "too many values to unpack (expected 2)"
                                        : "not enough values to unpack (expected 2, got " + std::to_string(got) + ")");
       double v[2];
       for (int c2 = 0; c2 < 2; ++c2) {  // float(re), float(im): not wrapped with the path (io.py:92)
-        std::string msg;
+        std::string fmsg;
         const char* q = el[c2];
-        const int rc = fio::json_float(q, ee[c2], v[c2], msg);
-        if (rc != FV_OK) return bail(rc, msg);
+        const int rc = fio::json_float(q, ee[c2], v[c2], fmsg);
+        if (rc != FV_OK) FV_FAILK(rc, fmsg);
       }
-      outs[w][2 * k] = v[0];
-      outs[w][2 * k + 1] = v[1];
+      ow[2 * k] = v[0];
+      ow[2 * k + 1] = v[1];
       s.ws();
       if (s.p < e && *s.p == ',') ++s.p;
+      }
+#undef FV_FAILK
+      return -1;
+    };
+    const int nch = (int)starts.size();
+    std::vector<long long> ek(nch, -1);
+    std::vector<int> ec(nch, 0);
+    std::vector<std::string> em(nch);
+    {
+      std::vector<std::thread> th;
+      for (int t = 1; t < nch; ++t)
+        th.emplace_back([&, t] { ek[t] = conv(t * CH, std::min(size, (t + 1) * CH), starts[t], ec[t], em[t]); });
+      if (nch) ek[0] = conv(0, std::min(size, CH), starts[0], ec[0], em[0]);
+      for (auto& x : th) x.join();
     }
+    for (int t = 0; t < nch; ++t)
+      if (ek[t] >= 0) return bail(ec[t], em[t]);
   }
   *lmax = (int)L;
   *a = outs[0];
