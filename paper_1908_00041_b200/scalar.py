@@ -17,7 +17,7 @@ from __future__ import annotations
 import numpy as np
 
 from .core import FOUR_PI, ScalarCoefficients, check_unit
-from .transforms import _to_host, grid_plan, points_plan
+from .transforms import _to_device, _to_host, grid_plan, points_plan
 
 
 def _plan_degree(lmax: int) -> int:
@@ -66,7 +66,7 @@ def forward_sht_fast(f, grid, lmax: int) -> ScalarCoefficients:
         return forward_sht_direct(vals, _GridRule(grid), lmax)
     plan = grid_plan(grid, _plan_degree(lmax))
     cols = _columns(vals)
-    out = np.concatenate([plan.forward_scalar(c.to(plan.device), lmax).cpu().numpy()
+    out = np.concatenate([_to_host(plan.forward_scalar(_to_device(c.numpy(), plan.device), lmax))
                           for c in cols.split(3 * plan.max_batch)])
     values = out.T if vals.ndim == 2 else out[0]
     return ScalarCoefficients(lmax, values)
@@ -98,7 +98,7 @@ def forward_sht_direct(f, rule, lmax: int) -> ScalarCoefficients:
     xyz = torch.from_numpy(np.ascontiguousarray(pts)).to(plan.device)
     w = torch.from_numpy(np.ascontiguousarray(rule.weights, dtype=np.float64)).to(plan.device)
     cols = _columns(vals)
-    out = np.concatenate([plan.forward_scalar(xyz, w, c.to(plan.device), lmax).cpu().numpy()
+    out = np.concatenate([_to_host(plan.forward_scalar(xyz, w, _to_device(c.numpy(), plan.device), lmax))
                           for c in cols.split(3 * plan.max_batch)])
     values = out.T if vals.ndim == 2 else out[0]
     return ScalarCoefficients(lmax, values)
