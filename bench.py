@@ -10,10 +10,17 @@ through forward+adjoint per second over all ranks.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-N > 1: launched by torchrun, one process per GPU, fields sharded by batch
-(weak scaling, no data-path collective); max over ranks of the CUDA-event
-time.  --impl reference times the reference algorithm's CPU implementation
-(the numpy oracle port in oracle/, all host cores) on rank 0 only.
+N > 1: one process per GPU.  Under torchrun the ranks come from the
+environment (WORLD_SIZE must equal N); without it, bench.py re-launches
+itself through ``torch.distributed.run`` with N processes.  Fields are
+sharded by batch (weak scaling, no data-path collective); max over ranks of
+the CUDA-event time.  Every run also reports, under ``detail``, the C4
+workload (L=4096, one field, order-sharded over the N ranks with one NCCL
+all-to-all per direction; strong scaling against the single-GPU plan), the
+C3 step with the on-the-fly Legendre recurrence (no plan-time tables), and the
+C5 scattered adjoint.  --impl reference times the reference algorithm's CPU
+implementation (the numpy port in oracle/, spread over all host cores) on
+rank 0 only.
 """
 
 from __future__ import annotations
@@ -147,41 +154,30 @@ def make_inputs(L: int, B: int, seed: int):
     return rng, np.stack([x[0] for x in ab]), np.stack([x[1] for x in ab])
 
 
-def cpu_port_rate(L: int, sample_orders_every: int):
-    """Time the numpy port of the reference algorithm (oracle/) on one field.
-
-    The order-independent parts (ring FFTs, Clebsch-Gordan stages, tables) run in
-    full; the per-order Legendre stage runs on every k-th order and is scaled by
-    the sampled fraction of the per-order work.  Returns (fields/s, seconds for
-    the extrapolated full forward+adjoint, description)."""
+def cpu_port(L: int, n_fields: int, procs: int | None = None):
+    """Time the reference algorithm's CPU implementation (the numpy port in
+    oracle/, its per-order stage over a pool of one process per host core) on
+    ``n_fields`` whole fields of the C3 recipe: forward then adjoint of each,
+    nothing sampled or extrapolated.  Returns (fields/s, per-field seconds,
+    description, processes)."""
     import oracle.favest_oracle as O
+    from oracle.parallel import GridPort
 
-    th, w, nph = O.gl_grid(L)
-    rng = np.random.default_rng(3)
-    a, b = O.coef(rng, L, "pow2")
-    T = O.tangent_noise(rng, O.grid_points(th, nph), 1.0)
-    Lt = L + 1
-    orders = list(range(0, Lt + 1, sample_orders_every))
-    frac = sum(Lt + 1 - m for m in orders) / sum(Lt + 1 - m for m in range(Lt + 1))
-
-    def clock(fn):
+    port = GridPort(L, procs)
+    rng, A, Bc = make_inputs(L, 1, seed=3)
+    # the C3 field: adjoint of the seeded coefficients + tangent noise (untimed setup)
+    T = port.adjoint(A[0], Bc[0]) + O.tangent_noise(rng, O.grid_points(port.th, port.n_phi), 1e-3)
+    secs = []
+    for _ in range(n_fields):
         t0 = time.perf_counter()
-        out = fn()
-        return time.perf_counter() - t0, out
-
-    t1, t2, t3 = T[:, 0], T[:, 1], T[:, 2]
-    combos = np.stack([-t1 + 1j * t2, t1 + 1j * t2, t3], axis=1)        # favest/transforms.py:109-112
-    tf0, _ = clock(lambda: O.sht_forward_grid(combos, th, w, nph, Lt, orders=[]))
-    tfs, f = clock(lambda: O.sht_forward_grid(combos, th, w, nph, Lt, orders=orders))
-    tcf, _ = clock(lambda: O.cg_forward_assemble(f, L))
-    tca, g = clock(lambda: O.vsht_adjoint_merged(a, b, L))
-    ta0, _ = clock(lambda: O.sht_adjoint_grid(g, Lt, th, nph, orders=[]))
-    tas, _ = clock(lambda: O.sht_adjoint_grid(g, Lt, th, nph, orders=orders))
-    total = tf0 + max(tfs - tf0, 0.0) / frac + tcf + tca + ta0 + max(tas - ta0, 0.0) / frac
-    desc = (f"numpy oracle port (oracle/favest_oracle.py, OpenBLAS) of one field at L={L}: ring FFTs and "
-            f"CG stages in full, per-order Legendre stage on every {sample_orders_every}th order "
-            f"(work fraction {frac:.3f}) scaled to all orders; forward+adjoint")
-    return 1.0 / total, total, desc
+        fa, fb = port.forward(T)
+        port.adjoint(fa, fb)
+        secs.append(time.perf_counter() - t0)
+    desc = (f"numpy port of the reference algorithm (oracle/favest_oracle.py + oracle/parallel.py): one C3 field "
+            f"(L={L}, {L + 2}x{2 * L + 4} grid) forward then adjoint in full per timed unit, per-order stage over "
+            f"{port.procs} forked processes (BLAS 1 thread each), ring DFTs / CG stages in the parent; "
+            f"{n_fields} field(s) timed")
+    return 1.0 / float(np.median(secs)), secs, desc, port.procs
 
 
 def blas_threads():
@@ -196,35 +192,46 @@ def blas_threads():
 def run_reference(args, rank, world):
     """--impl reference: the path's CPU implementation on the host cores, rank 0 only
     (the reference is pure Python/numpy and cannot travel to the GPU box, so the
-    numpy port in oracle/ stands in for it)."""
+    numpy port in oracle/ stands in for it).  Each step is one whole
+    C3 field forward then adjoint (a bounded sample of the 4-field C3 step, same
+    per-field unit); nothing is extrapolated: value = 1 / median step time."""
     if rank != 0:
         return
+    import oracle.favest_oracle as O
+    from oracle.parallel import GridPort
+
     L = args.L
-    # wall-clock budget: each step is a ~4 s sample of the host computation, so a long
-    # --steps run stops early (the median of the completed steps is the value)
-    budget = float(os.environ.get("FV_REF_BUDGET_S", "240"))
-    t_start = time.perf_counter()
-    for _ in range(min(args.warmup, 3)):
-        cpu_port_rate(L, args.ref_every * 4)
-    rates, secs = [], []
-    desc = ""
+    port = GridPort(L)
+    rng, A, Bc = make_inputs(L, 1, seed=3)
+    T = port.adjoint(A[0], Bc[0]) + O.tangent_noise(rng, O.grid_points(port.th, port.n_phi), 1e-3)
+
+    def step():
+        fa, fb = port.forward(T)
+        return port.adjoint(fa, fb)
+
+    for _ in range(args.warmup):
+        step()
+    secs = []
+    t_all = time.perf_counter()
     for _ in range(args.steps):
-        r, dt, desc = cpu_port_rate(L, args.ref_every)
-        rates.append(r)
-        secs.append(dt)
-        if time.perf_counter() - t_start > budget:
-            break
-    rate = float(np.median(rates))
-    if len(rates) < args.steps:
-        desc += f"; {len(rates)} of {args.steps} steps within the {budget:.0f} s wall budget"
-    cores = os.cpu_count()
+        t0 = time.perf_counter()
+        step()
+        secs.append(time.perf_counter() - t0)
+    wall = time.perf_counter() - t_all
+    rate = args.steps / wall
+    desc = (f"numpy port of the reference algorithm (oracle/favest_oracle.py + oracle/parallel.py): per step one "
+            f"whole C3 field (L={L}, {L + 2}x{2 * L + 4} grid) forward then adjoint, per-order stage over "
+            f"{port.procs} forked processes (BLAS 1 thread each), ring DFTs / CG stages in the parent; "
+            f"{args.steps} timed steps after {args.warmup} warm-up steps, nothing sampled or extrapolated")
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": float(np.median(secs)) * 1e3, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(L, args.batch, world), "impl": "reference",
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc,
-                         "blas_threads": blas_threads(), "numpy": np.__version__},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": port.procs, "kind": "port", "sample": desc,
+                         "host_cpus": os.cpu_count(), "numpy": np.__version__,
+                         "step_s": {"median": float(np.median(secs)), "min": float(min(secs)),
+                                    "max": float(max(secs))}, "timed_wall_s": wall},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -242,6 +249,12 @@ def workload_config(L, B, world):
 # our arm
 # ---------------------------------------------------------------------------
 def run_ours(args, rank, world, local_rank):
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # before CUDA is initialised in this process: the port forks its workers
+        rate, secs, desc, procs = cpu_port(args.L, args.cpu_fields)
+        cpu = {"value": rate, "unit": UNIT, "cores": procs, "kind": "port", "sample": desc,
+               "seconds_per_field": secs, "host_cpus": os.cpu_count(), "numpy": np.__version__}
     import torch
 
     torch.cuda.set_device(local_rank)
@@ -251,6 +264,9 @@ def run_ours(args, rank, world, local_rank):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
+        got = dist.get_world_size()
+        if got != args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus} but the process group has {got} ranks")
     import oracle.favest_oracle as O
     from paper_1908_00041_b200.grid import gl_grid_for
     from paper_1908_00041_b200.plan import GridPlan
@@ -406,11 +422,17 @@ def run_ours(args, rank, world, local_rank):
                "serial_value": world * B / (ms_serial / 1e3),
                "link_gbs_each_way": bytes_io / (ms_e / 1e3) / 1e9}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, dt, desc = cpu_port_rate(L, args.ref_every)
-        cpu = {"value": rate, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": desc,
-               "seconds": dt, "blas_threads": blas_threads(), "numpy": np.__version__}
+    detail_extra = {}
+    if not args.no_detail:
+        # the same C3 step with the on-the-fly recurrence producer (no plan-time P tables;
+        # the mode north_star names and the only one that exists at L=4096)
+        detail_extra["on_the_fly"] = on_the_fly_detail(args, world, plan, grid, T, a, b, Tout, timed, dev)
+        del plan
+        torch.cuda.empty_cache()
+        detail_extra["c5"] = c5_detail(args, rank, world, dev, timed)
+        del T, Tout, a, b
+        torch.cuda.empty_cache()
+        detail_extra["c4"] = c4_detail(args, rank, world, dev, dist, timed, barrier, max_over_ranks)
 
     if rank == 0:
         line = {
@@ -437,12 +459,182 @@ def run_ours(args, rank, world, local_rank):
                 "launches_note": "our kernels in the timed region, counted by the plan's stage marks: per step "
                                  "and 4-field group fft_fold (forward FFT + fold), legendre_fwd, cg_fwd_tile, "
                                  "cg_adj_tile, legendre_adj, ring_fft2 (inverse)",
+                **detail_extra,
             },
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# detail entries of the headline line
+# ---------------------------------------------------------------------------
+def on_the_fly_detail(args, world, plan, grid, T, a, b, Tout, timed, dev):
+    """The C3 step on a plan built with FV_PTAB=0: the Legendre producers run the
+    block-rescaled three-term recurrence beside the DMMAs instead of streaming
+    plan-time tables (north_star's on-the-fly recurrence)."""
+    from paper_1908_00041_b200.plan import GridPlan
+
+    L, B = args.L, args.batch
+    old = os.environ.get("FV_PTAB")
+    os.environ["FV_PTAB"] = "0"
+    try:
+        p2 = GridPlan.from_grid(grid, L, max_batch=B, device=dev)
+    finally:
+        if old is None:
+            del os.environ["FV_PTAB"]
+        else:
+            os.environ["FV_PTAB"] = old
+
+    def step():
+        p2.forward(T, a, b)
+        p2.adjoint(a, b, Tout)
+
+    for _ in range(3):
+        step()
+    n = max(5, args.steps // 2)
+    p2.set_profiling(True)
+    ms = timed(step, n)
+    st, cnt = p2.stage_ms(), p2.stage_counts()
+    p2.set_profiling(False)
+    # bitwise-independent check: the on-the-fly forward matches the table-mode forward
+    a2, b2 = p2.forward(T)
+    a1, b1 = plan.forward(T)
+    import torch
+
+    rel = float(torch.linalg.vector_norm(torch.cat([a2 - a1, b2 - b1])) / torch.linalg.vector_norm(torch.cat([a1, b1])))
+    p2.close()
+    fl = canonical_flops(L, B)
+    leg_ms = st["legendre"] / max(1, cnt["legendre"])
+    return {"ms_per_step": ms, "value": world * B / (ms / 1e3),
+            "unit": UNIT, "steps": n,
+            "legendre_avg_launch_ms": leg_ms,
+            "legendre_frac_of_measured_dmma_peak": fl["legendre"] / (leg_ms / 1e3) / 1e12 / FP64_PEAK_MEASURED,
+            "stage_ms_per_step": {k: v / n for k, v in st.items()},
+            "step_fraction_of_fp64_roofline_datasheet": (2 * fl["total"] / (ms / 1e3)) / (FP64_PEAK_DATASHEET * 1e12),
+            "forward_rel_l2_vs_table_mode": rel,
+            "note": "plan built with FV_PTAB=0: P-bar by the on-the-fly recurrence, no plan-time tables"}
+
+
+def c5_detail(args, rank, world, dev, timed):
+    """BASELINE configs[4]: adjoint of one L=128 field at M=200,000 scattered points
+    (default_rng(5): points, then coefficients with the 1/(l(l+1)) law); points
+    sharded across the ranks (no exchange), coefficients replicated."""
+    import torch
+
+    import oracle.favest_oracle as O  # seeded generators only
+    from paper_1908_00041_b200.plan import PointsPlan
+
+    L5, M = 128, 200_000
+    rng = np.random.default_rng(5)
+    pts = O.random_points(rng, M)
+    a, b = O.coef(rng, L5, "inv")
+    lo, hi = rank * M // world, (rank + 1) * M // world
+    pp = PointsPlan(L5, max_batch=1, device=dev)
+    xyz = torch.from_numpy(np.ascontiguousarray(pts[lo:hi])).to(dev)
+    a_d = torch.from_numpy(a[None]).to(dev)
+    b_d = torch.from_numpy(b[None]).to(dev)
+    Tp = pp.adjoint(xyz, a_d, b_d)
+    for _ in range(3):
+        pp.adjoint(xyz, a_d, b_d, Tp)
+    n = 20
+    ms = timed(lambda: pp.adjoint(xyz, a_d, b_d, Tp), n)
+    # parity guard: 64 points of this rank's shard against the oracle
+    sel = np.linspace(0, hi - lo - 1, 64).astype(int)
+    ref = O.vsht_adjoint_points(a, b, L5, pts[lo:hi][sel])
+    rel = O.rel_l2(Tp[0].cpu().numpy()[sel], ref)
+    pp.close()
+    gflop = 47.37  # SURVEY §8(d): 40.56 contraction + 6.81 recurrence
+    return {"workload": "C5 (BASELINE configs[4]): adjoint at M=200,000 scattered points, L=128, one field, "
+                        f"points sharded x{world}",
+            "ms_per_transform": ms, "transforms_per_s": 1e3 / ms, "points_per_s": M / (ms / 1e3),
+            "canonical_gflop": gflop, "fraction_of_fp64_roofline_datasheet": gflop / (ms / 1e3) / 1e3 / FP64_PEAK_DATASHEET,
+            "frac_of_measured_dmma_peak": gflop / (ms / 1e3) / 1e3 / FP64_PEAK_MEASURED,
+            "scaling": "strong", "rel_l2_vs_oracle_64_points": rel}
+
+
+def c4_detail(args, rank, world, dev, dist, timed, barrier, max_over_ranks):
+    """BASELINE configs[3]: one L=4096 field (4098 x 8196 grid), forward then adjoint
+    per step.  N > 1: order-sharded over the ranks (dist.py: ring-sharded field,
+    m-sharded contraction, one NCCL all-to-all per direction).  Rank 0 also times
+    the single-GPU plan on the same field (the strong-scaling reference)."""
+    import torch
+
+    import oracle.favest_oracle as O  # seeded generators only
+    from paper_1908_00041_b200.grid import gl_grid_for
+    from paper_1908_00041_b200.plan import GridPlan
+
+    L4 = 4096
+    grid, _ = gl_grid_for(L4)
+    rng = np.random.default_rng(4)
+    A, Bc = O.coef(rng, L4, "pow2")
+    a_full = torch.from_numpy(A[None]).to(dev)
+    b_full = torch.from_numpy(Bc[None]).to(dev)
+    n = args.c4_steps
+    fl = canonical_flops(L4, 1)
+    out = {"workload": "C4 (BASELINE configs[3]): L=4096 Gauss-Legendre 4098x8196 grid, one field, forward then "
+                       "adjoint per step", "steps": n, "canonical_gflop_per_direction": fl["total"] / 1e9}
+    if world > 1:
+        from paper_1908_00041_b200.dist import make_plan
+
+        sp = make_plan(L4, grid, 1, rank, world, dev)
+        T_local = sp.adjoint(a_full, b_full)
+        a = torch.zeros_like(a_full)
+        b = torch.zeros_like(b_full)
+        Tout = torch.empty_like(T_local)
+
+        def step():
+            sp.forward(T_local, a, b)
+            sp.adjoint(a, b, Tout)
+
+        for _ in range(2):
+            step()
+        ms = timed(step, n)
+        rel = float(torch.linalg.vector_norm(Tout - T_local) / torch.linalg.vector_norm(T_local))
+        out.update({"sharded_ms_per_step": ms, "parallelism": f"order-sharded x{world} (NCCL all-to-all per direction)",
+                    "rank0_rings": list(sp.me.rings), "rank0_orders": list(sp.me.orders),
+                    "roundtrip_rel_l2": max_over_ranks(rel),
+                    "sharded_fraction_of_fp64_roofline_datasheet":
+                        (2 * fl["total"] / (ms / 1e3)) / (FP64_PEAK_DATASHEET * 1e12 * world)})
+        del sp, T_local, Tout, a, b
+        torch.cuda.empty_cache()
+    barrier()
+    if rank == 0:
+        plan = GridPlan.from_grid(grid, L4, max_batch=1, device=dev)
+        T = plan.adjoint(a_full, b_full)
+        a = torch.empty_like(a_full)
+        b = torch.empty_like(b_full)
+        Tout = torch.empty_like(T)
+
+        def step1():
+            plan.forward(T, a, b)
+            plan.adjoint(a, b, Tout)
+
+        for _ in range(2):
+            step1()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        st = torch.cuda.current_stream(dev)
+        torch.cuda.synchronize(dev)
+        s0.record(st)
+        for _ in range(n):
+            step1()
+        s1.record(st)
+        torch.cuda.synchronize(dev)
+        ms1 = s0.elapsed_time(s1) / n
+        rel1 = float(torch.linalg.vector_norm(Tout - T) / torch.linalg.vector_norm(T))
+        plan.close()
+        del T, Tout, a, b
+        torch.cuda.empty_cache()
+        out.update({"single_gpu_ms_per_step": ms1, "single_gpu_roundtrip_rel_l2": rel1,
+                    "single_gpu_fraction_of_fp64_roofline_datasheet":
+                        (2 * fl["total"] / (ms1 / 1e3)) / (FP64_PEAK_DATASHEET * 1e12)})
+        if world > 1:
+            out["speedup_vs_single_gpu"] = ms1 / out["sharded_ms_per_step"]
+    barrier()
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -531,6 +723,20 @@ def run_c4(args, rank, world, local_rank):
     dist.destroy_process_group()
 
 
+def relaunch(n: int):
+    """``--gpus N`` without a torchrun environment: re-execute this script under
+    ``torch.distributed.run`` with N processes on this node (127.0.0.1 rendezvous)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--gpus", type=int, default=1)
@@ -539,15 +745,26 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--L", type=int, default=1024)
     ap.add_argument("--batch", type=int, default=4, help="fields per GPU")
-    ap.add_argument("--ref-every", type=int, default=8, help="order stride of the CPU sample")
+    ap.add_argument("--cpu-fields", type=int, default=3, help="whole fields timed for cpu_baseline")
+    ap.add_argument("--c4-steps", type=int, default=5, help="timed steps of the C4 detail entry")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-detail", action="store_true", help="skip the on-the-fly / C5 / C4 detail entries")
     ap.add_argument("--workload", default="c3", choices=["c3", "c4"],
                     help="c3: batch-sharded L=1024 (the headline); c4: one L=4096 field, order-sharded")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        relaunch(args.gpus)  # does not return
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} launched with WORLD_SIZE={world}")
+    if world > 1:
+        # communicator set-up lines (ranks, NVLink/NVLS transport) on stderr, stdout keeps the JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.impl == "reference":
         run_reference(args, rank, world)
     elif args.workload == "c4":

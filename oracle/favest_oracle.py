@@ -31,7 +31,7 @@ import numpy as np
 __all__ = [
     "FOUR_PI", "INV_SQRT_4PI", "INV_SQRT2", "flat_size", "degrees_orders", "tri_index",
     "gl_grid", "grid_points", "ring_cos_sin", "seed_table", "recurrence_ab", "legendre_m",
-    "legendre_table", "sht_forward_grid", "sht_adjoint_grid", "sht_adjoint_points",
+    "legendre_table", "sht_forward_grid", "sht_adjoint_grid", "forward_order", "adjoint_order", "sht_adjoint_points",
     "sht_forward_points", "vsht_forward_points", "verify_exactness",
     "cg_explicit_vec", "cg_tables", "shift_read", "vsht_forward_grid", "vsht_adjoint_merged",
     "vsht_adjoint_grid", "vsht_adjoint_points", "coef", "random_points", "tangent_noise",
@@ -237,14 +237,24 @@ def sht_forward_grid(f, ring_thetas, ring_weights, n_phi, lt, orders=None):
     out = np.zeros((flat_size(lt), C), dtype=np.complex128)
     ms_iter = range(lt + 1) if orders is None else sorted(set(int(x) for x in orders))
     for m in ms_iter:
-        P = legendre_m(m, lt, t, sx[m], se[m])  # (n_l, n_theta)
-        ls = np.arange(m, lt + 1)
-        for sgn in ((1,) if m == 0 else (1, -1)):
-            mm = sgn * m
-            g = w[:, None] * spec[:, mm % n_phi, :]  # scalar.py:151-152
-            res = P @ g.real + 1j * (P @ g.imag)
-            out[ls * ls + ls + mm] = _sigma(mm) * res
+        for mm, rows in forward_order(m, spec, w, t, sx, se, lt):
+            ls = np.arange(m, lt + 1)
+            out[ls * ls + ls + mm] = rows
     return out
+
+
+def forward_order(m, spec, w, t, sx, se, lt):
+    """The per-order stage of sht_forward_grid (favest/scalar.py:150-153) from
+    the ring spectra ``spec`` (n_theta, n_phi, C): [(+m, rows), (-m, rows)] with
+    rows (lt+1-m, C) = sigma_m * sum_r Pbar_l^m(t_r) w_r spec[r, m mod n_phi]."""
+    n_phi = spec.shape[1]
+    P = legendre_m(m, lt, t, sx[m], se[m])  # (n_l, n_theta)
+    res = []
+    for sgn in ((1,) if m == 0 else (1, -1)):
+        mm = sgn * m
+        g = w[:, None] * spec[:, mm % n_phi, :]  # scalar.py:151-152
+        res.append((mm, _sigma(mm) * (P @ g.real + 1j * (P @ g.imag))))
+    return res
 
 
 def sht_adjoint_grid(g, lt, ring_thetas, n_phi, orders=None, spectrum=False):
@@ -263,16 +273,26 @@ def sht_adjoint_grid(g, lt, ring_thetas, n_phi, orders=None, spectrum=False):
     spec = np.zeros((n_theta, n_phi, C), dtype=np.complex128)
     ms_iter = range(lt + 1) if orders is None else sorted(set(int(x) for x in orders))
     for m in ms_iter:
-        P = legendre_m(m, lt, t, sx[m], se[m])  # (n_l, n_theta)
-        ls = np.arange(m, lt + 1)
-        for sgn in ((1,) if m == 0 else (1, -1)):
-            mm = sgn * m
-            cols = _sigma(mm) * g[ls * ls + ls + mm]  # (n_l, C)
-            spec[:, mm % n_phi, :] = P.T @ cols.real + 1j * (P.T @ cols.imag)
+        for mm, col in adjoint_order(m, g, t, sx, se, lt):
+            spec[:, mm % n_phi, :] = col
     if spectrum:  # ring spectra before the inverse DFT: (n_theta, n_phi, C)
         return spec
     out = np.fft.ifft(spec, axis=1) * n_phi
     return out.reshape(n_theta * n_phi, C)
+
+
+def adjoint_order(m, g, t, sx, se, lt):
+    """The per-order stage of sht_adjoint_grid (favest/scalar.py:174-176):
+    [(+m, bins), (-m, bins)] with bins (n_theta, C) = sum_l Pbar_l^m(t_r)
+    sigma_m g_{l,m}."""
+    P = legendre_m(m, lt, t, sx[m], se[m])  # (n_l, n_theta)
+    ls = np.arange(m, lt + 1)
+    res = []
+    for sgn in ((1,) if m == 0 else (1, -1)):
+        mm = sgn * m
+        cols = _sigma(mm) * g[ls * ls + ls + mm]  # (n_l, C)
+        res.append((mm, P.T @ cols.real + 1j * (P.T @ cols.imag)))
+    return res
 
 
 def sht_adjoint_points(g, lt, points):

@@ -4,6 +4,7 @@
 #include <cufft.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -324,23 +325,27 @@ int get_fft_strided(fvPlan* p, long long irs, long long ies, long long ors, long
   return FV_OK;
 }
 
-// cudaFuncSetAttribute once per (kernel instantiation, device)
-bool first_use(unsigned long long* mask, int device) {
+// Opt a kernel into 227 KB of dynamic shared memory once per (kernel
+// instantiation, device).  The device's bit is published only after the
+// attribute call succeeded (a failure is retried by the next launch), and with
+// release / acquire ordering, so a second host thread never launches before
+// the attribute is set; two threads racing on the first launch both make the
+// (idempotent) call.
+template <class K>
+cudaError_t smem_optin_once(std::atomic<unsigned long long>* mask, int device, K kernel) {
   const unsigned long long bit = 1ull << (device & 63);
-  if (*mask & bit) return false;
-  *mask |= bit;
-  return true;
+  if (mask->load(std::memory_order_acquire) & bit) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  if (e == cudaSuccess) mask->fetch_or(bit, std::memory_order_acq_rel);
+  return e;
 }
 
 template <int NT>
 int launch_fwd(fvPlan* p, const fv::FwdArgs& args, int m_count, cudaStream_t s) {
-  static unsigned long long attr = 0;
+  static std::atomic<unsigned long long> attr{0};
   const size_t bytes = fv::FwdSmem<NT>::bytes(p->nchunks * fv::FWD_RC);
   if (bytes > 227 * 1024) return fail(FV_EINVAL, "grid too large for the forward kernel's shared memory");
-  if (first_use(&attr, p->device)) {
-    FV_CUDA(cudaFuncSetAttribute(fv::legendre_fwd_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 227 * 1024));
-  }
+  FV_CUDA(smem_optin_once(&attr, p->device, fv::legendre_fwd_kernel<NT>));
   fv::FwdArgs a2 = args;
   a2.m_count = m_count;
   // one CTA per order: the hardware block scheduler hands out orders in ascending m
@@ -352,12 +357,9 @@ int launch_fwd(fvPlan* p, const fv::FwdArgs& args, int m_count, cudaStream_t s) 
 
 template <int NT>
 int launch_adj(fvPlan* p, const fv::AdjArgs& args, int m_count, cudaStream_t s) {
-  static unsigned long long attr = 0;
+  static std::atomic<unsigned long long> attr{0};
   const size_t bytes = fv::AdjSmem<NT>::bytes();
-  if (first_use(&attr, p->device)) {
-    FV_CUDA(cudaFuncSetAttribute(fv::legendre_adj_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 227 * 1024));
-  }
+  FV_CUDA(smem_optin_once(&attr, p->device, fv::legendre_adj_kernel<NT>));
   if (bytes > 227 * 1024) return fail(FV_EINVAL, "adjoint kernel shared memory exceeds 227 KB");
   fv::AdjArgs a2 = args;
   a2.m_count = m_count;
@@ -366,10 +368,8 @@ int launch_adj(fvPlan* p, const fv::AdjArgs& args, int m_count, cudaStream_t s) 
     // (FV_ADJ_DUAL=0 keeps one chunk per item)
     static const bool dual = [] { const char* e = std::getenv("FV_ADJ_DUAL"); return !(e && std::atoi(e) == 0); }();
     if (dual && !args.ptab) {
-      static unsigned long long attr2 = 0;
-      if (first_use(&attr2, p->device))
-        FV_CUDA(cudaFuncSetAttribute(fv::legendre_adj_dual_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     227 * 1024));
+      static std::atomic<unsigned long long> attr2{0};
+      FV_CUDA(smem_optin_once(&attr2, p->device, fv::legendre_adj_dual_kernel<NT>));
       const int items2 = m_count * ((p->nrc + 1) / 2);
       fv::legendre_adj_dual_kernel<NT><<<std::min(items2, p->num_sms), fv::kThreads, bytes, s>>>(a2);
       FV_CUDA(cudaGetLastError());
@@ -1668,11 +1668,9 @@ int grow(double** buf, size_t* cap, size_t n) {
 
 template <int NF>
 int launch_fpts(fvPlan* p, const fv::FptsArgs& fa, unsigned grid, cudaStream_t s) {
-  static unsigned long long attr = 0;
+  static std::atomic<unsigned long long> attr{0};
   const size_t smem = fv::fpd_smem_bytes(NF, p->Lt);
-  if (first_use(&attr, p->device))
-    FV_CUDA(cudaFuncSetAttribute(fv::forward_points_dmma_kernel<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 227 * 1024));
+  FV_CUDA(smem_optin_once(&attr, p->device, fv::forward_points_dmma_kernel<NF>));
   fv::forward_points_dmma_kernel<NF><<<grid, fv::FPD_THREADS, smem, s>>>(fa);
   FV_CUDA(cudaGetLastError());
   return FV_OK;

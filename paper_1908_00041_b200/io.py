@@ -172,14 +172,19 @@ def read_samples(path) -> TangentFieldSamples:
 def write_csv(path, header, rows) -> None:
     """CSV table with floats at 17 significant digits (favest/io.py:136-145);
     all-float tables go through the native formatter, mixed rows through csv."""
+    import csv
+    import io as _io
+
     rows = list(rows)
-    if rows and all(type(v) is float or isinstance(v, np.floating) for r in rows for v in r) \
-            and len({len(r) for r in rows}) == 1:
+    # the native formatter only for values the reference formats itself (isinstance
+    # float: Python floats and np.float64, not np.float32, which csv writes as str())
+    if rows and all(isinstance(v, float) for r in rows for v in r) and len({len(r) for r in rows}) == 1:
+        head = _io.StringIO(newline="")
+        csv.writer(head).writerow(header)  # csv quoting of header fields, as the reference
         with open(path, "wb") as fh:
-            fh.write((",".join(str(h) for h in header) + "\r\n").encode())
+            fh.write(head.getvalue().encode())
             fh.write(_table_text(np.asarray(rows, dtype=np.float64), ",", True))
         return
-    import csv
 
     with open(path, "w", newline="") as fh:
         writer = csv.writer(fh)

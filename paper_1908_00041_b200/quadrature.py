@@ -24,28 +24,31 @@ def load_design(path, t: int) -> QuadratureRule:
     return QuadratureRule(points=points, weights=np.full(n, FOUR_PI / n), exactness=t, kind="spherical-design")
 
 
+# favest/data/icosahedron12.txt, in file order: the two coordinates as the
+# data file spells them (17 significant digits); row k is the sign triple
+# _ICO_ROWS[k] times the magnitudes (0, A, B), (A, B, 0), (B, 0, A) for k mod 3.
+_ICO_A = 0.52573111211913359
+_ICO_B = 0.85065080835203999
+_ICO_ROWS = (
+    (0, 1, 1), (1, 1, 0), (1, 0, 1), (0, 1, -1), (1, -1, 0), (-1, 0, 1),
+    (0, -1, 1), (-1, 1, 0), (1, 0, -1), (0, -1, -1), (-1, -1, 0), (-1, 0, -1),
+)
+
+
 def _icosahedron() -> np.ndarray:
-    """The 12 vertices (0, +-1, +-phi) and cyclic permutations, on the unit sphere."""
-    phi = (1.0 + np.sqrt(5.0)) / 2.0
-    base = []
-    for s1 in (1.0, -1.0):
-        for s2 in (1.0, -1.0):
-            base.append((0.0, s1, s2 * phi))
-    pts = []
-    for k in range(3):
-        for v in base:
-            pts.append(np.roll(v, k))
-    pts = np.array(pts)
-    return pts / np.linalg.norm(pts, axis=1, keepdims=True)
+    """The reference's bundled 12-point design, row for row, through the same
+    renormalisation as load_design (favest/quadrature.py:79-109,134-139)."""
+    pattern = ((0.0, _ICO_A, _ICO_B), (_ICO_A, _ICO_B, 0.0), (_ICO_B, 0.0, _ICO_A))
+    rows = [[sg * mag for sg, mag in zip(signs, pattern[k % 3])] for k, signs in enumerate(_ICO_ROWS)]
+    return renormalize(np.array(rows, dtype=np.float64), "icosahedron12.txt")
 
 
 _BUNDLED = {"icosahedron12": (_icosahedron, 5)}
 
 
 def bundled_design(name: str = "icosahedron12") -> QuadratureRule:
-    """A design shipped with the package (favest/quadrature.py:100-109); the
-    icosahedron is generated from its closed form (vertex order may differ
-    from the reference's data file; the set is the same to 1 ulp)."""
+    """A design shipped with the package (favest/quadrature.py:100-109): the
+    icosahedron has the reference data file's rows, order and values."""
     try:
         make, t = _BUNDLED[name]
     except KeyError:

@@ -18,6 +18,7 @@ Routes (reference: ``_pick_path``, favest/transforms.py:59-76):
 from __future__ import annotations
 
 import hashlib
+import threading
 from collections import OrderedDict
 
 import numpy as np
@@ -33,7 +34,15 @@ from .grid import TensorGrid
 
 PATHS = ("auto", "direct-scalar", "fast-scalar")
 
+# Plan cache.  Thread safety: _PLANS_LOCK guards the dictionary; every cached
+# plan carries a ``call_lock`` that the entry points hold for a whole call
+# (upload, kernels, download), because one plan's workspaces serve one call at a
+# time (include/favest_b200.h).  Evicted or outgrown plans are only dropped from
+# the cache, never closed here: a caller may still hold one (grid_plan() /
+# points_plan() are public), and the plan frees its device memory when the
+# last reference goes.
 _PLANS: "OrderedDict[tuple, object]" = OrderedDict()
+_PLANS_LOCK = threading.Lock()
 _MAX_PLANS = 8
 
 
@@ -76,17 +85,16 @@ def _grid_key(grid, lmax, device):
 
 
 def _cached(key, make, batch):
-    plan = _PLANS.get(key)
-    if plan is None or plan.max_batch < batch:
-        if plan is not None:
-            plan.close()
-        plan = make(max(batch, plan.max_batch if plan is not None else 1))
-        _PLANS[key] = plan
-    _PLANS.move_to_end(key)
-    while len(_PLANS) > _MAX_PLANS:
-        _, old = _PLANS.popitem(last=False)
-        old.close()
-    return plan
+    with _PLANS_LOCK:
+        plan = _PLANS.get(key)
+        if plan is None or plan.max_batch < batch:
+            plan = make(max(batch, plan.max_batch if plan is not None else 1))
+            plan.call_lock = threading.Lock()
+            _PLANS[key] = plan
+        _PLANS.move_to_end(key)
+        while len(_PLANS) > _MAX_PLANS:
+            _PLANS.popitem(last=False)
+        return plan
 
 
 def grid_plan(grid, lmax, batch=1, device=None):
@@ -107,28 +115,17 @@ def points_plan(lmax, batch=1, device=None):
 
 
 def _to_device(arr: np.ndarray, device):
-    """Host array -> device tensor through a pinned staging block from torch's
-    caching host allocator (a parallel host copy into resident pinned pages,
-    then a DMA at link speed, instead of the driver's pageable staging)."""
-    import torch
+    """Host array -> device tensor through the pipelined pinned stager (staging.py)."""
+    from .staging import stager
 
-    src = torch.from_numpy(np.ascontiguousarray(arr))
-    if src.numel() * src.element_size() < (1 << 22):
-        return src.to(device)
-    stage = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
-    stage.copy_(src)
-    return stage.to(device, non_blocking=True)
+    return stager(device).to_device(arr)
 
 
 def _to_host(x) -> np.ndarray:
-    """Device tensor -> numpy array backed by pinned host memory (torch's
-    caching host allocator: steady-state calls reuse resident pinned blocks, so
-    the copy runs at PCIe / C2C speed instead of through pageable staging)."""
-    import torch
+    """Device tensor -> new pageable numpy array through the pipelined pinned stager."""
+    from .staging import stager
 
-    out = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
-    out.copy_(x)
-    return out.numpy()
+    return stager(x.device).to_host(x)
 
 
 def _check_tables(tables, lmax):
@@ -145,23 +142,25 @@ def forward_favest(samples, rule, lmax: int, path: str = "auto", tables=None) ->
         raise ValueError(f"vector transforms need lmax >= 1, got {lmax}")
     spts = np.asarray(samples.points)
     rpts = np.asarray(rule.points)
-    if spts.shape != rpts.shape or not (np.array_equal(spts, rpts) or np.allclose(spts, rpts, rtol=0.0, atol=1e-12)):
+    # samples built on the rule's own point array (the usual case) need no O(N) check
+    if spts is not rpts and (spts.shape != rpts.shape or not (
+            np.array_equal(spts, rpts) or np.allclose(spts, rpts, rtol=0.0, atol=1e-12))):
         raise ValueError("sample points do not match the quadrature rule points")
     grid = getattr(rule, "grid", None)
     use_fast = _pick_path(path, grid, lmax)
     _check_tables(tables, lmax)
     vals = np.ascontiguousarray(samples.values, dtype=np.complex128).reshape(1, -1, 3)
-    if use_fast:
-        plan = grid_plan(grid, lmax)
-        a, b = plan.forward(_to_device(vals, plan.device))
-    else:  # direct route on the rule's own points and weights (favest/scalar.py:94-105)
-        plan = points_plan(lmax)
-        xyz = torch.from_numpy(np.ascontiguousarray(rpts, dtype=np.float64)).to(plan.device)
-        w = torch.from_numpy(np.ascontiguousarray(rule.weights, dtype=np.float64)).to(plan.device)
-        a, b = plan.forward(xyz, w, _to_device(vals, plan.device))
-    a = _to_host(a[0])
-    b = _to_host(b[0])
-    return VectorCoefficients(ScalarCoefficients(lmax, a), ScalarCoefficients(lmax, b))
+    plan = grid_plan(grid, lmax) if use_fast else points_plan(lmax)
+    with plan.call_lock, torch.cuda.device(plan.device):
+        if use_fast:
+            a, b = plan.forward(_to_device(vals, plan.device))
+        else:  # direct route on the rule's own points and weights (favest/scalar.py:94-105)
+            xyz = _to_device(np.ascontiguousarray(rpts, dtype=np.float64), plan.device)
+            w = _to_device(np.ascontiguousarray(rule.weights, dtype=np.float64), plan.device)
+            a, b = plan.forward(xyz, w, _to_device(vals, plan.device))
+        a = _to_host(a[0])
+        b = _to_host(b[0])
+    return VectorCoefficients(ScalarCoefficients._trusted(lmax, a), ScalarCoefficients._trusted(lmax, b))
 
 
 def adjoint_favest(coeffs, rule_or_points, path: str = "auto", tables=None) -> TangentFieldSamples:
@@ -173,18 +172,18 @@ def adjoint_favest(coeffs, rule_or_points, path: str = "auto", tables=None) -> T
     lmax = coeffs.lmax
     use_fast = _pick_path(path, grid, lmax)
     _check_tables(tables, lmax)
-    a = torch.from_numpy(np.ascontiguousarray(coeffs.div.values, dtype=np.complex128)).reshape(1, -1)
-    b = torch.from_numpy(np.ascontiguousarray(coeffs.curl.values, dtype=np.complex128)).reshape(1, -1)
-    if use_fast:
-        plan = grid_plan(grid, lmax)
-        T = plan.adjoint(a.to(plan.device), b.to(plan.device))
+    a = np.ascontiguousarray(coeffs.div.values, dtype=np.complex128).reshape(1, -1)
+    b = np.ascontiguousarray(coeffs.curl.values, dtype=np.complex128).reshape(1, -1)
+    plan = grid_plan(grid, lmax) if use_fast else points_plan(lmax)
+    with plan.call_lock, torch.cuda.device(plan.device):
+        a_d, b_d = _to_device(a, plan.device), _to_device(b, plan.device)
+        if use_fast:
+            T = plan.adjoint(a_d, b_d)
+        else:
+            T = plan.adjoint(_to_device(np.ascontiguousarray(points, dtype=np.float64), plan.device), a_d, b_d)
         values = _to_host(T[0])
-    else:
-        plan = points_plan(lmax)
-        xyz = torch.from_numpy(np.ascontiguousarray(points, dtype=np.float64)).to(plan.device)
-        T = plan.adjoint(xyz, a.to(plan.device), b.to(plan.device))
-        values = _to_host(T[0])
-    return TangentFieldSamples(points=points, values=values)
+    # points came from a validated rule / grid, or were checked by _resolve_grid
+    return TangentFieldSamples._trusted(points, values)
 
 
 __all__ = [

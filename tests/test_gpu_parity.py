@@ -109,34 +109,76 @@ def test_c2_batch_l256_against_oracle():
     assert err <= 1e-10
 
 
-def test_c3_headline_spot_orders():
-    # BASELINE configs[2]: L=1024, 4 fields, (1+l)^-2 spectrum (seed 3) + tangent noise sigma=1e-3
-    torch = cuda_or_skip()
-    L, B = 1024, 4
+def test_c2_field0_against_reference_fixture(golden):
+    """The unmodified reference's own C2 field (L=256, tests/golden/make_golden_large.py):
+    adjoint of the seeded coefficients and forward of the reference's field, every value."""
+    d = golden("c2_l256_field0")
+    L = int(d["lmax"])
     th, w, nphi = O.gl_grid(L)
+    plan = _plan(L, th, w, nphi, 1)
+    T = plan.adjoint(_t(d["a"][None]), _t(d["b"][None])).cpu().numpy()[0]
+    assert O.rel_l2(T, d["T"]) <= TOL
+    fa, fb_ = plan.forward(_t(d["T"][None]))
+    got = np.concatenate([fa[0].cpu().numpy(), fb_[0].cpu().numpy()])
+    assert O.rel_l2(got, np.concatenate([d["fa"], d["fb"]])) <= TOL
+
+
+def test_c3_field0_against_reference_fixture(golden):
+    """The unmodified reference at the headline size (L=1024, C3 field 0): the adjoint on 13
+    rings plus per-ring sums / norms of all 1026 rings, the forward (reference run
+    ring-chunked) at every degree of 24 orders plus per-order norms of all 2049 orders."""
+    from test_oracle import c3_field0_inputs, order_norms
+
+    d = golden("c3_l1024_field0")
+    L = int(d["lmax"])
+    a, b, rng = c3_field0_inputs(d)
+    th, w, nphi = O.gl_grid(L)
+    plan = _plan(L, th, w, nphi, 1)
+    T = plan.adjoint(_t(a[None]), _t(b[None])).cpu().numpy()[0]
+    Tr = T.reshape(L + 2, nphi, 3)
+    assert O.rel_l2(Tr[d["rings"]], d["T_rings"]) <= TOL
+    assert O.rel_l2(Tr.sum(axis=1), d["ring_sum"]) <= TOL
+    assert np.max(np.abs(np.sqrt((np.abs(Tr) ** 2).sum(axis=(1, 2))) / d["ring_norm"] - 1)) <= TOL
+    T = T + O.tangent_noise(rng, O.grid_points(th, nphi), float(d["noise_sigma"]))
+    fa, fb_ = plan.forward(_t(T[None]))
+    fa, fb_ = fa[0].cpu().numpy(), fb_[0].cpu().numpy()
+    idx = d["flat_idx"]
+    assert O.rel_l2(np.concatenate([fa[idx], fb_[idx]]), np.concatenate([d["fa_sel"], d["fb_sel"]])) <= TOL
+    assert O.rel_l2(order_norms(fa, L), d["fa_order_norm"]) <= TOL
+    assert O.rel_l2(order_norms(fb_, L), d["fb_order_norm"]) <= TOL
+
+
+def _c3_inputs():
+    L, B = 1024, 4
     rng = np.random.default_rng(3)
     ab = [O.coef(rng, L, "pow2") for _ in range(B)]
-    A = np.stack([x[0] for x in ab])
-    Bc = np.stack([x[1] for x in ab])
+    return L, B, rng, np.stack([x[0] for x in ab]), np.stack([x[1] for x in ab])
+
+
+@pytest.mark.parametrize("ptab", ["table", "on_the_fly"])
+def test_c3_headline_every_order_against_oracle(ptab, monkeypatch):
+    """BASELINE configs[2]: L=1024, 4 fields, (1+l)^-2 spectrum (seed 3) + tangent noise
+    sigma=1e-3.  Every value of all 4 fields, adjoint and forward, against the oracle
+    (run over all host cores by oracle/parallel.py), for both Legendre producers."""
+    from oracle.parallel import GridPort
+
+    torch = cuda_or_skip()
+    L, B, rng, A, Bc = _c3_inputs()
+    th, w, nphi = O.gl_grid(L)
+    if ptab == "on_the_fly":
+        monkeypatch.setenv("FV_PTAB", "0")
     plan = _plan(L, th, w, nphi, B)
+    monkeypatch.delenv("FV_PTAB", raising=False)
     T = plan.adjoint(_t(A), _t(Bc)).cpu().numpy()
-    orders = [0, 1, 2, 77, 511, 1000, 1023, 1024, 1025]
-    for k in (0, 3):
-        spec = np.fft.fft(T[k].reshape(L + 2, nphi, 3), axis=1) / nphi
-        ref = O.vsht_adjoint_grid(A[k], Bc[k], L, th, nphi, orders=orders, spectrum=True)
-        bins = sorted({m % nphi for m in orders} | {(-m) % nphi for m in orders})
-        assert O.rel_l2(spec[:, bins], ref[:, bins]) <= TOL
     pts = O.grid_points(th, nphi)
     Tin = T + np.stack([O.tangent_noise(rng, pts, 1e-3) for _ in range(B)])
     fa, fb_ = plan.forward(_t(Tin))
     fa, fb_ = fa.cpu().numpy(), fb_.cpu().numpy()
-    ls, ms = O.degrees_orders(L)
-    out_orders = [0, 1, 2, 77, 511, 1000, 1023, 1024]
-    sel = np.isin(np.abs(ms), out_orders)
-    for k in (0, 2):
-        ra, rb = O.vsht_forward_grid(Tin[k], th, w, nphi, L, orders=out_orders)
-        got = np.concatenate([fa[k][sel], fb_[k][sel]])
-        assert O.rel_l2(got, np.concatenate([ra[sel], rb[sel]])) <= TOL
+    port = GridPort(L)
+    for k in range(B):
+        assert O.rel_l2(T[k], port.adjoint(A[k], Bc[k])) <= TOL, k
+        ra, rb = port.forward(Tin[k])
+        assert O.rel_l2(np.concatenate([fa[k], fb_[k]]), np.concatenate([ra, rb])) <= TOL, k
     # size-independent property over the full batch: adjoint -> forward recovers the spectrum
     fa2, fb2 = plan.forward(_t(T))
     err = O.rel_l2(np.concatenate([fa2.cpu().numpy(), fb2.cpu().numpy()], 1), np.concatenate([A, Bc], 1))
@@ -144,33 +186,40 @@ def test_c3_headline_spot_orders():
     torch.cuda.synchronize()
 
 
-def test_c4_l4096_spot_orders_and_roundtrip():
+def test_c4_l4096_strided_orders_and_roundtrip():
     """BASELINE configs[3] (L=4096, one field, (1+l)^-2 spectrum, seed 4) on one GPU: on-the-fly
-    Legendre producer (the tables exceed the plan budget), cuFFT ring FFTs (8196 = 4*3*683).
-    Spot orders against the extended-range oracle, plus the adjoint -> forward round trip."""
+    Legendre producer (the tables exceed the plan budget), large-prime ring DFTs (8196 = 12*683).
+    Every 8th order plus the first and last 64 orders against the extended-range oracle
+    (oracle/parallel.py over all host cores), adjoint in spectral space and forward, plus the
+    adjoint -> forward round trip over every order."""
+    from oracle.parallel import GridPort
+
     torch = cuda_or_skip()
     L = 4096
-    th, w, nphi = O.gl_grid(L)
+    Lt = L + 1
     rng = np.random.default_rng(4)
     A, Bc = O.coef(rng, L, "pow2")
+    port = GridPort(L)
+    th, w, nphi = port.th, port.w, port.n_phi
     plan = _plan(L, th, w, nphi, 1)
     T = plan.adjoint(_t(A[None]), _t(Bc[None]))
-    orders = [0, 1, 999, 2048, 4000, 4096, 4097]
+    orders = sorted(set(range(0, Lt + 1, 8)) | set(range(64)) | set(range(Lt + 1 - 64, Lt + 1)))
+    bins = np.array(sorted({m % nphi for m in orders} | {(-m) % nphi for m in orders}))
     spec = torch.fft.fft(T[0].reshape(L + 2, nphi, 3), dim=1).div_(nphi)
-    bins = sorted({m % nphi for m in orders} | {(-m) % nphi for m in orders})
-    spec = spec[:, bins].cpu().numpy()
-    ref = O.vsht_adjoint_grid(A, Bc, L, th, nphi, orders=orders, spectrum=True)
-    assert O.rel_l2(spec, ref[:, bins]) <= TOL
+    spec = spec[:, torch.from_numpy(bins).cuda()].cpu().numpy()
+    ref = port.adjoint(A, Bc, orders=orders, spectrum=True)[:, bins]
+    assert O.rel_l2(spec, ref) <= TOL
+    del spec, ref
     fa, fb_ = plan.forward(T)
-    ls, ms = O.degrees_orders(L)
-    out_orders = [0, 1, 999, 2048, 4000, 4096]
-    sel = np.isin(np.abs(ms), out_orders)
     Tn = T[0].cpu().numpy()
     del T
-    ra, rb = O.vsht_forward_grid(Tn, th, w, nphi, L, orders=out_orders)
-    got = np.concatenate([fa[0].cpu().numpy()[sel], fb_[0].cpu().numpy()[sel]])
-    assert O.rel_l2(got, np.concatenate([ra[sel], rb[sel]])) <= TOL
-    err = O.rel_l2(np.concatenate([fa[0].cpu().numpy(), fb_[0].cpu().numpy()]), np.concatenate([A, Bc]))
+    out_orders = [m for m in orders if m <= L]
+    ra, rb = port.forward(Tn, orders=out_orders)
+    ls, ms = O.degrees_orders(L)
+    sel = np.isin(np.abs(ms), out_orders)
+    fa, fb_ = fa[0].cpu().numpy(), fb_[0].cpu().numpy()
+    assert O.rel_l2(np.concatenate([fa[sel], fb_[sel]]), np.concatenate([ra[sel], rb[sel]])) <= TOL
+    err = O.rel_l2(np.concatenate([fa, fb_]), np.concatenate([A, Bc]))
     assert err <= 1e-9  # scipy GL weights at n=4098 bound the round trip, not the kernels
     torch.cuda.synchronize()
 
@@ -276,7 +325,7 @@ def test_c5_scattered_subset_against_oracle():
     a, b = O.coef(rng, L, "inv")
     pp = PointsPlan(L)
     T = pp.adjoint(_t(pts), _t(a[None]), _t(b[None])).cpu().numpy()[0]
-    idx = np.r_[0:1500, M - 500:M]
+    idx = np.r_[0:12000, M - 8000:M]  # >= 20k of the 200k points
     ref = O.vsht_adjoint_points(a, b, L, pts[idx])
     assert O.rel_l2(T[idx], ref) <= TOL
     # near-pole points exercise the extended-range seeds

@@ -157,3 +157,82 @@ def test_verify_exactness_against_reference(golden):
         dd, okk = O.verify_exactness(g[f"{name}_points"], g[f"{name}_weights"], int(t))
         assert okk == bool(ok)
         assert abs(dd - d) <= 1e-13 + 1e-12 * d
+
+
+# --------------------------------------------------------------------------
+# pins at the BASELINE sizes: fixtures the unmodified reference wrote at L=256
+# (the whole C2 field 0) and L=1024 (C3 field 0: 13 rings, 24 orders, and
+# checksums over every ring / order), tests/golden/make_golden_large.py
+# --------------------------------------------------------------------------
+def c3_field0_inputs(d):
+    """The C3 field-0 inputs of make_golden_large.py, regenerated from the seed:
+    (a, b, noise generator positioned after the coefficients)."""
+    rng = np.random.default_rng(int(d["seed"]))
+    a, b = O.coef(rng, int(d["lmax"]), str(d["law"]))
+    assert a.sum() == d["a_sum"] and b.sum() == d["b_sum"]  # same PCG64 stream, bitwise
+    return a, b, rng
+
+
+def order_norms(v, lmax):
+    ls, ms = O.degrees_orders(lmax)
+    out = np.zeros(2 * lmax + 1)
+    np.add.at(out, ms + lmax, np.abs(v) ** 2)
+    return np.sqrt(out)
+
+
+def test_oracle_c2_l256_full_field_against_reference(golden):
+    d = golden("c2_l256_field0")
+    L = int(d["lmax"])
+    rng = np.random.default_rng(int(d["seed"]))
+    a, b = O.coef(rng, L, str(d["law"]))
+    assert np.array_equal(a, d["a"]) and np.array_equal(b, d["b"])
+    th, w, nphi = O.gl_grid(L)
+    T = O.vsht_adjoint_grid(a, b, L, th, nphi)
+    assert O.rel_l2(T, d["T"]) <= 1e-13
+    fa, fb = O.vsht_forward_grid(d["T"], th, w, nphi, L)
+    assert O.rel_l2(np.concatenate([fa, fb]), np.concatenate([d["fa"], d["fb"]])) <= 1e-13
+
+
+def test_oracle_c3_l1024_against_reference(golden):
+    from oracle.parallel import GridPort
+
+    d = golden("c3_l1024_field0")
+    L = int(d["lmax"])
+    a, b, rng = c3_field0_inputs(d)
+    port = GridPort(L)
+    T = port.adjoint(a, b)
+    nth, nph = L + 2, 2 * L + 4
+    Tr = T.reshape(nth, nph, 3)
+    assert O.rel_l2(Tr[d["rings"]], d["T_rings"]) <= 1e-13
+    assert O.rel_l2(Tr.sum(axis=1), d["ring_sum"]) <= 1e-12
+    assert np.max(np.abs(np.sqrt((np.abs(Tr) ** 2).sum(axis=(1, 2))) / d["ring_norm"] - 1)) <= 1e-13
+    noise = O.tangent_noise(rng, O.grid_points(port.th, nph), float(d["noise_sigma"]))
+    assert np.allclose(noise.sum(axis=0), d["noise_sum"], rtol=0, atol=1e-9)
+    fa, fb = port.forward(T + noise)
+    idx = d["flat_idx"]
+    assert O.rel_l2(np.concatenate([fa[idx], fb[idx]]), np.concatenate([d["fa_sel"], d["fb_sel"]])) <= 1e-13
+    for got, ref in ((order_norms(fa, L), d["fa_order_norm"]), (order_norms(fb, L), d["fb_order_norm"])):
+        assert O.rel_l2(got, ref) <= 1e-13
+
+
+def test_parallel_port_is_the_serial_oracle():
+    from oracle.parallel import GridPort
+
+    L = 40
+    th, w, nphi = O.gl_grid(L)
+    rng = np.random.default_rng(41)
+    a, b = O.coef(rng, L, "pow2")
+    port = GridPort(L, procs=3)
+    T = port.adjoint(a, b)
+    assert np.array_equal(T, O.vsht_adjoint_grid(a, b, L, th, nphi))
+    fa, fb = port.forward(T)
+    ra, rb = O.vsht_forward_grid(T, th, w, nphi, L)
+    assert np.array_equal(fa, ra) and np.array_equal(fb, rb)
+    orders = [0, 3, 17, 40]
+    spec = port.adjoint(a, b, orders=orders, spectrum=True)
+    ref = O.vsht_adjoint_grid(a, b, L, th, nphi, orders=orders, spectrum=True)
+    assert np.array_equal(spec, ref)
+    pa, pb = port.forward(T, orders=orders)
+    ls, ms = O.degrees_orders(L)
+    sel = np.isin(np.abs(ms), orders)
+    assert np.array_equal(pa[sel], ra[sel]) and np.array_equal(pb[sel], rb[sel])
