@@ -24,12 +24,14 @@ constexpr int FFT_MAXST = 16;
 constexpr int FFT_TWLO = 64;     // twiddle w^k = hi[k / 64] * lo[k % 64] (two small smem tables)
 constexpr int FFT_TWN = FFT_TWLO + (FFT_NMAX + FFT_TWLO - 1) / FFT_TWLO;
 
-// cos / sin(2 pi m / R) for the odd primes R = 3..19, packed: offset of R below
-__constant__ double kRootCos[3 + 5 + 7 + 11 + 13 + 17 + 19];
-__constant__ double kRootSin[3 + 5 + 7 + 11 + 13 + 17 + 19];
+// cos / sin(2 pi m / R) for the odd primes R = 3..19 and 31 (the Rader stage,
+// fft_rader.cuh), packed: offset of R below
+constexpr int kRootR[8] = {3, 5, 7, 11, 13, 17, 19, 31};
+__constant__ double kRootCos[3 + 5 + 7 + 11 + 13 + 17 + 19 + 31];
+__constant__ double kRootSin[3 + 5 + 7 + 11 + 13 + 17 + 19 + 31];
 
 __host__ __device__ constexpr int root_offset(int R) {
-  return R == 3 ? 0 : R == 5 ? 3 : R == 7 ? 8 : R == 11 ? 15 : R == 13 ? 26 : R == 17 ? 39 : 56;
+  return R == 3 ? 0 : R == 5 ? 3 : R == 7 ? 8 : R == 11 ? 15 : R == 13 ? 26 : R == 17 ? 39 : R == 19 ? 56 : 75;
 }
 
 struct RingFftArgs {
@@ -53,12 +55,12 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 
 // exp(-2 pi i e / R) for the composite radices' internal twiddles, packed by R
 // (offsets below; filled per device by plan.cu).
-constexpr int kCompR[11] = {4, 6, 8, 9, 10, 12, 14, 15, 16, 18, 20};
-__constant__ double kCompCos[4 + 6 + 8 + 9 + 10 + 12 + 14 + 15 + 16 + 18 + 20];
-__constant__ double kCompSin[4 + 6 + 8 + 9 + 10 + 12 + 14 + 15 + 16 + 18 + 20];
+constexpr int kCompR[12] = {4, 6, 8, 9, 10, 12, 14, 15, 16, 18, 20, 22};
+__constant__ double kCompCos[4 + 6 + 8 + 9 + 10 + 12 + 14 + 15 + 16 + 18 + 20 + 22];
+__constant__ double kCompSin[4 + 6 + 8 + 9 + 10 + 12 + 14 + 15 + 16 + 18 + 20 + 22];
 __host__ __device__ constexpr int comp_offset(int R) {
   return R == 4 ? 0 : R == 6 ? 4 : R == 8 ? 10 : R == 9 ? 18 : R == 10 ? 27 : R == 12 ? 37 : R == 14 ? 49
-       : R == 15 ? 63 : R == 16 ? 78 : R == 18 ? 94 : 112;
+       : R == 15 ? 63 : R == 16 ? 78 : R == 18 ? 94 : R == 20 ? 112 : 132;
 }
 __host__ __device__ constexpr int first_factor(int R) {
   return R % 4 == 0 ? 4 : R % 2 == 0 ? 2 : R % 3 == 0 ? 3 : R % 5 == 0 ? 5 : R % 7 == 0 ? 7 : R;

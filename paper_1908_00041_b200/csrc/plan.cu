@@ -23,6 +23,7 @@
 #include "fft.cuh"
 #include "fft2.cuh"
 #include "fft_blue.cuh"
+#include "fft_rader.cuh"
 #include "legendre.cuh"
 #include "points.cuh"
 #include "scalar.cuh"
@@ -139,6 +140,9 @@ struct fvPlan {
   bool custom_fft = false;
   // Bluestein ring FFT (fft_blue.cuh) for n_phi = R * P with a prime P > 19
   bool blue = false, smallp = false, rpfft = false;
+  bool rader = false;        // n_phi = R * P by Rader's algorithm (fft_rader.cuh), tables in blue_tab
+  int rader_R = 0, rader_P = 0;
+  fv::RaderArgs rd_args{};
   std::map<std::tuple<long long, long long, int>, cufftHandle> subffts;  // length-P sub-DFT plans (rpfft)
   fv::BlueArgs blue_args{};  // tables and factorisation (pointers owned below)
   fv::SmallPArgs sp_args{};
@@ -438,13 +442,11 @@ bool fft_factor(int n, int* radix, int* nst) {
   return true;
 }
 
-int setup_fft(fvPlan* p) {
-  const char* env = std::getenv("FV_FFT");
-  const bool force_cufft = env && std::string(env) == "cufft";
-  if (force_cufft || !fft_factor(p->n_phi, p->fft_radix, &p->fft_nst)) return FV_OK;
-  // roots of the odd-prime butterflies (per device: __constant__ lives in each context)
-  double rc[75], rs[75];
-  for (int R : {3, 5, 7, 11, 13, 17, 19})
+// roots of the odd-prime butterflies and the composites' internal twiddles
+// (per device: __constant__ lives in each context)
+int fill_root_tables() {
+  double rc[sizeof(fv::kRootCos) / sizeof(double)], rs[sizeof(fv::kRootSin) / sizeof(double)];
+  for (int R : fv::kRootR)
     for (int m = 0; m < R; ++m) {
       const long double a = 2.0L * 3.141592653589793238462643383279502884L * m / R;
       rc[fv::root_offset(R) + m] = (double)cosl(a);
@@ -461,6 +463,14 @@ int setup_fft(fvPlan* p) {
     }
   FV_CUDA(cudaMemcpyToSymbol(fv::kCompCos, cc, sizeof(cc)));
   FV_CUDA(cudaMemcpyToSymbol(fv::kCompSin, cs, sizeof(cs)));
+  return FV_OK;
+}
+
+int setup_fft(fvPlan* p) {
+  const char* env = std::getenv("FV_FFT");
+  const bool force_cufft = env && std::string(env) == "cufft";
+  if (force_cufft || !fft_factor(p->n_phi, p->fft_radix, &p->fft_nst)) return FV_OK;
+  FV_TRY(fill_root_tables());
   // factored twiddles: lo[k] = w^k (k < 64), hi[j] = w^(64 j)
   const int nhi = (p->n_phi + fv::FFT_TWLO - 1) / fv::FFT_TWLO;
   std::vector<double2> tw(fv::FFT_TWLO + nhi);
@@ -572,6 +582,116 @@ int setup_fft2(fvPlan* p) {
 
 // Bluestein ring FFT plan (fft_blue.cuh): n = R * P with P the largest prime
 // factor (> 19, which the radix kernels do not cover), every prime of R <= 19
+// Rader plans instantiated in fft_rader.cuh: (R, P, F1, F2) with P - 1 = F1 * F2,
+// F1 an odd prime with constant-bank roots, F2 a composite of dft<>.
+#define FV_RADER_PLANS(X) X(12, 683, 31, 22) /* 8196: L = 4096 */
+
+template <class F>
+int rader_dispatch(int R, int P, F f) {
+#define FV_RD_CASE(R_, P_, F1_, F2_) \
+  if (R == R_ && P == P_)            \
+    return f(std::integral_constant<int, R_>{}, std::integral_constant<int, P_>{}, \
+             std::integral_constant<int, F1_>{}, std::integral_constant<int, F2_>{});
+  FV_RADER_PLANS(FV_RD_CASE)
+#undef FV_RD_CASE
+  return fail(FV_EINVAL, "no Rader plan for this length");
+}
+
+bool rader_instantiated(int R, int P) {
+  bool ok = false;
+#define FV_RD_HAVE(R_, P_, F1_, F2_) ok |= (R == R_ && P == P_);
+  FV_RADER_PLANS(FV_RD_HAVE)
+#undef FV_RD_HAVE
+  return ok;
+}
+
+// Rader tables for n = R * P: primitive root g, slot table g^-p, modular inverses,
+// the P-1 roots, the transformed kernel DFT_{P-1}(w_P^{g^m}) / (P-1) (long double
+// sums), the n roots of the combine.  Packed into p->blue_tab.
+int setup_rader(fvPlan* p, int R, int P) {
+  const int n = R * P, M = P - 1;
+  auto powmod = [](long long b, long long e, long long m) {
+    long long r = 1;
+    b %= m;
+    while (e) {
+      if (e & 1) r = r * b % m;
+      b = b * b % m;
+      e >>= 1;
+    }
+    return r;
+  };
+  std::vector<int> pf;
+  for (int f = 2, rem = M; rem > 1; ++f)
+    if (rem % f == 0) {
+      pf.push_back(f);
+      while (rem % f == 0) rem /= f;
+    }
+  int g = 2;
+  for (;; ++g) {
+    bool prim = true;
+    for (int f : pf) prim &= powmod(g, M / f, P) != 1;
+    if (prim) break;
+  }
+  const long long ginv = powmod(g, P - 2, P);
+  const long double PI_ = 3.141592653589793238462643383279502884L;
+  const int nhi = (n + 127) / 128;
+  const size_t o_tw = 0, o_Bn = o_tw + M, o_lo = o_Bn + M, o_hi = o_lo + 128, o_idx = o_hi + nhi;
+  const size_t n_idx = ((size_t)(M + P) * sizeof(short) + sizeof(double2) - 1) / sizeof(double2);
+  std::vector<double2> tab(o_idx + n_idx);
+  for (int e = 0; e < M; ++e) {
+    const long double a = 2.0L * PI_ * e / M;
+    tab[o_tw + e] = make_double2((double)cosl(a), -(double)sinl(a));
+  }
+  std::vector<long double> br(M), bi(M);
+  for (int m = 0; m < M; ++m) {
+    const long double a = 2.0L * PI_ * (long double)powmod(g, m, P) / P;
+    br[m] = cosl(a);
+    bi[m] = -sinl(a);
+  }
+  for (int f = 0; f < M; ++f) {
+    long double re = 0.0L, im = 0.0L;
+    for (int m = 0; m < M; ++m) {
+      const long double a = 2.0L * PI_ * (long double)(((long long)m * f) % M) / M;
+      const long double c = cosl(a), sn = -sinl(a);
+      re += br[m] * c - bi[m] * sn;
+      im += br[m] * sn + bi[m] * c;
+    }
+    tab[o_Bn + f] = make_double2((double)(re / M), (double)(im / M));
+  }
+  for (int j = 0; j < 128; ++j) {
+    const long double a = 2.0L * PI_ * j / n;
+    tab[o_lo + j] = make_double2((double)cosl(a), -(double)sinl(a));
+  }
+  for (int j = 0; j < nhi; ++j) {
+    const long double a = 2.0L * PI_ * (128.0L * j) / n;
+    tab[o_hi + j] = make_double2((double)cosl(a), -(double)sinl(a));
+  }
+  short* idx = reinterpret_cast<short*>(tab.data() + o_idx);
+  for (int q = 0; q < M; ++q) idx[q] = (short)powmod(ginv, q, P);  // sig[p] = g^-p
+  idx[M] = 0;                                                      // inv[0]
+  for (int k = 1; k < P; ++k) idx[M + k] = (short)powmod(k, P - 2, P);
+  FV_TRY(fill_root_tables());
+  FV_TRY(dalloc(&p->blue_tab, tab.size()));
+  FV_CUDA(cudaMemcpy(p->blue_tab, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  fv::RaderArgs& a = p->rd_args;
+  a.tab = p->blue_tab + o_tw;
+  a.sig = reinterpret_cast<const short*>(p->blue_tab + o_idx);
+  FV_TRY(rader_dispatch(R, P, [&](auto R_, auto P_, auto F1_, auto F2_) -> int {
+    constexpr int bytes = (int)fv::RaderSmem<R_, P_>::bytes;
+    FV_CUDA(cudaFuncSetAttribute(fv::rader_fft_kernel<R_, P_, F1_, F2_>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    FV_CUDA(cudaFuncSetAttribute(fv::rader_fold_kernel<R_, P_, F1_, F2_>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    return FV_OK;
+  }));
+  p->rader_R = R;
+  p->rader_P = P;
+  const char* ff = std::getenv("FV_FUSED_FOLD");
+  p->fused_fold = !(ff && std::atoi(ff) == 0);
+  p->rader = true;
+  return FV_OK;
+}
+
 // and R an instantiated blue_r_kernel size; M = 2^a 3^b >= 2P - 1, M <= 4096.
 constexpr int kBlueR[] = {1, 2, 3, 4, 6, 8, 12, 16, 24};
 
@@ -625,6 +745,10 @@ int setup_blue(fvPlan* p) {
     p->smallp = true;
     return FV_OK;
   }
+  // hand-written Rader DFTs (fft_rader.cuh) where a plan is instantiated (FV_FFT=rp: the
+  // cuFFT sub-DFT path below)
+  if (rader_instantiated(R, P) && !(env && (std::string(env) == "blue" || std::string(env) == "rp")))
+    return setup_rader(p, R, P);
   bool ok = false;
   for (int x : kBlueR) ok |= (x == R);
   if (!ok) return FV_OK;
@@ -770,6 +894,30 @@ int ring_fft_smallp(fvPlan* p, bool inverse, const double2* in, long long in_cs,
   return FV_OK;
 }
 
+int ring_fft_rader(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
+                   double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s,
+                   int in_rblk = 0) {
+  fv::RaderArgs a = p->rd_args;
+  a.in = in;
+  a.in_cs = in_cs;
+  a.in_rs = in_rs;
+  a.in_es = in_es;
+  a.in_rblk = in_rblk;
+  a.out = out;
+  a.out_cs = out_cs;
+  a.out_rs = out_rs;
+  a.out_es = out_es;
+  a.nrings = nrings;
+  a.inverse = inverse ? 1 : 0;
+  a.ahead = fft_prefetch_ahead();
+  return rader_dispatch(p->rader_R, p->rader_P, [&](auto R_, auto P_, auto F1_, auto F2_) -> int {
+    fv::rader_fft_kernel<R_, P_, F1_, F2_>
+        <<<(unsigned)(3LL * nrings), fv::RD_T, fv::RaderSmem<R_, P_>::bytes, s>>>(a);
+    FV_CUDA(cudaGetLastError());
+    return FV_OK;
+  });
+}
+
 int ring_fft_rp(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
                 double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s) {
   const fv::BlueArgs& ba = p->blue_args;
@@ -888,6 +1036,28 @@ int ring_fft2_raw(fvPlan* p, bool inverse, const double2* in, long long in_cs, l
 // fused forward FFT + fold of fields b0 .. b0 + nf - 1 of T (B, N, 3) into X (all orders)
 int fft_fold(fvPlan* p, const double2* T, int b0, int nf, cudaStream_t s, double* X) {
   fv::Fft2Args a{};
+  if (p->rader) {  // Rader ring DFT, north / south ring of a pair on a two-CTA cluster (fft_rader.cuh)
+    const long long n = p->n_phi;
+    a.in_rs = 3 * n;
+    a.in_es = 3;
+    a.field_stride = 3 * n * p->n_theta;
+    a.in = T + (long long)b0 * a.field_stride;
+    a.X = X;
+    a.pair_n = p->pair_n;
+    a.pair_s = p->pair_s;
+    a.ring_w = p->ring_w;
+    a.nchunks = p->nchunks;
+    a.NT = ntiles_for(nf);
+    a.nfields = nf;
+    a.Lt = p->Lt;
+    a.ahead = fft_prefetch_ahead() / 2;
+    const unsigned grid = 2u * (unsigned)(p->nchunks * fv::FWD_RC * nf * 3);
+    return rader_dispatch(p->rader_R, p->rader_P, [&](auto R_, auto P_, auto F1_, auto F2_) -> int {
+      fv::rader_fold_kernel<R_, P_, F1_, F2_><<<grid, fv::RD_T, fv::RaderSmem<R_, P_>::bytes, s>>>(p->rd_args, a);
+      FV_CUDA(cudaGetLastError());
+      return FV_OK;
+    });
+  }
   if (p->smallp) {  // small-prime ring DFT (fft_blue.cuh smallp_fold_kernel)
     const long long n = p->n_phi;
     a.in_rs = 3 * n;
@@ -1115,7 +1285,7 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
     // 02 when the inverse ring DFT is hand-written, else 01: the forward FFT writes
     // contiguous rings, the adjoint epilogue writes 128-byte runs of one bin)
     const char* sl = std::getenv("FV_SLAYOUT");
-    const bool own_fft = p->fft2 || p->smallp;
+    const bool own_fft = p->fft2 || p->smallp || p->rader;
     const char fdig = (sl && sl[0]) ? sl[0] : '0';
     char adig = (sl && sl[0] && sl[1]) ? sl[1] : (own_fft ? '2' : '1');
     if (adig == '2' && !own_fft) adig = '1';
@@ -1367,7 +1537,9 @@ int ring_ffts(fvPlan* p, bool inverse, const double2* in, long long in_cs, long 
               double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s,
               int in_rblk = 0) {
   StageMark mk(p, 0, s);
-  if (in_rblk) {  // blocked rings: only the hand-written two-ring / small-prime kernels read them
+  if (in_rblk) {  // blocked rings: only the hand-written two-ring / small-prime / Rader kernels read them
+    if (p->rader)
+      return ring_fft_rader(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s, in_rblk);
     if (p->fft2)
       return ring_fft2_raw(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s, in_rblk);
     if (p->smallp)
@@ -1377,6 +1549,7 @@ int ring_ffts(fvPlan* p, bool inverse, const double2* in, long long in_cs, long 
   if (p->fft2) return ring_fft2_raw(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   if (p->custom_fft) return ring_fft_raw(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   if (p->smallp) return ring_fft_smallp(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
+  if (p->rader) return ring_fft_rader(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   if (p->rpfft) return ring_fft_rp(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   if (p->blue) return ring_fft_blue(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   cufftHandle h;
@@ -1396,7 +1569,7 @@ namespace {
 int forward_grid_impl(fvPlan* p, const double2* T, double* a, double* b, int B, cudaStream_t s,
                       const ScalarIO* sio = nullptr) {
   const long long n = p->n_phi;
-  if ((p->fft2 || p->smallp) && p->fused_fold)
+  if ((p->fft2 || p->smallp || p->rader) && p->fused_fold)
     return forward_orders(p, nullptr, p->lay_f, a, b, B, 0, p->Lt + 1, 0, p->L + 1, s, T, sio);
   FV_TRY(ring_ffts(p, false, T, 1, 3 * n, 3, p->Sf, p->lay_f.cs, p->lay_f.rs, p->lay_f.bs, B * p->n_theta, s));
   return forward_orders(p, p->Sf, p->lay_f, a, b, B, 0, p->Lt + 1, 0, p->L + 1, s, nullptr, sio);

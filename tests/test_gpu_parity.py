@@ -579,12 +579,13 @@ def test_direct_forward_batch_determinism_and_edges():
 def test_ring_fft_against_numpy(nphi):
     """fv_ring_fft alone (the sharded building block) on random rings, both
     directions, against numpy's pocketfft (favest/scalar.py:149, :178); the
-    large-prime lengths also through the opt-in Bluestein kernels."""
+    large-prime lengths also through the opt-in Bluestein kernels and the cuFFT
+    sub-DFT path (FV_FFT=rp; 8196 defaults to the Rader kernels)."""
     import ctypes
     import os
 
     torch = cuda_or_skip()
-    for fft in ("", "blue"):
+    for fft in ("", "blue", "rp"):
         os.environ["FV_FFT"] = fft
         try:
             _ring_fft_case(torch, nphi)
