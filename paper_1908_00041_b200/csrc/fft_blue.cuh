@@ -1,45 +1,28 @@
-// Ring DFTs of lengths with a prime factor P > 19 (C2: n_phi = 516 = 12 * 43,
-// C4: n_phi = 8196 = 12 * 683), replacing the cuFFT Bluestein plans (7.4 ms
-// per direction at C4).  favest/scalar.py:149 (np.fft.fft along a ring) and
+// Ring DFTs of lengths with a prime factor P > 19 and no Rader plan
+// (fft_rader.cuh): C2's n_phi = 516 = 12 * 43 and other small primes (P <= 64)
+// by direct conjugate-pair residue DFTs in one CTA per ring (smallp_kernel),
+// larger primes by batched cuFFT sub-DFTs of length P plus the R-point combine
+// (rp_combine_kernel).  favest/scalar.py:149 (np.fft.fft along a ring) and
 // :178 (np.fft.ifft * n_phi, i.e. the unnormalised inverse).
 //
 // n = R * P.  Decimation in time over the R residues:
 //   X[k + P s] = sum_r w_R^{r s} ( w_n^{r k} Y_r[k] ),   Y_r = DFT_P(x[r + R q], q < P)
-// * blue_p_kernel: one CTA per (component, ring, residue r) computes Y_r by
-//   Bluestein's chirp-z identity q k = (q^2 + k^2 - (k - q)^2) / 2:
-//   Y_r[k] = c_k * sum_q (x_q c_q) conj(c_{k-q}),  c_j = exp(-pi i j^2 / P),
-//   a cyclic convolution of length M >= 2P - 1 (M = 2^a 3^b) done as
-//   FFT_M -> x FFT_M(conj c) / M (plan-time table) -> inverse FFT_M, all in
-//   shared memory with a Stockham radix-{2,3,4,8} loop; then applies w_n^{r k}
-//   and stores Y'_r contiguously in a scratch buffer.
-// * blue_r_kernel: thread per (component, ring, k) forms the R outputs
-//   X[k + P s] from the R scratch values (direct R-point DFT) and writes them
-//   with the caller's strides.
-// The inverse direction is conj(DFT(conj(x))): conjugate on load (K1) and on
-// store (K2).  Tables (chirps, roots, FFT_M of the chirp) are exactly rounded
-// from long double on the host.
+// The inverse direction is conj(DFT(conj(x))).  Tables are exactly rounded from
+// long double on the host.  (A Bluestein chirp-z variant of the residue DFTs was
+// measured slower than cuFFT's sub-DFTs at C4 and removed; the Rader kernels
+// replaced both there.)
 #pragma once
 #include "fft2.cuh"
 
 namespace fv {
 
 constexpr int BLUE_T = 256;
-constexpr int BLUE_MAXST = 12;
 
+// factorisation and tables of the cuFFT sub-DFT path (ring_fft_rp)
 struct BlueArgs {
-  const double2* in;
-  long long in_cs, in_rs, in_es;
-  double2* out;
-  long long out_cs, out_rs, out_es;
-  double2* S1;            // scratch [3 * nrings][R][P]
-  const double2* rootM;   // exp(-2 pi i j / M), j < M
-  const double2* chirp;   // exp(-pi i q^2 / P), q < P
-  const double2* FB;      // FFT_M(b) / M, b_j = conj(chirp_|j|) wrapped cyclically
   const double2* rootN;   // exp(-2 pi i j / n), j < n
   const double2* rootR;   // exp(-2 pi i j / R), j < R
-  int n, R, P, M, nrings, inverse;
-  int nst;
-  int radix[BLUE_MAXST];  // M = prod radix (each 2, 3, 4 or 8)
+  int n, R, P;
 };
 
 __device__ __forceinline__ double2 bl_mul(double2 a, double2 b) {
@@ -49,161 +32,6 @@ __device__ __forceinline__ double2 bl_add(double2 a, double2 b) { return make_do
 __device__ __forceinline__ double2 bl_sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 // multiply by -i
 __device__ __forceinline__ double2 bl_mi(double2 a) { return make_double2(a.y, -a.x); }
-
-// forward-sign (exp(-2 pi i / R)) DFT codelets
-template <int R>
-__device__ __forceinline__ void bl_dft(double2 (&v)[8]);
-
-template <>
-__device__ __forceinline__ void bl_dft<2>(double2 (&v)[8]) {
-  const double2 a = v[0], b = v[1];
-  v[0] = bl_add(a, b);
-  v[1] = bl_sub(a, b);
-}
-
-template <>
-__device__ __forceinline__ void bl_dft<3>(double2 (&v)[8]) {
-  const double s3 = 0.86602540378443864676;  // sin(2 pi / 3)
-  const double2 t1 = bl_add(v[1], v[2]);
-  const double2 t2 = make_double2(v[0].x - 0.5 * t1.x, v[0].y - 0.5 * t1.y);
-  const double2 d = bl_sub(v[1], v[2]);
-  const double2 t3 = make_double2(s3 * d.y, -s3 * d.x);  // -i sin(2pi/3) (v1 - v2)
-  v[0] = bl_add(v[0], t1);
-  v[1] = bl_add(t2, t3);
-  v[2] = bl_sub(t2, t3);
-}
-
-template <>
-__device__ __forceinline__ void bl_dft<4>(double2 (&v)[8]) {
-  const double2 a = bl_add(v[0], v[2]), b = bl_sub(v[0], v[2]);
-  const double2 c = bl_add(v[1], v[3]), d = bl_mi(bl_sub(v[1], v[3]));
-  v[0] = bl_add(a, c);
-  v[2] = bl_sub(a, c);
-  v[1] = bl_add(b, d);
-  v[3] = bl_sub(b, d);
-}
-
-template <>
-__device__ __forceinline__ void bl_dft<8>(double2 (&v)[8]) {
-  const double h = 0.70710678118654752440;  // sqrt(2) / 2
-  double2 e[8] = {v[0], v[2], v[4], v[6]}, o[8] = {v[1], v[3], v[5], v[7]};
-  bl_dft<4>(e);
-  bl_dft<4>(o);
-  // w8^k o_k, w8 = exp(-i pi / 4)
-  const double2 o1 = make_double2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
-  const double2 o2 = bl_mi(o[2]);
-  const double2 o3 = make_double2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
-  v[0] = bl_add(e[0], o[0]);
-  v[4] = bl_sub(e[0], o[0]);
-  v[1] = bl_add(e[1], o1);
-  v[5] = bl_sub(e[1], o1);
-  v[2] = bl_add(e[2], o2);
-  v[6] = bl_sub(e[2], o2);
-  v[3] = bl_add(e[3], o3);
-  v[7] = bl_sub(e[3], o3);
-}
-
-// One Stockham stage x -> y of the length-M transform with sub-transform span Ns.
-template <int R>
-__device__ __forceinline__ void bl_stage(const double2* x, double2* y, const double2* __restrict__ rootM, int M,
-                                         int Ns) {
-  const int nb = M / R;
-  const int tstep = M / (Ns * R);
-  for (int j = threadIdx.x; j < nb; j += BLUE_T) {
-    const int k = j % Ns;
-    double2 v[8];
-#pragma unroll
-    for (int i = 0; i < R; ++i) v[i] = x[j + i * nb];
-    if (Ns > 1) {
-#pragma unroll
-      for (int i = 1; i < R; ++i) v[i] = bl_mul(v[i], __ldg(&rootM[i * k * tstep]));
-    }
-    bl_dft<R>(v);
-    const int base = (j / Ns) * Ns * R + k;
-#pragma unroll
-    for (int i = 0; i < R; ++i) y[base + i * Ns] = v[i];
-  }
-}
-
-// forward FFT_M of buf[0..M) (ping-pong with tmp); returns the buffer holding the result
-__device__ __forceinline__ double2* bl_fft(double2* buf, double2* tmp, const BlueArgs& a) {
-  int Ns = 1;
-  for (int s = 0; s < a.nst; ++s) {
-    const int R = a.radix[s];
-    switch (R) {
-      case 2: bl_stage<2>(buf, tmp, a.rootM, a.M, Ns); break;
-      case 3: bl_stage<3>(buf, tmp, a.rootM, a.M, Ns); break;
-      case 4: bl_stage<4>(buf, tmp, a.rootM, a.M, Ns); break;
-      default: bl_stage<8>(buf, tmp, a.rootM, a.M, Ns); break;
-    }
-    __syncthreads();
-    double2* t = buf;
-    buf = tmp;
-    tmp = t;
-    Ns *= R;
-  }
-  return buf;
-}
-
-__global__ void __launch_bounds__(BLUE_T) blue_p_kernel(BlueArgs a) {
-  extern __shared__ __align__(16) double2 bl_smem[];  // 2 x M
-  double2* b0 = bl_smem;
-  double2* b1 = bl_smem + a.M;
-  const int r = blockIdx.x % a.R;
-  const long long rc = blockIdx.x / a.R;  // c * nrings + ring
-  const int c = (int)(rc / a.nrings), ring = (int)(rc % a.nrings);
-  const double2* src = a.in + c * a.in_cs + ring * a.in_rs;
-  const double cj = a.inverse ? -1.0 : 1.0;
-  for (int q = threadIdx.x; q < a.M; q += BLUE_T) {
-    double2 v = make_double2(0.0, 0.0);
-    if (q < a.P) {
-      double2 x = src[(long long)(r + (long long)a.R * q) * a.in_es];
-      x.y *= cj;
-      v = bl_mul(x, __ldg(&a.chirp[q]));
-    }
-    b0[q] = v;
-  }
-  __syncthreads();
-  double2* X = bl_fft(b0, b1, a);
-  double2* T = (X == b0) ? b1 : b0;
-  // convolution with the chirp in the frequency domain; the inverse FFT_M as
-  // conj(FFT(conj(.))) (the 1 / M is folded into FB)
-  for (int q = threadIdx.x; q < a.M; q += BLUE_T) {
-    const double2 v = bl_mul(X[q], __ldg(&a.FB[q]));
-    X[q] = make_double2(v.x, -v.y);
-  }
-  __syncthreads();
-  double2* Y = bl_fft(X, T, a);
-  double2* dst = a.S1 + (rc * a.R + r) * (long long)a.P;
-  for (int k = threadIdx.x; k < a.P; k += BLUE_T) {
-    const double2 y = make_double2(Y[k].x, -Y[k].y);
-    const double2 v = bl_mul(bl_mul(y, __ldg(&a.chirp[k])), __ldg(&a.rootN[(long long)r * k]));
-    dst[k] = v;
-  }
-}
-
-template <int RR>
-__global__ void __launch_bounds__(BLUE_T) blue_r_kernel(BlueArgs a) {
-  const long long idx = (long long)blockIdx.x * BLUE_T + threadIdx.x;
-  const long long total = 3LL * a.nrings * a.P;
-  if (idx >= total) return;
-  const long long rc = idx / a.P;
-  const int k = (int)(idx - rc * a.P);
-  const int c = (int)(rc / a.nrings), ring = (int)(rc % a.nrings);
-  const double2* src = a.S1 + rc * RR * (long long)a.P + k;
-  double2 z[RR];
-#pragma unroll
-  for (int r = 0; r < RR; ++r) z[r] = src[(long long)r * a.P];
-  double2* dst = a.out + c * a.out_cs + ring * a.out_rs;
-  const double cj = a.inverse ? -1.0 : 1.0;
-#pragma unroll 1
-  for (int s = 0; s < RR; ++s) {
-    double2 acc = z[0];
-#pragma unroll
-    for (int r = 1; r < RR; ++r) acc = bl_add(acc, bl_mul(z[r], __ldg(&a.rootR[(r * s) % RR])));
-    dst[(long long)(k + (long long)a.P * s) * a.out_es] = make_double2(acc.x, cj * acc.y);
-  }
-}
 
 // ---------------------------------------------------------------------------
 // Small prime factor (P <= 64, e.g. C2's 516 = 12 * 43): one CTA per

@@ -139,7 +139,7 @@ struct fvPlan {
   // hand-written ring FFT (fft.cuh) when every prime factor of n_phi is <= 19
   bool custom_fft = false;
   // Bluestein ring FFT (fft_blue.cuh) for n_phi = R * P with a prime P > 19
-  bool blue = false, smallp = false, rpfft = false;
+  bool smallp = false, rpfft = false;
   bool rader = false;        // n_phi = R * P by Rader's algorithm (fft_rader.cuh), tables in blue_tab
   int rader_R = 0, rader_P = 0;
   fv::RaderArgs rd_args{};
@@ -692,7 +692,9 @@ int setup_rader(fvPlan* p, int R, int P) {
   return FV_OK;
 }
 
-// and R an instantiated blue_r_kernel size; M = 2^a 3^b >= 2P - 1, M <= 4096.
+// Lengths n = R * P with a prime P > 19: the small-prime kernels (P <= 64), a Rader
+// plan, or cuFFT sub-DFTs + rp_combine_kernel for R one of these (R = 1: cuFFT's own
+// plan for a prime length).  FV_FFT=rp forces the cuFFT sub-DFT path.
 constexpr int kBlueR[] = {1, 2, 3, 4, 6, 8, 12, 16, 24};
 
 int setup_blue(fvPlan* p) {
@@ -709,7 +711,7 @@ int setup_blue(fvPlan* p) {
   if (P <= 19) return FV_OK;
   const int R = n / P;
   const long double PI_ = 3.141592653589793238462643383279502884L;
-  if (P <= fv::SMALLP_MAX && R <= 64 && !(env && std::string(env) == "blue")) {
+  if (P <= fv::SMALLP_MAX && R <= 64 && !(env && std::string(env) == "rp")) {
     // direct conjugate-pair DFTs in one CTA per ring (smallp_kernel)
     const int H = (P - 1) / 2;
     std::vector<double2> tab((size_t)n + R * R + H * (H + 1));
@@ -747,15 +749,14 @@ int setup_blue(fvPlan* p) {
   }
   // hand-written Rader DFTs (fft_rader.cuh) where a plan is instantiated (FV_FFT=rp: the
   // cuFFT sub-DFT path below)
-  if (rader_instantiated(R, P) && !(env && (std::string(env) == "blue" || std::string(env) == "rp")))
+  if (rader_instantiated(R, P) && !(env && std::string(env) == "rp"))
     return setup_rader(p, R, P);
   bool ok = false;
   for (int x : kBlueR) ok |= (x == R);
   if (!ok) return FV_OK;
-  // large P: batched cuFFT sub-DFTs of length P + the combine kernel (rp_combine_kernel);
-  // the Bluestein kernels are correct but slower (9.4 vs 8.2 ms per direction at C4),
-  // opt-in with FV_FFT=blue
-  if (!(env && std::string(env) == "blue")) {
+  // large P without a Rader plan: batched cuFFT sub-DFTs of length P + the combine
+  // kernel (rp_combine_kernel)
+  {
     if (R == 1) return FV_OK;  // a prime length: cuFFT's own plan
     std::vector<double2> tab(n + R);
     for (int j = 0; j < n; ++j) {
@@ -776,83 +777,6 @@ int setup_blue(fvPlan* p) {
     p->rpfft = true;
     return FV_OK;
   }
-  int M = 1 << 30;
-  for (long long a2 = 1; a2 <= 4096; a2 *= 2)
-    for (long long a3 = a2; a3 <= 4096; a3 *= 3)
-      if (a3 >= 2LL * P - 1) M = std::min<long long>(M, a3);
-  if (M > 4096) return FV_OK;
-  fv::BlueArgs& a = p->blue_args;
-  a.n = n;
-  a.R = R;
-  a.P = P;
-  a.M = M;
-  a.nst = 0;
-  {
-    int m = M;
-    while (m % 3 == 0) {
-      a.radix[a.nst++] = 3;
-      m /= 3;
-    }
-    while (m % 8 == 0) {
-      a.radix[a.nst++] = 8;
-      m /= 8;
-    }
-    if (m % 4 == 0) {
-      a.radix[a.nst++] = 4;
-      m /= 4;
-    }
-    if (m % 2 == 0) {
-      a.radix[a.nst++] = 2;
-      m /= 2;
-    }
-  }
-  const long double PI = 3.141592653589793238462643383279502884L;
-  auto root = [&](long long num, long long den) {  // exp(-2 pi i num / den)
-    const long double ang = 2.0L * PI * (long double)(num % den) / (long double)den;
-    return std::make_pair(cosl(ang), -sinl(ang));
-  };
-  std::vector<double2> tab;
-  std::vector<std::pair<long double, long double>> chirp(P), rootM(M);
-  for (int j = 0; j < M; ++j) rootM[j] = root(j, M);
-  for (int q = 0; q < P; ++q) chirp[q] = root((long long)q * q % (2LL * P), 2LL * P);  // exp(-pi i q^2 / P)
-  // b_j = conj(chirp_|j|) on the cyclic index, FB = DFT_M(b) / M (direct sum in long double)
-  std::vector<std::pair<long double, long double>> b(M, {0.0L, 0.0L});
-  for (int j = 0; j < P; ++j) {
-    b[j] = {chirp[j].first, -chirp[j].second};
-    if (j > 0) b[M - j] = b[j];
-  }
-  const size_t o_rootM = 0, o_chirp = o_rootM + M, o_FB = o_chirp + P, o_rootN = o_FB + M, o_rootR = o_rootN + n;
-  tab.resize(o_rootR + R);
-  for (int j = 0; j < M; ++j) tab[o_rootM + j] = make_double2((double)rootM[j].first, (double)rootM[j].second);
-  for (int q = 0; q < P; ++q) tab[o_chirp + q] = make_double2((double)chirp[q].first, (double)chirp[q].second);
-  for (int k = 0; k < M; ++k) {
-    long double re = 0.0L, im = 0.0L;
-    for (int j = 0; j < M; ++j) {
-      if (b[j].first == 0.0L && b[j].second == 0.0L) continue;
-      const auto& w = rootM[(long long)j * k % M];
-      re += b[j].first * w.first - b[j].second * w.second;
-      im += b[j].first * w.second + b[j].second * w.first;
-    }
-    tab[o_FB + k] = make_double2((double)(re / M), (double)(im / M));
-  }
-  for (int j = 0; j < n; ++j) {
-    const auto w = root(j, n);
-    tab[o_rootN + j] = make_double2((double)w.first, (double)w.second);
-  }
-  for (int j = 0; j < R; ++j) {
-    const auto w = root(j, R);
-    tab[o_rootR + j] = make_double2((double)w.first, (double)w.second);
-  }
-  FV_TRY(dalloc(&p->blue_tab, tab.size()));
-  FV_CUDA(cudaMemcpy(p->blue_tab, tab.data(), tab.size() * sizeof(double2), cudaMemcpyHostToDevice));
-  a.rootM = p->blue_tab + o_rootM;
-  a.chirp = p->blue_tab + o_chirp;
-  a.FB = p->blue_tab + o_FB;
-  a.rootN = p->blue_tab + o_rootN;
-  a.rootR = p->blue_tab + o_rootR;
-  FV_CUDA(cudaFuncSetAttribute(fv::blue_p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)(2 * (size_t)M * sizeof(double2))));
-  p->blue = true;
   return FV_OK;
 }
 
@@ -967,49 +891,6 @@ int ring_fft_rp(fvPlan* p, bool inverse, const double2* in, long long in_cs, lon
   return FV_OK;
 }
 
-int ring_fft_blue(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
-                  double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s) {
-  fv::BlueArgs a = p->blue_args;
-  const size_t need = (size_t)3 * nrings * a.n;
-  if (p->blue_s1_cap < need) {
-    if (p->blue_s1) {
-      FV_CUDA(cudaDeviceSynchronize());
-      cudaFree(p->blue_s1);
-      p->blue_s1 = nullptr;
-      p->blue_s1_cap = 0;
-    }
-    FV_TRY(dalloc(&p->blue_s1, need));
-    p->blue_s1_cap = need;
-  }
-  a.in = in;
-  a.in_cs = in_cs;
-  a.in_rs = in_rs;
-  a.in_es = in_es;
-  a.out = out;
-  a.out_cs = out_cs;
-  a.out_rs = out_rs;
-  a.out_es = out_es;
-  a.S1 = p->blue_s1;
-  a.nrings = nrings;
-  a.inverse = inverse ? 1 : 0;
-  const long long ntr = 3LL * nrings * a.R;
-  fv::blue_p_kernel<<<(unsigned)ntr, fv::BLUE_T, 2 * (size_t)a.M * sizeof(double2), s>>>(a);
-  FV_CUDA(cudaGetLastError());
-  const unsigned g2 = (unsigned)((3LL * nrings * a.P + fv::BLUE_T - 1) / fv::BLUE_T);
-  switch (a.R) {
-    case 1: fv::blue_r_kernel<1><<<g2, fv::BLUE_T, 0, s>>>(a); break;
-    case 2: fv::blue_r_kernel<2><<<g2, fv::BLUE_T, 0, s>>>(a); break;
-    case 3: fv::blue_r_kernel<3><<<g2, fv::BLUE_T, 0, s>>>(a); break;
-    case 4: fv::blue_r_kernel<4><<<g2, fv::BLUE_T, 0, s>>>(a); break;
-    case 6: fv::blue_r_kernel<6><<<g2, fv::BLUE_T, 0, s>>>(a); break;
-    case 8: fv::blue_r_kernel<8><<<g2, fv::BLUE_T, 0, s>>>(a); break;
-    case 12: fv::blue_r_kernel<12><<<g2, fv::BLUE_T, 0, s>>>(a); break;
-    case 16: fv::blue_r_kernel<16><<<g2, fv::BLUE_T, 0, s>>>(a); break;
-    default: fv::blue_r_kernel<24><<<g2, fv::BLUE_T, 0, s>>>(a); break;
-  }
-  FV_CUDA(cudaGetLastError());
-  return FV_OK;
-}
 
 int ring_fft2_raw(fvPlan* p, bool inverse, const double2* in, long long in_cs, long long in_rs, long long in_es,
                   double2* out, long long out_cs, long long out_rs, long long out_es, int nrings, cudaStream_t s,
@@ -1551,7 +1432,6 @@ int ring_ffts(fvPlan* p, bool inverse, const double2* in, long long in_cs, long 
   if (p->smallp) return ring_fft_smallp(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   if (p->rader) return ring_fft_rader(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   if (p->rpfft) return ring_fft_rp(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
-  if (p->blue) return ring_fft_blue(p, inverse, in, in_cs, in_rs, in_es, out, out_cs, out_rs, out_es, nrings, s);
   cufftHandle h;
   FV_TRY(get_fft_strided(p, in_rs, in_es, out_rs, out_es, nrings, &h));
   FV_CUFFT(cufftSetStream(h, s));

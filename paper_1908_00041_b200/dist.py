@@ -35,7 +35,9 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from .shard import order_work
+def order_work(Lt: int, m: int) -> int:
+    """Legendre work of order m at scalar degree Lt: number of degrees l in [m, Lt]."""
+    return max(0, Lt + 1 - m)
 
 
 def _torch():

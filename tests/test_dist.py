@@ -23,19 +23,16 @@ def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_1908_00041_b200.shard import order_blocks, order_work, rank_env, shard_batch
+        from paper_1908_00041_b200.dist import order_work, rank_layouts
 
-        r, w, _ = rank_env()
-        assert (r, w) == (rank, world)
-        B, Lt = 5, 1025
-        lo, hi = shard_batch(B, world, rank)
-        mine = order_blocks(Lt, world)[rank]
-        cover = torch.zeros(B + Lt + 1, dtype=torch.int64)
-        cover[lo:hi] += 1
-        for m in mine:
-            cover[B + m] += 1
+        n_theta, L = 1026, 1024
+        Lt = L + 1
+        me = rank_layouts(n_theta, L, world)[rank]
+        cover = torch.zeros(n_theta + Lt + 1, dtype=torch.int64)
+        cover[me.rings[0]:me.rings[1]] += 1
+        cover[n_theta + me.orders[0]:n_theta + me.orders[1]] += 1
         dist.all_reduce(cover)
-        work = torch.tensor([sum(order_work(Lt, m) for m in mine)], dtype=torch.int64)
+        work = torch.tensor([sum(order_work(Lt, m) + 1 for m in range(*me.orders))], dtype=torch.int64)
         works = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
         dist.all_gather(works, work)
         if rank == 0:
@@ -56,8 +53,8 @@ def test_partition_over_two_gloo_ranks():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert all(c == 1 for c in cover)
-    assert abs(works[0] - works[1]) <= 1027
+    assert all(c == 1 for c in cover)  # every ring and every order owned exactly once
+    assert abs(works[0] - works[1]) <= 2 * 1027
 
 
 # ---------------------------------------------------------------------------
@@ -160,8 +157,7 @@ def test_order_sharded_simulated_ranks_match_oracle(world):
 
 
 def test_order_partition_properties():
-    from paper_1908_00041_b200.dist import natural_bins, order_ranges, rank_layouts, ring_blocks
-    from paper_1908_00041_b200.shard import order_work
+    from paper_1908_00041_b200.dist import natural_bins, order_ranges, order_work, rank_layouts, ring_blocks
 
     for Lt, world in ((1025, 8), (4097, 8), (33, 4), (10, 11), (5, 2)):
         rr = order_ranges(Lt, world)

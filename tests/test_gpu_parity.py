@@ -293,12 +293,12 @@ def test_odd_and_asymmetric_grids():
 @pytest.mark.parametrize("nphi", [24, 30, 36, 40, 42, 48, 49, 64, 75, 128, 286, 342, 2052,
                                   46, 23, 58, 86, 111, 496, 516, 984, 8196, 115, 134, 303, 1668])
 def test_ring_fft_radix_plans(nphi):
-    """Every packed radix (2..16 composites, primes 11..19), the Bluestein
-    lengths R * P with a prime P > 19 (46 = 2 * 23, 23, 58, 86, 111 = 3 * 37,
-    496 = 16 * 31, C2's 516 = 12 * 43, 984 = 24 * 41, C4's 8196 = 12 * 683) and
-    the cuFFT sub-DFT + combine path for P > 64 (134 = 2 * 67, 303 = 3 * 101,
-    1668 = 12 * 139, 8196) and the cuFFT fallback (115 = 5 * 23), forward and
-    adjoint against the oracle."""
+    """Every packed radix (2..16 composites, primes 11..19), the small-prime
+    lengths R * P with a prime 19 < P <= 64 (46 = 2 * 23, 23, 58, 86, 111 = 3 * 37,
+    496 = 16 * 31, C2's 516 = 12 * 43, 984 = 24 * 41), the Rader plan (C4's
+    8196 = 12 * 683), the cuFFT sub-DFT + combine path for P > 64 (134 = 2 * 67,
+    303 = 3 * 101, 1668 = 12 * 139) and the cuFFT fallback (115 = 5 * 23),
+    forward and adjoint against the oracle."""
     cuda_or_skip()
     rng = np.random.default_rng(nphi)
     L = 8
@@ -579,13 +579,13 @@ def test_direct_forward_batch_determinism_and_edges():
 def test_ring_fft_against_numpy(nphi):
     """fv_ring_fft alone (the sharded building block) on random rings, both
     directions, against numpy's pocketfft (favest/scalar.py:149, :178); the
-    large-prime lengths also through the opt-in Bluestein kernels and the cuFFT
-    sub-DFT path (FV_FFT=rp; 8196 defaults to the Rader kernels)."""
+    large-prime lengths also through the cuFFT sub-DFT path (FV_FFT=rp; 8196
+    defaults to the Rader kernels, 516 / 46 to the small-prime kernels)."""
     import ctypes
     import os
 
     torch = cuda_or_skip()
-    for fft in ("", "blue", "rp"):
+    for fft in ("", "rp"):
         os.environ["FV_FFT"] = fft
         try:
             _ring_fft_case(torch, nphi)

@@ -80,16 +80,3 @@ def test_type_validators_mirror_reference():
         fb.flat_index(2, 3)
 
 
-def test_shard_batch_and_order_blocks():
-    from paper_1908_00041_b200.shard import order_blocks, order_work, shard_batch
-
-    for B, W in ((4, 1), (4, 3), (16, 8), (3, 8)):
-        spans = [shard_batch(B, W, r) for r in range(W)]
-        assert spans[0][0] == 0 and spans[-1][1] == B
-        assert all(spans[i][1] == spans[i + 1][0] for i in range(W - 1))
-    for Lt, W in ((1025, 8), (4097, 8), (33, 2), (10, 4)):
-        blocks = order_blocks(Lt, W)
-        flat = sorted(m for b in blocks for m in b)
-        assert flat == list(range(Lt + 1))
-        work = [sum(order_work(Lt, m) for m in b) for b in blocks]
-        assert max(work) - min(work) <= Lt + 2
