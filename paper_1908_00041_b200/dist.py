@@ -35,6 +35,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
+
 def order_work(Lt: int, m: int) -> int:
     """Legendre work of order m at scalar degree Lt: number of degrees l in [m, Lt]."""
     return max(0, Lt + 1 - m)
@@ -116,6 +118,26 @@ def rank_layouts(n_theta: int, L: int, world: int) -> list[RankLayout]:
     return out
 
 
+def order_chunks(rng: tuple[int, int], Lt: int, chunks: int) -> list[tuple[int, int]]:
+    """[m0, m1) cut into ``chunks`` contiguous pieces of near-equal Legendre work
+    (empty pieces when there are fewer orders than chunks)."""
+    m0, m1 = rng
+    if chunks == 1 or m1 - m0 <= 1:
+        return [(m0, m1)] + [(m1, m1)] * (chunks - 1)
+    w = [order_work(Lt, m) + 1 for m in range(m0, m1)]
+    total = float(sum(w))
+    cuts, acc, k = [m0], 0.0, 1
+    for i, m in enumerate(range(m0, m1)):
+        acc += w[i]
+        while k < chunks and acc >= total * k / chunks:
+            cuts.append(m + 1)
+            k += 1
+    while len(cuts) < chunks:
+        cuts.append(m1)
+    cuts.append(m1)
+    return [(cuts[i], cuts[i + 1]) for i in range(chunks)]
+
+
 def natural_bins(m0: int, m1: int, n_phi: int):
     """(compact index, natural DFT bin) pairs of orders [m0, m1): +m then −m,
     the −0 duplicate of m = 0 left out."""
@@ -191,10 +213,12 @@ class OrderShardedPlan:
     ``device`` with ``max_batch`` fields.
     """
 
-    def __init__(self, stages, L, n_theta, n_phi, max_batch, rank, world, device, group=None):
+    def __init__(self, stages, L, n_theta, n_phi, max_batch, rank, world, device, group=None, chunks=1):
         torch = _torch()
         if not 0 <= rank < world:
             raise ValueError(f"bad rank {rank} of {world}")
+        if chunks < 1:
+            raise ValueError("chunks must be >= 1")
         self.stages = stages
         self.L, self.Lt = int(L), int(L) + 1
         self.n_theta, self.n_phi = int(n_theta), int(n_phi)
@@ -202,6 +226,7 @@ class OrderShardedPlan:
         self.rank, self.world = int(rank), int(world)
         self.device = torch.device(device)
         self.group = group
+        self.chunks = int(chunks)
         self.layouts = rank_layouts(self.n_theta, self.L, self.world)
         me = self.layouts[self.rank]
         self.me = me
@@ -210,105 +235,174 @@ class OrderShardedPlan:
         c128 = torch.complex128
         B, n = self.max_batch, self.n_phi
         # local ring spectra: forward FFT output, and the adjoint's inverse-FFT input whose
-        # bins no rank owns (n_phi > 2 Lt + 1) must stay zero — hence two buffers
+        # bins no rank owns (n_phi > 2 Lt + 1) must stay zero -- hence two buffers
         self.S_loc = torch.empty((3, B, self.nloc, n), dtype=c128, device=self.device)
         self.S_loc_a = torch.zeros((3, B, self.nloc, n), dtype=c128, device=self.device)
-        # forward: compact bins of the Legendre orders; adjoint: compact bins of the owned orders
-        nbf = me.legendre[1] - me.legendre[0]
-        nba = me.orders[1] - me.orders[0]
-        self.S_fwd = torch.zeros((3, B, self.n_theta, 2 * nbf), dtype=c128, device=self.device)
-        self.S_adj = torch.zeros((3, B, self.n_theta, 2 * nba), dtype=c128, device=self.device)
-        # index tensors for the transposes
-        self._send_bins = []  # forward: natural bins destination h needs (its Legendre orders)
-        for h in range(self.world):
-            lo, hi = self.layouts[h].legendre
-            idx = list(range(lo, hi)) + [(n - m) % n for m in range(lo, hi)]
-            self._send_bins.append(torch.tensor(idx, dtype=torch.long, device=self.device))
-        self._recv_bins = []  # adjoint: (compact index, natural bin) of owner h's orders
-        for h in range(self.world):
-            m0, m1 = self.layouts[h].orders
-            pairs = natural_bins(m0, m1, n)
-            self._recv_bins.append((torch.tensor([p[0] for p in pairs], dtype=torch.long, device=self.device),
-                                    torch.tensor([p[1] for p in pairs], dtype=torch.long, device=self.device)))
+        # per chunk q and rank h: forward coefficient / Legendre order ranges, adjoint orders
+        Lt = self.Lt
+        self._fc, self._fl, self._ao = [], [], []
+        for lay in self.layouts:
+            cs = order_chunks(lay.coef, Lt, self.chunks)
+            self._fc.append(cs)
+            self._fl.append([(max(0, c0 - 1), min(Lt + 1, c1 + 1)) if c1 > c0 else (c0, c0) for c0, c1 in cs])
+            self._ao.append(order_chunks(lay.orders, Lt, self.chunks))
+        self._send_bins = []  # [q][h]: natural bins of h's chunk-q Legendre orders (+m then -m)
+        self._recv_bins = []  # [q][h]: (compact index, natural bin) of h's chunk-q adjoint orders
+        for q in range(self.chunks):
+            sb, rb = [], []
+            for h in range(self.world):
+                lo, hi = self._fl[h][q]
+                idx = list(range(lo, hi)) + [(n - m) % n for m in range(lo, hi)]
+                sb.append(torch.tensor(idx, dtype=torch.long, device=self.device))
+                pairs = natural_bins(*self._ao[h][q], n)
+                rb.append((torch.tensor([p[0] for p in pairs], dtype=torch.long, device=self.device),
+                           torch.tensor([p[1] for p in pairs], dtype=torch.long, device=self.device)))
+            self._send_bins.append(sb)
+            self._recv_bins.append(rb)
 
     # ---- transport -------------------------------------------------------
-    def _all_to_all(self, sends, out_splits):
-        """sends[h]: contiguous complex tensor for rank h; out_splits[g]: float64 count from rank g."""
+    def _pack(self, blocks):
+        """One flat float64 send buffer of the per-destination complex blocks (each
+        written once, by index_select / copy straight into its slice)."""
+        torch = _torch()
+        sizes = [int(np.prod(shape)) * 2 for shape, _ in blocks]
+        flat = torch.empty(sum(sizes), dtype=torch.float64, device=self.device)
+        o = 0
+        for (shape, fill), k in zip(blocks, sizes):
+            fill(torch.view_as_complex(flat[o:o + k].view(-1, 2)).view(shape))
+            o += k
+        return flat, sizes
+
+    def _all_to_all(self, flat_in, in_splits, out_splits, async_op=False):
+        """Returns (work or None, received complex blocks per source rank)."""
         torch = _torch()
         import torch.distributed as dist
 
-        flat_in = torch.cat([torch.view_as_real(s).reshape(-1) for s in sends])
-        in_splits = [s.numel() * 2 for s in sends]
         flat_out = torch.empty(sum(out_splits), dtype=torch.float64, device=self.device)
-        dist.all_to_all_single(flat_out, flat_in, out_splits, in_splits, group=self.group)
+        work = dist.all_to_all_single(flat_out, flat_in, out_splits, in_splits, group=self.group,
+                                      async_op=async_op)
         outs, o = [], 0
         for k in out_splits:
             outs.append(torch.view_as_complex(flat_out[o:o + k].view(-1, 2)))
             o += k
-        return outs
+        return work, outs
 
     # ---- forward ---------------------------------------------------------
-    def forward_send(self, T_local):
-        """Local FFTs, then the per-destination blocks (3, B, nloc, 2*nb_h)."""
+    def forward_fft(self, T_local):
+        """Local ring FFTs of the owned rings -> S_loc (3, B, nloc, n_phi)."""
         B = int(T_local.shape[0])
         S = self.S_loc[:, :B]
         self.stages.fft_fields(T_local, S)
-        return [S.index_select(3, self._send_bins[h]).contiguous() for h in range(self.world)]
+        return S
 
-    def forward_recv_sizes(self, B):
-        nb = self.me.legendre[1] - self.me.legendre[0]
-        return [3 * B * (l.rings[1] - l.rings[0]) * 2 * nb * 2 for l in self.layouts]
+    def forward_send(self, S, q=0):
+        """Chunk q's per-destination blocks (3, B, nloc, 2 nb_hq): one packed buffer."""
+        torch = _torch()
+        B = int(S.shape[1])
+        blocks = []
+        for h in range(self.world):
+            idx = self._send_bins[q][h]
+            blocks.append(((3, B, self.nloc, int(idx.numel())),
+                           lambda out, idx=idx: torch.index_select(S, 3, idx, out=out)))
+        return self._pack(blocks)
 
-    def forward_finish(self, recvs, B, a, b):
-        nb = self.me.legendre[1] - self.me.legendre[0]
-        S = self.S_fwd[:, :B]
+    def forward_recv_sizes(self, B, q=0):
+        lo, hi = self._fl[self.rank][q]
+        return [3 * B * (l.rings[1] - l.rings[0]) * 2 * (hi - lo) * 2 for l in self.layouts]
+
+    def forward_finish(self, recvs, B, a, b, q=0):
+        """Chunk q: the received blocks of every source's rings -> compact spectra of all
+        rings -> fold + Legendre + CG of this rank's chunk-q orders."""
+        torch = _torch()
+        lo, hi = self._fl[self.rank][q]
+        c0, c1 = self._fc[self.rank][q]
+        if c1 <= c0:
+            return a, b
+        nb = hi - lo
+        S = torch.empty((3, B, self.n_theta, 2 * nb), dtype=torch.complex128, device=self.device)
         for g, r in enumerate(recvs):
             r0, r1 = self.layouts[g].rings
             S[:, :, r0:r1, :] = r.view(3, B, r1 - r0, 2 * nb)
-        self.stages.forward_orders(S, self.me.legendre[0], nb, a, b, self.me.legendre, self.me.coef)
+        self.stages.forward_orders(S, lo, nb, a, b, (lo, hi), (c0, c1))
         return a, b
 
     def forward(self, T_local, a=None, b=None):
-        """T_local (B, nloc*n_phi, 3) -> a, b (B, (L+1)^2), valid at this rank's coef orders."""
+        """T_local (B, nloc*n_phi, 3) -> a, b (B, (L+1)^2), valid at this rank's coef orders.
+
+        The transpose runs in ``chunks`` order chunks: every chunk's all-to-all is
+        issued asynchronously up front (NCCL's stream carries them back to back), then
+        chunk q's Legendre / CG runs as soon as chunk q has arrived, overlapping the
+        transfers of the chunks after it."""
         torch = _torch()
         B = int(T_local.shape[0])
         if a is None:
             a = torch.zeros((B, self.K), dtype=torch.complex128, device=self.device)
         if b is None:
             b = torch.zeros((B, self.K), dtype=torch.complex128, device=self.device)
-        sends = self.forward_send(T_local)
-        recvs = self._all_to_all(sends, self.forward_recv_sizes(B))
-        return self.forward_finish(recvs, B, a, b)
+        S = self.forward_fft(T_local)
+        pending = []
+        for q in range(self.chunks):
+            flat, sizes = self.forward_send(S, q)
+            work, recvs = self._all_to_all(flat, sizes, self.forward_recv_sizes(B, q), async_op=True)
+            pending.append((work, recvs, flat))
+        for q, (work, recvs, _) in enumerate(pending):
+            if work is not None:
+                work.wait()
+            self.forward_finish(recvs, B, a, b, q)
+        return a, b
 
     # ---- adjoint ---------------------------------------------------------
-    def adjoint_send(self, a, b):
+    def adjoint_send(self, a, b, q=0):
+        """Chunk q: synthesis of this rank's chunk-q orders into compact spectra of every
+        ring, packed per destination ring block."""
+        torch = _torch()
         B = int(a.shape[0])
-        S = self.S_adj[:, :B]
-        self.stages.adjoint_orders(a, b, self.me.orders, S)
-        return [S[:, :, l.rings[0]:l.rings[1], :].contiguous() for l in self.layouts]
+        m0, m1 = self._ao[self.rank][q]
+        nb = m1 - m0
+        S = torch.zeros((3, B, self.n_theta, 2 * nb), dtype=torch.complex128, device=self.device)
+        if nb:
+            self.stages.adjoint_orders(a, b, (m0, m1), S)
+        blocks = [((3, B, l.rings[1] - l.rings[0], 2 * nb),
+                   lambda out, l=l: out.copy_(S[:, :, l.rings[0]:l.rings[1], :])) for l in self.layouts]
+        return self._pack(blocks)
 
-    def adjoint_recv_sizes(self, B):
-        return [3 * B * self.nloc * 2 * (l.orders[1] - l.orders[0]) * 2 for l in self.layouts]
+    def adjoint_recv_sizes(self, B, q=0):
+        return [3 * B * self.nloc * 2 * (o[q][1] - o[q][0]) * 2 for o in self._ao]
 
-    def adjoint_finish(self, recvs, B, T_local):
+    def adjoint_unpack(self, recvs, B, q=0):
         S = self.S_loc_a[:, :B]
         for h, r in enumerate(recvs):
-            nb = self.layouts[h].orders[1] - self.layouts[h].orders[0]
-            blk = r.view(3, B, self.nloc, 2 * nb)
-            ci, nat = self._recv_bins[h]
+            m0, m1 = self._ao[h][q]
+            if m1 <= m0:
+                continue
+            blk = r.view(3, B, self.nloc, 2 * (m1 - m0))
+            ci, nat = self._recv_bins[q][h]
             S.index_copy_(3, nat, blk.index_select(3, ci))
-        self.stages.ifft_fields(S, T_local)
+
+    def adjoint_finish(self, B, T_local):
+        self.stages.ifft_fields(self.S_loc_a[:, :B], T_local)
         return T_local
 
     def adjoint(self, a, b, T_local=None):
-        """a, b (B, (L+1)^2) with this rank's orders ±1 valid -> T_local (B, nloc*n_phi, 3)."""
+        """a, b (B, (L+1)^2) with this rank's orders +-1 valid -> T_local (B, nloc*n_phi, 3).
+
+        Chunk q's synthesis is followed by its asynchronous all-to-all, which then
+        overlaps the synthesis of chunk q + 1; the inverse ring FFTs run once every
+        chunk has arrived."""
         torch = _torch()
         B = int(a.shape[0])
         if T_local is None:
             T_local = torch.empty((B, self.nloc * self.n_phi, 3), dtype=torch.complex128, device=self.device)
-        sends = self.adjoint_send(a, b)
-        recvs = self._all_to_all(sends, self.adjoint_recv_sizes(B))
-        return self.adjoint_finish(recvs, B, T_local)
+        pending = []
+        for q in range(self.chunks):
+            flat, sizes = self.adjoint_send(a, b, q)
+            work, recvs = self._all_to_all(flat, sizes, self.adjoint_recv_sizes(B, q), async_op=True)
+            pending.append((work, recvs, flat))
+        for q, (work, recvs, _) in enumerate(pending):
+            if work is not None:
+                work.wait()
+            self.adjoint_unpack(recvs, B, q)
+        return self.adjoint_finish(B, T_local)
 
     # ---- coefficients ------------------------------------------------------
     def order_mask(self, orders=None):
@@ -335,13 +429,14 @@ class OrderShardedPlan:
         return out[0], out[1]
 
 
-def make_plan(L, grid, max_batch, rank, world, device=None, group=None):
-    """Production constructor: one GridPlan on this rank's GPU + its shard layout."""
+def make_plan(L, grid, max_batch, rank, world, device=None, group=None, chunks=4):
+    """Production constructor: one GridPlan on this rank's GPU + its shard layout; the
+    transposes run in ``chunks`` order chunks overlapped with the per-order stages."""
     from .plan import GridPlan
 
     plan = GridPlan.from_grid(grid, L, max_batch=max_batch, device=device)
     return OrderShardedPlan(CudaStages(plan), L, grid.n_theta, grid.n_phi, max_batch, rank, world,
-                            plan.device, group)
+                            plan.device, group, chunks=chunks)
 
 
 # ---------------------------------------------------------------------------
@@ -350,23 +445,38 @@ def make_plan(L, grid, max_batch, rank, world, device=None, group=None):
 def simulate_forward(plans, T_locals):
     torch = _torch()
     B = int(T_locals[0].shape[0])
-    sends = [p.forward_send(T) for p, T in zip(plans, T_locals)]
+    S = [p.forward_fft(T) for p, T in zip(plans, T_locals)]
     outs = []
-    for h, p in enumerate(plans):
-        recvs = [sends[g][h] for g in range(len(plans))]
+    for p in plans:
         a = torch.zeros((B, p.K), dtype=torch.complex128, device=p.device)
-        b = torch.zeros_like(a)
-        outs.append(p.forward_finish(recvs, B, a, b))
+        outs.append((a, torch.zeros_like(a)))
+    for q in range(plans[0].chunks):
+        sends = [_unflatten(p.forward_send(s, q), p) for p, s in zip(plans, S)]
+        for h, p in enumerate(plans):
+            p.forward_finish([sends[g][h] for g in range(len(plans))], B, outs[h][0], outs[h][1], q)
     return outs
 
 
 def simulate_adjoint(plans, ab):
     torch = _torch()
     B = int(ab[0][0].shape[0])
-    sends = [p.adjoint_send(a, b) for p, (a, b) in zip(plans, ab)]
+    for q in range(plans[0].chunks):
+        sends = [_unflatten(p.adjoint_send(a, b, q), p) for p, (a, b) in zip(plans, ab)]
+        for g, p in enumerate(plans):
+            p.adjoint_unpack([sends[h][g] for h in range(len(plans))], B, q)
     outs = []
-    for g, p in enumerate(plans):
-        recvs = [sends[h][g] for h in range(len(plans))]
+    for p in plans:
         T = torch.empty((B, p.nloc * p.n_phi, 3), dtype=torch.complex128, device=p.device)
-        outs.append(p.adjoint_finish(recvs, B, T))
+        outs.append(p.adjoint_finish(B, T))
     return outs
+
+
+def _unflatten(packed, plan):
+    """The per-destination complex blocks of a packed send buffer."""
+    torch = _torch()
+    flat, sizes = packed
+    out, o = [], 0
+    for k in sizes:
+        out.append(torch.view_as_complex(flat[o:o + k].view(-1, 2)))
+        o += k
+    return out

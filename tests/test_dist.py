@@ -75,7 +75,7 @@ def _field_and_coeffs(L, B, seed):
     return th, w, n, T
 
 
-def _sharded_worker(rank, world, port, q):
+def _sharded_worker(rank, world, port, q, chunks=1):
     import numpy as np
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
@@ -88,7 +88,7 @@ def _sharded_worker(rank, world, port, q):
         L, B = 9, 2
         th, w, n, T = _field_and_coeffs(L, B, 11)
         nth = len(th)
-        plan = OrderShardedPlan(OracleStages(L, th, w, n), L, nth, n, B, rank, world, "cpu")
+        plan = OrderShardedPlan(OracleStages(L, th, w, n), L, nth, n, B, rank, world, "cpu", chunks=chunks)
         r0, r1 = plan.me.rings
         T_local = torch.from_numpy(T.reshape(B, nth, n, 3)[:, r0:r1].reshape(B, -1, 3).copy())
         a, b = plan.forward(T_local)
@@ -111,12 +111,15 @@ def _sharded_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_order_sharded_transform_over_two_gloo_ranks():
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_order_sharded_transform_over_two_gloo_ranks(chunks):
+    """world 2 over gloo; chunks 3: the transposes split into order chunks whose
+    asynchronous all-to-alls overlap the per-chunk stages (dist.py forward / adjoint)."""
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, q, chunks)) for r in range(world)]
     for p in procs:
         p.start()
     ef, ea = q.get(timeout=300)
@@ -126,8 +129,8 @@ def test_order_sharded_transform_over_two_gloo_ranks():
     assert ef <= 1e-13 and ea <= 1e-13
 
 
-@pytest.mark.parametrize("world", [1, 3, 4])
-def test_order_sharded_simulated_ranks_match_oracle(world):
+@pytest.mark.parametrize("world,chunks", [(1, 1), (3, 1), (4, 1), (1, 3), (3, 2), (4, 5)])
+def test_order_sharded_simulated_ranks_match_oracle(world, chunks):
     """The same driver, ranks simulated in one process (local copies for the transposes)."""
     import numpy as np
 
@@ -138,7 +141,8 @@ def test_order_sharded_simulated_ranks_match_oracle(world):
     L, B = 8, 2
     th, w, n, T = _field_and_coeffs(L, B, 5 + world)
     nth = len(th)
-    plans = [OrderShardedPlan(OracleStages(L, th, w, n), L, nth, n, 3, r, world, "cpu") for r in range(world)]
+    plans = [OrderShardedPlan(OracleStages(L, th, w, n), L, nth, n, 3, r, world, "cpu", chunks=chunks)
+             for r in range(world)]
     T4 = T.reshape(B, nth, n, 3)
     Tl = [torch.from_numpy(T4[:, p.me.rings[0]:p.me.rings[1]].reshape(B, -1, 3).copy()) for p in plans]
     outs = simulate_forward(plans, Tl)
@@ -173,3 +177,16 @@ def test_order_partition_properties():
         assert lay.legendre[0] <= max(0, lay.coef[0] - 1) and lay.legendre[1] >= min(1026, lay.coef[1] + 1)
     nb = natural_bins(0, 3, 20)
     assert nb == [(0, 0), (1, 1), (2, 2), (4, 19), (5, 18)]
+
+
+def test_order_chunks_cover_and_balance():
+    from paper_1908_00041_b200.dist import order_chunks, order_work
+
+    for rng, Lt, k in (((0, 1026), 1025, 4), ((300, 700), 1025, 3), ((5, 7), 1025, 4), ((0, 4098), 4097, 8),
+                       ((9, 10), 9, 2)):
+        cs = order_chunks(rng, Lt, k)
+        assert len(cs) == k and cs[0][0] == rng[0] and cs[-1][1] == rng[1]
+        assert all(cs[i][1] == cs[i + 1][0] for i in range(k - 1)) and all(a <= b for a, b in cs)
+        if rng[1] - rng[0] >= 100:
+            works = [sum(order_work(Lt, m) + 1 for m in range(a, b)) for a, b in cs]
+            assert max(works) - min(works) <= 2 * (Lt + 2)

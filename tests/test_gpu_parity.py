@@ -409,11 +409,12 @@ def test_host_pipeline_matches_device_path():
         pipe.submit_roundtrip(T, outs[0])  # device tensor, not pinned host
 
 
-@pytest.mark.parametrize("L,world", [(40, 1), (40, 2), (40, 3), (21, 2)])
-def test_order_sharded_path_matches_single_plan(L, world):
+@pytest.mark.parametrize("L,world,chunks", [(40, 1, 1), (40, 2, 1), (40, 3, 1), (21, 2, 1), (40, 2, 3), (21, 3, 4)])
+def test_order_sharded_path_matches_single_plan(L, world, chunks):
     """The order-sharded building blocks (fv_ring_fft / fv_forward_orders / fv_adjoint_orders,
-    dist.py) with ranks simulated in one process reproduce GridPlan.forward/adjoint; with the
-    hand-written FFT (n_phi = 84) bitwise, with the cuFFT fallback (n_phi = 46) to rounding."""
+    dist.py) with ranks simulated in one process reproduce GridPlan.forward/adjoint, also with
+    the transposes cut into order chunks; with the hand-written FFT (n_phi = 84) bitwise,
+    with the cuFFT fallback (n_phi = 46) to rounding."""
     torch = cuda_or_skip()
     from paper_1908_00041_b200.dist import CudaStages, OrderShardedPlan, simulate_adjoint, simulate_forward
 
@@ -428,7 +429,8 @@ def test_order_sharded_path_matches_single_plan(L, world):
     T = T + _t(np.stack([O.tangent_noise(rng, O.grid_points(th, nphi), 0.1) for _ in range(B)]))
     a_ref, b_ref = plan.forward(T)
     T_ref = plan.adjoint(a_ref, b_ref)
-    plans = [OrderShardedPlan(CudaStages(plan), L, nth, nphi, maxB, r, world, plan.device) for r in range(world)]
+    plans = [OrderShardedPlan(CudaStages(plan), L, nth, nphi, maxB, r, world, plan.device, chunks=chunks)
+             for r in range(world)]
     T4 = T.view(B, nth, nphi, 3)
     Tl = [T4[:, p.me.rings[0]:p.me.rings[1]].reshape(B, -1, 3).contiguous() for p in plans]
     outs = simulate_forward(plans, Tl)
