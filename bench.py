@@ -625,14 +625,31 @@ def c4_detail(args, rank, world, dev, dist, timed, barrier, max_over_ranks):
         torch.cuda.synchronize(dev)
         ms1 = s0.elapsed_time(s1) / n
         rel1 = float(torch.linalg.vector_norm(Tout - T) / torch.linalg.vector_norm(T))
-        plan.close()
-        del T, Tout, a, b
-        torch.cuda.empty_cache()
         out.update({"single_gpu_ms_per_step": ms1, "single_gpu_roundtrip_rel_l2": rel1,
                     "single_gpu_fraction_of_fp64_roofline_datasheet":
                         (2 * fl["total"] / (ms1 / 1e3)) / (FP64_PEAK_DATASHEET * 1e12)})
         if world > 1:
             out["speedup_vs_single_gpu"] = ms1 / out["sharded_ms_per_step"]
+        if world == 1 and not args.no_rank_share:
+            # the order-sharded step's per-rank device work at 2 / 4 / 8 ranks, each simulated
+            # rank timed alone on this GPU (tools/c4_rank_share.py; no kernel waits on another
+            # rank), plus the all-to-all volume at NVLink speed (modelled, not measured)
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from c4_rank_share import rank_share
+
+            del Tout
+            rs = rank_share(plan, T, a_full, b_full, worlds=(2, 4, 8), single=ms1)
+            out["order_sharded_projection"] = {
+                "method": "per-rank device work of dist.OrderShardedPlan (chunks 2, cost-balanced orders) timed "
+                          "rank by rank on one GPU, transposes replaced by local copies; NVLink time = max bytes "
+                          "sent per rank / 900 GB/s (modelled: one GPU)",
+                **{str(w): {"slowest_rank_ms": v["slowest_rank_ms"], "nvlink_ms_at_900GBs": v["nvlink_ms_at_900GBs"],
+                            "speedup_compute_only": v["speedup_vs_single_gpu_plan_compute_only"],
+                            "speedup_with_serial_nvlink": v["speedup_vs_single_gpu_plan_with_serial_nvlink"]}
+                   for w, v in rs["ranks"].items()}}
+        plan.close()
+        del T, a, b
+        torch.cuda.empty_cache()
     barrier()
     return out
 
@@ -750,6 +767,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-detail", action="store_true", help="skip the on-the-fly / C5 / C4 detail entries")
+    ap.add_argument("--no-rank-share", action="store_true", help="skip the C4 per-rank projection at N=1")
     ap.add_argument("--workload", default="c3", choices=["c3", "c4"],
                     help="c3: batch-sharded L=1024 (the headline); c4: one L=4096 field, order-sharded")
     args = ap.parse_args()

@@ -86,6 +86,14 @@ void fv_plan_destroy(fvPlan* plan);
 /* Plan properties: 1 if the grid was folded about the equator (mirror pairs). */
 int fv_plan_info(const fvPlan* plan, int* L, int* n_theta, int* n_phi, int* n_pairs, int* paired);
 
+/* Per-order Legendre work of a grid plan, for balancing the order-sharded
+ * partition (the multi-GPU layout of paper_1908_00041_b200/dist.py): cost[m],
+ * m = 0..L+1, is the number of (degree, ring pair) products the contraction of
+ * order m actually runs -- pairs count from their polar start (the first degree
+ * whose |Pbar| reaches 2^-100), not from l = m.  Blocking (a device -> host
+ * copy).  Replaces the reference's nothing: favest has one process. */
+int fv_order_cost(const fvPlan* plan, double* cost);
+
 /* Forward VSHT of B tangent fields on the plan's grid: T -> (a, b). */
 int fv_forward_grid(fvPlan* plan, const double* T, double* a, double* b, int B, void* stream);
 

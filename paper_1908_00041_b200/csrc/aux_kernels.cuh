@@ -271,6 +271,12 @@ struct CgFwdArgs {
   const double* cgt;    // cg_table_kernel: 9 x K_t (xi1..6, mu1..3)
   int L, ncolF, B_total, b0, nfields;
   int c_lo, c_hi;       // orders |m| written: [c_lo, c_hi) (F rows of c_lo-1 .. c_hi must be current)
+  // pair-chunk split of the forward Legendre launch (legendre.cuh FwdArgs::ksplit): F
+  // is the sum of nsplit partial buffers, F then Fx + (s - 1) * fx_stride for s = 1..,
+  // added in this order (pointer arithmetic: an indexed pointer array would go to local memory)
+  int nsplit;
+  const double* Fx;
+  long long fx_stride;
 };
 
 // U = -x + i y, V = x + i y, W = z (favest/transforms.py:112) from the
@@ -345,11 +351,11 @@ __global__ void cg_fwd_kernel(CgFwdArgs a) {
 constexpr int CGF_THREADS = 256, CGF_MB = 32;
 __host__ __device__ constexpr int cgf_nt(int nf) { return (12 * nf + 7) / 8; }
 __host__ __device__ constexpr int cgf_rs(int nf) { return 4 * cgf_nt(nf) + 1; }  // odd double2 row stride
-template <int NF>
+template <int NF, bool SPLIT = false>
 __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
   constexpr int NV = 4 * cgf_nt(NF), RS = cgf_rs(NF), ROWS = CGF_MB + 2;
   const int l = blockIdx.y;
-  const int m0 = blockIdx.x * CGF_MB;
+  const int m0 = (blockIdx.x + a.c_lo / CGF_MB) * CGF_MB;  // the grid starts at the first written block
   if (m0 > l) return;
   extern __shared__ __align__(16) double2 cgf_smem[];  // [3][ROWS][RS]
   constexpr int NE = 3 * ROWS * NV, PER = (NE + CGF_THREADS - 1) / CGF_THREADS;
@@ -374,15 +380,33 @@ __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
   const double x5 = tab(4, l - 1, M), x6 = tab(5, l + 1, M);
   const double u1 = tab(6, l, M - 1), u2 = tab(7, l, M), u3 = tab(8, l, M + 1);
   double2 x[PER];
+  int off[PER];  // double2 offset of the staged F entry, -1 outside the table
 #pragma unroll
   for (int u = 0; u < PER; ++u) {  // all loads of the thread in flight before the stores
     const int e = threadIdx.x + u * CGF_THREADS;
     x[u] = make_double2(0.0, 0.0);
+    off[u] = -1;
     if (e < NE) {
       const int i = e / (ROWS * NV), r = (e / NV) % ROWS, v = e % NV;
       const int lp = l - 1 + i, mp = m0 - 1 + r;
-      if (lp >= 0 && lp <= Lt && mp >= 0 && mp <= lp)
-        x[u] = __ldg(reinterpret_cast<const double2*>(a.F) + ((size_t)(lp * (lp + 1) / 2 + mp) * NV + v));
+      if (lp >= 0 && lp <= Lt && mp >= 0 && mp <= lp) {
+        off[u] = (lp * (lp + 1) / 2 + mp) * NV + v;
+        x[u] = __ldg(reinterpret_cast<const double2*>(a.F) + off[u]);
+      }
+    }
+  }
+  // split forward launches (SPLIT instantiation only: the unsplit kernel keeps its
+  // 80 registers and three CTAs per SM): add the partial F buffers 1.. in split order
+  if (SPLIT)
+  for (int sp = 1; sp < a.nsplit; ++sp) {
+    const double2* Fp = reinterpret_cast<const double2*>(a.Fx + (sp - 1) * a.fx_stride);
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      if (off[u] >= 0) {
+        const double2 y = __ldg(Fp + off[u]);
+        x[u].x += y.x;
+        x[u].y += y.y;
+      }
     }
   }
 #pragma unroll

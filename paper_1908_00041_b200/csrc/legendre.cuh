@@ -120,6 +120,12 @@ struct FwdArgs {
   // CTA b works on group b % ngroups, X / F of group g at + g * x_gstride / f_gstride
   int ngroups;
   long long x_gstride, f_gstride;
+  // pair-chunk split (launches with few orders: the order-sharded chunks): split s
+  // of ksplit contracts the chunks c = s (mod ksplit) of every order into its own
+  // partial F buffer (s = 0: F, s > 0: Fx + (s - 1) * f_gstride); the forward CG
+  // adds them in split order
+  int ksplit;
+  double* Fx;
 };
 
 // chunk starts of one order held across the warp (chunk 32 g + lane in v[g])
@@ -128,13 +134,16 @@ struct ChunkStarts {
   int ng;  // 0: no skipping (more than 128 chunks)
 };
 
-__device__ __forceinline__ ChunkStarts load_chunk_starts(const int* cmin_m, int nchunks, int lane) {
+__device__ __forceinline__ ChunkStarts load_chunk_starts(const int* cmin_m, int nchunks, int lane, int split = 0,
+                                                         int S = 1) {
+  // the chunks of one split: u = 0 .. nu-1 is chunk split + S u
+  const int nu = (nchunks - split + S - 1) / S;
   ChunkStarts cs;
-  cs.ng = nchunks <= 128 ? (nchunks + 31) / 32 : 0;
+  cs.ng = nu <= 128 ? (nu + 31) / 32 : 0;
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
-    const int c = 32 * g + lane;
-    cs.v[g] = (g < cs.ng && c < nchunks) ? __ldg(&cmin_m[c]) : 0x7fffffff;
+    const int u = 32 * g + lane;
+    cs.v[g] = (g < cs.ng && u < nu) ? __ldg(&cmin_m[split + S * u]) : 0x7fffffff;
   }
   return cs;
 }
@@ -329,7 +338,7 @@ __device__ __forceinline__ void fwd_mtile_dmma(int kfirst, int nt0, double (&acc
 // (m ascending = work descending), which balances the per-order work (L+2-m).
 __device__ __forceinline__ int fwd_item(int k, int b, int G) { return (k & 1) ? k * G + (G - 1 - b) : k * G + b; }
 
-template <int NT>
+template <int NT, bool SPLIT = false>
 __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args) {
   extern __shared__ __align__(128) double smem[];
   using SM = FwdSmem<NT>;
@@ -347,6 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
 
   const int Lt = args.Lt;
   const int nchunks = args.nchunks;
+  const int S = (SPLIT && args.ksplit > 1) ? args.ksplit : 1;  // compile-time 1 in the unsplit kernel
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   {  // field group of this CTA (blocks interleave the groups: heavy orders of every group first)
@@ -379,11 +389,13 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
     const uint64_t pol_first = l2_evict_first(), pol_last = l2_evict_last();
     uint32_t tbase = 0;  // tile counter across this CTA's orders
     for (int k = 0;; ++k) {
-      const int item = fwd_item(k, bxg, gdg);
-      if (item >= args.m_count) break;
+      const int it = fwd_item(k, bxg, gdg);
+      if (it >= args.m_count * S) break;
+      const int item = it / S, split = it - item * S;
+      const int nu = (nchunks - split + S - 1) / S;  // this split's chunks c = split + S u
       const int m = args.m_begin + item;
       const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
-      // Tile ownership.  Warp pw owns the chunks c = pw (mod 4) (their recurrence
+      // Tile ownership (u: the split's chunk index, c = split + S u).  Warp pw owns the chunks c = pw (mod 4) (their recurrence
       // state never changes hands).  Each l-block's leading all-zero chunks
       // (polar start past the block) are skipped by producers and consumers
       // alike, so tile t of the pipeline is the t-th live tile.  A producer
@@ -392,8 +404,8 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       // apart here, so it first waits until consumer warp 0 has finished tile
       // t - 5 (which implies every consumer has finished tile t - 10).
       if (!table) {
-        for (int c = pw; c < nchunks; c += kProducerWarps) {
-          const int p = c * FWD_RC + lane;
+        for (int u = pw; u < nu; u += kProducerWarps) {
+          const int p = (split + S * u) * FWD_RC + lane;
           st_t[p] = args.pair_t[p];
           st_ls[p] = args.start_l[(size_t)m * args.nPpad + p];
           st_p1[p] = 0.0;
@@ -401,16 +413,17 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
         }
         __syncwarp();
       }
-      const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane);
+      const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane, split, S);
       uint32_t tb = tbase;
       for (int j = 0; j < nlb; ++j) {
         const int l0 = m + FWD_LB * j;
-        const int c0 = first_live_chunk(cst, l0, nchunks);
-        const int cfirst = c0 + ((pw - c0) & (kProducerWarps - 1));
-        if (!table && cfirst < nchunks) fwd_stage_coefs(abw, args, m, l0, lane);
-        for (int c = cfirst; c < nchunks; c += kProducerWarps) {
+        const int u0 = first_live_chunk(cst, l0, nu);
+        const int ufirst = u0 + ((pw - u0) & (kProducerWarps - 1));
+        if (!table && ufirst < nu) fwd_stage_coefs(abw, args, m, l0, lane);
+        for (int u = ufirst; u < nu; u += kProducerWarps) {
+          const int c = split + S * u;
           const int tl = j * nchunks + c;  // table tile index (all chunks)
-          const uint32_t t = tb + (c - c0);
+          const uint32_t t = tb + (u - u0);
           if (t >= 2 * FWD_STAGES)
             while (*cons0 < (int)t - (FWD_STAGES - 1)) __nanosleep(32);
         {
@@ -450,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
           mbar_arrive(&full[stage]);
         }
         }
-        tb += nchunks - c0;
+        tb += nu - u0;
       }
       tbase = tb;
     }
@@ -479,15 +492,18 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       for (int jn = 0; jn < NT; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
     uint32_t tbase = 0;
     for (int k = 0;; ++k) {
-      const int item = fwd_item(k, bxg, gdg);
-      if (item >= args.m_count) break;
+      const int it = fwd_item(k, bxg, gdg);
+      if (it >= args.m_count * S) break;
+      const int item = it / S, split = it - item * S;
+      const int nu = (nchunks - split + S - 1) / S;
+      double* const Fout = split ? args.Fx + (size_t)(split - 1) * args.f_gstride : args.F;
       const int m = args.m_begin + item;
       const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
       const double2* dgm = args.dg + args.dgofs[m];
-      const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane);
+      const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane, split, S);
       for (int j = 0; j < nlb; ++j) {
         const int l0 = m + FWD_LB * j;
-        const int c0 = first_live_chunk(cst, l0, nchunks);
+        const int u0 = first_live_chunk(cst, l0, nu);
         // gamma of this warp's epilogue rows, loaded before the tiles (not after them)
         double gam4[4];
 #pragma unroll
@@ -550,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
         // two register sets alternate: tile t + 1 is awaited and loaded into the
         // other set while tile t's DMMAs execute
         Frag f0, f1;
-        const uint32_t tend = tbase + (uint32_t)(nchunks - c0);
+        const uint32_t tend = tbase + (uint32_t)(nu - u0);
         if (tbase < tend) fetch(tbase, f0);
         for (uint32_t t = tbase; t < tend; t += 2) {
           mma(f0);
@@ -561,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
           release(t + 1);
           if (t + 2 < tend) fetch(t + 2, f0);
         }
-        tbase += nchunks - c0;
+        tbase += nu - u0;
         // epilogue of the l-block: k-quarters 1..3 park their partial sums, quarter 0
         // adds them in order and writes rows l = l0 + 2 (8 i + g) + par
         double* rp = red + (size_t)(par * 3) * 4 * NT * 64;
@@ -593,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
               }
             }
             if (l <= Lt) {
-              double* row = args.F + ((size_t)l * (l + 1) / 2 + m) * ncolF;
+              double* row = Fout + ((size_t)l * (l + 1) / 2 + m) * ncolF;
               const double gam = gam4[i];  // P_l = gamma_l R_l
 #pragma unroll
               for (int jn = 0; jn < NT; ++jn)
@@ -629,16 +645,19 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
 
   uint32_t tbase = 0;
   for (int k = 0;; ++k) {
-  const int item = fwd_item(k, bxg, gdg);
-  if (item >= args.m_count) break;
+  const int it = fwd_item(k, bxg, gdg);
+  if (it >= args.m_count * S) break;
+  const int item = it / S, split = it - item * S;
+  const int nu = (nchunks - split + S - 1) / S;
+  double* const Fout = split ? args.Fx + (size_t)(split - 1) * args.f_gstride : args.F;
   const int m = args.m_begin + item;
   const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
-  const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane);
+  const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane, split, S);
   for (int j = 0; j < nlb; ++j) {
     const int l0 = m + FWD_LB * j;
-    const int c0 = first_live_chunk(cst, l0, nchunks);
-    for (int c = c0; c < nchunks; ++c) {
-      const uint32_t t = tbase + (c - c0);
+    const int u0 = first_live_chunk(cst, l0, nu);
+    for (int u = u0; u < nu; ++u) {
+      const uint32_t t = tbase + (u - u0);
       const int stage = t % FWD_STAGES;
       const uint32_t round = t / FWD_STAGES;
       const bool tr = args.trace && blockIdx.x == args.trace_cta && lane == 0 && cw == 0 && t < 4096;
@@ -681,14 +700,14 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       mbar_arrive(&empty[stage]);
       if (cw == 0 && lane == 0) *cons0 = (int)t + 1;
     }
-    tbase += nchunks - c0;
+    tbase += nu - u0;
     // epilogue for this l-block: rows l = l0 + 2*(8*i + g) + par
 #pragma unroll
     for (int ii = 0; ii < 2; ++ii) {
       const int i = 2 * mh + ii;
       const int l = l0 + 2 * (8 * i + g) + par;
       if (l <= Lt) {
-        double* row = args.F + ((size_t)l * (l + 1) / 2 + m) * ncolF;
+        double* row = Fout + ((size_t)l * (l + 1) / 2 + m) * ncolF;
         const double gam = args.ptab ? 1.0 : args.dg[args.dgofs[m] + (l - m)].y;  // P_l = gamma_l R_l
 #pragma unroll
         for (int jn = 0; jn < NTW; ++jn) {

@@ -132,6 +132,7 @@ struct fvPlan {
   double2* Sa = nullptr;
   double* X = nullptr;
   double* F = nullptr;
+  double* Fx = nullptr;  // partial F buffers 1..3 of split forward launches (lazily, 3 x f_gstride)
   double* G = nullptr;
   int ngroups_buf = 1;                            // 4-field groups whose X / F / G fit side by side
   size_t x_gstride = 0, f_gstride = 0, g_gstride = 0;  // doubles per group
@@ -179,7 +180,7 @@ void free_plan(fvPlan* p) {
   void* ptrs[] = {p->pair_t, p->pair_sin, p->pair_n, p->pair_s, p->ring_w, p->seed_x,
                   p->seed_e, p->start_l,  p->start_v, p->ab,   p->abofs,  p->gofs,
                   p->dg,     p->dgofs,  p->cgt,     p->cga,     p->ptab_f,  p->mtab_f, p->tofs,   p->ptab_a, p->aofs,
-                  p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->G,
+                  p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->Fx,     p->G,
                   p->seedk,  p->fitems,   p->Fpart,   p->blue_tab, p->blue_s1, p->cmin, p->cmin_a, p->Tp,
                   p->fft_tw, p->f2_tw};
   for (void* q : ptrs)
@@ -346,15 +347,22 @@ cudaError_t smem_optin_once(std::atomic<unsigned long long>* mask, int device, K
 
 template <int NT>
 int launch_fwd(fvPlan* p, const fv::FwdArgs& args, int m_count, cudaStream_t s) {
-  static std::atomic<unsigned long long> attr{0};
+  static std::atomic<unsigned long long> attr{0}, attr_split{0};
   const size_t bytes = fv::FwdSmem<NT>::bytes(p->nchunks * fv::FWD_RC);
   if (bytes > 227 * 1024) return fail(FV_EINVAL, "grid too large for the forward kernel's shared memory");
-  FV_CUDA(smem_optin_once(&attr, p->device, fv::legendre_fwd_kernel<NT>));
   fv::FwdArgs a2 = args;
   a2.m_count = m_count;
-  // one CTA per order: the hardware block scheduler hands out orders in ascending m
-  // (descending work) dynamically, which balances better than a static persistent split
-  fv::legendre_fwd_kernel<NT><<<m_count * std::max(1, a2.ngroups), fv::kThreads, bytes, s>>>(a2);
+  // one CTA per order (and split): the hardware block scheduler hands out orders in
+  // ascending m (descending work) dynamically, which balances better than a static
+  // persistent split
+  const unsigned grid = (unsigned)(m_count * std::max(1, a2.ngroups) * std::max(1, a2.ksplit));
+  if (a2.ksplit > 1) {
+    FV_CUDA(smem_optin_once(&attr_split, p->device, fv::legendre_fwd_kernel<NT, true>));
+    fv::legendre_fwd_kernel<NT, true><<<grid, fv::kThreads, bytes, s>>>(a2);
+  } else {
+    FV_CUDA(smem_optin_once(&attr, p->device, fv::legendre_fwd_kernel<NT, false>));
+    fv::legendre_fwd_kernel<NT, false><<<grid, fv::kThreads, bytes, s>>>(a2);
+  }
   FV_CUDA(cudaGetLastError());
   return FV_OK;
 }
@@ -1245,6 +1253,21 @@ int fv_plan_info(const fvPlan* p, int* L, int* n_theta, int* n_phi, int* n_pairs
   return FV_OK;
 }
 
+int fv_order_cost(const fvPlan* p, double* cost) {
+  if (!p) return fail(FV_EINVAL, "null plan");
+  if (p->kind != 0) return fail(FV_EINVAL, "order cost needs a grid plan");
+  if (!cost) return fail(FV_EINVAL, "null output");
+  const int Lt = p->Lt;
+  std::vector<int> ls((size_t)(Lt + 1) * p->nPpad);
+  FV_CUDA(cudaMemcpy(ls.data(), p->start_l, ls.size() * sizeof(int), cudaMemcpyDeviceToHost));
+  for (int m = 0; m <= Lt; ++m) {
+    double c = 0.0;
+    for (int q = 0; q < p->nP; ++q) c += std::max(0, Lt + 1 - std::max(m, ls[(size_t)m * p->nPpad + q]));
+    cost[m] = c;
+  }
+  return FV_OK;
+}
+
 int fv_set_profiling(fvPlan* p, int enable) {
   if (!p) return fail(FV_EINVAL, "null plan");
   if (p->profiling && !p->marks.empty()) cudaEventSynchronize(p->marks.back().second.second);
@@ -1288,18 +1311,23 @@ int check_grid_call(fvPlan* p, int B, const void* x, const void* y, const void* 
 // CG assembly (favest/transforms.py:120-146) of coefficient orders [c_lo, c_hi) of fields
 // b0 .. b0 + nf - 1 from the forward Legendre rows in p->F (ncol = 8 NT)
 int cg_forward(fvPlan* p, double* a, double* b, int B, int b0, int nf, int NT, int c_lo, int c_hi, cudaStream_t s,
-               const double* F = nullptr) {
+               const double* F = nullptr, int nsplit = 1, const double* Fx = nullptr) {
   StageMark mk(p, 3, s);
   fv::CgFwdArgs ca{F ? F : p->F, reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), p->cgt, p->L, 8 * NT, B, b0,
-                   nf, c_lo, c_hi};
-  dim3 grid((c_hi + fv::CGF_MB - 1) / fv::CGF_MB, p->L + 1);
+                   nf, c_lo, c_hi, nsplit, nsplit > 1 ? Fx : nullptr, (long long)p->f_gstride};
+  dim3 grid((c_hi + fv::CGF_MB - 1) / fv::CGF_MB - c_lo / fv::CGF_MB, p->L + 1);
   const size_t smem = (size_t)3 * (fv::CGF_MB + 2) * fv::cgf_rs(nf) * sizeof(double2);
-  switch (nf) {
-    case 1: fv::cg_fwd_tile_kernel<1><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
-    case 2: fv::cg_fwd_tile_kernel<2><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
-    case 3: fv::cg_fwd_tile_kernel<3><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
-    default: fv::cg_fwd_tile_kernel<4><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
-  }
+  auto go = [&](auto split) {
+    constexpr bool SP = decltype(split)::value;
+    switch (nf) {
+      case 1: fv::cg_fwd_tile_kernel<1, SP><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
+      case 2: fv::cg_fwd_tile_kernel<2, SP><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
+      case 3: fv::cg_fwd_tile_kernel<3, SP><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
+      default: fv::cg_fwd_tile_kernel<4, SP><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
+    }
+  };
+  if (nsplit > 1) go(std::true_type{});
+  else go(std::false_type{});
   FV_CUDA(cudaGetLastError());
   return FV_OK;
 }
@@ -1320,6 +1348,15 @@ int scalar_unpack(const ScalarIO& io, const double* F, int NT, int pf0, int nfp,
   fv::scalar_unpack_kernel<<<grid, 128, 0, s>>>(F, 8 * NT, io.lmax, pf0, nfp, io.B, io.out);
   FV_CUDA(cudaGetLastError());
   return FV_OK;
+}
+
+// pair-chunk split of a forward Legendre launch of mc orders: about two CTAs per SM
+// (one CTA per (order, split)), at most 4 splits and one chunk per split; 1 when the
+// orders alone fill the GPU (every full-grid launch).  FV_FWD_KSPLIT=n forces n.
+int fwd_ksplit(const fvPlan* p, int mc) {
+  static const int forced = [] { const char* e = std::getenv("FV_FWD_KSPLIT"); return e ? std::atoi(e) : -1; }();
+  int ks = forced >= 0 ? std::max(1, forced) : (int)std::lround(2.0 * p->num_sms / std::max(1, mc));
+  return std::max(1, std::min({ks, 4, p->nchunks}));
 }
 
 int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* a, double* b, int B, int m_lo,
@@ -1347,11 +1384,15 @@ int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* 
         FV_TRY(fft_fold(p, Tfield, bg, nf, s, Xg));
       }
     }
+    // launches with few orders (the order-sharded chunks) split every order's pair
+    // chunks over up to 4 CTAs, each into its own partial F buffer (the CG adds them)
+    const int ks = (ng == 1 && !sio) ? fwd_ksplit(p, mc) : 1;
+    if (ks > 1 && !p->Fx) FV_TRY(dalloc(&p->Fx, (size_t)3 * p->f_gstride));
     {
       StageMark mk(p, 2, s);
       fv::FwdArgs args{p->X, p->F, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, Lt, p->nP, p->nPpad,
                        p->nchunks, m_lo, dbg_mode(), mc, trace_buf(), trace_cta(), p->ptab_f, p->mtab_f, p->tofs, p->cmin,
-                       ng, (long long)p->x_gstride, (long long)p->f_gstride};
+                       ng, (long long)p->x_gstride, (long long)p->f_gstride, ks, p->Fx};
       FV_TRY(dispatch_fwd(p, NT, args, mc, s));
     }
     if (sio)
@@ -1361,7 +1402,7 @@ int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* 
       }
     else if (c_hi > c_lo)
       for (int g = 0; g < ng; ++g)
-        FV_TRY(cg_forward(p, a, b, B, b0 + 4 * g, nf, NT, c_lo, c_hi, s, p->F + (size_t)g * p->f_gstride));
+        FV_TRY(cg_forward(p, a, b, B, b0 + 4 * g, nf, NT, c_lo, c_hi, s, p->F + (size_t)g * p->f_gstride, ks, p->Fx));
     b0 += ng > 1 ? 4 * ng : nf;
   }
   return FV_OK;

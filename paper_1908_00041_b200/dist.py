@@ -64,19 +64,38 @@ def ring_blocks(n_theta: int, world: int) -> list[tuple[int, int]]:
     return out
 
 
-def order_ranges(Lt: int, world: int) -> list[tuple[int, int]]:
-    """Contiguous order ranges [m0, m1) over 0..Lt with balanced Legendre work.
+def order_weights(Lt: int, cost=None) -> list[float]:
+    """Per-order work used to balance the partition: without ``cost``, Lt+1-m degrees
+    plus one unit for the order's FFT bins / fold; with ``cost`` (GridPlan.order_cost:
+    the (degree, pair) products the contraction of order m really runs -- high orders
+    skip their polar pairs, so their work falls faster than Lt+1-m), that plus a
+    per-order share for the fold / CG / epilogue of ORDER_OVERHEAD pair-rows."""
+    if cost is None:
+        return [order_work(Lt, m) + 1 for m in range(Lt + 1)]
+    c = [float(x) for x in cost]
+    if len(c) != Lt + 1:
+        raise ValueError(f"order cost has {len(c)} entries, expected {Lt + 1}")
+    over = ORDER_OVERHEAD * sum(c) / max(1, Lt + 1)
+    return [x + over for x in c]
 
-    Work of order m is Lt+1−m degrees (plus one unit for its FFT bins / fold);
-    the cut points are placed at the cumulative-work quantiles.  Every rank gets
-    at least one order when world <= Lt+1.
+
+#: per-order work that does not shrink with the polar skip (fold, CG, the Legendre
+#: kernels' per-order pipeline fill and epilogues), as a fraction of the mean order
+#: cost; fitted to the C4 per-rank stage times (tools/c4_rank_share.py)
+ORDER_OVERHEAD = 0.08
+
+
+def order_ranges(Lt: int, world: int, cost=None) -> list[tuple[int, int]]:
+    """Contiguous order ranges [m0, m1) over 0..Lt with balanced Legendre work
+    (order_weights); the cut points are placed at the cumulative-work quantiles.
+    Every rank gets at least one order when world <= Lt+1.
     """
     if world < 1:
         raise ValueError("world must be >= 1")
     n = Lt + 1
     if world > n:
         raise ValueError(f"{world} ranks for {n} orders")
-    w = [order_work(Lt, m) + 1 for m in range(n)]
+    w = order_weights(Lt, cost)
     total = float(sum(w))
     cuts, acc, k = [0], 0.0, 1
     for m in range(n):
@@ -105,10 +124,10 @@ class RankLayout:
     legendre: tuple[int, int]     # forward Legendre orders [l0, l1) feeding coef (one more each side)
 
 
-def rank_layouts(n_theta: int, L: int, world: int) -> list[RankLayout]:
+def rank_layouts(n_theta: int, L: int, world: int, cost=None) -> list[RankLayout]:
     Lt = L + 1
     rb = ring_blocks(n_theta, world)
-    ob = order_ranges(Lt, world)
+    ob = order_ranges(Lt, world, cost)
     out = []
     for h in range(world):
         m0, m1 = ob[h]
@@ -118,13 +137,13 @@ def rank_layouts(n_theta: int, L: int, world: int) -> list[RankLayout]:
     return out
 
 
-def order_chunks(rng: tuple[int, int], Lt: int, chunks: int) -> list[tuple[int, int]]:
+def order_chunks(rng: tuple[int, int], Lt: int, chunks: int, cost=None) -> list[tuple[int, int]]:
     """[m0, m1) cut into ``chunks`` contiguous pieces of near-equal Legendre work
-    (empty pieces when there are fewer orders than chunks)."""
+    (order_weights; empty pieces when there are fewer orders than chunks)."""
     m0, m1 = rng
     if chunks == 1 or m1 - m0 <= 1:
         return [(m0, m1)] + [(m1, m1)] * (chunks - 1)
-    w = [order_work(Lt, m) + 1 for m in range(m0, m1)]
+    w = order_weights(Lt, cost)[m0:m1]
     total = float(sum(w))
     cuts, acc, k = [m0], 0.0, 1
     for i, m in enumerate(range(m0, m1)):
@@ -213,7 +232,8 @@ class OrderShardedPlan:
     ``device`` with ``max_batch`` fields.
     """
 
-    def __init__(self, stages, L, n_theta, n_phi, max_batch, rank, world, device, group=None, chunks=1):
+    def __init__(self, stages, L, n_theta, n_phi, max_batch, rank, world, device, group=None, chunks=1,
+                 cost=None):
         torch = _torch()
         if not 0 <= rank < world:
             raise ValueError(f"bad rank {rank} of {world}")
@@ -227,7 +247,8 @@ class OrderShardedPlan:
         self.device = torch.device(device)
         self.group = group
         self.chunks = int(chunks)
-        self.layouts = rank_layouts(self.n_theta, self.L, self.world)
+        self.cost = None if cost is None else [float(x) for x in cost]
+        self.layouts = rank_layouts(self.n_theta, self.L, self.world, self.cost)
         me = self.layouts[self.rank]
         self.me = me
         self.nloc = me.rings[1] - me.rings[0]
@@ -242,10 +263,10 @@ class OrderShardedPlan:
         Lt = self.Lt
         self._fc, self._fl, self._ao = [], [], []
         for lay in self.layouts:
-            cs = order_chunks(lay.coef, Lt, self.chunks)
+            cs = order_chunks(lay.coef, Lt, self.chunks, self.cost)
             self._fc.append(cs)
             self._fl.append([(max(0, c0 - 1), min(Lt + 1, c1 + 1)) if c1 > c0 else (c0, c0) for c0, c1 in cs])
-            self._ao.append(order_chunks(lay.orders, Lt, self.chunks))
+            self._ao.append(order_chunks(lay.orders, Lt, self.chunks, self.cost))
         self._send_bins = []  # [q][h]: natural bins of h's chunk-q Legendre orders (+m then -m)
         self._recv_bins = []  # [q][h]: (compact index, natural bin) of h's chunk-q adjoint orders
         for q in range(self.chunks):
@@ -429,14 +450,17 @@ class OrderShardedPlan:
         return out[0], out[1]
 
 
-def make_plan(L, grid, max_batch, rank, world, device=None, group=None, chunks=4):
+def make_plan(L, grid, max_batch, rank, world, device=None, group=None, chunks=2, balance="cost"):
     """Production constructor: one GridPlan on this rank's GPU + its shard layout; the
-    transposes run in ``chunks`` order chunks overlapped with the per-order stages."""
+    transposes run in ``chunks`` order chunks overlapped with the per-order stages.
+    ``balance="cost"`` partitions the orders by the plan's measured per-order work
+    (GridPlan.order_cost, identical on every rank), ``"degrees"`` by Lt+1-m."""
     from .plan import GridPlan
 
     plan = GridPlan.from_grid(grid, L, max_batch=max_batch, device=device)
+    cost = plan.order_cost() if balance == "cost" else None
     return OrderShardedPlan(CudaStages(plan), L, grid.n_theta, grid.n_phi, max_batch, rank, world,
-                            plan.device, group, chunks=chunks)
+                            plan.device, group, chunks=chunks, cost=cost)
 
 
 # ---------------------------------------------------------------------------

@@ -96,6 +96,13 @@ class GridPlan:
         except Exception:
             pass
 
+    def order_cost(self) -> np.ndarray:
+        """(lmax+2,) float64: the (degree, ring pair) products the contraction of each
+        order m runs (pairs counted from their polar start); fv_order_cost."""
+        out = np.zeros(self.lmax + 2, dtype=np.float64)
+        _lib.check(self.lib.fv_order_cost(self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        return out
+
     def set_profiling(self, enable: bool = True):
         _lib.check(self.lib.fv_set_profiling(self._h, int(bool(enable))))
 

@@ -409,12 +409,14 @@ def test_host_pipeline_matches_device_path():
         pipe.submit_roundtrip(T, outs[0])  # device tensor, not pinned host
 
 
-@pytest.mark.parametrize("L,world,chunks", [(40, 1, 1), (40, 2, 1), (40, 3, 1), (21, 2, 1), (40, 2, 3), (21, 3, 4)])
+@pytest.mark.parametrize("L,world,chunks", [(40, 1, 1), (40, 2, 1), (40, 3, 1), (21, 2, 1), (40, 2, 3), (21, 3, 4),
+                                           (300, 4, 3), (300, 1, 1)])
 def test_order_sharded_path_matches_single_plan(L, world, chunks):
     """The order-sharded building blocks (fv_ring_fft / fv_forward_orders / fv_adjoint_orders,
     dist.py) with ranks simulated in one process reproduce GridPlan.forward/adjoint, also with
     the transposes cut into order chunks; with the hand-written FFT (n_phi = 84) bitwise,
-    with the cuFFT fallback (n_phi = 46) to rounding."""
+    with the cuFFT fallback (n_phi = 46) to rounding; L = 300 (5 pair chunks) with few orders
+    per launch splits the forward contraction over CTAs (FwdArgs::ksplit) -- to rounding."""
     torch = cuda_or_skip()
     from paper_1908_00041_b200.dist import CudaStages, OrderShardedPlan, simulate_adjoint, simulate_forward
 
