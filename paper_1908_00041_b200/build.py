@@ -59,7 +59,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         _nvcc(), *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
         "-Xptxas", "-v" if verbose else "-O3",
         "-o", tmp, os.path.join(CSRC, "plan.cu"),
-        f"-L{libdir}", "-lcufft", "-Xlinker", f"-rpath,{libdir}",
+        f"-L{libdir}", "-lcufft", "-ldl", "-Xlinker", f"-rpath,{libdir}",
     ]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if verbose or res.returncode != 0:

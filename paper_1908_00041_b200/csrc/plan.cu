@@ -2,6 +2,7 @@
 // sequence of the forward / adjoint VSHT on B200 (sm_100a).
 #include <cuda_runtime.h>
 #include <cufft.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -295,12 +296,17 @@ cudaEvent_t next_event(fvPlan* p) {
   return p->ev_pool[p->ev_used++];
 }
 
+// One pipeline stage's launches: an NVTX range on the host (fv:fft, fv:fold,
+// fv:legendre, fv:cg -- visible in nsys / ncu --nvtx timelines; a no-op without a
+// tool attached) and, with profiling on, CUDA events on the stream.
 struct StageMark {
   fvPlan* p;
   int stage;
   cudaStream_t s;
   cudaEvent_t e0 = nullptr;
   StageMark(fvPlan* p_, int st, cudaStream_t s_) : p(p_), stage(st), s(s_) {
+    static const char* const names[] = {"fv:fft", "fv:fold", "fv:legendre", "fv:cg"};
+    nvtxRangePushA(names[st & 3]);
     if (p->profiling) {
       e0 = next_event(p);
       cudaEventRecord(e0, s);
@@ -312,6 +318,7 @@ struct StageMark {
       cudaEventRecord(e1, s);
       p->marks.push_back({stage, {e0, e1}});
     }
+    nvtxRangePop();
   }
 };
 
