@@ -430,6 +430,7 @@ def run_ours(args, rank, world, local_rank):
         del plan
         torch.cuda.empty_cache()
         detail_extra["c5"] = c5_detail(args, rank, world, dev, timed)
+        detail_extra["c2"] = c2_detail(args, world, dev, timed)
         del T, Tout, a, b
         torch.cuda.empty_cache()
         detail_extra["c4"] = c4_detail(args, rank, world, dev, dist, timed, barrier, max_over_ranks)
@@ -516,6 +517,42 @@ def on_the_fly_detail(args, world, plan, grid, T, a, b, Tout, timed, dev):
             "step_fraction_of_fp64_roofline_datasheet": (2 * fl["total"] / (ms / 1e3)) / (FP64_PEAK_DATASHEET * 1e12),
             "forward_rel_l2_vs_table_mode": rel,
             "note": "plan built with FV_PTAB=0: P-bar by the on-the-fly recurrence, no plan-time tables"}
+
+
+def c2_detail(args, world, dev, timed):
+    """BASELINE configs[1]: L=256, a batch of 16 fields per GPU (default_rng(2), the
+    1/(l(l+1)) law), forward and adjoint each timed separately."""
+    import torch
+
+    import oracle.favest_oracle as O  # seeded generators only
+    from paper_1908_00041_b200.grid import gl_grid_for
+    from paper_1908_00041_b200.plan import GridPlan
+
+    L2, B2 = 256, 16
+    grid, _ = gl_grid_for(L2)
+    plan = GridPlan.from_grid(grid, L2, max_batch=B2, device=dev)
+    rng = np.random.default_rng(2)
+    ab = [O.coef(rng, L2, "inv") for _ in range(B2)]
+    a = torch.from_numpy(np.stack([x[0] for x in ab])).to(dev)
+    b = torch.from_numpy(np.stack([x[1] for x in ab])).to(dev)
+    T = plan.adjoint(a, b)
+    fa, fb = plan.forward(T)
+    for _ in range(3):
+        plan.adjoint(a, b, T)
+        plan.forward(T, fa, fb)
+    n = 20
+    ms_a = timed(lambda: plan.adjoint(a, b, T), n)
+    ms_f = timed(lambda: plan.forward(T, fa, fb), n)
+    rt = float(torch.linalg.vector_norm(torch.cat([fa - a, fb - b], 1)) / torch.linalg.vector_norm(torch.cat([a, b], 1)))
+    plan.close()
+    fl = canonical_flops(L2, B2)
+    frac = lambda ms: fl["total"] / (ms / 1e3) / (FP64_PEAK_DATASHEET * 1e12)  # noqa: E731
+    return {"workload": "C2 (BASELINE configs[1]): L=256 Gauss-Legendre 258x516 grid, 16 fields per GPU, forward and "
+                        "adjoint timed separately", "forward_ms": ms_f, "adjoint_ms": ms_a,
+            "forward_fields_per_s": world * B2 / (ms_f / 1e3), "adjoint_fields_per_s": world * B2 / (ms_a / 1e3),
+            "forward_fraction_of_fp64_roofline_datasheet": frac(ms_f),
+            "adjoint_fraction_of_fp64_roofline_datasheet": frac(ms_a),
+            "roundtrip_rel_l2": rt}
 
 
 def c5_detail(args, rank, world, dev, timed):
@@ -640,7 +677,7 @@ def c4_detail(args, rank, world, dev, dist, timed, barrier, max_over_ranks):
             del Tout
             rs = rank_share(plan, T, a_full, b_full, worlds=(2, 4, 8), single=ms1)
             out["order_sharded_projection"] = {
-                "method": "per-rank device work of dist.OrderShardedPlan (chunks 2, cost-balanced orders) timed "
+                "method": "per-rank device work of dist.OrderShardedPlan (make_plan defaults: one chunk, cost-balanced orders) timed "
                           "rank by rank on one GPU, transposes replaced by local copies; NVLink time = max bytes "
                           "sent per rank / 900 GB/s (modelled: one GPU)",
                 **{str(w): {"slowest_rank_ms": v["slowest_rank_ms"], "nvlink_ms_at_900GBs": v["nvlink_ms_at_900GBs"],

@@ -450,9 +450,12 @@ class OrderShardedPlan:
         return out[0], out[1]
 
 
-def make_plan(L, grid, max_batch, rank, world, device=None, group=None, chunks=2, balance="cost"):
+def make_plan(L, grid, max_batch, rank, world, device=None, group=None, chunks=1, balance="cost"):
     """Production constructor: one GridPlan on this rank's GPU + its shard layout; the
-    transposes run in ``chunks`` order chunks overlapped with the per-order stages.
+    transposes run in ``chunks`` order chunks overlapped with the per-order stages
+    (default 1: at C4 on 8 ranks a second chunk costs ~0.6 ms of per-chunk launches
+    and packing per rank, more than the ~0.4 ms of all-to-all it could hide;
+    tools/c4_rank_share.py).
     ``balance="cost"`` partitions the orders by the plan's measured per-order work
     (GridPlan.order_cost, identical on every rank), ``"degrees"`` by Lt+1-m."""
     from .plan import GridPlan

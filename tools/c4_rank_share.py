@@ -36,7 +36,7 @@ def timed(fn, reps=3):
     return e0.elapsed_time(e1) / reps
 
 
-def rank_share(base, T, A, Bc, worlds=(1, 2, 4, 8), chunks=2, balance="cost", single=None, stages_detail=False):
+def rank_share(base, T, A, Bc, worlds=(1, 2, 4, 8), chunks=1, balance="cost", single=None, stages_detail=False):
     """Per-rank forward / adjoint device times of the order-sharded step on ``base``'s
     grid for each world size (one field: T (1, N, 3), A / Bc (1, K)); see module doc."""
     L, nth, nphi = base.lmax, base.n_theta, base.n_phi
@@ -99,7 +99,7 @@ def rank_share(base, T, A, Bc, worlds=(1, 2, 4, 8), chunks=2, balance="cost", si
 
 def main():
     L = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
-    chunks = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    chunks = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     balance = sys.argv[3] if len(sys.argv) > 3 else "cost"
     th, w, nphi = O.gl_grid(L)
     rng = np.random.default_rng(4)
