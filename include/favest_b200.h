@@ -163,6 +163,17 @@ int fv_forward_orders(fvPlan* plan, const double* S, long long cs, long long rs,
 int fv_adjoint_orders(fvPlan* plan, const double* a, const double* b, int B, int m_lo, int m_hi, double* S,
                       long long cs, long long rs, long long bs, int bin_lo, int nbins, void* stream);
 
+/* The same two stages on "packed" spectra: element (component c, ring R, bin j)
+ * at ring_offsets[c * rts + R] + j complex units (ring_offsets: device int64,
+ * 3 x rts entries, rts >= B * n_theta; compact bins, nbins > 0), so the blocks
+ * of an all-to-all buffer -- one contiguous block per peer rank -- are read
+ * (forward) or written (adjoint) in place, with no pack / unpack copies. */
+int fv_forward_orders_packed(fvPlan* plan, const double* S, const long long* ring_offsets, long long rts, int bin_lo,
+                             int nbins, double* a, double* b, int B, int m_lo, int m_hi, int c_lo, int c_hi,
+                             void* stream);
+int fv_adjoint_orders_packed(fvPlan* plan, const double* a, const double* b, int B, int m_lo, int m_hi, double* S,
+                             const long long* ring_offsets, long long rts, int bin_lo, int nbins, void* stream);
+
 /*
  * Stage timing (milliseconds, CUDA events recorded on each call's stream):
  * fv_set_profiling(plan, 1) starts accumulating over all following calls,

@@ -221,16 +221,17 @@ __global__ void fold_fwd_kernel(FoldArgs a) {
   if (rn >= 0) {
     const double wn = a.ring_w[rn];
     const double ws = rs >= 0 ? a.ring_w[rs] : 0.0;
-    const double2* base = a.S + c * a.lay.cs;
     const long long rb = (long long)(a.b0 + b) * a.n_theta;
+    const double2* base_n = a.S + spec_cr(a.lay, c, rb + rn);
+    const double2* base_s = rs >= 0 ? a.S + spec_cr(a.lay, c, rb + rs) : base_n;
     for (int sgn = 0; sgn < 2; ++sgn) {
       if (sgn == 1 && m == 0) break;
       const long long bin = spec_bin(a.lay, m, sgn, a.n_phi);
       const double sig = (sgn == 1 && (m & 1)) ? -1.0 : 1.0;
-      const double2 Tn = base[spec_ring(a.lay, rb + rn) + bin * a.lay.bs];
+      const double2 Tn = base_n[bin * a.lay.bs];
       const double nr = wn * Tn.x, ni = wn * Tn.y;
       if (rs >= 0) {
-        const double2 Ts = base[spec_ring(a.lay, rb + rs) + bin * a.lay.bs];
+        const double2 Ts = base_s[bin * a.lay.bs];
         const double sr = ws * Ts.x, si = ws * Ts.y;
         E[sgn] = make_double2(sig * (nr + sr), sig * (ni + si));
         O[sgn] = make_double2(sig * (nr - sr), sig * (ni - si));

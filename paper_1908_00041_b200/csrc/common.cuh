@@ -29,12 +29,22 @@ namespace fv {
 struct SLayout {
   long long cs, rs, bs;
   int bin_lo, nbins;
-  int rblk;  // 0: ring R at R * rs; 2^k: ring R at (R >> k) * rs + (R & (2^k - 1))
-  int rbsh;  // k
+  int rblk = 0;  // 0: ring R at R * rs; 2^k: ring R at (R >> k) * rs + (R & (2^k - 1))
+  int rbsh = 0;  // k
+  // ring-offset table (order-sharded transposes, dist.py): when set, element
+  // (component c, ring R, bin j) is at rtab[c * rts + R] + j * bs, so a kernel
+  // can read / write the per-rank blocks of an all-to-all buffer in place
+  const long long* rtab = nullptr;
+  long long rts = 0;
 };
 
 __host__ __device__ __forceinline__ long long spec_ring(const SLayout& l, long long R) {
   return l.rblk ? (R >> l.rbsh) * l.rs + (R & (l.rblk - 1)) : R * l.rs;
+}
+
+// offset of (component c, ring R) without the bin term
+__device__ __forceinline__ long long spec_cr(const SLayout& l, int c, long long R) {
+  return l.rtab ? __ldg(l.rtab + c * l.rts + R) : c * l.cs + spec_ring(l, R);
 }
 
 __device__ __forceinline__ long long spec_bin(const SLayout& l, int m, int sgn, int n_phi) {

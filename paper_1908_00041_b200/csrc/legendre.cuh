@@ -1102,13 +1102,15 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
       const long long bin0 = spec_bin(args.lay, m, 0, args.n_phi), bin1 = spec_bin(args.lay, m, 1, args.n_phi);
       double2* dst[NT];
       long long rbase[NT];
+      int comps[NT];
       bool ok[NT];
 #pragma unroll
       for (int jn = 0; jn < NT; ++jn) {
         const int ser = 4 * jn + q;  // 6*field + 2*comp + sign
         const int b = ser / 6, comp = (ser % 6) >> 1, sgn = ser & 1;
         ok[jn] = b < args.nfields && !(sgn == 1 && m == 0);
-        dst[jn] = args.S + comp * args.lay.cs + (sgn ? bin1 : bin0) * args.lay.bs;
+        dst[jn] = args.S + (sgn ? bin1 : bin0) * args.lay.bs;
+        comps[jn] = comp;
         rbase[jn] = (long long)(fb0 + b) * args.n_theta;
       }
 #pragma unroll
@@ -1120,8 +1122,8 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
           if (!ok[jn]) continue;
           const double er = acc[0][ii][jn][0], ei = acc[0][ii][jn][1];
           const double orr = acc[1][ii][jn][0], oi = acc[1][ii][jn][1];
-          dst[jn][spec_ring(args.lay, rbase[jn] + rn)] = make_double2(er + orr, ei + oi);
-          if (rs >= 0) dst[jn][spec_ring(args.lay, rbase[jn] + rs)] = make_double2(er - orr, ei - oi);
+          dst[jn][spec_cr(args.lay, comps[jn], rbase[jn] + rn)] = make_double2(er + orr, ei + oi);
+          if (rs >= 0) dst[jn][spec_cr(args.lay, comps[jn], rbase[jn] + rs)] = make_double2(er - orr, ei - oi);
         }
       }
     }
@@ -1215,7 +1217,7 @@ __device__ __forceinline__ void adj_store(const AdjArgs& args, const double (&ac
     const int ser = 4 * jn + q;  // 6*field + 2*comp + sign
     const int b = ser / 6, comp = (ser % 6) >> 1, sgn = ser & 1;
     if (!(b < args.nfields && !(sgn == 1 && m == 0))) continue;
-    double2* dst = args.S + comp * args.lay.cs + (sgn ? bin1 : bin0) * args.lay.bs;
+    double2* dst = args.S + (sgn ? bin1 : bin0) * args.lay.bs;
     const long long rbase = (long long)(args.b0 + b) * args.n_theta;
 #pragma unroll
     for (int ii = 0; ii < 2; ++ii) {
@@ -1223,8 +1225,8 @@ __device__ __forceinline__ void adj_store(const AdjArgs& args, const double (&ac
       if (rn < 0) continue;
       const double er = acc[0][ii][jn][0], ei = acc[0][ii][jn][1];
       const double orr = acc[1][ii][jn][0], oi = acc[1][ii][jn][1];
-      dst[spec_ring(args.lay, rbase + rn)] = make_double2(er + orr, ei + oi);
-      if (rs >= 0) dst[spec_ring(args.lay, rbase + rs)] = make_double2(er - orr, ei - oi);
+      dst[spec_cr(args.lay, comp, rbase + rn)] = make_double2(er + orr, ei + oi);
+      if (rs >= 0) dst[spec_cr(args.lay, comp, rbase + rs)] = make_double2(er - orr, ei - oi);
     }
   }
 }

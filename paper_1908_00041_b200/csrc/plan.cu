@@ -1633,6 +1633,36 @@ int fv_adjoint_orders(fvPlan* p, const double* a, const double* b, int B, int m_
                         reinterpret_cast<cudaStream_t>(stream));
 }
 
+int fv_forward_orders_packed(fvPlan* p, const double* S, const long long* ring_offsets, long long rts, int bin_lo,
+                             int nbins, double* a, double* b, int B, int m_lo, int m_hi, int c_lo, int c_hi,
+                             void* stream) {
+  FV_TRY(check_grid_call(p, B, S, a, b));
+  FV_TRY(check_orders(p, 1, 1, bin_lo, nbins, m_lo, m_hi));
+  if (nbins <= 0) return fail(FV_EINVAL, "packed spectra need compact bins");
+  if (!ring_offsets || rts < (long long)B * p->n_theta) return fail(FV_EINVAL, "ring-offset table too small");
+  if (c_lo < 0 || c_hi > p->L + 1 || c_lo > c_hi) return fail(FV_EINVAL, "coefficient order range invalid");
+  if (c_hi > c_lo && ((c_lo > 0 && c_lo - 1 < m_lo) || c_hi > m_hi - 1 || (c_lo == 0 && m_lo > 0)))
+    return fail(FV_EINVAL, "coefficient orders need the Legendre orders c_lo-1 .. c_hi");
+  fv::SLayout lay{0, 1, 1, bin_lo, nbins};
+  lay.rtab = ring_offsets;
+  lay.rts = rts;
+  return forward_orders(p, reinterpret_cast<const double2*>(S), lay, a, b, B, m_lo, m_hi, c_lo, c_hi,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
+int fv_adjoint_orders_packed(fvPlan* p, const double* a, const double* b, int B, int m_lo, int m_hi, double* S,
+                             const long long* ring_offsets, long long rts, int bin_lo, int nbins, void* stream) {
+  FV_TRY(check_grid_call(p, B, S, a, b));
+  FV_TRY(check_orders(p, 1, 1, bin_lo, nbins, m_lo, m_hi));
+  if (nbins <= 0) return fail(FV_EINVAL, "packed spectra need compact bins");
+  if (!ring_offsets || rts < (long long)B * p->n_theta) return fail(FV_EINVAL, "ring-offset table too small");
+  fv::SLayout lay{0, 1, 1, bin_lo, nbins};
+  lay.rtab = ring_offsets;
+  lay.rts = rts;
+  return adjoint_orders(p, a, b, reinterpret_cast<double2*>(S), lay, B, m_lo, m_hi,
+                        reinterpret_cast<cudaStream_t>(stream));
+}
+
 namespace {
 int adjoint_points_impl(fvPlan* p, const double* xyz, long long M, const double* a, const double* b, double* T, int B,
                         cudaStream_t s, const ScalarIO* sio = nullptr);

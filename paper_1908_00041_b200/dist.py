@@ -1,8 +1,11 @@
 """Order-sharded VSHT across GPUs (the C4 layout).
 
 Each rank owns a contiguous block of rings of the grid (its slice of every
-field) and a contiguous range of orders m, chosen so that the per-order
-Legendre work (∝ Lt+1−m) is balanced.  One transpose per direction:
+field) and a contiguous range of orders m.  The order ranges balance the
+Legendre work actually run per order (``GridPlan.order_cost`` / C ABI
+``fv_order_cost``: high orders skip their polar pairs, so their work falls
+much faster than Lt+1-m) plus a per-order overhead.  One transpose per
+direction:
 
 forward
   1. local ring FFTs of the owned rings (``fv_ring_fft``);
@@ -19,8 +22,10 @@ or full tables)
   2. all-to-all: every ring block goes back to its owner;
   3. local inverse ring FFTs → the owned rings of T.
 
-``gather_coefficients`` turns m-sharded a, b into full tables on every rank
-(entries are disjoint: an all-reduce of zero-masked tables is exact).
+Both transposes can be cut into ``chunks`` order chunks whose asynchronous
+all-to-alls overlap the per-chunk stages.  ``gather_coefficients`` turns
+m-sharded a, b into full tables on every rank (entries are disjoint: an
+all-reduce of zero-masked tables is exact).
 
 The transport is ``torch.distributed.all_to_all_single`` (NCCL on GPUs, one
 process per GPU); ``simulate_forward`` / ``simulate_adjoint`` drive several
@@ -28,7 +33,8 @@ ranks' plans in one process with local copies in place of the collective
 (used to check the sharded path against the single-plan path on one GPU —
 nothing in it waits on another rank's kernels).  The per-rank arithmetic is
 the same kernels on the same values as ``GridPlan.forward/adjoint``, so the
-sharded results are bitwise identical to the unsharded ones.
+sharded results are bitwise identical to the unsharded ones unless a forward
+launch with few orders splits its pair chunks over CTAs (then to rounding).
 """
 
 from __future__ import annotations
@@ -36,6 +42,7 @@ from __future__ import annotations
 from dataclasses import dataclass
 
 import numpy as np
+
 
 def order_work(Lt: int, m: int) -> int:
     """Legendre work of order m at scalar degree Lt: number of degrees l in [m, Lt]."""
@@ -220,6 +227,22 @@ class CudaStages:
                 self.plan._h, a.data_ptr(), b.data_ptr(), B, orders[0], orders[1], S_own.data_ptr(),
                 S_own.stride(0), 2 * nb, 1, orders[0], nb, self._stream()))
 
+    # packed spectra: element (c, ring R, bin j) at rtab[c, R] + j of a flat complex buffer
+    # (the per-rank blocks of an all-to-all buffer, read / written in place)
+    def forward_orders_packed(self, flat, rtab, B, bin_lo, nb, a, b, legendre, coef):
+        torch = _torch()
+        with torch.cuda.device(self.plan.device):
+            self._check(self.lib.fv_forward_orders_packed(
+                self.plan._h, flat.data_ptr(), rtab.data_ptr(), rtab.shape[1], bin_lo, nb, a.data_ptr(), b.data_ptr(),
+                B, legendre[0], legendre[1], coef[0], coef[1], self._stream()))
+
+    def adjoint_orders_packed(self, a, b, B, orders, flat, rtab, nb):
+        torch = _torch()
+        with torch.cuda.device(self.plan.device):
+            self._check(self.lib.fv_adjoint_orders_packed(
+                self.plan._h, a.data_ptr(), b.data_ptr(), B, orders[0], orders[1], flat.data_ptr(), rtab.data_ptr(),
+                rtab.shape[1], orders[0], nb, self._stream()))
+
 
 # ---------------------------------------------------------------------------
 # per-rank plan
@@ -267,6 +290,7 @@ class OrderShardedPlan:
             self._fc.append(cs)
             self._fl.append([(max(0, c0 - 1), min(Lt + 1, c1 + 1)) if c1 > c0 else (c0, c0) for c0, c1 in cs])
             self._ao.append(order_chunks(lay.orders, Lt, self.chunks, self.cost))
+        self._rtabs = {}
         self._send_bins = []  # [q][h]: natural bins of h's chunk-q Legendre orders (+m then -m)
         self._recv_bins = []  # [q][h]: (compact index, natural bin) of h's chunk-q adjoint orders
         for q in range(self.chunks):
@@ -280,6 +304,27 @@ class OrderShardedPlan:
                            torch.tensor([p[1] for p in pairs], dtype=torch.long, device=self.device)))
             self._send_bins.append(sb)
             self._recv_bins.append(rb)
+
+    # ---- packed ring-offset tables -------------------------------------------
+    def _rtab(self, B, nb_of, key):
+        """(3, B * n_theta) int64 on the device: complex offset of (component c, field b,
+        ring r) in a buffer of one block per rank h, block h = [3][B][rings of h][2 nb_of(h)]
+        (the all-to-all order).  Cached per key."""
+        torch = _torch()
+        t = self._rtabs.get(key)
+        if t is None:
+            n = self.n_theta
+            tab = np.zeros((3, B * n), dtype=np.int64)
+            off = 0
+            for h, lay in enumerate(self.layouts):
+                r0, r1 = lay.rings
+                nr, w = r1 - r0, 2 * nb_of(h)
+                cc, bb, rr = np.meshgrid(np.arange(3), np.arange(B), np.arange(nr), indexing="ij")
+                tab[cc, bb * n + r0 + rr] = off + ((cc * B + bb) * nr + rr) * w
+                off += 3 * B * nr * w
+            t = torch.from_numpy(tab).to(self.device)
+            self._rtabs[key] = t
+        return t
 
     # ---- transport -------------------------------------------------------
     def _pack(self, blocks):
@@ -295,18 +340,15 @@ class OrderShardedPlan:
         return flat, sizes
 
     def _all_to_all(self, flat_in, in_splits, out_splits, async_op=False):
-        """Returns (work or None, received complex blocks per source rank)."""
+        """Returns (work or None, the receive buffer as one flat complex tensor: the
+        per-source blocks back to back in rank order)."""
         torch = _torch()
         import torch.distributed as dist
 
         flat_out = torch.empty(sum(out_splits), dtype=torch.float64, device=self.device)
         work = dist.all_to_all_single(flat_out, flat_in, out_splits, in_splits, group=self.group,
                                       async_op=async_op)
-        outs, o = [], 0
-        for k in out_splits:
-            outs.append(torch.view_as_complex(flat_out[o:o + k].view(-1, 2)))
-            o += k
-        return work, outs
+        return work, torch.view_as_complex(flat_out.view(-1, 2))
 
     # ---- forward ---------------------------------------------------------
     def forward_fft(self, T_local):
@@ -331,20 +373,17 @@ class OrderShardedPlan:
         lo, hi = self._fl[self.rank][q]
         return [3 * B * (l.rings[1] - l.rings[0]) * 2 * (hi - lo) * 2 for l in self.layouts]
 
-    def forward_finish(self, recvs, B, a, b, q=0):
-        """Chunk q: the received blocks of every source's rings -> compact spectra of all
-        rings -> fold + Legendre + CG of this rank's chunk-q orders."""
-        torch = _torch()
+    def forward_finish(self, recv, B, a, b, q=0):
+        """Chunk q: fold + Legendre + CG of this rank's chunk-q orders, read in place from
+        the receive buffer (one block (3, B, rings of g, 2 nb) per source rank g, in rank
+        order) through a ring-offset table: no unpack copy."""
         lo, hi = self._fl[self.rank][q]
         c0, c1 = self._fc[self.rank][q]
         if c1 <= c0:
             return a, b
         nb = hi - lo
-        S = torch.empty((3, B, self.n_theta, 2 * nb), dtype=torch.complex128, device=self.device)
-        for g, r in enumerate(recvs):
-            r0, r1 = self.layouts[g].rings
-            S[:, :, r0:r1, :] = r.view(3, B, r1 - r0, 2 * nb)
-        self.stages.forward_orders(S, lo, nb, a, b, (lo, hi), (c0, c1))
+        rtab = self._rtab(B, lambda g: nb, ("f", B, q))
+        self.stages.forward_orders_packed(recv, rtab, B, lo, nb, a, b, (lo, hi), (c0, c1))
         return a, b
 
     def forward(self, T_local, a=None, b=None):
@@ -366,34 +405,41 @@ class OrderShardedPlan:
             flat, sizes = self.forward_send(S, q)
             work, recvs = self._all_to_all(flat, sizes, self.forward_recv_sizes(B, q), async_op=True)
             pending.append((work, recvs, flat))
-        for q, (work, recvs, _) in enumerate(pending):
+        for q, (work, recv, _) in enumerate(pending):
             if work is not None:
                 work.wait()
-            self.forward_finish(recvs, B, a, b, q)
+            self.forward_finish(recv, B, a, b, q)
         return a, b
 
     # ---- adjoint ---------------------------------------------------------
     def adjoint_send(self, a, b, q=0):
-        """Chunk q: synthesis of this rank's chunk-q orders into compact spectra of every
-        ring, packed per destination ring block."""
+        """Chunk q: synthesis of this rank's chunk-q orders written straight into the send
+        buffer, one block (3, B, rings of h, 2 nb) per destination rank h (ring-offset
+        table: no pack copy).  Returns (flat float64 buffer, per-destination sizes)."""
         torch = _torch()
         B = int(a.shape[0])
         m0, m1 = self._ao[self.rank][q]
         nb = m1 - m0
-        S = torch.zeros((3, B, self.n_theta, 2 * nb), dtype=torch.complex128, device=self.device)
+        sizes = [3 * B * (l.rings[1] - l.rings[0]) * 2 * nb * 2 for l in self.layouts]
+        flat = torch.empty(sum(sizes), dtype=torch.float64, device=self.device)
         if nb:
-            self.stages.adjoint_orders(a, b, (m0, m1), S)
-        blocks = [((3, B, l.rings[1] - l.rings[0], 2 * nb),
-                   lambda out, l=l: out.copy_(S[:, :, l.rings[0]:l.rings[1], :])) for l in self.layouts]
-        return self._pack(blocks)
+            rtab = self._rtab(B, lambda h: nb, ("a", B, q))
+            self.stages.adjoint_orders_packed(a, b, B, (m0, m1), torch.view_as_complex(flat.view(-1, 2)), rtab, nb)
+        return flat, sizes
 
     def adjoint_recv_sizes(self, B, q=0):
         return [3 * B * self.nloc * 2 * (o[q][1] - o[q][0]) * 2 for o in self._ao]
 
-    def adjoint_unpack(self, recvs, B, q=0):
+    def adjoint_unpack(self, recv, B, q=0):
+        """Chunk q: the received compact bins of every source rank's orders (blocks
+        (3, B, nloc, 2 nb_h) in rank order) -> their natural bins of S_loc_a."""
         S = self.S_loc_a[:, :B]
-        for h, r in enumerate(recvs):
+        o = 0
+        for h in range(self.world):
             m0, m1 = self._ao[h][q]
+            k = 3 * B * self.nloc * 2 * (m1 - m0)
+            r = recv[o:o + k]
+            o += k
             if m1 <= m0:
                 continue
             blk = r.view(3, B, self.nloc, 2 * (m1 - m0))
@@ -419,10 +465,10 @@ class OrderShardedPlan:
             flat, sizes = self.adjoint_send(a, b, q)
             work, recvs = self._all_to_all(flat, sizes, self.adjoint_recv_sizes(B, q), async_op=True)
             pending.append((work, recvs, flat))
-        for q, (work, recvs, _) in enumerate(pending):
+        for q, (work, recv, _) in enumerate(pending):
             if work is not None:
                 work.wait()
-            self.adjoint_unpack(recvs, B, q)
+            self.adjoint_unpack(recv, B, q)
         return self.adjoint_finish(B, T_local)
 
     # ---- coefficients ------------------------------------------------------
@@ -478,9 +524,10 @@ def simulate_forward(plans, T_locals):
         a = torch.zeros((B, p.K), dtype=torch.complex128, device=p.device)
         outs.append((a, torch.zeros_like(a)))
     for q in range(plans[0].chunks):
-        sends = [_unflatten(p.forward_send(s, q), p) for p, s in zip(plans, S)]
+        sends = [_unflatten(p.forward_send(s, q)) for p, s in zip(plans, S)]
         for h, p in enumerate(plans):
-            p.forward_finish([sends[g][h] for g in range(len(plans))], B, outs[h][0], outs[h][1], q)
+            recv = torch.cat([sends[g][h].reshape(-1) for g in range(len(plans))])
+            p.forward_finish(recv, B, outs[h][0], outs[h][1], q)
     return outs
 
 
@@ -488,9 +535,9 @@ def simulate_adjoint(plans, ab):
     torch = _torch()
     B = int(ab[0][0].shape[0])
     for q in range(plans[0].chunks):
-        sends = [_unflatten(p.adjoint_send(a, b, q), p) for p, (a, b) in zip(plans, ab)]
+        sends = [_unflatten(p.adjoint_send(a, b, q)) for p, (a, b) in zip(plans, ab)]
         for g, p in enumerate(plans):
-            p.adjoint_unpack([sends[h][g] for h in range(len(plans))], B, q)
+            p.adjoint_unpack(torch.cat([sends[h][g].reshape(-1) for h in range(len(plans))]), B, q)
     outs = []
     for p in plans:
         T = torch.empty((B, p.nloc * p.n_phi, 3), dtype=torch.complex128, device=p.device)
@@ -498,7 +545,7 @@ def simulate_adjoint(plans, ab):
     return outs
 
 
-def _unflatten(packed, plan):
+def _unflatten(packed):
     """The per-destination complex blocks of a packed send buffer."""
     torch = _torch()
     flat, sizes = packed

@@ -47,3 +47,18 @@ class OracleStages:
                 S_own[:, f, :, j] = torch.from_numpy(spec[:, m, :].T.copy())
                 if m:
                     S_own[:, f, :, nb + j] = torch.from_numpy(spec[:, (n - m) % n, :].T.copy())
+
+    # packed spectra (dist.py ring-offset tables): gather / scatter around the dense stages
+    def _dense_index(self, rtab, B, nb):
+        n = len(self.th)
+        base = rtab.view(3, B, n, 1)
+        return base + torch.arange(2 * nb, dtype=torch.long).view(1, 1, 1, -1)
+
+    def forward_orders_packed(self, flat, rtab, B, bin_lo, nb, a, b, legendre, coef):
+        S_own = flat[self._dense_index(rtab, B, nb)]
+        self.forward_orders(S_own, bin_lo, nb, a, b, legendre, coef)
+
+    def adjoint_orders_packed(self, a, b, B, orders, flat, rtab, nb):
+        S_own = torch.zeros((3, B, len(self.th), 2 * nb), dtype=torch.complex128)
+        self.adjoint_orders(a, b, orders, S_own)
+        flat[self._dense_index(rtab, B, nb).reshape(-1)] = S_own.reshape(-1)

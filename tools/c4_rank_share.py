@@ -53,10 +53,15 @@ def rank_share(base, T, A, Bc, worlds=(1, 2, 4, 8), chunks=1, balance="cost", si
         Tl = [T4[:, p.me.rings[0]:p.me.rings[1]].reshape(1, -1, 3).contiguous() for p in plans]
         # every rank's sends (computed once; each receiving rank reuses them)
         S = [p.forward_fft(t).clone() for p, t in zip(plans, Tl)]
-        sends = [[_unflatten(p.forward_send(s, q), p) for q in range(chunks)] for p, s in zip(plans, S)]
+        sends = [[_unflatten(p.forward_send(s, q)) for q in range(chunks)] for p, s in zip(plans, S)]
         a = torch.zeros_like(A)
         b = torch.zeros_like(Bc)
-        adj_sends = [[_unflatten(p.adjoint_send(A, Bc, q), p) for q in range(chunks)] for p in plans]
+        adj_sends = [[_unflatten(p.adjoint_send(A, Bc, q)) for q in range(chunks)] for p in plans]
+        # each rank's receive buffers (the blocks of every source in rank order)
+        recv_f = [[torch.cat([sends[g][q][h].reshape(-1) for g in range(world)]) for q in range(chunks)]
+                  for h in range(world)]
+        recv_a = [[torch.cat([adj_sends[g][q][h].reshape(-1) for g in range(world)]) for q in range(chunks)]
+                  for h in range(world)]
         per = []
         vol = 0
         for h, p in enumerate(plans):
@@ -64,12 +69,12 @@ def rank_share(base, T, A, Bc, worlds=(1, 2, 4, 8), chunks=1, balance="cost", si
                 s = p.forward_fft(Tl[h])
                 for q in range(chunks):
                     p.forward_send(s, q)
-                    p.forward_finish([sends[g][q][h] for g in range(world)], 1, a, b, q)
+                    p.forward_finish(recv_f[h][q], 1, a, b, q)
 
             def adj():
                 for q in range(chunks):
                     p.adjoint_send(A, Bc, q)
-                    p.adjoint_unpack([adj_sends[g][q][h] for g in range(world)], 1, q)
+                    p.adjoint_unpack(recv_a[h][q], 1, q)
                 p.adjoint_finish(1, Tl[h])
 
             rec = {"rank": h, "rings": list(p.me.rings), "orders": list(p.me.orders)}
@@ -92,7 +97,7 @@ def rank_share(base, T, A, Bc, worlds=(1, 2, 4, 8), chunks=1, balance="cost", si
                                "nvlink_ms_at_900GBs": vol / 900e9 * 1e3,
                                "speedup_vs_single_gpu_plan_compute_only": single / slow,
                                "speedup_vs_single_gpu_plan_with_serial_nvlink": single / (slow + vol / 900e9 * 1e3)}
-        del plans, S, sends, adj_sends
+        del plans, S, sends, adj_sends, recv_f, recv_a
         torch.cuda.empty_cache()
     return out
 
