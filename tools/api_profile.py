@@ -55,15 +55,11 @@ t("plan.adjoint device", lambda: plan.adjoint(a, b))
 t("grid_plan lookup (hash)", lambda: tr.grid_plan(grid, L))
 
 # pieces of the adjoint's host path (staging.py)
-from paper_1908_00041_b200.staging import HostResult, stager
+from paper_1908_00041_b200.staging import stager
 
 st = stager(torch.device("cuda", 0))
 Tdev = plan.adjoint(a, b)
-t("HostResult 101 MB: alloc + first touch", lambda: HostResult((len(rule), 3), np.complex128).wait())
-t("np.empty 101 MB + torch zero_ (main thread)", lambda: torch.from_numpy(np.empty((len(rule), 3), np.complex128)).zero_())
+t("np.empty 101 MB + torch zero_ (first touch)", lambda: torch.from_numpy(np.empty((len(rule), 3), np.complex128)).zero_())
 t("stager.to_host 101 MB into fresh pages", lambda: st.to_host(Tdev[0]))
-pre = HostResult((len(rule), 3), np.complex128)
-pre.wait()
-t("stager.to_host 101 MB into touched pages", lambda: st.to_host(Tdev[0], pre))
 t("stager.to_device coefficients 2 x 16.8 MB", lambda: (st.to_device(raw[0:1]), st.to_device(raw[1:2])))
 print("torch threads", torch.get_num_threads())
