@@ -64,6 +64,14 @@ typedef struct fvPlan fvPlan;
 /* Version string of the library ("favest_b200 <version> sm_100a"). */
 const char* fv_version(void);
 
+/* Gauss-Legendre rule of n nodes computed on the device (Newton on the
+ * colatitude; replaces scipy.special.roots_legendre inside
+ * favest/quadrature.py:29-48 when requested): thetas[k] ascending colatitudes
+ * (= arccos of the nodes, descending in cos), weights[k] the Gauss weights
+ * (summing to 2), host arrays of n doubles.  Blocking.  Not bitwise scipy's
+ * (more accurate polar weights). */
+int fv_gauss_legendre(int n, double* thetas, double* weights, int device);
+
 /* Message of the last failing call on this thread ("" if none). */
 const char* fv_last_error(void);
 

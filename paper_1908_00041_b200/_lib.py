@@ -19,7 +19,7 @@ EXPORTED = (
     "fv_plan_destroy", "fv_plan_info", "fv_forward_grid", "fv_adjoint_grid",
     "fv_adjoint_points", "fv_forward_points", "fv_set_profiling", "fv_stage_ms", "fv_stage_count",
     "fv_ring_fft", "fv_forward_orders", "fv_adjoint_orders", "fv_order_cost",
-    "fv_forward_orders_packed", "fv_adjoint_orders_packed",
+    "fv_forward_orders_packed", "fv_adjoint_orders_packed", "fv_gauss_legendre",
     "fv_forward_scalar_grid", "fv_adjoint_scalar_grid", "fv_forward_scalar_points", "fv_adjoint_scalar_points",
 )
 
@@ -65,6 +65,7 @@ def load(path: str | None = None) -> ctypes.CDLL:
         "fv_forward_orders": (i, [vp, vp, ll, ll, ll, i, i, vp, vp, i, i, i, i, i, vp]),
         "fv_adjoint_orders": (i, [vp, vp, vp, i, i, i, vp, ll, ll, ll, i, i, vp]),
         "fv_order_cost": (i, [vp, dp]),
+        "fv_gauss_legendre": (i, [i, dp, dp, i]),
         "fv_forward_orders_packed": (i, [vp, vp, vp, ll, i, i, vp, vp, i, i, i, i, i, vp]),
         "fv_adjoint_orders_packed": (i, [vp, vp, vp, i, i, i, vp, vp, ll, i, i, vp]),
         "fv_forward_scalar_grid": (i, [vp, vp, vp, i, i, vp]),

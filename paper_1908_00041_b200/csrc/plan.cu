@@ -27,6 +27,7 @@
 #include "fft_rader.cuh"
 #include "legendre.cuh"
 #include "points.cuh"
+#include "quadrature.cuh"
 #include "scalar.cuh"
 
 namespace {
@@ -1041,6 +1042,29 @@ int begin_call(fvPlan* p) {
 extern "C" {
 
 const char* fv_version(void) { return "favest_b200 0.1.0 sm_100a"; }
+
+int fv_gauss_legendre(int n, double* thetas, double* weights, int device) {
+  if (n < 1) return fail(FV_EINVAL, "Gauss-Legendre rule needs at least one node, got " + std::to_string(n));
+  if (!thetas || !weights) return fail(FV_EINVAL, "null output");
+  int prev = 0;
+  FV_CUDA(cudaGetDevice(&prev));
+  FV_CUDA(cudaSetDevice(device));
+  double* d = nullptr;
+  int rc = FV_OK;
+  if (cudaMalloc(&d, 2 * (size_t)n * sizeof(double)) != cudaSuccess) {
+    cudaSetDevice(prev);
+    return fail(FV_ENOMEM, "device allocation failed");
+  }
+  const int half = (n + 1) / 2;
+  fv::gauss_legendre_kernel<<<(half + 127) / 128, 128>>>(n, d, d + n);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpy(thetas, d, n * sizeof(double), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(weights, d + n, n * sizeof(double), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) rc = fail(FV_ECUDA, std::string("Gauss-Legendre rule: ") + cudaGetErrorString(e));
+  cudaFree(d);
+  cudaSetDevice(prev);
+  return rc;
+}
 
 // debug: copy the forward pipeline trace (4096 tiles x 8 stamps) to the host
 int fv_debug_trace(long long* host) {

@@ -67,20 +67,51 @@ class TensorGrid:
         )
 
 
-def gen_gl_tensor(t: int) -> tuple[TensorGrid, QuadratureRule]:
+def gen_gl_tensor(t: int, on_device: bool = False) -> tuple[TensorGrid, QuadratureRule]:
     """Gauss-Legendre tensor rule exact to degree t (favest/quadrature.py:29-48):
-    (t+2)//2 rings, t+1 longitudes, weights (2 pi / n_phi) * gauss weight."""
-    from scipy.special import roots_legendre
+    (t+2)//2 rings, t+1 longitudes, weights (2 pi / n_phi) * gauss weight.
 
+    Default: scipy's roots_legendre, as the reference (bitwise its weights).
+    ``on_device=True``: the rule from the CUDA library (fv_gauss_legendre: Newton
+    on the colatitudes, the Legendre recurrence in difference form on
+    1 - cos(theta), ring colatitudes without an arccos), a deliberate deviation:
+    polar weights accurate to ~1e-11 where scipy's are off by 1e-9 .. 1e-7, and
+    an exactness defect of ~1e-14 against scipy's ~4e-13 at n = 4098 (SURVEY
+    §0.6; tests/test_gpu_edges.py), so not bitwise the reference's rule."""
     if t < 0:
         raise ValueError(f"exactness degree must be non-negative, got {t}")
     n_theta = (t + 2) // 2
     n_phi = t + 1
-    nodes, gauss_w = roots_legendre(n_theta)
-    thetas = np.arccos(nodes[::-1])
-    weights = gauss_w[::-1] * (2.0 * np.pi / n_phi)
+    if on_device:
+        thetas, gauss_w = gauss_legendre_device(n_theta)
+        weights = gauss_w * (2.0 * np.pi / n_phi)
+    else:
+        from scipy.special import roots_legendre
+
+        nodes, gauss_w = roots_legendre(n_theta)
+        thetas = np.arccos(nodes[::-1])
+        weights = gauss_w[::-1] * (2.0 * np.pi / n_phi)
     grid = TensorGrid(ring_thetas=thetas, ring_weights=weights, n_phi=n_phi)
     return grid, grid.to_rule(exactness=t)
+
+
+def gauss_legendre_device(n: int, device=None) -> tuple[np.ndarray, np.ndarray]:
+    """(colatitudes ascending, Gauss weights) of the n-node rule, computed on the GPU."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("gauss_legendre_device needs a CUDA device (no CPU fallback)")
+    dev = torch.cuda.current_device() if device is None else torch.device(device).index or 0
+    th = np.empty(int(n), dtype=np.float64)
+    w = np.empty(int(n), dtype=np.float64)
+    dp = ctypes.POINTER(ctypes.c_double)
+    lib = _lib.load()
+    _lib.check(lib.fv_gauss_legendre(int(n), th.ctypes.data_as(dp), w.ctypes.data_as(dp), int(dev)))
+    return th, w
 
 
 def gl_grid_for(lmax: int) -> tuple[TensorGrid, QuadratureRule]:

@@ -92,3 +92,89 @@ def test_ragged_batch_groups(B):
         ra, rb = O.vsht_forward_grid(T[k], th, w, nphi, L)
         got = np.concatenate([fa[k].cpu().numpy(), fb[k].cpu().numpy()])
         assert O.rel_l2(got, np.concatenate([ra, rb])) <= TOL
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 34, 515, 4098])
+def test_device_gauss_legendre_rule(n):
+    """fv_gauss_legendre: the n-node rule on the device against scipy's
+    roots_legendre (what favest/quadrature.py:29-48 uses) and against exactness."""
+    from scipy.special import roots_legendre
+
+    from paper_1908_00041_b200.grid import gauss_legendre_device
+
+    cuda_or_skip()
+    th, w = gauss_legendre_device(n)
+    nodes, gw = roots_legendre(n)
+    assert np.all(np.diff(th) > 0) and th[0] > 0 and th[-1] < np.pi
+    assert np.max(np.abs(np.cos(th) - nodes[::-1])) <= 4e-16 * max(1, n) ** 0.5
+    assert np.max(np.abs(w / gw[::-1] - 1)[n // 4:n - n // 4 or None]) <= 1e-11  # scipy's are accurate mid-range
+    assert abs(w.sum() - 2.0) <= 1e-14 * n
+
+    def defect(x, ww):
+        """max_l |sum_k w_k P_l(x_k) - 2 delta_l0| over l <= 2n - 1 (float64 recurrence)."""
+        p0, p1 = np.ones(n), x.copy()
+        d = max(abs(np.dot(ww, p0) - 2.0), abs(np.dot(ww, p1)))
+        for l in range(2, 2 * n):
+            p0, p1 = p1, ((2 * l - 1) * x * p1 - (l - 1) * p0) / l
+            d = max(d, abs(np.dot(ww, p1)))
+        return d
+
+    # exactness at least as good as scipy's (measured: 6e-15 .. 2e-14 against scipy's
+    # 1e-13 .. 5e-13 for n = 515 .. 4098)
+    dd, ds = defect(np.cos(th), w), defect(nodes[::-1], gw[::-1])
+    assert dd <= max(ds, 1e-13), (dd, ds)
+    # polar weights against a 50-digit Newton (decimal): the device rule is accurate to
+    # ~1e-11 where scipy's polar weights are off by 1e-9 .. 1e-7 (SURVEY §0.6)
+    if n >= 100:
+        for k in range(2):
+            z_ref, w_ref = _gl_root_decimal(n, k)
+            assert abs(np.cos(th[k]) - z_ref) <= 2e-16
+            assert abs(w[k] / w_ref - 1) <= 1e-11, (k, w[k], w_ref)
+
+
+def _gl_root_decimal(n, k):
+    """(node, weight) of the (k+1)-th largest Gauss-Legendre node, 50-digit Newton."""
+    import math
+    from decimal import Decimal as D, localcontext
+
+    with localcontext() as ctx:
+        ctx.prec = 50
+
+        def pair(z):
+            p1, p0 = D(1), D(0)
+            for j in range(1, n + 1):
+                p2, p0 = p0, p1
+                p1 = ((2 * j - 1) * z * p0 - (j - 1) * p2) / j
+            return p1, p0
+
+        z = D(math.cos(math.pi * (4 * (k + 1) - 1) / (4 * n + 2)))
+        for _ in range(60):
+            pn, pn1 = pair(z)
+            dz = pn / (n * (z * pn - pn1) / (z * z - 1))
+            z -= dz
+            if abs(dz) < D(10) ** -45:
+                break
+        pn, pn1 = pair(z)
+        dp = n * (z * pn - pn1) / (z * z - 1)
+        return float(z), float(2 / ((1 - z * z) * dp * dp))
+
+
+def test_device_gl_tensor_round_trip():
+    """gen_gl_tensor(on_device=True) rule through the transforms: adjoint -> forward
+    recovers the coefficients at least as well as with scipy's weights."""
+    import paper_1908_00041_b200 as fb
+    from paper_1908_00041_b200.plan import GridPlan
+
+    cuda_or_skip()
+    L = 200
+    rng = np.random.default_rng(700)
+    a, b = O.coef(rng, L, "inv")
+    errs = []
+    for dev_rule in (False, True):
+        grid, rule = fb.gen_gl_tensor(2 * L + 3, on_device=dev_rule)
+        assert grid.n_theta == L + 2 and len(rule) == grid.n_theta * grid.n_phi
+        plan = GridPlan.from_grid(grid, L)
+        T = plan.adjoint(_t(a[None]), _t(b[None]))
+        fa, fb_ = plan.forward(T)
+        errs.append(O.rel_l2(np.concatenate([fa[0].cpu().numpy(), fb_[0].cpu().numpy()]), np.concatenate([a, b])))
+    assert errs[1] <= max(errs[0], 1e-14), errs
