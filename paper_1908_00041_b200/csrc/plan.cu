@@ -1390,15 +1390,33 @@ int fwd_ksplit(const fvPlan* p, int mc) {
   return std::max(1, std::min({ks, 4, p->nchunks}));
 }
 
+// Fields per forward Legendre launch: up to 4, fewer when the shared memory of
+// the launch's n-tile count (5 stages + per-pair recurrence state) would exceed
+// 227 KB -- 4 fields (NT = 6) fit up to L ~ 1900, 2 fields (NT = 3) up to L ~ 4000.
+int fwd_group_cap(const fvPlan* p) {
+  const int nPx = p->nchunks * fv::FWD_RC;
+  for (int nf = 4; nf > 1; --nf) {
+    size_t bytes = 0;
+    switch (ntiles_for(nf)) {
+      case 3: bytes = fv::FwdSmem<3>::bytes(nPx); break;
+      case 5: bytes = fv::FwdSmem<5>::bytes(nPx); break;
+      default: bytes = fv::FwdSmem<6>::bytes(nPx); break;
+    }
+    if (bytes <= 227 * 1024) return nf;
+  }
+  return 1;
+}
+
 int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* a, double* b, int B, int m_lo,
                    int m_hi, int c_lo, int c_hi, cudaStream_t s, const double2* Tfield = nullptr,
                    const ScalarIO* sio = nullptr) {
   const int Lt = p->Lt;
   const int mc = m_hi - m_lo;
+  const int cap = fwd_group_cap(p);
   for (int b0 = 0; b0 < B;) {
     // up to ngroups_buf full 4-field groups go through one Legendre launch
-    const int ng = std::max(1, std::min((B - b0) / 4, p->ngroups_buf));
-    const int nf = ng > 1 ? 4 : std::min(4, B - b0);
+    const int ng = cap == 4 ? std::max(1, std::min((B - b0) / 4, p->ngroups_buf)) : 1;
+    const int nf = ng > 1 ? 4 : std::min(cap, B - b0);
     const int NT = ntiles_for(nf);
     for (int g = 0; g < ng; ++g) {
       double* Xg = p->X + (size_t)g * p->x_gstride;

@@ -178,3 +178,31 @@ def test_device_gl_tensor_round_trip():
         fa, fb_ = plan.forward(T)
         errs.append(O.rel_l2(np.concatenate([fa[0].cpu().numpy(), fb_[0].cpu().numpy()]), np.concatenate([a, b])))
     assert errs[1] <= max(errs[0], 1e-14), errs
+
+
+@pytest.mark.parametrize("L,B", [(2048, 4), (1999, 3)])
+def test_large_degree_batches_fit_shared_memory(L, B):
+    """Past L ~ 1900 four fields per forward launch no longer fit the kernel's shared
+    memory; the plan then launches fewer fields at a time.  Batch results equal the
+    single-field plan's to rounding, and the device-rule round trip holds to 5e-12."""
+    import paper_1908_00041_b200 as fb
+    from paper_1908_00041_b200.plan import GridPlan
+
+    torch = cuda_or_skip()
+    grid, _ = fb.gen_gl_tensor(2 * L + 3, on_device=True)
+    rng = np.random.default_rng(L)
+    ab = [O.coef(rng, L, "pow2") for _ in range(B)]
+    A = _t(np.stack([x[0] for x in ab]))
+    Bc = _t(np.stack([x[1] for x in ab]))
+    plan = GridPlan.from_grid(grid, L, max_batch=B)
+    T = plan.adjoint(A, Bc)
+    fa, fb_ = plan.forward(T)
+    err = float(torch.linalg.vector_norm(torch.cat([fa - A, fb_ - Bc], 1)) / torch.linalg.vector_norm(torch.cat([A, Bc], 1)))
+    assert err <= 5e-12, err
+    one = GridPlan.from_grid(grid, L, max_batch=1)
+    k = B - 1
+    T1 = one.adjoint(A[k:k + 1].contiguous(), Bc[k:k + 1].contiguous())
+    assert float(torch.linalg.vector_norm(T1[0] - T[k]) / torch.linalg.vector_norm(T[k])) <= 1e-14
+    a1, b1 = one.forward(T[k:k + 1].contiguous())
+    assert float(torch.linalg.vector_norm(torch.cat([a1[0] - fa[k], b1[0] - fb_[k]])) /
+                 torch.linalg.vector_norm(torch.cat([fa[k], fb_[k]]))) <= 1e-14
