@@ -523,7 +523,14 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
         };
         auto fetch = [&](uint32_t t, Frag& f) {
           const int stage = t % FWD_STAGES;
+#ifdef FV_TRACE_CONSUMERS
+          const bool tr = args.trace && blockIdx.x == args.trace_cta && lane == 0 && cw == 0 && t < 4096;
+          if (tr) args.trace[t * 8 + 3] = clock64();
+#endif
           mbar_wait(&full[stage], (t / FWD_STAGES) & 1);
+#ifdef FV_TRACE_CONSUMERS
+          if (tr) args.trace[t * 8 + 4] = clock64();
+#endif
           const double* Ps = smem + stage * SM::STAGE;
           const double* Xs = Ps + FWD_PTILE;
           f.km0 = meta[stage].kmin[2 * kq];
@@ -560,6 +567,10 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
           }
         };
         auto release = [&](uint32_t t) {
+#ifdef FV_TRACE_CONSUMERS
+          if (args.trace && blockIdx.x == args.trace_cta && lane == 0 && cw == 0 && t < 4096)
+            args.trace[t * 8 + 5] = clock64();  // DMMAs of tile t issued
+#endif
           mbar_arrive(&empty[t % FWD_STAGES]);  // the fragments are in registers
           if (cw == 0 && lane == 0) *cons0 = (int)t + 1;
         };
