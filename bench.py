@@ -777,6 +777,29 @@ def run_c4(args, rank, world, local_rank):
     dist.destroy_process_group()
 
 
+def dry_run(args, rank, world):
+    """--dry-run: the multi-rank plumbing of run_ours (process group, world check,
+    barrier, max over ranks, rank 0 prints one line) over gloo on the CPU."""
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+        if dist.get_world_size() != args.gpus:
+            raise SystemExit(f"bench.py --gpus {args.gpus} but the process group has {dist.get_world_size()} ranks")
+        dist.barrier()
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "dry_run": True, "max_over_ranks": float(t.item()),
+                          "config": workload_config(args.L, args.batch, world)}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def relaunch(n: int):
     """``--gpus N`` without a torchrun environment: re-execute this script under
     ``torch.distributed.run`` with N processes on this node (127.0.0.1 rendezvous)."""
@@ -805,6 +828,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-detail", action="store_true", help="skip the on-the-fly / C5 / C4 detail entries")
     ap.add_argument("--no-rank-share", action="store_true", help="skip the C4 per-rank projection at N=1")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check without a GPU: the same re-launch and rank set-up over gloo, "
+                         "one max-over-ranks reduction, the JSON line's rank bookkeeping (no timing)")
     ap.add_argument("--workload", default="c3", choices=["c3", "c4"],
                     help="c3: batch-sharded L=1024 (the headline); c4: one L=4096 field, order-sharded")
     args = ap.parse_args()
@@ -820,7 +846,9 @@ def main():
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
-    if args.impl == "reference":
+    if args.dry_run:
+        dry_run(args, rank, world)
+    elif args.impl == "reference":
         run_reference(args, rank, world)
     elif args.workload == "c4":
         run_c4(args, rank, world, local_rank)
