@@ -288,6 +288,28 @@ __device__ __forceinline__ double2 combo_uvw(int comp, double2 x, double2 y, dou
   return z;
 }
 
+// One output (a_lm, b_lm) from its nine factors x = (xi1..6, mu1..3) and the U / V / W
+// coefficients at degrees l-1 (a), l+1 (b), l (c): favest/transforms.py:137-144 in the
+// reference's association order with every product and sum rounded separately, as
+// numpy evaluates it (no FMA contraction), shared by all forward CG kernels so they
+// agree bitwise.
+__device__ __forceinline__ void cg_fwd_combine(const double (&x)[9], double2 ua, double2 ub, double2 uc, double2 va,
+                                               double2 vb, double2 vc, double2 wa, double2 wb, double2 wc,
+                                               double2& A, double2& B) {
+  const double is2 = 0.7071067811865475;  // favest/transforms.py:46 (1/np.sqrt(2.0))
+  auto part = [&](double p1, double p2, double p3, double p4, double p5, double p6) {
+    const double s4 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(x[0], p1), __dmul_rn(x[1], p2)), __dmul_rn(x[2], p3)),
+                                __dmul_rn(x[3], p4));
+    return __dadd_rn(__dadd_rn(__dmul_rn(is2, s4), __dmul_rn(x[4], p5)), __dmul_rn(x[5], p6));
+  };
+  A = make_double2(part(ua.x, ub.x, va.x, vb.x, wa.x, wb.x), part(ua.y, ub.y, va.y, vb.y, wa.y, wb.y));
+  // b = -i/sqrt2 (mu1 fu + mu3 fv) - i mu2 fw
+  const double sr = __dadd_rn(__dmul_rn(x[6], uc.x), __dmul_rn(x[8], vc.x));
+  const double si = __dadd_rn(__dmul_rn(x[6], uc.y), __dmul_rn(x[8], vc.y));
+  B = make_double2(__dadd_rn(__dmul_rn(is2, si), __dmul_rn(x[7], wc.y)),
+                   __dsub_rn(-__dmul_rn(is2, sr), __dmul_rn(x[7], wc.x)));
+}
+
 __device__ __forceinline__ double2 f_read(const CgFwdArgs& a, int b, int comp, long long l, long long m) {
   // scalar coefficient F^comp_{l,m} (comp 0 U, 1 V, 2 W), zero outside 0 <= l <= L+1, |m| <= l
   if (l < 0 || l > a.L + 1 || llabs(m) > l) return make_double2(0.0, 0.0);
@@ -304,7 +326,6 @@ __global__ void cg_fwd_kernel(CgFwdArgs a) {
   const long long l = blockIdx.y;
   const long long am = blockIdx.x * blockDim.x + threadIdx.x;
   if (am > l) return;
-  const double is2 = 0.7071067811865475;  // favest/transforms.py:46 (1/np.sqrt(2.0))
   const long long K = (long long)(a.L + 1) * (a.L + 1);
   for (int sg = 0; sg < (am == 0 ? 1 : 2); ++sg) {
     const long long M = sg ? -am : am;
@@ -328,13 +349,10 @@ __global__ void cg_fwd_kernel(CgFwdArgs a) {
       const double2 fw_a = f_read(a, b, 2, l - 1, M), fw_b = f_read(a, b, 2, l + 1, M);
       const double2 fu_c = f_read(a, b, 0, l, M - 1), fv_c = f_read(a, b, 1, l, M + 1);
       const double2 fw_c = f_read(a, b, 2, l, M);
-      // a = 1/sqrt2 * (x1 fu + x2 fu + x3 fv + x4 fv) + x5 fw + x6 fw
-      double ar = is2 * (((x1 * fu_a.x + x2 * fu_b.x) + x3 * fv_a.x) + x4 * fv_b.x) + x5 * fw_a.x + x6 * fw_b.x;
-      double ai = is2 * (((x1 * fu_a.y + x2 * fu_b.y) + x3 * fv_a.y) + x4 * fv_b.y) + x5 * fw_a.y + x6 * fw_b.y;
-      // b = -i/sqrt2 (u1 fu + u3 fv) - i u2 fw
-      const double sr = u1 * fu_c.x + u3 * fv_c.x, si = u1 * fu_c.y + u3 * fv_c.y;
-      double br = is2 * si + u2 * fw_c.y;
-      double bi = -is2 * sr - u2 * fw_c.x;
+      const double xs[9] = {x1, x2, x3, x4, x5, x6, u1, u2, u3};
+      double2 ca, cb;
+      cg_fwd_combine(xs, fu_a, fu_b, fu_c, fv_a, fv_b, fv_c, fw_a, fw_b, fw_c, ca, cb);
+      double ar = ca.x, ai = ca.y, br = cb.x, bi = cb.y;
       if (l == 0) ar = ai = br = bi = 0.0;  // favest/transforms.py:145-146
       const size_t o = (size_t)(a.b0 + b) * K + l * l + l + M;
       a.A[o] = make_double2(ar, ai);
@@ -417,7 +435,6 @@ __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
   }
   __syncthreads();
   if (!work) return;
-  const double is2 = 0.7071067811865475;  // favest/transforms.py:46 (1/np.sqrt(2.0))
   // staged F^{x,y,z}_{l+dl, mm}: row |mm| - (m0 - 1); out-of-range rows were staged as 0;
   // combo comp of favest/transforms.py:112 formed on read
   auto f = [&](int comp, int dl, int mm) -> double2 {
@@ -429,15 +446,20 @@ __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
   const double2 fw_a = f(2, -1, M), fw_b = f(2, 1, M);
   const double2 fu_c = f(0, 0, M - 1), fv_c = f(1, 0, M + 1);
   const double2 fw_c = f(2, 0, M);
-  double ar = is2 * (((x1 * fu_a.x + x2 * fu_b.x) + x3 * fv_a.x) + x4 * fv_b.x) + x5 * fw_a.x + x6 * fw_b.x;
-  double ai = is2 * (((x1 * fu_a.y + x2 * fu_b.y) + x3 * fv_a.y) + x4 * fv_b.y) + x5 * fw_a.y + x6 * fw_b.y;
-  const double sr = u1 * fu_c.x + u3 * fv_c.x, si = u1 * fu_c.y + u3 * fv_c.y;
-  double br = is2 * si + u2 * fw_c.y;
-  double bi = -is2 * sr - u2 * fw_c.x;
+  const double xs[9] = {x1, x2, x3, x4, x5, x6, u1, u2, u3};
+  double2 ca, cb;
+  cg_fwd_combine(xs, fu_a, fu_b, fu_c, fv_a, fv_b, fv_c, fw_a, fw_b, fw_c, ca, cb);
+  double ar = ca.x, ai = ca.y, br = cb.x, bi = cb.y;
   if (l == 0) ar = ai = br = bi = 0.0;  // favest/transforms.py:145-146
   const size_t o = (size_t)(a.b0 + b) * K + (l * l + l + M);
   a.A[o] = make_double2(ar, ai);
   a.Bc[o] = make_double2(br, bi);
+}
+
+// 16-byte cp.async global -> shared; ok == false zero-fills (src-size 0; src must still be a valid address)
+__device__ __forceinline__ void cgs_cp16(void* dst_smem, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst_smem)), "l"(src), "r"(ok ? 16 : 0)
+               : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -643,6 +665,115 @@ __global__ void __launch_bounds__(CGA_THREADS) cg_adj_tile_kernel(CgAdjArgs a) {
   for (int i = threadIdx.x; i < TILE / 2; i += CGA_THREADS) {
     const int blk = i / BH, o = i - blk * BH;
     dst[i] = reinterpret_cast<const double2*>(Gs + blk * BS)[o];
+  }
+}
+
+// Grid-path adjoint CG over runs of NO consecutive orders: CTA per (run of orders
+// am0 .. am0 + NO - 1, 32-row chunk c).  cg_adj_tile_kernel stages, per (order, chunk),
+// the orders m-1 .. m+1 of both signs: every a / b entry is read by three CTAs, in
+// 48-byte pieces that straddle sectors, ~780 MB of L2 -> SM traffic at C3 for 437 MB of
+// HBM traffic.  Here the a / b window of the whole run (degrees l0-1 .. l0+NO+32, orders
+// am0-1 .. am0+NO of both signs: (NO+2) x 16-byte contiguous pieces) is staged once,
+// together with the run's factor and gamma rows, all by 16-byte cp.async (nothing passes
+// through registers), and the NO tiles are assembled one after the other in two
+// alternating padded buffers (the copy-out of tile o overlaps the assembly of tile o+1;
+// one CTA barrier per tile).  Same arithmetic as cg_adj_kernel (cg_adj_merge: bitwise equal).
+template <int NF, int NO>
+struct CgaMulti {
+  static constexpr int LC = 32, KS = LC / 8, NT = cgf_nt(NF), BS = cga_bstride(NF);
+  static constexpr int R = NO + LC + 1;     // staged degrees
+  static constexpr int NC = NO + 2;         // staged orders per sign block
+  static constexpr int CS = 2 * NC + 1;     // odd row stride (double2): conflict-free LDS.128 over rows
+  static constexpr int GBUF = 2 * KS * BS;  // doubles per padded tile buffer
+  static constexpr size_t bytes =
+      (size_t)2 * GBUF * 8 + (size_t)2 * NF * R * CS * 16 + (size_t)NO * 18 * 32 * 8 + (size_t)NO * 32 * 16;
+};
+template <int NF, int NO>
+__global__ void __launch_bounds__(CGA_THREADS) cg_adj_multi_kernel(CgAdjArgs a, int m_count) {
+  using C = CgaMulti<NF, NO>;
+  constexpr int LC = C::LC, KS = C::KS, NT = C::NT, BS = C::BS, R = C::R, NC = C::NC, CS = C::CS;
+  constexpr int TILE = 2 * KS * NT * 32;  // doubles
+  static_assert(LC * NF * 2 <= CGA_THREADS, "one (row, field, sign) per thread");
+  const int Lt = a.L + 1;
+  const int o0 = blockIdx.y * NO;
+  const int am0 = a.m_begin + o0;
+  const int c = blockIdx.x;
+  if (c * LC >= Lt + 1 - am0) return;
+  const int no = min(NO, m_count - o0);
+  extern __shared__ __align__(16) double cgm_smem[];
+  double* Gs = cgm_smem;                                          // [2][GBUF]
+  double2* As = reinterpret_cast<double2*>(Gs + 2 * C::GBUF);     // [NF][R][CS]
+  double2* Bs = As + NF * R * CS;
+  double* Fs = reinterpret_cast<double*>(Bs + NF * R * CS);       // factors [NO][9 x 2 signs][32 rows]
+  double2* Ds = reinterpret_cast<double2*>(Fs + NO * 18 * 32);    // (d, gamma) [NO][32 rows]
+  const int K = (a.L + 1) * (a.L + 1);
+  const int lp0 = am0 + c * LC - 1;
+  constexpr int NE = NF * R * 2 * NC;
+  for (int e = threadIdx.x; e < NE; e += CGA_THREADS) {
+    const int j = e % (2 * NC), r = (e / (2 * NC)) % R, bb = e / (2 * NC * R);
+    const int lp = lp0 + r;
+    const int mp = j < NC ? am0 - 1 + j : -(am0 + NO) + (j - NC);
+    const bool ok = lp >= 0 && lp <= a.L && abs(mp) <= lp;
+    const size_t o = ok ? (size_t)(a.b0 + bb) * K + (lp * lp + lp + mp) : 0;
+    cgs_cp16(&As[(bb * R + r) * CS + j], a.A + o, ok);
+    cgs_cp16(&Bs[(bb * R + r) * CS + j], a.Bc + o, ok);
+  }
+  for (int e = threadIdx.x; e < NO * 18 * 16; e += CGA_THREADS) {
+    const int h = e % 16, k = (e / 16) % 18, o = e / (16 * 18);
+    const int am = am0 + o;
+    const bool ok = o < no && c * LC < Lt + 1 - am;
+    cgs_cp16(&Fs[(o * 18 + k) * 32 + 2 * h], a.cga + (ok ? (a.gofs[am] + c) * 32 + (long long)k * a.nrow + 2 * h : 0), ok);
+  }
+  for (int e = threadIdx.x; e < NO * 32; e += CGA_THREADS) {
+    const int idx = e % 32, o = e / 32;
+    const int am = am0 + o;
+    const bool ok = o < no && am + c * LC + idx <= Lt;
+    cgs_cp16(&Ds[e], a.dg + (ok ? a.dgofs[am] + c * LC + idx : 0), ok);
+  }
+  for (int i = threadIdx.x; i < 2 * C::GBUF; i += CGA_THREADS) Gs[i] = 0.0;
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+  const int w = threadIdx.x;
+  const int idx = w % LC, b = (w / LC) % NF, sg = w / (LC * NF);
+  const int par = idx & 1, kk = idx >> 1, ks = kk >> 2, q = kk & 3;
+  const int n0 = 12 * b + 2 * sg;
+  for (int o = 0; o < no; ++o) {
+    const int am = am0 + o;
+    if (c * LC >= Lt + 1 - am) break;  // the higher orders of the run have no chunk c either
+    double* G = Gs + (o & 1) * C::GBUF;
+    if (w < LC * NF * 2) {
+      const int l = am + c * LC + idx;
+      const bool work = l <= Lt && !(sg == 1 && am == 0);
+      double2 gx = make_double2(0.0, 0.0), gy = gx, gz = gx;
+      double sig = 0.0;
+      if (work) {
+        double cfv[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) cfv[i] = Fs[(o * 18 + 2 * i + sg) * 32 + idx];
+        sig = (sg && (am & 1)) ? -1.0 : 1.0;  // favest/legendre.py:101-103
+        sig *= Ds[o * 32 + idx].y;             // gamma_l (legendre.cuh)
+        // staged row of degree l + dr: o + idx + 1 + dr; column of order +-am + dm
+        const int col = sg ? NC + NO - o : o + 1;
+        auto at = [&](const double2* t, int dr, int dm) { return t[(b * R + o + idx + 1 + dr) * CS + col + dm]; };
+        CgAdjIn v;
+        v.ap1p = at(As, 1, 1); v.ap1m = at(As, 1, -1); v.am1p = at(As, -1, 1); v.am1m = at(As, -1, -1);
+        v.ap10 = at(As, 1, 0); v.am10 = at(As, -1, 0);
+        v.bp = at(Bs, 0, 1); v.bm = at(Bs, 0, -1); v.b0 = at(Bs, 0, 0);
+        cg_adj_merge(cfv, v, gx, gy, gz);
+      }
+      double* gb = G + (par * KS + ks) * BS + q;
+      auto put = [&](int n, double v) { gb[(n >> 3) * 32 + ((n & 7) << 2)] = work ? v : 0.0; };
+      put(n0 + 0, sig * gx.x); put(n0 + 1, sig * gx.y);
+      put(n0 + 4, sig * gy.x); put(n0 + 5, sig * gy.y);
+      put(n0 + 8, sig * gz.x); put(n0 + 9, sig * gz.y);
+    }
+    __syncthreads();
+    double2* dst = reinterpret_cast<double2*>(a.G + (size_t)(a.gofs[am] + c) * TILE);
+    constexpr int BH = NT * 16;  // double2 per block
+    for (int i = threadIdx.x; i < TILE / 2; i += CGA_THREADS) {
+      const int blk = i / BH, oo = i - blk * BH;
+      dst[i] = reinterpret_cast<const double2*>(G + blk * BS)[oo];
+    }
   }
 }
 

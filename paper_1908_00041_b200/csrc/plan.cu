@@ -1483,11 +1483,36 @@ int adjoint_orders(fvPlan* p, const double* a, const double* b, double2* S, cons
       dim3 grid((Lt + 1 - m_lo + fv::ADJ_LC - 1) / fv::ADJ_LC, mc);
       const size_t smem = (size_t)2 * fv::ADJ_KS * fv::cga_bstride(nf) * sizeof(double) +
                           2 * (size_t)nf * 34 * 7 * sizeof(double2);
-      switch (nf) {
-        case 1: fv::cg_adj_tile_kernel<1><<<grid, fv::CGA_THREADS, smem, s>>>(ca); break;
-        case 2: fv::cg_adj_tile_kernel<2><<<grid, fv::CGA_THREADS, smem, s>>>(ca); break;
-        case 3: fv::cg_adj_tile_kernel<3><<<grid, fv::CGA_THREADS, smem, s>>>(ca); break;
-        default: fv::cg_adj_tile_kernel<4><<<grid, fv::CGA_THREADS, smem, s>>>(ca); break;
+      // runs of consecutive orders per CTA (cg_adj_multi_kernel): two at 3-4 fields (three CTAs
+      // per SM), four at 1-2 fields; FV_CGA_MULTI=0 selects the one-order tile kernel
+      static const int multi = [] { const char* e = std::getenv("FV_CGA_MULTI"); return e ? std::atoi(e) : -1; }();
+      auto launch_multi = [&](auto nfc, auto noc) -> int {
+        constexpr int NF_ = decltype(nfc)::value, NO_ = decltype(noc)::value;
+        static std::atomic<unsigned long long> attr{0};
+        FV_CUDA(smem_optin_once(&attr, p->device, fv::cg_adj_multi_kernel<NF_, NO_>));
+        const dim3 mgrid(grid.x, (mc + NO_ - 1) / NO_);
+        fv::cg_adj_multi_kernel<NF_, NO_><<<mgrid, fv::CGA_THREADS, fv::CgaMulti<NF_, NO_>::bytes, s>>>(ca, mc);
+        return FV_OK;
+      };
+      auto by_run = [&](auto nfc) -> int {
+        const int run = multi > 0 ? multi : (decltype(nfc)::value >= 3 ? 2 : 4);
+        if (run == 2) return launch_multi(nfc, std::integral_constant<int, 2>{});
+        return launch_multi(nfc, std::integral_constant<int, 4>{});
+      };
+      if (multi) {
+        switch (nf) {
+          case 1: FV_TRY(by_run(std::integral_constant<int, 1>{})); break;
+          case 2: FV_TRY(by_run(std::integral_constant<int, 2>{})); break;
+          case 3: FV_TRY(by_run(std::integral_constant<int, 3>{})); break;
+          default: FV_TRY(by_run(std::integral_constant<int, 4>{})); break;
+        }
+      } else {
+        switch (nf) {
+          case 1: fv::cg_adj_tile_kernel<1><<<grid, fv::CGA_THREADS, smem, s>>>(ca); break;
+          case 2: fv::cg_adj_tile_kernel<2><<<grid, fv::CGA_THREADS, smem, s>>>(ca); break;
+          case 3: fv::cg_adj_tile_kernel<3><<<grid, fv::CGA_THREADS, smem, s>>>(ca); break;
+          default: fv::cg_adj_tile_kernel<4><<<grid, fv::CGA_THREADS, smem, s>>>(ca); break;
+        }
       }
       FV_CUDA(cudaGetLastError());
     }
