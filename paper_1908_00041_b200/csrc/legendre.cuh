@@ -338,19 +338,51 @@ __device__ __forceinline__ void fwd_mtile_dmma(int kfirst, int nt0, double (&acc
 // (m ascending = work descending), which balances the per-order work (L+2-m).
 __device__ __forceinline__ int fwd_item(int k, int b, int G) { return (k & 1) ? k * G + (G - 1 - b) : k * G + b; }
 
-// Producer warp pw of a forward CTA: walks the CTA's orders / l-blocks / live chunks, fills
-// the pipeline stages (X tile by TMA bulk copy; Pbar tile by the recurrence, or by bulk copy
-// from the plan tables) and arrives on the stage's full barrier.  Shared by the forward
-// kernels (legendre_fwd_kernel, legendre_fwd1_kernel).
-template <int NT, bool SPLIT>
-__device__ __forceinline__ void fwd_producer(const FwdArgs& args, double* smem, uint64_t* full, uint64_t* empty,
-                                             volatile int* cons0, StageMeta* meta, double2* abw_all, double* st_p1,
-                                             double* st_p2, double* st_t, int* st_ls, int pw, int lane, int bxg,
-                                             int gdg) {
+template <int NT, bool SPLIT = false>
+__global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args) {
+  extern __shared__ __align__(128) double smem[];
   using SM = FwdSmem<NT>;
+  const int nPx = args.nchunks * FWD_RC;  // pairs covered by the forward chunks
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + FWD_STAGES * SM::STAGE);
+  uint64_t* empty = full + FWD_STAGES;
+  // consumer warp 0's count of finished tiles (the producers' aliasing guard)
+  volatile int* cons0 = reinterpret_cast<volatile int*>(empty + FWD_STAGES);
+  StageMeta* meta = reinterpret_cast<StageMeta*>(empty + FWD_STAGES + 2);
+  double2* abw_all = reinterpret_cast<double2*>(meta + FWD_STAGES);
+  double* st_p1 = reinterpret_cast<double*>(abw_all + kProducerWarps * FWD_LB);
+  double* st_p2 = st_p1 + nPx;
+  double* st_t = st_p2 + nPx;
+  int* st_ls = reinterpret_cast<int*>(st_t + nPx);
+
   const int Lt = args.Lt;
   const int nchunks = args.nchunks;
-  const int S = (SPLIT && args.ksplit > 1) ? args.ksplit : 1;
+  const int S = (SPLIT && args.ksplit > 1) ? args.ksplit : 1;  // compile-time 1 in the unsplit kernel
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  {  // field group of this CTA (blocks interleave the groups: heavy orders of every group first)
+    const int ng = args.ngroups > 0 ? args.ngroups : 1;
+    const int gi = blockIdx.x % ng;
+    args.X += gi * args.x_gstride;
+    args.F += gi * args.f_gstride;
+  }
+  const int bxg = blockIdx.x / (args.ngroups > 0 ? args.ngroups : 1);
+  const int gdg = gridDim.x / (args.ngroups > 0 ? args.ngroups : 1);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < FWD_STAGES; ++s) {
+      mbar_init(&full[s], 32);
+      mbar_init(&empty[s], 32 * kConsumerWarps);
+    }
+    *cons0 = 0;
+    fence_barrier_init();
+  }
+  unsigned long long gt0 = 0;
+  if (args.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
+  __syncthreads();
+
+  if (is_producer(warp)) {
+    // ------------------------------ producer ------------------------------
+    const int pw = producer_index(warp);
     double2* abw = abw_all + pw * FWD_LB;
     FwdState st{st_p1, st_p2, st_t, st_ls};
     const bool table = args.ptab != nullptr;
@@ -435,54 +467,6 @@ __device__ __forceinline__ void fwd_producer(const FwdArgs& args, double* smem, 
       }
       tbase = tb;
     }
-}
-
-
-template <int NT, bool SPLIT = false>
-__global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args) {
-  extern __shared__ __align__(128) double smem[];
-  using SM = FwdSmem<NT>;
-  const int nPx = args.nchunks * FWD_RC;  // pairs covered by the forward chunks
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + FWD_STAGES * SM::STAGE);
-  uint64_t* empty = full + FWD_STAGES;
-  // consumer warp 0's count of finished tiles (the producers' aliasing guard)
-  volatile int* cons0 = reinterpret_cast<volatile int*>(empty + FWD_STAGES);
-  StageMeta* meta = reinterpret_cast<StageMeta*>(empty + FWD_STAGES + 2);
-  double2* abw_all = reinterpret_cast<double2*>(meta + FWD_STAGES);
-  double* st_p1 = reinterpret_cast<double*>(abw_all + kProducerWarps * FWD_LB);
-  double* st_p2 = st_p1 + nPx;
-  double* st_t = st_p2 + nPx;
-  int* st_ls = reinterpret_cast<int*>(st_t + nPx);
-
-  const int Lt = args.Lt;
-  const int nchunks = args.nchunks;
-  const int S = (SPLIT && args.ksplit > 1) ? args.ksplit : 1;  // compile-time 1 in the unsplit kernel
-  const int warp = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  {  // field group of this CTA (blocks interleave the groups: heavy orders of every group first)
-    const int ng = args.ngroups > 0 ? args.ngroups : 1;
-    const int gi = blockIdx.x % ng;
-    args.X += gi * args.x_gstride;
-    args.F += gi * args.f_gstride;
-  }
-  const int bxg = blockIdx.x / (args.ngroups > 0 ? args.ngroups : 1);
-  const int gdg = gridDim.x / (args.ngroups > 0 ? args.ngroups : 1);
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < FWD_STAGES; ++s) {
-      mbar_init(&full[s], 32);
-      mbar_init(&empty[s], 32 * kConsumerWarps);
-    }
-    *cons0 = 0;
-    fence_barrier_init();
-  }
-  unsigned long long gt0 = 0;
-  if (args.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
-  __syncthreads();
-
-  if (is_producer(warp)) {
-    fwd_producer<NT, SPLIT>(args, smem, full, empty, cons0, meta, abw_all, st_p1, st_p2, st_t, st_ls,
-                            producer_index(warp), lane, bxg, gdg);
     return;
   }
 
