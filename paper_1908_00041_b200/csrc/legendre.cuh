@@ -370,8 +370,8 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < FWD_STAGES; ++s) {
-      mbar_init(&full[s], 32);
-      mbar_init(&empty[s], 32 * kConsumerWarps);
+      mbar_init(&full[s], (args.dbg & 32) ? 1 : 32);
+      mbar_init(&empty[s], (args.dbg & 32) ? kConsumerWarps : 32 * kConsumerWarps);
     }
     *cons0 = 0;
     fence_barrier_init();
@@ -460,7 +460,12 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
             if (!table && !(args.dbg & 2)) fwd_compute(args, st, tc, Ps, abw, m, j, nlb, p, l0, lane);
           }
           if (tr) args.trace[t * 8 + 2] = clock64() | ((long long)tc.zero << 62) | ((long long)tc.mixed << 61);
-          mbar_arrive(&full[stage]);
+          if (args.dbg & 32) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[stage]);
+          } else {
+            mbar_arrive(&full[stage]);
+          }
         }
         }
         tb += nu - u0;
@@ -536,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
           f.km0 = meta[stage].kmin[2 * kq];
           f.km1 = meta[stage].kmin[2 * kq + 1];
           f.live = !meta[stage].zero && !(args.dbg & 1);
-          if (f.live) {
+          if (f.live && !(args.dbg & 8)) {
 #pragma unroll
             for (int kk = 0; kk < 2; ++kk) {
               const int ks = 2 * kq + kk;
@@ -552,6 +557,19 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
         // started (kmin[ks] <= last row) and it is not padding past Lt; real branches
         auto mma = [&](const Frag& f) {
           if (!f.live) return;
+          if (l0 + 48 <= Lt && max(f.km0, f.km1) <= l0 + 15) {
+            // every M-tile runs both k-steps (all but the tiles on the polar-start boundary and
+            // the last l-block): one straight-line run.  A guarded mma.sync costs a WARPSYNC and
+            // a predicate wait per guard (ncu: as many stall samples as the DMMAs themselves)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+#pragma unroll
+              for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+                for (int jn = 0; jn < NT; ++jn) dmma_m8n8k4(acc[i][jn][0], acc[i][jn][1], f.a[kk][i], f.bb[kk][jn]);
+            }
+            return;
+          }
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const int r0 = l0 + 16 * i;
@@ -571,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
           if (args.trace && blockIdx.x == args.trace_cta && lane == 0 && cw == 0 && t < 4096)
             args.trace[t * 8 + 5] = clock64();  // DMMAs of tile t issued
 #endif
-          mbar_arrive(&empty[t % FWD_STAGES]);  // the fragments are in registers
+          if (!(args.dbg & 32) || lane == 0) mbar_arrive(&empty[t % FWD_STAGES]);  // the fragments are in registers
           if (cw == 0 && lane == 0) *cons0 = (int)t + 1;
         };
         // two register sets alternate: tile t + 1 is awaited and loaded into the
@@ -704,11 +722,18 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
           if (r0 <= Lt && kmin[ks] <= r0 + 15) kf0 = ks;
           if (r1 <= Lt && kmin[ks] <= r1 + 15) kf1 = ks;
         }
-        fwd_mtile_dmma<NTW, NT>(kf0, nt0, acc[0], a0, bb);
-        fwd_mtile_dmma<NTW, NT>(kf1, nt0, acc[1], a1, bb);
+        if (kf0 == 0 && kf1 == 0) {
+          // both M-tiles fully active (all but boundary tiles): one straight-line run, one
+          // convergence point instead of one per M-tile
+          fwd_mtile_run<0, NTW, NT>(nt0, acc[0], a0, bb);
+          fwd_mtile_run<0, NTW, NT>(nt0, acc[1], a1, bb);
+        } else {
+          fwd_mtile_dmma<NTW, NT>(kf0, nt0, acc[0], a0, bb);
+          fwd_mtile_dmma<NTW, NT>(kf1, nt0, acc[1], a1, bb);
+        }
       }
       if (tr) args.trace[t * 8 + 5] = clock64();
-      mbar_arrive(&empty[stage]);
+      if (!(args.dbg & 32) || lane == 0) mbar_arrive(&empty[stage]);
       if (cw == 0 && lane == 0) *cons0 = (int)t + 1;
     }
     tbase += nu - u0;
@@ -1086,6 +1111,16 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
           for (int jn = 0; jn < NT; ++jn) b[bufi][jn] = lds_f64(&Gs[((par * ADJ_KS + ks) * NT + jn) * 32 + lane]);
         };
         load(0, 0);
+        if (mt_start[0] <= l0s + 7 && l0s + 8 * (ADJ_KS - 1) <= Lt) {
+          // both M-tiles run every k-step (all but the stages on the polar-start boundary
+          // and the last degrees): one straight-line run without guarded mma.sync groups
+          // (each guard costs a WARPSYNC and a predicate wait)
+#pragma unroll
+          for (int t = 0; t < 2 * ADJ_KS; ++t) {
+            if (t + 1 < 2 * ADJ_KS) load(t + 1, (t + 1) & 1);
+            adj_ks_run<0, NT>(acc[t & 1], a[t & 1], b[t & 1]);
+          }
+        } else
 #pragma unroll
         for (int t = 0; t < 2 * ADJ_KS; ++t) {
           if (t + 1 < 2 * ADJ_KS) load(t + 1, (t + 1) & 1);
@@ -1206,6 +1241,16 @@ __device__ __forceinline__ void adj_consume(const double* Ps, const double* Gs, 
     for (int jn = 0; jn < NT; ++jn) b[bufi][jn] = lds_f64(&Gs[((par * ADJ_KS + ks) * NT + jn) * 32 + lane]);
   };
   load(0, 0);
+  if (mt_start[0] <= l0s + 7 && l0s + 8 * (ADJ_KS - 1) <= Lt) {
+    // both M-tiles run every k-step (all but the stages on the polar-start boundary and the
+    // last degrees): one straight-line run, no guarded mma.sync (WARPSYNC + predicate wait each)
+#pragma unroll
+    for (int t = 0; t < 2 * ADJ_KS; ++t) {
+      if (t + 1 < 2 * ADJ_KS) load(t + 1, (t + 1) & 1);
+      adj_ks_run<0, NT>(acc[t & 1], a[t & 1], b[t & 1]);
+    }
+    return;
+  }
 #pragma unroll
   for (int t = 0; t < 2 * ADJ_KS; ++t) {
     if (t + 1 < 2 * ADJ_KS) load(t + 1, (t + 1) & 1);
