@@ -5,6 +5,8 @@ Tolerance: relative l2 <= 1e-11 in float64 (BASELINE.json north_star);
 observed values are 1e-16..1e-13.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -736,3 +738,25 @@ def test_multi_group_launch_matches_single_fields():
         assert O.rel_l2(S[f].cpu().numpy(), Sf[0].cpu().numpy()) <= 1e-15
     ra, rb = O.vsht_forward_grid(T[6], th, w, nphi, L)
     assert O.rel_l2(np.concatenate([a[6].cpu().numpy(), b[6].cpu().numpy()]), np.concatenate([ra, rb])) <= TOL
+
+
+@pytest.mark.parametrize("L,B", [(33, 1), (100, 3), (257, 4)])
+def test_adjoint_cg_runs_of_orders_bitwise_equal_to_one_order_kernel(L, B, tmp_path):
+    """cg_adj_multi_kernel (runs of consecutive orders per CTA, the default) against
+    cg_adj_tile_kernel (FV_CGA_MULTI=0): the same cg_adj_merge arithmetic, so the adjoint
+    field must agree bitwise; the kernel choice is read once per process, hence two
+    processes (tools/stage_ab.py)."""
+    cuda_or_skip()
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for tag, env in (("multi", {}), ("tile", {"FV_CGA_MULTI": "0"})):
+        out = str(tmp_path / f"{tag}.npz")
+        r = subprocess.run([sys.executable, os.path.join(root, "tools", "stage_ab.py"), str(L), str(B), out, "1"],
+                           env={**os.environ, **env}, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(out))
+    for k in ("T", "fa", "fb"):
+        assert np.array_equal(outs[0][k], outs[1][k]), k
