@@ -9,6 +9,7 @@
 //   the reference (favest/coupling.py:39-78), so xi/mu are bitwise equal.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace fv {

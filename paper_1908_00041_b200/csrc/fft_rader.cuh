@@ -101,18 +101,18 @@ __device__ __forceinline__ void idft_prime_put(double2 (&v)[R], Store put) {
 }
 
 // shared-memory layout of one CTA: the ring, the tables, the index arrays
-template <int R, int P>
+template <int R, int P, int NRG = 1>
 struct RaderSmem {
   static constexpr int N = R * P, M = P - 1;
   static constexpr int NHI = (N + 127) / 128;
   static constexpr int TAB = 2 * M + 128 + NHI;  // double2 entries of RaderArgs::tab
-  static constexpr size_t bytes = (size_t)(N + TAB) * 16 + (size_t)(M + P) * 2;
-  double2* buf;
+  static constexpr size_t bytes = (size_t)(NRG * N + TAB) * 16 + (size_t)(M + P) * 2;
+  double2* buf;  // NRG rings of N
   const double2 *tw, *Bn, *lo, *hi;
   const short *sig, *inv;
   __device__ explicit RaderSmem(double2* base) {
     buf = base;
-    tw = base + N;
+    tw = base + NRG * N;
     Bn = tw + M;
     lo = Bn + M;
     hi = lo + 128;
@@ -124,9 +124,9 @@ struct RaderSmem {
 };
 
 // copy the tables (RaderArgs::tab, sig, inv) into shared memory
-template <int R, int P>
-__device__ __forceinline__ void rader_tables(const RaderSmem<R, P>& sm, const RaderArgs& a) {
-  using S = RaderSmem<R, P>;
+template <int R, int P, int NRG = 1>
+__device__ __forceinline__ void rader_tables(const RaderSmem<R, P, NRG>& sm, const RaderArgs& a) {
+  using S = RaderSmem<R, P, NRG>;
   double2* dt = const_cast<double2*>(sm.tw);
   for (int i = threadIdx.x; i < S::TAB; i += RD_T) dt[i] = __ldg(a.tab + i);
   short* di = const_cast<short*>(sm.sig);
@@ -135,13 +135,14 @@ __device__ __forceinline__ void rader_tables(const RaderSmem<R, P>& sm, const Ra
 
 // Rader DFTs of the R residues of one ring held in buf[n]; on exit slot q of
 // residue r (buf[r + R q]) holds X_r[q^-1] (q >= 1) and slot 0 holds X_r[0].
-template <int R, int P, int F1, int F2>
-__device__ __forceinline__ void rader_residues(const RaderSmem<R, P>& sm) {
-  double2* buf = sm.buf;
+template <int R, int P, int F1, int F2, int NRG = 1>
+__device__ __forceinline__ void rader_residues(const RaderSmem<R, P, NRG>& sm) {
   const short* sig = sm.sig;
   static_assert(F1 * F2 == P - 1, "P - 1 = F1 * F2");
   // pass 1: radix F1 over stride F2 (logical p = F2 n1 + n2), twiddle w^(n2 k1)
-  for (int it = threadIdx.x; it < R * F2; it += RD_T) {
+  for (int itg = threadIdx.x; itg < NRG * R * F2; itg += RD_T) {
+    const int it = NRG > 1 ? itg % (R * F2) : itg;
+    double2* buf = sm.buf + (NRG > 1 ? itg / (R * F2) : 0) * (R * P);
     const int r = it % R, n2 = it / R;
     double2 v[F1];
 #pragma unroll
@@ -155,7 +156,9 @@ __device__ __forceinline__ void rader_residues(const RaderSmem<R, P>& sm) {
   // pass 2: radix F2 over contiguous positions F2 k1 + k2 (frequency k1 + F1 k2),
   // times the transformed kernel, x_r[0] into the zero bin, then the first inverse
   // pass (radix F2, twiddle w^-(k1 j2)) in registers
-  for (int it = threadIdx.x; it < R * F1; it += RD_T) {
+  for (int itg = threadIdx.x; itg < NRG * R * F1; itg += RD_T) {
+    const int it = NRG > 1 ? itg % (R * F1) : itg;
+    double2* buf = sm.buf + (NRG > 1 ? itg / (R * F1) : 0) * (R * P);
     const int r = it % R, k1 = it / R;
     double2 v[F2];
     const short* sg = sig + F2 * k1;
@@ -184,7 +187,9 @@ __device__ __forceinline__ void rader_residues(const RaderSmem<R, P>& sm) {
   }
   __syncthreads();
   // pass 3: inverse radix F1 over stride F2: logical j = F2 j1 + j2 <- c[j] + x_r[0]
-  for (int it = threadIdx.x; it < R * F2; it += RD_T) {
+  for (int itg = threadIdx.x; itg < NRG * R * F2; itg += RD_T) {
+    const int it = NRG > 1 ? itg % (R * F2) : itg;
+    double2* buf = sm.buf + (NRG > 1 ? itg / (R * F2) : 0) * (R * P);
     const int r = it % R, j2 = it / R;
     double2 v[F1];
 #pragma unroll
@@ -194,10 +199,10 @@ __device__ __forceinline__ void rader_residues(const RaderSmem<R, P>& sm) {
 }
 
 // the R-point combine of output bin k: Y_r[k] from slot inv[k], twiddles w_n^{r k}
-template <int R, int P>
-__device__ __forceinline__ void rader_combine(const RaderSmem<R, P>& sm, int k, double2 (&y)[R]) {
+template <int R, int P, int NRG = 1>
+__device__ __forceinline__ void rader_combine(const RaderSmem<R, P, NRG>& sm, int k, double2 (&y)[R], int ring = 0) {
   const int q = sm.inv[k];
-  const double2* src = sm.buf + R * q;
+  const double2* src = sm.buf + ring * (R * P) + R * q;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     y[r] = src[r];
@@ -351,6 +356,123 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(RD_T, 1) rader_fold_
     }
   }
   cluster.sync();  // the partner may still read this CTA's spectrum
+}
+
+// ---------------------------------------------------------------------------
+// Short rings (C2: n_phi = 516 = 12 * 43, P - 1 = 7 * 6): NRG rings per CTA so the
+// passes fill the CTA (one ring has 72 / 84 butterflies and 43 combine bins for 384
+// threads), two CTAs per SM.  The forward variant takes ring PAIRS (north ring 2 i,
+// south ring 2 i + 1 of item i in the same CTA), so the fold needs no cluster.
+// Replaces the direct 43-point DFTs of fft_blue.cuh smallp_kernel (~2 P flops per
+// point, issue bound).
+// ---------------------------------------------------------------------------
+template <int R, int P, int F1, int F2, int NRG>
+__global__ void __launch_bounds__(RD_T, 2) rader_multi_fft_kernel(RaderArgs a) {
+  extern __shared__ __align__(16) double2 rd_smem[];
+  constexpr int N = R * P;
+  const RaderSmem<R, P, NRG> sm(rd_smem);
+  const int nitems = 3 * a.nrings, item0 = blockIdx.x * NRG;
+  auto ring_base = [&](int rg) {
+    return a.in_rblk ? (long long)(rg >> (31 - __clz(a.in_rblk))) * a.in_rs + (rg & (a.in_rblk - 1))
+                     : (long long)rg * a.in_rs;
+  };
+  const bool inv = a.inverse != 0;
+  rader_tables<R, P, NRG>(sm, a);
+#pragma unroll
+  for (int i = 0; i < NRG; ++i) {
+    const int item = min(item0 + i, nitems - 1);  // a short last CTA repeats its last ring (never stored)
+    rader_load<N>(sm.buf + i * N, a.in + (item % 3) * a.in_cs + ring_base(item / 3), a.in_es, inv);
+  }
+  __syncthreads();
+  rader_residues<R, P, F1, F2, NRG>(sm);
+  __syncthreads();
+  for (int w = threadIdx.x; w < NRG * P; w += RD_T) {
+    const int i = w / P, k = w - i * P, item = item0 + i;
+    if (item >= nitems) continue;
+    double2 y[R];
+    rader_combine<R, P, NRG>(sm, k, y, i);
+    double2* dst = a.out + (item % 3) * a.out_cs + (long long)(item / 3) * a.out_rs;
+#pragma unroll
+    for (int s = 0; s < R; ++s) dst[(long long)(k + P * s) * a.out_es] = make_double2(y[s].x, inv ? -y[s].y : y[s].y);
+  }
+}
+
+template <int R, int P, int F1, int F2, int NPR>
+__global__ void __launch_bounds__(RD_T, 2) rader_multi_fold_kernel(RaderArgs a, Fft2Args f, int nitems) {
+  extern __shared__ __align__(16) double2 rd_smem[];
+  constexpr int N = R * P, NRG = 2 * NPR;
+  static_assert(NRG * P <= RD_T, "one combine bin per thread");
+  const RaderSmem<R, P, NRG> sm(rd_smem);
+  const int item0 = blockIdx.x * NPR;
+  rader_tables<R, P, NRG>(sm, a);
+#pragma unroll
+  for (int i = 0; i < NPR; ++i) {
+    const int item = min(item0 + i, nitems - 1);
+    const int c = item % 3, b = (item / 3) % f.nfields, p = item / (3 * f.nfields);
+    const int rn = f.pair_n[p], rs = f.pair_s[p];
+    const double2* base = f.in + (long long)b * f.field_stride + c;
+    // an absent ring's buffer is transformed as it is and never read by the epilogue
+    if (rn >= 0) rader_load<N>(sm.buf + (2 * i) * N, base + (long long)rn * f.in_rs, f.in_es, false);
+    if (rs >= 0) rader_load<N>(sm.buf + (2 * i + 1) * N, base + (long long)rs * f.in_rs, f.in_es, false);
+  }
+  __syncthreads();
+  rader_residues<R, P, F1, F2, NRG>(sm);
+  __syncthreads();
+  {  // combine in place: every thread holds its bin's outputs across one barrier
+    const int w = threadIdx.x, i = w / P, k = w - i * P;
+    double2 y[R];
+    if (w < NRG * P) rader_combine<R, P, NRG>(sm, k, y, i);
+    __syncthreads();
+    if (w < NRG * P) {
+#pragma unroll
+      for (int s = 0; s < R; ++s) sm.buf[i * N + k + P * s] = y[s];
+    }
+  }
+  __syncthreads();
+  // epilogue (fft2.cuh fft_fold_kernel's): thread per (item, order m)
+  const size_t tile = (size_t)2 * 8 * f.NT * 32;
+  const size_t par_stride = (size_t)8 * f.NT * 32;
+  for (int w = threadIdx.x; w < NPR * (f.Lt + 1); w += RD_T) {
+    const int i = w / (f.Lt + 1), m = w - i * (f.Lt + 1), item = item0 + i;
+    if (item >= nitems) continue;
+    const int c = item % 3, b = (item / 3) % f.nfields, p = item / (3 * f.nfields);
+    const int rn = f.pair_n[p], rs = f.pair_s[p];
+    const int chunk = p >> 5, ks = (p >> 2) & 7, kq = p & 3;
+    const int col = 12 * b + 4 * c;
+    const size_t off = ((size_t)ks * f.NT + (col >> 3)) * 32 + ((col >> 2) & 1) * 16 + kq * 4;
+    const bool padcols = (b == f.nfields - 1) && c == 2 && ((12 * f.nfields) & 7) == 4;
+    const int pcol = 12 * f.nfields;
+    const size_t poff = ((size_t)ks * f.NT + (pcol >> 3)) * 32 + ((pcol >> 2) & 1) * 16 + kq * 4;
+    const double wn = rn >= 0 ? f.ring_w[rn] : 0.0;
+    const double ws = rs >= 0 ? f.ring_w[rs] : 0.0;
+    const double2* Sn = sm.buf + (2 * i) * N;
+    const double2* Ss = Sn + N;
+    double2 Ep = make_double2(0.0, 0.0), Em = Ep, Op = Ep, Om = Ep;
+    if (rn >= 0) {
+      const int bm = m ? N - m : 0;
+      const double2 np = Sn[m], nm = Sn[bm];
+      const double sg = (m & 1) ? -1.0 : 1.0;  // sigma_{-m} on the -m bin
+      if (rs >= 0) {
+        const double2 sp = Ss[m], sm2 = Ss[bm];
+        Ep = make_double2(wn * np.x + ws * sp.x, wn * np.y + ws * sp.y);
+        Op = make_double2(wn * np.x - ws * sp.x, wn * np.y - ws * sp.y);
+        Em = make_double2(sg * (wn * nm.x + ws * sm2.x), sg * (wn * nm.y + ws * sm2.y));
+        Om = make_double2(sg * (wn * nm.x - ws * sm2.x), sg * (wn * nm.y - ws * sm2.y));
+      } else {  // unpaired ring: both parities see the ring itself
+        Ep = Op = make_double2(wn * np.x, wn * np.y);
+        Em = Om = make_double2(sg * (wn * nm.x), sg * (wn * nm.y));
+      }
+      if (m == 0) Em = Om = make_double2(0.0, 0.0);
+    }
+    double* xt = f.X + ((size_t)m * f.nchunks + chunk) * tile;
+    st_global_v4(xt + off, Ep, Em);
+    st_global_v4(xt + par_stride + off, Op, Om);
+    if (padcols) {
+      const double2 z = make_double2(0.0, 0.0);
+      st_global_v4(xt + poff, z, z);
+      st_global_v4(xt + par_stride + poff, z, z);
+    }
+  }
 }
 
 }  // namespace fv

@@ -310,11 +310,20 @@ __global__ void __launch_bounds__(32 * kProducerWarps) ptab_fwd_kernel(FwdArgs a
 template <int KS0, int NTW, int NT>
 __device__ __forceinline__ void fwd_mtile_run(int nt0, double (&acc)[NTW][2], const double (&a)[8],
                                               const double (&bb)[8][NTW]) {
+  // odd NT: the second column half holds one n-tile fewer; two unguarded instantiations
+  // selected by one branch (a per-DMMA guard would make every mma.sync predicated)
+  auto run = [&](auto nj) {
 #pragma unroll
-  for (int ks = KS0; ks < 8; ++ks)
+    for (int ks = KS0; ks < 8; ++ks)
 #pragma unroll
-    for (int jn = 0; jn < NTW; ++jn)
-      if (nt0 + jn < NT) dmma_m8n8k4(acc[jn][0], acc[jn][1], a[ks], bb[ks][jn]);
+      for (int jn = 0; jn < decltype(nj)::value; ++jn) dmma_m8n8k4(acc[jn][0], acc[jn][1], a[ks], bb[ks][jn]);
+  };
+  if constexpr (NT % 2 == 0) {
+    run(std::integral_constant<int, NTW>{});
+  } else {
+    if (nt0 == 0) run(std::integral_constant<int, NTW>{});
+    else run(std::integral_constant<int, NTW - 1>{});
+  }
 }
 
 // DMMAs of one M-tile from its first active k-step on (switch = real branch)

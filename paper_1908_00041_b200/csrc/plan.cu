@@ -600,7 +600,13 @@ int setup_fft2(fvPlan* p) {
 // factor (> 19, which the radix kernels do not cover), every prime of R <= 19
 // Rader plans instantiated in fft_rader.cuh: (R, P, F1, F2) with P - 1 = F1 * F2,
 // F1 an odd prime with constant-bank roots, F2 a composite of dft<>.
-#define FV_RADER_PLANS(X) X(12, 683, 31, 22) /* 8196: L = 4096 */
+#define FV_RADER_PLANS(X)                  \
+  X(12, 683, 31, 22) /* 8196: L = 4096 */ \
+  X(12, 43, 7, 6)    /* 516: L = 256 */
+
+// rings of at most kRaderMultiMaxN points go kRaderMultiRings to a CTA (fft_rader.cuh
+// rader_multi_*_kernel: the forward takes kRaderMultiRings / 2 mirror pairs)
+constexpr int kRaderMultiMaxN = 1024, kRaderMultiRings = 4;
 
 template <class F>
 int rader_dispatch(int R, int P, F f) {
@@ -698,6 +704,13 @@ int setup_rader(fvPlan* p, int R, int P) {
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     FV_CUDA(cudaFuncSetAttribute(fv::rader_fold_kernel<R_, P_, F1_, F2_>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    if constexpr (R_ * P_ <= kRaderMultiMaxN) {  // short rings: several per CTA
+      constexpr int mbytes = (int)fv::RaderSmem<R_, P_, kRaderMultiRings>::bytes;
+      FV_CUDA(cudaFuncSetAttribute(fv::rader_multi_fft_kernel<R_, P_, F1_, F2_, kRaderMultiRings>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, mbytes));
+      FV_CUDA(cudaFuncSetAttribute(fv::rader_multi_fold_kernel<R_, P_, F1_, F2_, kRaderMultiRings / 2>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, mbytes));
+    }
     return FV_OK;
   }));
   p->rader_R = R;
@@ -727,7 +740,10 @@ int setup_blue(fvPlan* p) {
   if (P <= 19) return FV_OK;
   const int R = n / P;
   const long double PI_ = 3.141592653589793238462643383279502884L;
-  if (P <= fv::SMALLP_MAX && R <= 64 && !(env && std::string(env) == "rp")) {
+  // a Rader plan, where instantiated, replaces the direct small-prime DFTs (C2: forward
+  // FFT + fold 0.237 -> 0.183 ms, inverse 0.165 -> 0.109 ms); FV_FFT=smallp keeps them
+  const bool want_rader = rader_instantiated(R, P) && !(env && std::string(env) == "smallp");
+  if (P <= fv::SMALLP_MAX && R <= 64 && !(env && std::string(env) == "rp") && !want_rader) {
     // direct conjugate-pair DFTs in one CTA per ring (smallp_kernel)
     const int H = (P - 1) / 2;
     std::vector<double2> tab((size_t)n + R * R + H * (H + 1));
@@ -851,8 +867,14 @@ int ring_fft_rader(fvPlan* p, bool inverse, const double2* in, long long in_cs, 
   a.inverse = inverse ? 1 : 0;
   a.ahead = fft_prefetch_ahead();
   return rader_dispatch(p->rader_R, p->rader_P, [&](auto R_, auto P_, auto F1_, auto F2_) -> int {
-    fv::rader_fft_kernel<R_, P_, F1_, F2_>
-        <<<(unsigned)(3LL * nrings), fv::RD_T, fv::RaderSmem<R_, P_>::bytes, s>>>(a);
+    if constexpr (R_ * P_ <= kRaderMultiMaxN) {
+      const unsigned grid = (unsigned)((3LL * nrings + kRaderMultiRings - 1) / kRaderMultiRings);
+      fv::rader_multi_fft_kernel<R_, P_, F1_, F2_, kRaderMultiRings>
+          <<<grid, fv::RD_T, fv::RaderSmem<R_, P_, kRaderMultiRings>::bytes, s>>>(a);
+    } else {
+      fv::rader_fft_kernel<R_, P_, F1_, F2_>
+          <<<(unsigned)(3LL * nrings), fv::RD_T, fv::RaderSmem<R_, P_>::bytes, s>>>(a);
+    }
     FV_CUDA(cudaGetLastError());
     return FV_OK;
   });
@@ -948,9 +970,17 @@ int fft_fold(fvPlan* p, const double2* T, int b0, int nf, cudaStream_t s, double
     a.nfields = nf;
     a.Lt = p->Lt;
     a.ahead = fft_prefetch_ahead() / 2;
-    const unsigned grid = 2u * (unsigned)(p->nchunks * fv::FWD_RC * nf * 3);
+    const int nitems = p->nchunks * fv::FWD_RC * nf * 3;  // (pair, field, component)
     return rader_dispatch(p->rader_R, p->rader_P, [&](auto R_, auto P_, auto F1_, auto F2_) -> int {
-      fv::rader_fold_kernel<R_, P_, F1_, F2_><<<grid, fv::RD_T, fv::RaderSmem<R_, P_>::bytes, s>>>(p->rd_args, a);
+      if constexpr (R_ * P_ <= kRaderMultiMaxN) {
+        constexpr int NPR = kRaderMultiRings / 2;
+        fv::rader_multi_fold_kernel<R_, P_, F1_, F2_, NPR>
+            <<<(unsigned)((nitems + NPR - 1) / NPR), fv::RD_T, fv::RaderSmem<R_, P_, kRaderMultiRings>::bytes, s>>>(
+                p->rd_args, a, nitems);
+      } else {
+        fv::rader_fold_kernel<R_, P_, F1_, F2_>
+            <<<2u * (unsigned)nitems, fv::RD_T, fv::RaderSmem<R_, P_>::bytes, s>>>(p->rd_args, a);
+      }
       FV_CUDA(cudaGetLastError());
       return FV_OK;
     });

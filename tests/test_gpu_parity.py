@@ -605,13 +605,14 @@ def test_direct_forward_batch_determinism_and_edges():
 def test_ring_fft_against_numpy(nphi):
     """fv_ring_fft alone (the sharded building block) on random rings, both
     directions, against numpy's pocketfft (favest/scalar.py:149, :178); the
-    large-prime lengths also through the cuFFT sub-DFT path (FV_FFT=rp; 8196
-    defaults to the Rader kernels, 516 / 46 to the small-prime kernels)."""
+    large-prime lengths also through the cuFFT sub-DFT path (FV_FFT=rp) and the
+    direct small-prime kernels (FV_FFT=smallp); 8196 and 516 default to the Rader
+    kernels (516: several rings per CTA), 46 to the small-prime kernels."""
     import ctypes
     import os
 
     torch = cuda_or_skip()
-    for fft in ("", "rp"):
+    for fft in ("", "rp", "smallp"):
         os.environ["FV_FFT"] = fft
         try:
             _ring_fft_case(torch, nphi)
