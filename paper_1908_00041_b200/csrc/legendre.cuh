@@ -104,7 +104,9 @@ struct FwdArgs {
   const long long* dgofs;
   const double* pair_t;     // [nPpad] cos(theta) of the north ring of each pair
   int Lt, nP, nPpad, nchunks, m_begin;
-  int dbg;  // timing isolation (FV_DEBUG_MODE): 1 consumers skip MMAs, 2 producers skip the recurrence, 4 no adjoint epilogue
+  // timing isolation (FV_DEBUG_MODE): 1 consumers skip MMAs, 2 producers skip the recurrence, 4 no adjoint
+  // epilogue, 8 single-field consumers skip their fragment loads, 32 one elected mbarrier arrival per warp
+  int dbg;
   int m_count;  // orders m_begin .. m_begin + m_count - 1 (persistent CTAs walk them)
   long long* trace;  // optional pipeline timeline of CTA trace_cta (clock64 stamps), normally null
   int trace_cta;
