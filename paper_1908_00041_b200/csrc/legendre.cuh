@@ -128,6 +128,9 @@ struct FwdArgs {
   // adds them in split order
   int ksplit;
   double* Fx;
+  // legendre_fwd2_kernel: plan-time recurrence state (P_{l0-1}, P_{l0-2}) of every pair at every
+  // tile start (fseed_kernel), [tofs[m] + j * nchunks + c][lane]; null -> legendre_fwd_kernel
+  const double2* seed;
 };
 
 // chunk starts of one order held across the warp (chunk 32 g + lane in v[g])
@@ -778,6 +781,421 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
     ct[0] = (long long)gt0;
     ct[1] = (long long)gt1;
     ct[2] = smid;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward, single field, on the fly: two recurrence chains per producer lane
+// ---------------------------------------------------------------------------
+// With the guard-free consumers the single-field forward (C4) is bound by its producers:
+// a lane runs ONE dependent chain (one DFMA per degree on the chain) whose latency the
+// consumers' DMMAs stretch on the shared FP64 datapath (10 -> 20-30 cycles per step), and
+// the recurrence state carried from l-block to l-block ties every chunk to one warp and
+// takes 58 KB of shared memory.  Here the plan stores the state of every pair at every tile
+// start (fseed_kernel: 16 bytes per (order, l-block, pair), 4.4 GB at L = 4096, exactly the
+// carried state, so results are bitwise those of legendre_fwd_kernel).  Tiles are then
+// independent: no state in shared memory, EIGHT 24 KB stages, and a producer warp fills
+// TWO tiles at once (adjacent live chunks of one l-block), its lanes running the two
+// chains interleaved.  Warp pw owns the slots 2 pw, 2 pw + 1 for good (pairs are aligned
+// to even pipeline positions; an l-block with an odd live count gets one dummy zero tile),
+// so its parity waits are exact and the aliasing guard of legendre_fwd_kernel is gone.
+// Consumers are those of legendre_fwd_kernel's single-field path.
+constexpr int FWD2_STAGES = 8;
+
+template <int NT>
+struct Fwd2Smem {
+  static constexpr int XTILE = 2 * 8 * NT * 32;
+  static constexpr int STAGE = FWD_PTILE + XTILE;
+  static constexpr int KRED = 2 * 3 * 4 * NT * 2 * 32;  // k-quarter partial sums (as FwdSmem)
+  static constexpr size_t bytes = (size_t)FWD2_STAGES * STAGE * 8 + 2 * FWD2_STAGES * 8 +
+                                  FWD2_STAGES * sizeof(StageMeta) + kProducerWarps * FWD_LB * 16 + (size_t)KRED * 8;
+};
+
+// Plan time: the recurrence state of every pair at the start of every (l-block, chunk)
+// tile, walking the tiles exactly as the on-the-fly producer does (one CTA per order).
+__global__ void __launch_bounds__(32 * kProducerWarps) fseed_kernel(FwdArgs args, double2* seed) {
+  extern __shared__ __align__(128) double smem[];
+  const int nPx = args.nchunks * FWD_RC;
+  double* scratch = smem;  // [producer warp][FWD_PTILE]: the tiles themselves are not kept
+  double2* abw_all = reinterpret_cast<double2*>(scratch + kProducerWarps * FWD_PTILE);
+  FwdState st;
+  double* sp1 = reinterpret_cast<double*>(abw_all + kProducerWarps * FWD_LB);
+  st.p1 = sp1;
+  st.p2 = sp1 + nPx;
+  double* st_t = sp1 + 2 * nPx;
+  int* st_ls = reinterpret_cast<int*>(st_t + nPx);
+  st.t = st_t;
+  st.ls = st_ls;
+  const int m = args.m_begin + blockIdx.x;
+  const int nlb = (args.Lt + 1 - m + FWD_LB - 1) / FWD_LB;
+  for (int p = threadIdx.x; p < nPx; p += blockDim.x) {
+    st_t[p] = args.pair_t[p];
+    st_ls[p] = args.start_l[(size_t)m * args.nPpad + p];
+    st.p1[p] = 0.0;
+    st.p2[p] = 0.0;
+  }
+  __syncthreads();
+  const int pw = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2* abw = abw_all + pw * FWD_LB;
+  const long long base = args.tofs[m];
+  for (int j = 0; j < nlb; ++j) {
+    const int l0 = m + FWD_LB * j;
+    fwd_stage_coefs(abw, args, m, l0, lane);
+    for (int c = pw; c < args.nchunks; c += kProducerWarps) {
+      const long long tile = base + (long long)j * args.nchunks + c;
+      const int p = c * FWD_RC + lane;
+      const TileClass tc = fwd_classify(st, p, l0, lane);
+      seed[tile * 32 + lane] = make_double2(st.p1[p], st.p2[p]);
+      if (!tc.zero) fwd_compute(args, st, tc, scratch + pw * FWD_PTILE, abw, m, j, nlb, p, l0, lane);
+    }
+  }
+}
+
+// rows 0..63 of two tiles of one l-block at once (lane = the same pair slot in both
+// chunks): fwd_produce's arithmetic, the two chains interleaved
+__device__ __forceinline__ void fwd_produce2(double* PsA, double* PsB, const double2* dgw, double ttA, double ttB,
+                                             double a1, double a2, double b1, double b2, int lane) {
+  const int s = lane >> 2, q = lane & 3, sx = s & 3;
+  int off[8];
+#pragma unroll
+  for (int g = 0; g < 8; ++g) off[g] = s * 32 + q + ((g ^ sx) << 2);
+#pragma unroll
+  for (int b0 = 0; b0 < FWD_LB; b0 += 8) {
+    double dd[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dd[k] = dgw[b0 + k].x;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int idx = b0 + k;
+      const double va = fma(ttA, a1, -(dd[k] * a2));
+      const double vb = fma(ttB, b1, -(dd[k] * b2));
+      a2 = a1;
+      a1 = va;
+      b2 = b1;
+      b1 = vb;
+      const int par = idx & 1, rp = idx >> 1, i = rp >> 3, g = rp & 7;
+      const int o = off[g] + (par * 4 + i) * 8 * 32;
+      PsA[o] = va;
+      PsB[o] = vb;
+      if ((idx & 31) == 31) {
+        const double g1 = dgw[idx].y, g2 = dgw[idx - 1].y;
+        a1 *= g1;
+        a2 *= g2;
+        b1 *= g1;
+        b2 *= g2;
+      }
+    }
+  }
+}
+
+template <int NT, bool SPLIT = false>
+__global__ void __launch_bounds__(kThreads, 1) legendre_fwd2_kernel(FwdArgs args) {
+  static_assert(NT <= 2, "single-field forward");
+  extern __shared__ __align__(128) double smem[];
+  using SM = Fwd2Smem<NT>;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + FWD2_STAGES * SM::STAGE);
+  uint64_t* empty = full + FWD2_STAGES;
+  StageMeta* meta = reinterpret_cast<StageMeta*>(empty + FWD2_STAGES);
+  double2* abw_all = reinterpret_cast<double2*>(meta + FWD2_STAGES);
+  double* red_base = reinterpret_cast<double*>(abw_all + kProducerWarps * FWD_LB);
+
+  const int Lt = args.Lt;
+  const int nchunks = args.nchunks;
+  const int S = (SPLIT && args.ksplit > 1) ? args.ksplit : 1;  // compile-time 1 in the unsplit kernel
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  {
+    const int ng = args.ngroups > 0 ? args.ngroups : 1;
+    const int gi = blockIdx.x % ng;
+    args.X += gi * args.x_gstride;
+    args.F += gi * args.f_gstride;
+  }
+  const int bxg = blockIdx.x / (args.ngroups > 0 ? args.ngroups : 1);
+  const int gdg = gridDim.x / (args.ngroups > 0 ? args.ngroups : 1);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < FWD2_STAGES; ++s) {
+      mbar_init(&full[s], 32);
+      mbar_init(&empty[s], 32 * kConsumerWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (is_producer(warp)) {
+    // ------------------------------ producer ------------------------------
+    const int pw = producer_index(warp);
+    double2* abw = abw_all + pw * FWD_LB;
+    const uint64_t pol_last = l2_evict_last();
+    const int sA = 2 * pw, sB = 2 * pw + 1;  // this warp's stage slots
+    double* const PsA = smem + sA * SM::STAGE;
+    double* const PsB = smem + sB * SM::STAGE;
+    uint32_t tbase = 0;  // pipeline position of the l-block's first tile (always even)
+    for (int k = 0;; ++k) {
+      const int it = fwd_item(k, bxg, gdg);
+      if (it >= args.m_count * S) break;
+      const int item = it / S, split = it - item * S;
+      const int nu = (nchunks - split + S - 1) / S;  // this split's chunks c = split + S u
+      const int m = args.m_begin + item;
+      const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
+      const int* ls_m = args.start_l + (size_t)m * args.nPpad;
+      const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane, split, S);
+      for (int j = 0; j < nlb; ++j) {
+        const int l0 = m + FWD_LB * j;
+        const int u0 = first_live_chunk(cst, l0, nu);
+        const int npairs = (nu - u0 + 1) >> 1;
+        // pair q of the l-block sits at pipeline positions tbase + 2 q, + 1: owner ((tbase >> 1) + q) & 3
+        const int q0 = (pw - (int)(tbase >> 1)) & (kProducerWarps - 1);
+        if (q0 < npairs) fwd_stage_coefs(abw, args, m, l0, lane);
+        for (int q = q0; q < npairs; q += kProducerWarps) {
+          const int uA = u0 + 2 * q;
+          const bool hasB = uA + 1 < nu;  // an odd live count: the last pair's second tile is a dummy
+          const int cA = split + S * uA, cB = split + S * (uA + 1);
+          const int pA = cA * FWD_RC + lane, pB = cB * FWD_RC + lane;
+          const int lsA = __ldg(&ls_m[pA]);
+          const int lsB = hasB ? __ldg(&ls_m[pB]) : 0x7fffffff;
+          const long long tl = args.tofs[m] + (long long)j * nchunks;
+          const double2 sdA = __ldg(&args.seed[(tl + cA) * 32 + lane]);
+          const double2 sdB = hasB ? __ldg(&args.seed[(tl + cB) * 32 + lane]) : make_double2(0.0, 0.0);
+          const double ttA = __ldg(&args.pair_t[pA]);
+          const double ttB = hasB ? __ldg(&args.pair_t[pB]) : 0.0;
+          const TileClass tcA = fwd_classify_ls(lsA, l0);
+          TileClass tcB = fwd_classify_ls(lsB, l0);  // a dummy classifies as zero
+          const uint32_t round = (tbase + 2u * (uint32_t)q) / FWD2_STAGES;
+          mbar_wait(&empty[sA], (round & 1) ^ 1);
+          mbar_wait(&empty[sB], (round & 1) ^ 1);
+          if (lane == 0) {
+            meta[sA].zero = tcA.zero;
+            meta[sB].zero = tcB.zero;
+          }
+          if ((lane & 3) == 0) {
+            meta[sA].kmin[lane >> 2] = tcA.km;
+            meta[sB].kmin[lane >> 2] = tcB.km;
+          }
+          if (lane == 0) {
+            if (!tcA.zero) {
+              asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[sA])),
+                           "r"((uint32_t)(SM::XTILE * 8))
+                           : "memory");
+              bulk_g2s_hint(PsA + FWD_PTILE, args.X + ((size_t)(m - args.m_begin) * nchunks + cA) * SM::XTILE,
+                            SM::XTILE * 8, &full[sA], pol_last);
+            }
+            if (!tcB.zero) {
+              asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[sB])),
+                           "r"((uint32_t)(SM::XTILE * 8))
+                           : "memory");
+              bulk_g2s_hint(PsB + FWD_PTILE, args.X + ((size_t)(m - args.m_begin) * nchunks + cB) * SM::XTILE,
+                            SM::XTILE * 8, &full[sB], pol_last);
+            }
+          }
+          if (!(args.dbg & 2)) {
+            if (!tcA.zero && !tcB.zero && !tcA.mixed && !tcB.mixed) {
+              fwd_produce2(PsA, PsB, abw, ttA, ttB, sdA.x, sdA.y, sdB.x, sdB.y, lane);
+            } else {
+              // boundary tiles (a polar start inside the tile) and lone tiles: one chain at a time
+              auto one = [&](const TileClass& tc, double* Ps, int ls, int p, double tt, double2 sd) {
+                if (tc.zero) return;
+                Inject in;
+                in.ls = ls;
+                in.A = in.B = 0.0;
+                if (tc.mixed) {
+                  const double2 v = args.start_v[(size_t)m * args.nPpad + p];
+                  in.A = v.x;
+                  in.B = v.y;
+                }
+                double p1 = sd.x, p2 = sd.y;
+                if (tc.mixed) fwd_produce<true>(Ps, abw, tt, p1, p2, lane, l0, in);
+                else fwd_produce<false>(Ps, abw, tt, p1, p2, lane, l0, in);
+              };
+              one(tcA, PsA, lsA, pA, ttA, sdA);
+              one(tcB, PsB, lsB, pB, ttB, sdB);
+            }
+          }
+          mbar_arrive(&full[sA]);
+          mbar_arrive(&full[sB]);
+        }
+        tbase += 2u * (uint32_t)npairs;
+      }
+    }
+    return;
+  }
+
+  // -------------------------------- consumers --------------------------------
+  // (legendre_fwd_kernel's single-field consumers on eight stages)
+  // Single-field launches (NT <= 2: 12 columns): with the (parity, row half,
+  // column half) split below every warp would hold one n-tile, 1.5 fragment
+  // loads per DMMA, and the consumers become shared-memory-issue bound (C4:
+  // 30.7 of 32.7 ms with the recurrence switched off).  K-split instead: warp
+  // (par, kq) takes all four M-tiles x NT n-tiles of its parity over k-steps
+  // 2 kq, 2 kq + 1 (0.75 loads per DMMA); the four k-quarter partial sums are
+  // added in a fixed order (kq 0, 1, 2, 3) at each l-block's epilogue.
+  const int cw = consumer_index(warp);
+  const int par = cw >> 2, kq = cw & 3;
+  const int g = lane >> 2, q = lane & 3;
+  const int xq = (g >> 2) * 16 + q * 4 + (g & 3);
+  const int ncolF = 8 * NT;
+  double* red = red_base;
+  double acc[4][NT][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int jn = 0; jn < NT; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
+  uint32_t tbase = 0;
+  for (int k = 0;; ++k) {
+    const int it = fwd_item(k, bxg, gdg);
+    if (it >= args.m_count * S) break;
+    const int item = it / S, split = it - item * S;
+    const int nu = (nchunks - split + S - 1) / S;
+    double* const Fout = split ? args.Fx + (size_t)(split - 1) * args.f_gstride : args.F;
+    const int m = args.m_begin + item;
+    const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
+    const double2* dgm = args.dg + args.dgofs[m];
+    const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane, split, S);
+    for (int j = 0; j < nlb; ++j) {
+      const int l0 = m + FWD_LB * j;
+      const int u0 = first_live_chunk(cst, l0, nu);
+      // gamma of this warp's epilogue rows, loaded before the tiles (not after them)
+      double gam4[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int l = l0 + 2 * (8 * i + g) + par;
+        gam4[i] = (args.ptab || l > Lt) ? 1.0 : __ldg(&dgm[l - m].y);
+      }
+      // Tiles of the l-block software-pipelined by one: the DMMAs of tile t are
+      // issued, tile t is released, then tile t + 1 is awaited and its fragments
+      // loaded while those DMMAs execute (without this both consumer warps of an
+      // SMSP woke on the same barrier and loaded together, leaving the DMMA pipe
+      // idle for the load latency of every tile).
+      struct Frag {
+        double a[2][4], bb[2][NT];
+        int km0, km1;
+        bool live;
+      };
+      auto fetch = [&](uint32_t t, Frag& f) {
+        const int stage = t % FWD2_STAGES;
+#ifdef FV_TRACE_CONSUMERS
+        const bool tr = args.trace && blockIdx.x == args.trace_cta && lane == 0 && cw == 0 && t < 4096;
+        if (tr) args.trace[t * 8 + 3] = clock64();
+#endif
+        mbar_wait(&full[stage], (t / FWD2_STAGES) & 1);
+#ifdef FV_TRACE_CONSUMERS
+        if (tr) args.trace[t * 8 + 4] = clock64();
+#endif
+        const double* Ps = smem + stage * SM::STAGE;
+        const double* Xs = Ps + FWD_PTILE;
+        f.km0 = meta[stage].kmin[2 * kq];
+        f.km1 = meta[stage].kmin[2 * kq + 1];
+        f.live = !meta[stage].zero && !(args.dbg & 1);
+        if (f.live && !(args.dbg & 8)) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const int ks = 2 * kq + kk;
+            const int sw = ((g ^ (ks & 3)) << 2) + q;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) f.a[kk][i] = lds_f64(&Ps[((par * 4 + i) * 8 + ks) * 32 + sw]);
+#pragma unroll
+            for (int jn = 0; jn < NT; ++jn) f.bb[kk][jn] = lds_f64(&Xs[((par * 8 + ks) * NT + jn) * 32 + xq]);
+          }
+        }
+      };
+      // M-tile i (rows l0 + 16 i .. + 15) runs k-step ks once some pair of it has
+      // started (kmin[ks] <= last row) and it is not padding past Lt; real branches
+      auto mma = [&](const Frag& f) {
+        if (!f.live) return;
+        if (l0 + 48 <= Lt && max(f.km0, f.km1) <= l0 + 15) {
+          // every M-tile runs both k-steps (all but the tiles on the polar-start boundary and
+          // the last l-block): one straight-line run.  A guarded mma.sync costs a WARPSYNC and
+          // a predicate wait per guard (ncu: as many stall samples as the DMMAs themselves)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+              for (int jn = 0; jn < NT; ++jn) dmma_m8n8k4(acc[i][jn][0], acc[i][jn][1], f.a[kk][i], f.bb[kk][jn]);
+          }
+          return;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r0 = l0 + 16 * i;
+          if (r0 > Lt) continue;
+          if (f.km0 <= r0 + 15) {
+#pragma unroll
+            for (int jn = 0; jn < NT; ++jn) dmma_m8n8k4(acc[i][jn][0], acc[i][jn][1], f.a[0][i], f.bb[0][jn]);
+          }
+          if (f.km1 <= r0 + 15) {
+#pragma unroll
+            for (int jn = 0; jn < NT; ++jn) dmma_m8n8k4(acc[i][jn][0], acc[i][jn][1], f.a[1][i], f.bb[1][jn]);
+          }
+        }
+      };
+      auto release = [&](uint32_t t) {
+#ifdef FV_TRACE_CONSUMERS
+        if (args.trace && blockIdx.x == args.trace_cta && lane == 0 && cw == 0 && t < 4096)
+          args.trace[t * 8 + 5] = clock64();  // DMMAs of tile t issued
+#endif
+        mbar_arrive(&empty[t % FWD2_STAGES]);  // the fragments are in registers
+      };
+      // two register sets alternate: tile t + 1 is awaited and loaded into the
+      // other set while tile t's DMMAs execute
+      Frag f0, f1;
+      // an odd live count is padded with one dummy zero tile so that pairs never span l-blocks
+      const uint32_t tend = tbase + 2u * (uint32_t)((nu - u0 + 1) >> 1);
+      if (tbase < tend) fetch(tbase, f0);
+      for (uint32_t t = tbase; t < tend; t += 2) {
+        mma(f0);
+        release(t);
+        if (t + 1 >= tend) break;
+        fetch(t + 1, f1);
+        mma(f1);
+        release(t + 1);
+        if (t + 2 < tend) fetch(t + 2, f0);
+      }
+      tbase = tend;
+      // epilogue of the l-block: k-quarters 1..3 park their partial sums, quarter 0
+      // adds them in order and writes rows l = l0 + 2 (8 i + g) + par
+      double* rp = red + (size_t)(par * 3) * 4 * NT * 64;
+      if (kq > 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int jn = 0; jn < NT; ++jn) {
+            double* r = rp + (((kq - 1) * 4 + i) * NT + jn) * 64;
+            r[lane] = acc[i][jn][0];
+            r[32 + lane] = acc[i][jn][1];
+          }
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * kConsumerWarps) : "memory");
+      if (kq == 0) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int l = l0 + 2 * (8 * i + g) + par;
+          double v[NT][2];
+#pragma unroll
+          for (int jn = 0; jn < NT; ++jn) {
+            v[jn][0] = acc[i][jn][0];
+            v[jn][1] = acc[i][jn][1];
+#pragma unroll
+            for (int w = 0; w < 3; ++w) {
+              const double* r = rp + ((w * 4 + i) * NT + jn) * 64;
+              v[jn][0] += r[lane];
+              v[jn][1] += r[32 + lane];
+            }
+          }
+          if (l <= Lt) {
+            double* row = Fout + ((size_t)l * (l + 1) / 2 + m) * ncolF;
+            const double gam = gam4[i];  // P_l = gamma_l R_l
+#pragma unroll
+            for (int jn = 0; jn < NT; ++jn)
+              *reinterpret_cast<double2*>(row + jn * 8 + 2 * q) = make_double2(gam * v[jn][0], gam * v[jn][1]);
+          }
+        }
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * kConsumerWarps) : "memory");
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jn = 0; jn < NT; ++jn) acc[i][jn][0] = acc[i][jn][1] = 0.0;
+    }
   }
 }
 

@@ -113,6 +113,7 @@ struct fvPlan {
   long long* dgofs = nullptr;
   // table mode: plan-time Legendre tiles streamed by TMA instead of the on-the-fly producer
   double* ptab_f = nullptr;
+  double2* fseed = nullptr;   // legendre_fwd2_kernel: recurrence state at every forward tile start (fseed_tables)
   fv::StageMeta* mtab_f = nullptr;
   long long* tofs = nullptr;
   double* ptab_a = nullptr;
@@ -181,7 +182,7 @@ void free_plan(fvPlan* p) {
   cudaSetDevice(p->device);
   void* ptrs[] = {p->pair_t, p->pair_sin, p->pair_n, p->pair_s, p->ring_w, p->seed_x,
                   p->seed_e, p->start_l,  p->start_v, p->ab,   p->abofs,  p->gofs,
-                  p->dg,     p->dgofs,  p->cgt,     p->cga,     p->ptab_f,  p->mtab_f, p->tofs,   p->ptab_a, p->aofs,
+                  p->dg,     p->dgofs,  p->cgt,     p->cga,     p->ptab_f,  p->mtab_f, p->tofs,   p->ptab_a, p->aofs, p->fseed,
                   p->rowofs, p->Sf,       p->Sa,      p->X,    p->F,      p->Fx,     p->G,
                   p->seedk,  p->fitems,   p->Fpart,   p->blue_tab, p->blue_s1, p->cmin, p->cmin_a, p->Tp,
                   p->fft_tw, p->f2_tw};
@@ -288,6 +289,50 @@ int ptab_tables(fvPlan* p) {
   return FV_OK;
 }
 
+// On-the-fly plans (no Legendre tables: large L): the recurrence state of every pair at
+// every forward tile start, for the single-field forward with two chains per producer lane
+// (legendre.cuh legendre_fwd2_kernel).  16 bytes per (order, l-block, pair): 4.4 GB at
+// L = 4096; skipped past FV_FSEED_GB (default 16) or half of the free memory, and with
+// FV_FWD2=0.
+int fseed_tables(fvPlan* p) {
+  if (p->ptab_f) return FV_OK;
+  const char* en = std::getenv("FV_FWD2");
+  if (en && std::atoi(en) == 0) return FV_OK;
+  const char* gb = std::getenv("FV_FSEED_GB");
+  const double budget = (gb ? std::atof(gb) : 16.0) * 1e9;
+  const int Lt = p->Lt;
+  std::vector<long long> tofs(Lt + 2, 0);
+  for (int m = 0; m <= Lt; ++m)
+    tofs[m + 1] = tofs[m] + (long long)((Lt + 1 - m + fv::FWD_LB - 1) / fv::FWD_LB) * p->nchunks;
+  const size_t bytes = (size_t)tofs[Lt + 1] * 32 * sizeof(double2);
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  if ((double)bytes > budget || bytes > free_b / 2) return FV_OK;
+  const size_t smem = (size_t)fv::kProducerWarps * fv::FWD_PTILE * 8 + fv::kProducerWarps * fv::FWD_LB * 16 +
+                      (size_t)p->nchunks * fv::FWD_RC * 28;
+  if (smem > 227 * 1024) return FV_OK;
+  if (!p->tofs) {
+    FV_TRY(dalloc(&p->tofs, Lt + 1));
+    FV_CUDA(cudaMemcpy(p->tofs, tofs.data(), (Lt + 1) * 8, cudaMemcpyHostToDevice));
+  }
+  FV_TRY(dalloc(&p->fseed, (size_t)tofs[Lt + 1] * 32));
+  fv::FwdArgs fa{};
+  fa.start_l = p->start_l;
+  fa.start_v = p->start_v;
+  fa.dg = p->dg;
+  fa.dgofs = p->dgofs;
+  fa.pair_t = p->pair_t;
+  fa.Lt = Lt;
+  fa.nP = p->nP;
+  fa.nPpad = p->nPpad;
+  fa.nchunks = p->nchunks;
+  fa.tofs = p->tofs;
+  FV_CUDA(cudaFuncSetAttribute(fv::fseed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fv::fseed_kernel<<<Lt + 1, 32 * fv::kProducerWarps, smem>>>(fa, p->fseed);
+  FV_CUDA(cudaGetLastError());
+  return FV_OK;
+}
+
 cudaEvent_t next_event(fvPlan* p) {
   if (p->ev_used == p->ev_pool.size()) {
     cudaEvent_t e;
@@ -364,6 +409,24 @@ int launch_fwd(fvPlan* p, const fv::FwdArgs& args, int m_count, cudaStream_t s) 
   // ascending m (descending work) dynamically, which balances better than a static
   // persistent split
   const unsigned grid = (unsigned)(m_count * std::max(1, a2.ngroups) * std::max(1, a2.ksplit));
+  if constexpr (NT <= 2) {
+    // single field on the fly with plan-time seeds: two recurrence chains per producer lane
+    if (!a2.ptab && p->fseed) {
+      static std::atomic<unsigned long long> attr2{0}, attr2_split{0};
+      a2.seed = p->fseed;
+      a2.tofs = p->tofs;
+      const size_t b2 = fv::Fwd2Smem<NT>::bytes;
+      if (a2.ksplit > 1) {
+        FV_CUDA(smem_optin_once(&attr2_split, p->device, fv::legendre_fwd2_kernel<NT, true>));
+        fv::legendre_fwd2_kernel<NT, true><<<grid, fv::kThreads, b2, s>>>(a2);
+      } else {
+        FV_CUDA(smem_optin_once(&attr2, p->device, fv::legendre_fwd2_kernel<NT, false>));
+        fv::legendre_fwd2_kernel<NT, false><<<grid, fv::kThreads, b2, s>>>(a2);
+      }
+      FV_CUDA(cudaGetLastError());
+      return FV_OK;
+    }
+  }
   if (a2.ksplit > 1) {
     FV_CUDA(smem_optin_once(&attr_split, p->device, fv::legendre_fwd_kernel<NT, true>));
     fv::legendre_fwd_kernel<NT, true><<<grid, fv::kThreads, bytes, s>>>(a2);
@@ -1214,6 +1277,7 @@ int fv_plan_create_grid(fvPlan** out, int L, int n_theta, int n_phi, const doubl
     if (cudaGetLastError() != cudaSuccess) return bail(fail(FV_ECUDA, "chunk-start kernel launch failed"));
   }
   if ((rc = ptab_tables(p))) return bail(rc);
+  if ((rc = fseed_tables(p))) return bail(rc);
   // G layout tile offsets: nlc(m) = ceil((Lt+1-m)/ADJ_LC) tiles per order
   std::vector<long long> gofs(Lt + 2, 0);
   for (int m = 0; m <= Lt; ++m) gofs[m + 1] = gofs[m] + (Lt + 1 - m + fv::ADJ_LC - 1) / fv::ADJ_LC;
