@@ -761,3 +761,43 @@ def test_adjoint_cg_runs_of_orders_bitwise_equal_to_one_order_kernel(L, B, tmp_p
         outs.append(np.load(out))
     for k in ("T", "fa", "fb"):
         assert np.array_equal(outs[0][k], outs[1][k]), k
+
+
+@pytest.mark.parametrize("L", [300, 450])
+def test_seeded_single_field_forward_bitwise_and_split(L):
+    """legendre_fwd2_kernel (plans without Legendre tables: plan-time recurrence seeds, two
+    chains per producer lane, eight stages) against legendre_fwd_kernel (FV_FWD2=0): the seeds
+    are the state the one-chain producer carries, so the single-field forward agrees bitwise;
+    and its pair-chunk split instantiation (order-sharded launches with few orders) against
+    the single plan to rounding."""
+    torch = cuda_or_skip()
+    from paper_1908_00041_b200.dist import CudaStages, OrderShardedPlan, simulate_forward
+
+    th, w, nphi = O.gl_grid(L)
+    nth = len(th)
+    rng = np.random.default_rng(L)
+    a0, b0 = O.coef(rng, L, "inv")
+    plans = {}
+    for tag, env in (("seeded", {"FV_PTAB": "0"}), ("plain", {"FV_PTAB": "0", "FV_FWD2": "0"})):
+        os.environ.update(env)
+        try:
+            plans[tag] = _plan(L, th, w, nphi, B=1)
+        finally:
+            for k in env:
+                os.environ.pop(k, None)
+    T = plans["plain"].adjoint(_t(a0[None]), _t(b0[None]))
+    T = T + _t(O.tangent_noise(rng, O.grid_points(th, nphi), 0.1)[None])
+    fa, fb = plans["seeded"].forward(T)
+    ga, gb = plans["plain"].forward(T)
+    assert torch.equal(fa, ga) and torch.equal(fb, gb)
+    ra, rb = O.vsht_forward_grid(T[0].cpu().numpy(), th, w, nphi, L)
+    assert O.rel_l2(np.concatenate([fa[0].cpu().numpy(), fb[0].cpu().numpy()]), np.concatenate([ra, rb])) <= TOL
+    world = 4
+    sh = [OrderShardedPlan(CudaStages(plans["seeded"]), L, nth, nphi, 1, r, world, plans["seeded"].device, chunks=3)
+          for r in range(world)]
+    T4 = T.view(1, nth, nphi, 3)
+    Tl = [T4[:, p.me.rings[0]:p.me.rings[1]].reshape(1, -1, 3).contiguous() for p in sh]
+    for p, (a, b) in zip(sh, simulate_forward(sh, Tl)):
+        sel = p.order_mask(p.me.coef)
+        for x, ref in ((a, fa), (b, fb)):
+            assert O.rel_l2(x[:, sel].cpu().numpy(), ref[:, sel].cpu().numpy()) <= 1e-14
