@@ -154,12 +154,15 @@ __device__ __forceinline__ ChunkStarts load_chunk_starts(const int* cmin_m, int 
 }
 
 // first chunk of the l-block [l0, l0 + FWD_LB) with a started pair (chunks before it are all-zero tiles)
-__device__ __forceinline__ int first_live_chunk(const ChunkStarts& cs, int l0, int nchunks) {
+// (a pair that never starts has l_s = Lt + 1: the bound is clamped to Lt, or every chunk of an
+// order's last l-block, whose padding rows reach past Lt + 1, would count as live)
+__device__ __forceinline__ int first_live_chunk(const ChunkStarts& cs, int l0, int Lt, int nchunks) {
   if (cs.ng == 0) return 0;
+  const int lhi = min(l0 + FWD_LB - 1, Lt);
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
     if (g >= cs.ng) break;
-    const unsigned b = __ballot_sync(0xffffffffu, cs.v[g] <= l0 + FWD_LB - 1);
+    const unsigned b = __ballot_sync(0xffffffffu, cs.v[g] <= lhi);
     if (b) return min(32 * g + __ffs(b) - 1, nchunks);
   }
   return nchunks;
@@ -431,7 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       uint32_t tb = tbase;
       for (int j = 0; j < nlb; ++j) {
         const int l0 = m + FWD_LB * j;
-        const int u0 = first_live_chunk(cst, l0, nu);
+        const int u0 = first_live_chunk(cst, l0, Lt, nu);
         const int ufirst = u0 + ((pw - u0) & (kProducerWarps - 1));
         if (!table && ufirst < nu) fwd_stage_coefs(abw, args, m, l0, lane);
         for (int u = ufirst; u < nu; u += kProducerWarps) {
@@ -522,7 +525,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane, split, S);
       for (int j = 0; j < nlb; ++j) {
         const int l0 = m + FWD_LB * j;
-        const int u0 = first_live_chunk(cst, l0, nu);
+        const int u0 = first_live_chunk(cst, l0, Lt, nu);
         // gamma of this warp's epilogue rows, loaded before the tiles (not after them)
         double gam4[4];
 #pragma unroll
@@ -698,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
   const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane, split, S);
   for (int j = 0; j < nlb; ++j) {
     const int l0 = m + FWD_LB * j;
-    const int u0 = first_live_chunk(cst, l0, nu);
+    const int u0 = first_live_chunk(cst, l0, Lt, nu);
     for (int u = u0; u < nu; ++u) {
       const uint32_t t = tbase + (u - u0);
       const int stage = t % FWD_STAGES;
@@ -712,13 +715,23 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       const int4 km0 = *reinterpret_cast<const int4*>(&meta[stage].kmin[0]);
       const int4 km1 = *reinterpret_cast<const int4*>(&meta[stage].kmin[4]);
       const int kmin[8] = {km0.x, km0.y, km0.z, km0.w, km1.x, km1.y, km1.z, km1.w};
-      if (!meta[stage].zero && !(args.dbg & 1)) {
-        // all fragments of the tile first (unconditional loads, hoisted), then the
-        // DMMAs.  M-tile i = 2*mh + ii holds rows l0 + 16 i .. l0 + 16 i + 15 (one
-        // parity); its k-steps below the polar start form a prefix (pairs further
-        // from the pole start earlier) and M-tiles past Lt are padding, so each
-        // M-tile runs its DMMAs from its first active k-step on, selected with a
-        // real branch (a predicated-off DMMA still occupies the FP64 tensor pipe).
+      // M-tile i = 2*mh + ii holds rows l0 + 16 i .. l0 + 16 i + 15 (one parity); its
+      // k-steps below the polar start form a prefix (pairs further from the pole start
+      // earlier) and M-tiles past Lt are padding, so each M-tile runs its DMMAs from its
+      // first active k-step on.  A warp whose two M-tiles are both inactive (the rows past
+      // Lt of an order's last l-block, the polar-start boundary) skips the tile's fragment
+      // loads too: those tiles cost their 40 LDS.64 per warp and nothing else (traced: the
+      // one-row order m = Lt spent 1150 cycles per tile on them).
+      const int r0 = l0 + 32 * mh, r1 = r0 + 16;
+      int kf0 = 8, kf1 = 8;
+#pragma unroll
+      for (int ks = 7; ks >= 0; --ks) {
+        if (r0 <= Lt && kmin[ks] <= r0 + 15) kf0 = ks;
+        if (r1 <= Lt && kmin[ks] <= r1 + 15) kf1 = ks;
+      }
+      if (!meta[stage].zero && !(args.dbg & 1) && (kf0 < 8 || kf1 < 8)) {
+        // all fragments of the tile first (loads hoisted), then the DMMAs, selected with
+        // real branches (a predicated-off DMMA still occupies the FP64 tensor pipe)
         double a0[8], a1[8], bb[8][NTW];
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
@@ -728,13 +741,6 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
 #pragma unroll
           for (int jn = 0; jn < NTW; ++jn)
             bb[ks][jn] = (nt0 + jn < NT) ? lds_f64(&Xs[((par * 8 + ks) * NT + nt0 + jn) * 32 + xq]) : 0.0;
-        }
-        const int r0 = l0 + 32 * mh, r1 = r0 + 16;
-        int kf0 = 8, kf1 = 8;
-#pragma unroll
-        for (int ks = 7; ks >= 0; --ks) {
-          if (r0 <= Lt && kmin[ks] <= r0 + 15) kf0 = ks;
-          if (r1 <= Lt && kmin[ks] <= r1 + 15) kf1 = ks;
         }
         if (kf0 == 0 && kf1 == 0) {
           // both M-tiles fully active (all but boundary tiles): one straight-line run, one
@@ -941,7 +947,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd2_kernel(FwdArgs args
       const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane, split, S);
       for (int j = 0; j < nlb; ++j) {
         const int l0 = m + FWD_LB * j;
-        const int u0 = first_live_chunk(cst, l0, nu);
+        const int u0 = first_live_chunk(cst, l0, Lt, nu);
         const int npairs = (nu - u0 + 1) >> 1;
         // pair q of the l-block sits at pipeline positions tbase + 2 q, + 1: owner ((tbase >> 1) + q) & 3
         const int q0 = (pw - (int)(tbase >> 1)) & (kProducerWarps - 1);
@@ -1052,7 +1058,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd2_kernel(FwdArgs args
     const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane, split, S);
     for (int j = 0; j < nlb; ++j) {
       const int l0 = m + FWD_LB * j;
-      const int u0 = first_live_chunk(cst, l0, nu);
+      const int u0 = first_live_chunk(cst, l0, Lt, nu);
       // gamma of this warp's epilogue rows, loaded before the tiles (not after them)
       double gam4[4];
 #pragma unroll
