@@ -315,14 +315,14 @@ __global__ void __launch_bounds__(32 * kProducerWarps) ptab_fwd_kernel(FwdArgs a
   }
 }
 
-template <int KS0, int NTW, int NT>
+template <int KS0, int NTW, int NT, int KS1 = 8>
 __device__ __forceinline__ void fwd_mtile_run(int nt0, double (&acc)[NTW][2], const double (&a)[8],
                                               const double (&bb)[8][NTW]) {
   // odd NT: the second column half holds one n-tile fewer; two unguarded instantiations
   // selected by one branch (a per-DMMA guard would make every mma.sync predicated)
   auto run = [&](auto nj) {
 #pragma unroll
-    for (int ks = KS0; ks < 8; ++ks)
+    for (int ks = KS0; ks < KS1; ++ks)
 #pragma unroll
       for (int jn = 0; jn < decltype(nj)::value; ++jn) dmma_m8n8k4(acc[jn][0], acc[jn][1], a[ks], bb[ks][jn]);
   };
@@ -722,12 +722,22 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       // Lt of an order's last l-block, the polar-start boundary) skips the tile's fragment
       // loads too: those tiles cost their 40 LDS.64 per warp and nothing else (traced: the
       // one-row order m = Lt spent 1150 cycles per tile on them).
+      // The bound is clamped to Lt: padding pairs (the last chunk holds n_theta / 2 mod 32
+      // real pairs: ONE on the benchmark grids) and pairs that never start have l_s = Lt + 1.
+      // ke = 1: only k-step 0 is active (that last chunk), and only it is run.
       const int r0 = l0 + 32 * mh, r1 = r0 + 16;
-      int kf0 = 8, kf1 = 8;
+      const int h0 = min(r0 + 15, Lt), h1 = min(r1 + 15, Lt);
+      int kf0 = 8, kf1 = 8, ke0 = 0, ke1 = 0;
 #pragma unroll
       for (int ks = 7; ks >= 0; --ks) {
-        if (r0 <= Lt && kmin[ks] <= r0 + 15) kf0 = ks;
-        if (r1 <= Lt && kmin[ks] <= r1 + 15) kf1 = ks;
+        if (r0 <= Lt && kmin[ks] <= h0) {
+          kf0 = ks;
+          ke0 = max(ke0, ks + 1);
+        }
+        if (r1 <= Lt && kmin[ks] <= h1) {
+          kf1 = ks;
+          ke1 = max(ke1, ks + 1);
+        }
       }
       if (!meta[stage].zero && !(args.dbg & 1) && (kf0 < 8 || kf1 < 8)) {
         // all fragments of the tile first (loads hoisted), then the DMMAs, selected with
@@ -742,11 +752,15 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
           for (int jn = 0; jn < NTW; ++jn)
             bb[ks][jn] = (nt0 + jn < NT) ? lds_f64(&Xs[((par * 8 + ks) * NT + nt0 + jn) * 32 + xq]) : 0.0;
         }
-        if (kf0 == 0 && kf1 == 0) {
+        if (kf0 == 0 && kf1 == 0 && ke0 == 8 && ke1 == 8) {
           // both M-tiles fully active (all but boundary tiles): one straight-line run, one
           // convergence point instead of one per M-tile
           fwd_mtile_run<0, NTW, NT>(nt0, acc[0], a0, bb);
           fwd_mtile_run<0, NTW, NT>(nt0, acc[1], a1, bb);
+        } else if (max(ke0, ke1) == 1) {
+          // the padded last chunk: one real k-step
+          if (kf0 == 0) fwd_mtile_run<0, NTW, NT, 1>(nt0, acc[0], a0, bb);
+          if (kf1 == 0) fwd_mtile_run<0, NTW, NT, 1>(nt0, acc[1], a1, bb);
         } else {
           fwd_mtile_dmma<NTW, NT>(kf0, nt0, acc[0], a0, bb);
           fwd_mtile_dmma<NTW, NT>(kf1, nt0, acc[1], a1, bb);
@@ -1334,12 +1348,12 @@ __global__ void __launch_bounds__(32 * kProducerWarps) ptab_adj_kernel(AdjArgs a
 }
 
 // DMMAs of one (k-step, parity) for a consumer warp: M-tiles ii >= I0 of its two
-template <int I0, int NT>
+template <int I0, int NT, int I1 = 2>
 __device__ __forceinline__ void adj_ks_run(double (&acc)[2][NT][2], const double (&a)[2], const double (&b)[NT]) {
 #pragma unroll
   for (int jn = 0; jn < NT; ++jn)
 #pragma unroll
-    for (int ii = I0; ii < 2; ++ii) dmma_m8n8k4(acc[ii][jn][0], acc[ii][jn][1], a[ii], b[jn]);
+    for (int ii = I0; ii < I1; ++ii) dmma_m8n8k4(acc[ii][jn][0], acc[ii][jn][1], a[ii], b[jn]);
 }
 
 // Persistent: one CTA per SM walks the (order m, 128-pair chunk) items in
@@ -1530,7 +1544,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
       const double* Ps = smem + stage * SM::STAGE;
       const double* Gs = Ps + ADJ_PTILE;
       const int mts = min(mt_start[0], mt_start[1]);
-      if (!(args.dbg & 1) && mts <= l0s + ADJ_LC - 1 && l0s <= Lt) {
+      if (!(args.dbg & 1) && mts <= min(l0s + ADJ_LC - 1, Lt) && l0s <= Lt) {
         // half-steps t = (k-step ks = t / 2, parity t % 2), fragments double-buffered
         // in registers: the loads of half-step t + 1 are in flight while the DMMAs
         // of half-step t issue
@@ -1546,7 +1560,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
           for (int jn = 0; jn < NT; ++jn) b[bufi][jn] = lds_f64(&Gs[((par * ADJ_KS + ks) * NT + jn) * 32 + lane]);
         };
         load(0, 0);
-        if (mt_start[0] <= l0s + 7 && l0s + 8 * (ADJ_KS - 1) <= Lt) {
+        if (mt_start[0] <= l0s + 7 && mt_start[1] <= l0s + 7 && l0s + 8 * (ADJ_KS - 1) <= Lt) {
           // both M-tiles run every k-step (all but the stages on the polar-start boundary
           // and the last degrees): one straight-line run without guarded mma.sync groups
           // (each guard costs a WARPSYNC and a predicate wait)
@@ -1564,10 +1578,12 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
           // earlier); k-steps past Lt hold zero coefficient rows.  Real branches:
           // a predicated-off DMMA still occupies the pipe.
           const int ks = t >> 1, par = t & 1;
-          const int khi = l0s + 8 * ks + 7;
+          const int khi = min(l0s + 8 * ks + 7, Lt);  // never-started and padding pairs have l_s = Lt + 1
           if (l0s + 8 * ks <= Lt) {
-            if (mt_start[0] <= khi) adj_ks_run<0, NT>(acc[par], a[t & 1], b[t & 1]);
-            else if (mt_start[1] <= khi) adj_ks_run<1, NT>(acc[par], a[t & 1], b[t & 1]);
+            const bool on0 = mt_start[0] <= khi, on1 = mt_start[1] <= khi;
+            if (on0 && on1) adj_ks_run<0, NT>(acc[par], a[t & 1], b[t & 1]);
+            else if (on1) adj_ks_run<1, NT>(acc[par], a[t & 1], b[t & 1]);
+            else if (on0) adj_ks_run<0, NT, 1>(acc[par], a[t & 1], b[t & 1]);  // the padded last chunk
           }
         }
       }
@@ -1663,7 +1679,7 @@ __device__ __forceinline__ void adj_consume(const double* Ps, const double* Gs, 
                                             const int (&mt_start)[2], int l0s, int Lt, int cw, int g, int q,
                                             int lane) {
   const int mts = min(mt_start[0], mt_start[1]);
-  if (!(mts <= l0s + ADJ_LC - 1 && l0s <= Lt)) return;
+  if (!(mts <= min(l0s + ADJ_LC - 1, Lt) && l0s <= Lt)) return;
   double a[2][2], b[2][NT];
   auto load = [&](int t, int bufi) {
     const int ks = t >> 1, par = t & 1;
@@ -1676,7 +1692,7 @@ __device__ __forceinline__ void adj_consume(const double* Ps, const double* Gs, 
     for (int jn = 0; jn < NT; ++jn) b[bufi][jn] = lds_f64(&Gs[((par * ADJ_KS + ks) * NT + jn) * 32 + lane]);
   };
   load(0, 0);
-  if (mt_start[0] <= l0s + 7 && l0s + 8 * (ADJ_KS - 1) <= Lt) {
+  if (mt_start[0] <= l0s + 7 && mt_start[1] <= l0s + 7 && l0s + 8 * (ADJ_KS - 1) <= Lt) {
     // both M-tiles run every k-step (all but the stages on the polar-start boundary and the
     // last degrees): one straight-line run, no guarded mma.sync (WARPSYNC + predicate wait each)
 #pragma unroll
@@ -1690,10 +1706,12 @@ __device__ __forceinline__ void adj_consume(const double* Ps, const double* Gs, 
   for (int t = 0; t < 2 * ADJ_KS; ++t) {
     if (t + 1 < 2 * ADJ_KS) load(t + 1, (t + 1) & 1);
     const int ks = t >> 1, par = t & 1;
-    const int khi = l0s + 8 * ks + 7;
+    const int khi = min(l0s + 8 * ks + 7, Lt);  // never-started and padding pairs have l_s = Lt + 1
     if (l0s + 8 * ks <= Lt) {
-      if (mt_start[0] <= khi) adj_ks_run<0, NT>(acc[par], a[t & 1], b[t & 1]);
-      else if (mt_start[1] <= khi) adj_ks_run<1, NT>(acc[par], a[t & 1], b[t & 1]);
+      const bool on0 = mt_start[0] <= khi, on1 = mt_start[1] <= khi;
+      if (on0 && on1) adj_ks_run<0, NT>(acc[par], a[t & 1], b[t & 1]);
+      else if (on1) adj_ks_run<1, NT>(acc[par], a[t & 1], b[t & 1]);
+      else if (on0) adj_ks_run<0, NT, 1>(acc[par], a[t & 1], b[t & 1]);  // the padded last chunk
     }
   }
 }
