@@ -278,6 +278,8 @@ struct CgFwdArgs {
   int nsplit;
   const double* Fx;
   long long fx_stride;
+  // several 4-field groups in one launch (grid.z = group): F of group g at + g * fg_stride, fields b0 + 4 g ..
+  long long fg_stride;
 };
 
 // U = -x + i y, V = x + i y, W = z (favest/transforms.py:112) from the
@@ -370,12 +372,17 @@ __global__ void cg_fwd_kernel(CgFwdArgs a) {
 constexpr int CGF_THREADS = 256, CGF_MB = 32;
 __host__ __device__ constexpr int cgf_nt(int nf) { return (12 * nf + 7) / 8; }
 __host__ __device__ constexpr int cgf_rs(int nf) { return 4 * cgf_nt(nf) + 1; }  // odd double2 row stride
-template <int NF, bool SPLIT = false>
+template <int NF, bool SPLIT = false, bool GROUPS = false>
 __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
   constexpr int NV = 4 * cgf_nt(NF), RS = cgf_rs(NF), ROWS = CGF_MB + 2;
   const int l = blockIdx.y;
   const int m0 = (blockIdx.x + a.c_lo / CGF_MB) * CGF_MB;  // the grid starts at the first written block
   if (m0 > l) return;
+  // field group of this CTA (grid.z = 1: group 0); locals, not writes to the parameter struct
+  // (a mutated kernel parameter is copied out of the constant bank: +29 us at C3)
+  // (GROUPS instantiation only: the one-group kernel keeps its 80 registers and three CTAs per SM)
+  const double* const Fg = GROUPS ? a.F + blockIdx.z * a.fg_stride : a.F;
+  const int b0g = GROUPS ? a.b0 + 4 * blockIdx.z : a.b0;
   extern __shared__ __align__(16) double2 cgf_smem[];  // [3][ROWS][RS]
   constexpr int NE = 3 * ROWS * NV, PER = (NE + CGF_THREADS - 1) / CGF_THREADS;
   const int Lt = a.L + 1;
@@ -410,7 +417,7 @@ __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
       const int lp = l - 1 + i, mp = m0 - 1 + r;
       if (lp >= 0 && lp <= Lt && mp >= 0 && mp <= lp) {
         off[u] = (lp * (lp + 1) / 2 + mp) * NV + v;
-        x[u] = __ldg(reinterpret_cast<const double2*>(a.F) + off[u]);
+        x[u] = __ldg(reinterpret_cast<const double2*>(Fg) + off[u]);
       }
     }
   }
@@ -451,7 +458,7 @@ __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
   cg_fwd_combine(xs, fu_a, fu_b, fu_c, fv_a, fv_b, fv_c, fw_a, fw_b, fw_c, ca, cb);
   double ar = ca.x, ai = ca.y, br = cb.x, bi = cb.y;
   if (l == 0) ar = ai = br = bi = 0.0;  // favest/transforms.py:145-146
-  const size_t o = (size_t)(a.b0 + b) * K + (l * l + l + M);
+  const size_t o = (size_t)(b0g + b) * K + (l * l + l + M);
   a.A[o] = make_double2(ar, ai);
   a.Bc[o] = make_double2(br, bi);
 }
@@ -480,6 +487,9 @@ struct CgAdjArgs {
   int rows_mode;            // 0: DMMA fragment tiles (grid path), 1: plain rows (points path)
   const double* cga;        // cg_adj_tile_kernel: factors in G-row order ((i * 2 + sign) * nrow + row)
   long long nrow;
+  // cg_adj_multi_kernel, several 4-field groups in one launch (grid.z = group): G of group g at
+  // + g * gg_stride, fields b0 + 4 g ..
+  long long gg_stride;
 };
 
 // cgt -> G-row order: row (gofs[|m|] + chunk) * 32 + idx holds degree
@@ -699,6 +709,9 @@ __global__ void __launch_bounds__(CGA_THREADS) cg_adj_multi_kernel(CgAdjArgs a, 
   const int am0 = a.m_begin + o0;
   const int c = blockIdx.x;
   if (c * LC >= Lt + 1 - am0) return;
+  // field group of this CTA (grid.z = 1: group 0); locals, not writes to the parameter struct
+  double* const Gg = a.G + blockIdx.z * a.gg_stride;
+  const int b0g = a.b0 + 4 * blockIdx.z;
   const int no = min(NO, m_count - o0);
   extern __shared__ __align__(16) double cgm_smem[];
   double* Gs = cgm_smem;                                          // [2][GBUF]
@@ -714,7 +727,7 @@ __global__ void __launch_bounds__(CGA_THREADS) cg_adj_multi_kernel(CgAdjArgs a, 
     const int lp = lp0 + r;
     const int mp = j < NC ? am0 - 1 + j : -(am0 + NO) + (j - NC);
     const bool ok = lp >= 0 && lp <= a.L && abs(mp) <= lp;
-    const size_t o = ok ? (size_t)(a.b0 + bb) * K + (lp * lp + lp + mp) : 0;
+    const size_t o = ok ? (size_t)(b0g + bb) * K + (lp * lp + lp + mp) : 0;
     cgs_cp16(&As[(bb * R + r) * CS + j], a.A + o, ok);
     cgs_cp16(&Bs[(bb * R + r) * CS + j], a.Bc + o, ok);
   }
@@ -768,7 +781,7 @@ __global__ void __launch_bounds__(CGA_THREADS) cg_adj_multi_kernel(CgAdjArgs a, 
       put(n0 + 8, sig * gz.x); put(n0 + 9, sig * gz.y);
     }
     __syncthreads();
-    double2* dst = reinterpret_cast<double2*>(a.G + (size_t)(a.gofs[am] + c) * TILE);
+    double2* dst = reinterpret_cast<double2*>(Gg + (size_t)(a.gofs[am] + c) * TILE);
     constexpr int BH = NT * 16;  // double2 per block
     for (int i = threadIdx.x; i < TILE / 2; i += CGA_THREADS) {
       const int blk = i / BH, oo = i - blk * BH;

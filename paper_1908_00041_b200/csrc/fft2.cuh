@@ -76,6 +76,10 @@ struct Fft2Args {
   long long field_stride;            // complex units between fields of the input
   int nchunks, NT, nfields, Lt;
   int ahead;                         // L2 prefetch of the input of item blockIdx.x + ahead (0: off)
+  // rader_multi_fold_kernel: nfields spans several groups of gfields fields, the X of group g at
+  // + g * x_gstride (0: one group)
+  int gfields;
+  long long x_gstride;
 };
 
 // cp.async.bulk.prefetch.L2: one instruction per contiguous block (16-byte

@@ -435,13 +435,16 @@ __global__ void __launch_bounds__(RD_T, 2) rader_multi_fold_kernel(RaderArgs a, 
   for (int w = threadIdx.x; w < NPR * (f.Lt + 1); w += RD_T) {
     const int i = w / (f.Lt + 1), m = w - i * (f.Lt + 1), item = item0 + i;
     if (item >= nitems) continue;
-    const int c = item % 3, b = (item / 3) % f.nfields, p = item / (3 * f.nfields);
+    const int c = item % 3, bg = (item / 3) % f.nfields, p = item / (3 * f.nfields);
+    const int nfg = f.gfields ? f.gfields : f.nfields;  // fields per X buffer
+    const int b = bg % nfg;
+    double* const X = f.X + (size_t)(bg / nfg) * f.x_gstride;
     const int rn = f.pair_n[p], rs = f.pair_s[p];
     const int chunk = p >> 5, ks = (p >> 2) & 7, kq = p & 3;
     const int col = 12 * b + 4 * c;
     const size_t off = ((size_t)ks * f.NT + (col >> 3)) * 32 + ((col >> 2) & 1) * 16 + kq * 4;
-    const bool padcols = (b == f.nfields - 1) && c == 2 && ((12 * f.nfields) & 7) == 4;
-    const int pcol = 12 * f.nfields;
+    const bool padcols = (b == nfg - 1) && c == 2 && ((12 * nfg) & 7) == 4;
+    const int pcol = 12 * nfg;
     const size_t poff = ((size_t)ks * f.NT + (pcol >> 3)) * 32 + ((pcol >> 2) & 1) * 16 + kq * 4;
     const double wn = rn >= 0 ? f.ring_w[rn] : 0.0;
     const double ws = rs >= 0 ? f.ring_w[rs] : 0.0;
@@ -464,7 +467,7 @@ __global__ void __launch_bounds__(RD_T, 2) rader_multi_fold_kernel(RaderArgs a, 
       }
       if (m == 0) Em = Om = make_double2(0.0, 0.0);
     }
-    double* xt = f.X + ((size_t)m * f.nchunks + chunk) * tile;
+    double* xt = X + ((size_t)m * f.nchunks + chunk) * tile;
     st_global_v4(xt + off, Ep, Em);
     st_global_v4(xt + par_stride + off, Op, Om);
     if (padcols) {

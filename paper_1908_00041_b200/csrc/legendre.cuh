@@ -376,12 +376,12 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
   const int S = (SPLIT && args.ksplit > 1) ? args.ksplit : 1;  // compile-time 1 in the unsplit kernel
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  {  // field group of this CTA (blocks interleave the groups: heavy orders of every group first)
-    const int ng = args.ngroups > 0 ? args.ngroups : 1;
-    const int gi = blockIdx.x % ng;
-    args.X += gi * args.x_gstride;
-    args.F += gi * args.f_gstride;
-  }
+  // field group of this CTA (blocks interleave the groups: heavy orders of every group first);
+  // locals, not writes to the kernel parameter struct (a mutated parameter is copied out of the
+  // constant bank)
+  const int gi_ = blockIdx.x % (args.ngroups > 0 ? args.ngroups : 1);
+  const double* const Xg = args.X + gi_ * args.x_gstride;
+  double* const Fg = args.F + gi_ * args.f_gstride;
   const int bxg = blockIdx.x / (args.ngroups > 0 ? args.ngroups : 1);
   const int gdg = gridDim.x / (args.ngroups > 0 ? args.ngroups : 1);
 
@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
                            : "memory");
               // X chunks are re-read by every l-block of the order: keep them in L2;
               // the table tiles are read once: let them go first
-              bulk_g2s_hint(Xs, args.X + ((size_t)(m - args.m_begin) * nchunks + c) * SM::XTILE, SM::XTILE * 8,
+              bulk_g2s_hint(Xs, Xg + ((size_t)(m - args.m_begin) * nchunks + c) * SM::XTILE, SM::XTILE * 8,
                             &full[stage], pol_last);
               if (table) {
                 const long long tile = args.tofs[m] + tl;
@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
       if (it >= args.m_count * S) break;
       const int item = it / S, split = it - item * S;
       const int nu = (nchunks - split + S - 1) / S;
-      double* const Fout = split ? args.Fx + (size_t)(split - 1) * args.f_gstride : args.F;
+      double* const Fout = split ? args.Fx + (size_t)(split - 1) * args.f_gstride : Fg;
       const int m = args.m_begin + item;
       const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
       const double2* dgm = args.dg + args.dgofs[m];
@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd_kernel(FwdArgs args)
   if (it >= args.m_count * S) break;
   const int item = it / S, split = it - item * S;
   const int nu = (nchunks - split + S - 1) / S;
-  double* const Fout = split ? args.Fx + (size_t)(split - 1) * args.f_gstride : args.F;
+  double* const Fout = split ? args.Fx + (size_t)(split - 1) * args.f_gstride : Fg;
   const int m = args.m_begin + item;
   const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
   const ChunkStarts cst = load_chunk_starts(args.cmin + (size_t)m * nchunks, nchunks, lane, split, S);
@@ -924,12 +924,12 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd2_kernel(FwdArgs args
   const int S = (SPLIT && args.ksplit > 1) ? args.ksplit : 1;  // compile-time 1 in the unsplit kernel
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  {
-    const int ng = args.ngroups > 0 ? args.ngroups : 1;
-    const int gi = blockIdx.x % ng;
-    args.X += gi * args.x_gstride;
-    args.F += gi * args.f_gstride;
-  }
+  // field group of this CTA (blocks interleave the groups: heavy orders of every group first);
+  // locals, not writes to the kernel parameter struct (a mutated parameter is copied out of the
+  // constant bank)
+  const int gi_ = blockIdx.x % (args.ngroups > 0 ? args.ngroups : 1);
+  const double* const Xg = args.X + gi_ * args.x_gstride;
+  double* const Fg = args.F + gi_ * args.f_gstride;
   const int bxg = blockIdx.x / (args.ngroups > 0 ? args.ngroups : 1);
   const int gdg = gridDim.x / (args.ngroups > 0 ? args.ngroups : 1);
   if (threadIdx.x == 0) {
@@ -996,14 +996,14 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd2_kernel(FwdArgs args
               asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[sA])),
                            "r"((uint32_t)(SM::XTILE * 8))
                            : "memory");
-              bulk_g2s_hint(PsA + FWD_PTILE, args.X + ((size_t)(m - args.m_begin) * nchunks + cA) * SM::XTILE,
+              bulk_g2s_hint(PsA + FWD_PTILE, Xg + ((size_t)(m - args.m_begin) * nchunks + cA) * SM::XTILE,
                             SM::XTILE * 8, &full[sA], pol_last);
             }
             if (!tcB.zero) {
               asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[sB])),
                            "r"((uint32_t)(SM::XTILE * 8))
                            : "memory");
-              bulk_g2s_hint(PsB + FWD_PTILE, args.X + ((size_t)(m - args.m_begin) * nchunks + cB) * SM::XTILE,
+              bulk_g2s_hint(PsB + FWD_PTILE, Xg + ((size_t)(m - args.m_begin) * nchunks + cB) * SM::XTILE,
                             SM::XTILE * 8, &full[sB], pol_last);
             }
           }
@@ -1065,7 +1065,7 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_fwd2_kernel(FwdArgs args
     if (it >= args.m_count * S) break;
     const int item = it / S, split = it - item * S;
     const int nu = (nchunks - split + S - 1) / S;
-    double* const Fout = split ? args.Fx + (size_t)(split - 1) * args.f_gstride : args.F;
+    double* const Fout = split ? args.Fx + (size_t)(split - 1) * args.f_gstride : Fg;
     const int m = args.m_begin + item;
     const int nlb = (Lt + 1 - m + FWD_LB - 1) / FWD_LB;
     const double2* dgm = args.dg + args.dgofs[m];

@@ -1016,7 +1016,9 @@ int ring_fft2_raw(fvPlan* p, bool inverse, const double2* in, long long in_cs, l
 }
 
 // fused forward FFT + fold of fields b0 .. b0 + nf - 1 of T (B, N, 3) into X (all orders)
-int fft_fold(fvPlan* p, const double2* T, int b0, int nf, cudaStream_t s, double* X) {
+// (ngroups > 1: that many full 4-field groups in one launch, X buffers x_gstride apart; only the
+// several-rings-per-CTA Rader kernel takes it, see fft_fold_groups)
+int fft_fold(fvPlan* p, const double2* T, int b0, int nf, cudaStream_t s, double* X, int ngroups = 1) {
   fv::Fft2Args a{};
   if (p->rader) {  // Rader ring DFT, north / south ring of a pair on a two-CTA cluster (fft_rader.cuh)
     const long long n = p->n_phi;
@@ -1030,10 +1032,12 @@ int fft_fold(fvPlan* p, const double2* T, int b0, int nf, cudaStream_t s, double
     a.ring_w = p->ring_w;
     a.nchunks = p->nchunks;
     a.NT = ntiles_for(nf);
-    a.nfields = nf;
+    a.nfields = nf * ngroups;
+    a.gfields = ngroups > 1 ? nf : 0;
+    a.x_gstride = (long long)p->x_gstride;
     a.Lt = p->Lt;
     a.ahead = fft_prefetch_ahead() / 2;
-    const int nitems = p->nchunks * fv::FWD_RC * nf * 3;  // (pair, field, component)
+    const int nitems = p->nchunks * fv::FWD_RC * nf * ngroups * 3;  // (pair, field, component)
     return rader_dispatch(p->rader_R, p->rader_P, [&](auto R_, auto P_, auto F1_, auto F2_) -> int {
       if constexpr (R_ * P_ <= kRaderMultiMaxN) {
         constexpr int NPR = kRaderMultiRings / 2;
@@ -1436,11 +1440,12 @@ int check_grid_call(fvPlan* p, int B, const void* x, const void* y, const void* 
 // CG assembly (favest/transforms.py:120-146) of coefficient orders [c_lo, c_hi) of fields
 // b0 .. b0 + nf - 1 from the forward Legendre rows in p->F (ncol = 8 NT)
 int cg_forward(fvPlan* p, double* a, double* b, int B, int b0, int nf, int NT, int c_lo, int c_hi, cudaStream_t s,
-               const double* F = nullptr, int nsplit = 1, const double* Fx = nullptr) {
+               const double* F = nullptr, int nsplit = 1, const double* Fx = nullptr, int ngroups = 1) {
   StageMark mk(p, 3, s);
   fv::CgFwdArgs ca{F ? F : p->F, reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), p->cgt, p->L, 8 * NT, B, b0,
-                   nf, c_lo, c_hi, nsplit, nsplit > 1 ? Fx : nullptr, (long long)p->f_gstride};
-  dim3 grid((c_hi + fv::CGF_MB - 1) / fv::CGF_MB - c_lo / fv::CGF_MB, p->L + 1);
+                   nf, c_lo, c_hi, nsplit, nsplit > 1 ? Fx : nullptr, (long long)p->f_gstride, (long long)p->f_gstride};
+  // ngroups full 4-field groups (F buffers f_gstride apart) in one launch: grid.z
+  dim3 grid((c_hi + fv::CGF_MB - 1) / fv::CGF_MB - c_lo / fv::CGF_MB, p->L + 1, ngroups);
   const size_t smem = (size_t)3 * (fv::CGF_MB + 2) * fv::cgf_rs(nf) * sizeof(double2);
   auto go = [&](auto split) {
     constexpr bool SP = decltype(split)::value;
@@ -1451,8 +1456,13 @@ int cg_forward(fvPlan* p, double* a, double* b, int B, int b0, int nf, int NT, i
       default: fv::cg_fwd_tile_kernel<4, SP><<<grid, fv::CGF_THREADS, smem, s>>>(ca); break;
     }
   };
-  if (nsplit > 1) go(std::true_type{});
-  else go(std::false_type{});
+  if (ngroups > 1 && nsplit == 1 && nf == 4) {
+    fv::cg_fwd_tile_kernel<4, false, true><<<grid, fv::CGF_THREADS, smem, s>>>(ca);
+  } else {
+    if (ngroups > 1) return fail(FV_EINVAL, "grouped forward CG launches take full 4-field groups without splits");
+    if (nsplit > 1) go(std::true_type{});
+    else go(std::false_type{});
+  }
   FV_CUDA(cudaGetLastError());
   return FV_OK;
 }
@@ -1501,6 +1511,9 @@ int fwd_group_cap(const fvPlan* p) {
   return 1;
 }
 
+// the several-rings-per-CTA Rader fold kernel takes all groups of a launch at once
+bool fft_fold_groups(const fvPlan* p) { return p->rader && p->rader_R * p->rader_P <= kRaderMultiMaxN; }
+
 int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* a, double* b, int B, int m_lo,
                    int m_hi, int c_lo, int c_hi, cudaStream_t s, const double2* Tfield = nullptr,
                    const ScalarIO* sio = nullptr) {
@@ -1522,6 +1535,11 @@ int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* 
         dim3 grid((p->nchunks * fv::FWD_RC + 127) / 128, mc, 3 * nf + 1);
         fv::fold_fwd_kernel<<<grid, 128, 0, s>>>(fa);
         FV_CUDA(cudaGetLastError());
+      } else if (ng > 1 && fft_fold_groups(p)) {  // all groups in one launch
+        if (g == 0) {
+          StageMark mk(p, 0, s);
+          FV_TRY(fft_fold(p, Tfield, b0, nf, s, p->X, ng));
+        }
       } else {  // fused FFT + fold straight from the field (fft2.cuh / fft_blue.cuh)
         StageMark mk(p, 0, s);
         FV_TRY(fft_fold(p, Tfield, bg, nf, s, Xg));
@@ -1544,8 +1562,7 @@ int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* 
         FV_TRY(scalar_unpack(*sio, p->F + (size_t)g * p->f_gstride, NT, b0 + 4 * g, nf, Lt, s));
       }
     else if (c_hi > c_lo)
-      for (int g = 0; g < ng; ++g)
-        FV_TRY(cg_forward(p, a, b, B, b0 + 4 * g, nf, NT, c_lo, c_hi, s, p->F + (size_t)g * p->f_gstride, ks, p->Fx));
+      FV_TRY(cg_forward(p, a, b, B, b0, nf, NT, c_lo, c_hi, s, p->F, ks, p->Fx, ng));
     b0 += ng > 1 ? 4 * ng : nf;
   }
   return FV_OK;
@@ -1569,22 +1586,23 @@ int adjoint_orders(fvPlan* p, const double* a, const double* b, double2* S, cons
       fv::scalar_pack_kernel<<<grid, 32, 0, s>>>(sa);
       FV_CUDA(cudaGetLastError());
     }
-    for (int g = 0; g < ng && !sio; ++g) {
+    static const int multi = [] { const char* e = std::getenv("FV_CGA_MULTI"); return e ? std::atoi(e) : -1; }();
+    // the multi-order kernel takes all ng groups in one launch (grid.z); the tile kernel one per group
+    for (int g = 0; g < (multi ? 1 : ng) && !sio; ++g) {
       StageMark mk(p, 3, s);
       fv::CgAdjArgs ca{reinterpret_cast<const double2*>(a), reinterpret_cast<const double2*>(b), p->dg, p->dgofs,
                        p->cgt, p->G + (size_t)g * p->g_gstride, p->gofs, nullptr, p->L, NT, B, b0 + 4 * g, nf, m_lo,
-                       0, p->cga, 32 * p->g_tiles};
+                       0, p->cga, 32 * p->g_tiles, (long long)p->g_gstride};
       dim3 grid((Lt + 1 - m_lo + fv::ADJ_LC - 1) / fv::ADJ_LC, mc);
       const size_t smem = (size_t)2 * fv::ADJ_KS * fv::cga_bstride(nf) * sizeof(double) +
                           2 * (size_t)nf * 34 * 7 * sizeof(double2);
       // runs of consecutive orders per CTA (cg_adj_multi_kernel): two at 3-4 fields (three CTAs
       // per SM), four at 1-2 fields; FV_CGA_MULTI=0 selects the one-order tile kernel
-      static const int multi = [] { const char* e = std::getenv("FV_CGA_MULTI"); return e ? std::atoi(e) : -1; }();
       auto launch_multi = [&](auto nfc, auto noc) -> int {
         constexpr int NF_ = decltype(nfc)::value, NO_ = decltype(noc)::value;
         static std::atomic<unsigned long long> attr{0};
         FV_CUDA(smem_optin_once(&attr, p->device, fv::cg_adj_multi_kernel<NF_, NO_>));
-        const dim3 mgrid(grid.x, (mc + NO_ - 1) / NO_);
+        const dim3 mgrid(grid.x, (mc + NO_ - 1) / NO_, ng);
         fv::cg_adj_multi_kernel<NF_, NO_><<<mgrid, fv::CGA_THREADS, fv::CgaMulti<NF_, NO_>::bytes, s>>>(ca, mc);
         return FV_OK;
       };
