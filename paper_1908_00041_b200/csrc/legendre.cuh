@@ -1356,6 +1356,62 @@ __device__ __forceinline__ void adj_ks_run(double (&acc)[2][NT][2], const double
     for (int ii = I0; ii < I1; ++ii) dmma_m8n8k4(acc[ii][jn][0], acc[ii][jn][1], a[ii], b[jn]);
 }
 
+// A chunk that holds a single M-tile of real pairs (the benchmark grids: n_theta / 2 = 1 mod 128,
+// so every order's last chunk is ONE pair): with the regular split only consumer warp 0 has work,
+// 48 DMMAs per stage on one sub-partition.  Here the item's six (NT) n-tiles go to NT warps, both
+// parities each, eight DMMAs per stage and warp (every k-step that lies within Lt is run; before
+// the polar start the Legendre values are zeros).  Kept out of line: the item runs once per order
+// and must not add registers to legendre_adj_kernel's main loop.
+// (scalar arguments, not the AdjArgs struct: a reference to the kernel's parameter struct would
+// force a stack copy of it in the caller)
+struct AdjSoloOut {
+  double2* S;
+  SLayout lay;
+  int n_phi, n_theta, nfields, dbg;
+};
+template <int NT>
+__device__ __noinline__ uint32_t adj_solo_item(AdjSoloOut args, const int* pair_n, const int* pair_s, int Lt,
+                                               const double* smem, int stage_doubles, uint64_t* full, uint64_t* empty,
+                                               uint32_t sc, int m, int rc, int fb0, int lc0, int nlc, int cw,
+                                               int lane) {
+  const int g = lane >> 2, q = lane & 3;
+  const bool mine = cw < NT && !(args.dbg & 1);
+  const int p = rc * ADJ_RC + g;  // M-tile 0, row g
+  const int rn = __ldg(&pair_n[p]), rs = __ldg(&pair_s[p]);
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [parity][re/im] of n-tile cw
+  for (int lc = lc0; lc < nlc; ++lc, ++sc) {
+    const int stage = sc % ADJ_STAGES;
+    const int l0s = m + ADJ_LC * lc;
+    mbar_wait(&full[stage], (sc / ADJ_STAGES) & 1);
+    if (mine) {
+      const double* Ps = smem + (size_t)stage * stage_doubles;
+      const double* Gs = Ps + ADJ_PTILE;
+#pragma unroll
+      for (int t = 0; t < 2 * ADJ_KS; ++t) {
+        const int ks = t >> 1, par = t & 1;
+        if (l0s + 8 * ks <= Lt) {
+          const double a = lds_f64(&Ps[(par * ADJ_KS + ks) * 32 + adj_swz(g, q, 0)]);
+          const double b = lds_f64(&Gs[((par * ADJ_KS + ks) * NT + cw) * 32 + lane]);
+          dmma_m8n8k4(acc[par][0], acc[par][1], a, b);
+        }
+      }
+    }
+    mbar_arrive(&empty[stage]);
+  }
+  if (mine && !(args.dbg & 4) && rn >= 0) {
+    const int ser = 4 * cw + q;  // 6*field + 2*comp + sign
+    const int b = ser / 6, comp = (ser % 6) >> 1, sgn = ser & 1;
+    if (b < args.nfields && !(sgn == 1 && m == 0)) {
+      double2* dst = args.S + spec_bin(args.lay, m, sgn, args.n_phi) * args.lay.bs;
+      const long long rbase = (long long)(fb0 + b) * args.n_theta;
+      const double er = acc[0][0], ei = acc[0][1], orr = acc[1][0], oi = acc[1][1];
+      dst[spec_cr(args.lay, comp, rbase + rn)] = make_double2(er + orr, ei + oi);
+      if (rs >= 0) dst[spec_cr(args.lay, comp, rbase + rs)] = make_double2(er - orr, ei - oi);
+    }
+  }
+  return sc;
+}
+
 // Persistent: one CTA per SM walks the (order m, 128-pair chunk) items in
 // descending-work order (item = blockIdx.x + k * gridDim.x; m ascending), with
 // one stage counter across items, so the producers fill the next item's stages
@@ -1515,6 +1571,13 @@ __global__ void __launch_bounds__(kThreads, 1) legendre_adj_kernel(AdjArgs args)
       for (int o = 1; o < 8; o <<= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
 #pragma unroll
       for (int ii = 0; ii < 2; ++ii) mt_start[ii] = __shfl_sync(0xffffffffu, v, 8 * ii);
+    }
+    if (NT > 2 && args.nP - rc * ADJ_RC <= 8 && !args.trace) {
+      // a chunk with one M-tile of real pairs: its n-tiles over NT warps (adj_solo_item)
+      const AdjSoloOut so{args.S, args.lay, args.n_phi, args.n_theta, args.nfields, args.dbg};
+      sc = adj_solo_item<NT>(so, args.pair_n, args.pair_s, Lt, smem, SM::STAGE, full, empty, sc, m, rc, fb0,
+                             adj_first_stage(args, m, rc), nlc, cw, lane);
+      continue;
     }
     // the epilogue's ring indices, loaded now (their latency hides behind the item's
     // stages instead of sitting between the last DMMA and the stores)
