@@ -1554,6 +1554,7 @@ int forward_orders(fvPlan* p, const double2* S, const fv::SLayout& lay, double* 
       fv::FwdArgs args{p->X, p->F, p->start_l, p->start_v, p->dg, p->dgofs, p->pair_t, Lt, p->nP, p->nPpad,
                        p->nchunks, m_lo, dbg_mode(), mc, trace_buf(), trace_cta(), p->ptab_f, p->mtab_f, p->tofs, p->cmin,
                        ng, (long long)p->x_gstride, (long long)p->f_gstride, ks, p->Fx};
+      args.klast = (p->nP - fv::FWD_RC * (p->nchunks - 1) + 3) / 4;
       FV_TRY(dispatch_fwd(p, NT, args, mc, s));
     }
     if (sio)
