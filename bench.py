@@ -54,8 +54,8 @@ def canonical_flops(L: int, B: int) -> dict:
 
 
 # DMMA.8x8x4 instructions x 512 flops per C3 launch (ncu sm__inst_executed_pipe_tensor_subpipe_dmma.sum,
-# profiles/r02h_legendre_counts.csv; 42.54 M / 41.06 M before the padding pairs and dead chunks were skipped)
-EXEC_GFLOP_C3 = {"forward": 39326880 * 512 / 1e9, "adjoint": 39547014 * 512 / 1e9}
+# profiles/r02j_legendre_counts.csv; 42.54 M / 41.06 M before the padding pairs and dead chunks were skipped)
+EXEC_GFLOP_C3 = {"forward": 39326880 * 512 / 1e9, "adjoint": 39611148 * 512 / 1e9}
 
 
 def hbm_peak():
@@ -368,7 +368,7 @@ def run_ours(args, rank, world, local_rank):
                 "avg_launch_ms": leg_ms, "share_of_step": stage_ms["legendre"] / ms_total}
     if L == 1024 and B == 4:
         # executed DMMA work (the polar skip leaves out whole M-tile k-steps): ncu DMMA
-        # instruction counts x 512 flops of the C3 launches, profiles/r02h_legendre_counts.csv
+        # instruction counts x 512 flops of the C3 launches, profiles/r02j_legendre_counts.csv
         ex = (EXEC_GFLOP_C3["forward"] + EXEC_GFLOP_C3["adjoint"]) / 2
         roofline["executed_gflop_per_launch"] = dict(EXEC_GFLOP_C3, source="ncu DMMA count x 512")
         roofline["executed_frac"] = ex / (leg_ms / 1e3) / 1e3 / FP64_PEAK_MEASURED
