@@ -370,13 +370,17 @@ __global__ void cg_fwd_kernel(CgFwdArgs a) {
 // NF (fields in the group) is a template parameter so that every index
 // division is by a compile-time constant; all indices fit 32 bits.
 constexpr int CGF_THREADS = 256, CGF_MB = 32;
+// orders per CTA: 32 at three or four fields (one (order, field, sign) output per thread); a
+// one-field launch (C4) takes 128 orders and a two-field launch 64, so every thread has an output
+__host__ __device__ constexpr int cgf_mb(int nf) { return nf == 1 ? 128 : nf == 2 ? 64 : CGF_MB; }
 __host__ __device__ constexpr int cgf_nt(int nf) { return (12 * nf + 7) / 8; }
 __host__ __device__ constexpr int cgf_rs(int nf) { return 4 * cgf_nt(nf) + 1; }  // odd double2 row stride
 template <int NF, bool SPLIT = false, bool GROUPS = false>
 __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
-  constexpr int NV = 4 * cgf_nt(NF), RS = cgf_rs(NF), ROWS = CGF_MB + 2;
+  constexpr int MB = cgf_mb(NF);
+  constexpr int NV = 4 * cgf_nt(NF), RS = cgf_rs(NF), ROWS = MB + 2;
   const int l = blockIdx.y;
-  const int m0 = (blockIdx.x + a.c_lo / CGF_MB) * CGF_MB;  // the grid starts at the first written block
+  const int m0 = (blockIdx.x + a.c_lo / MB) * MB;  // the grid starts at the first written block
   if (m0 > l) return;
   // field group of this CTA (grid.z = 1: group 0); locals, not writes to the parameter struct
   // (a mutated kernel parameter is copied out of the constant bank: +29 us at C3)
@@ -390,10 +394,10 @@ __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
   // this thread's output (order m0 + mi, field b, sign sg); its nine factors are
   // loaded together with the staging loads (one memory round trip, not one more
   // after the barrier)
-  constexpr int NW = CGF_MB * NF * 2;
+  constexpr int NW = MB * NF * 2;
   static_assert(NW <= CGF_THREADS, "one (order, field, sign) output per thread");
   const int w = threadIdx.x;
-  const int mi = w % CGF_MB, b = (w / CGF_MB) % NF, sg = w / (CGF_MB * NF);
+  const int mi = w % MB, b = (w / MB) % NF, sg = w / (MB * NF);
   const int am = m0 + mi;
   const bool work = w < NW && am <= l && !(sg == 1 && am == 0) && am >= a.c_lo && am < a.c_hi;
   const int M = sg ? -am : am;

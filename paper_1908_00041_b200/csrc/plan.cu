@@ -1445,8 +1445,14 @@ int cg_forward(fvPlan* p, double* a, double* b, int B, int b0, int nf, int NT, i
   fv::CgFwdArgs ca{F ? F : p->F, reinterpret_cast<double2*>(a), reinterpret_cast<double2*>(b), p->cgt, p->L, 8 * NT, B, b0,
                    nf, c_lo, c_hi, nsplit, nsplit > 1 ? Fx : nullptr, (long long)p->f_gstride, (long long)p->f_gstride};
   // ngroups full 4-field groups (F buffers f_gstride apart) in one launch: grid.z
-  dim3 grid((c_hi + fv::CGF_MB - 1) / fv::CGF_MB - c_lo / fv::CGF_MB, p->L + 1, ngroups);
-  const size_t smem = (size_t)3 * (fv::CGF_MB + 2) * fv::cgf_rs(nf) * sizeof(double2);
+  const int mb = fv::cgf_mb(nf);
+  dim3 grid((c_hi + mb - 1) / mb - c_lo / mb, p->L + 1, ngroups);
+  const size_t smem = (size_t)3 * (mb + 2) * fv::cgf_rs(nf) * sizeof(double2);
+  if (nf == 1) {  // 56 KB of staging at 128 orders per CTA
+    static std::atomic<unsigned long long> attr{0}, attr_split{0};
+    FV_CUDA(smem_optin_once(&attr, p->device, fv::cg_fwd_tile_kernel<1, false>));
+    FV_CUDA(smem_optin_once(&attr_split, p->device, fv::cg_fwd_tile_kernel<1, true>));
+  }
   auto go = [&](auto split) {
     constexpr bool SP = decltype(split)::value;
     switch (nf) {
