@@ -363,6 +363,12 @@ __global__ void cg_fwd_kernel(CgFwdArgs a) {
   }
 }
 
+// 16-byte cp.async global -> shared; ok == false zero-fills (src-size 0; src must still be a valid address)
+__device__ __forceinline__ void cgs_cp16(void* dst_smem, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst_smem)), "l"(src), "r"(ok ? 16 : 0)
+               : "memory");
+}
+
 // Tiled forward CG: CTA per (degree l, block of 32 orders |m|).  The F rows it
 // reads (degrees l-1, l, l+1; orders m0-1 .. m0+32, contiguous in the tri
 // layout) are staged in shared memory with coalesced 16-byte loads; thread per
@@ -388,7 +394,6 @@ __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
   const double* const Fg = GROUPS ? a.F + blockIdx.z * a.fg_stride : a.F;
   const int b0g = GROUPS ? a.b0 + 4 * blockIdx.z : a.b0;
   extern __shared__ __align__(16) double2 cgf_smem[];  // [3][ROWS][RS]
-  constexpr int NE = 3 * ROWS * NV, PER = (NE + CGF_THREADS - 1) / CGF_THREADS;
   const int Lt = a.L + 1;
   const int K = (a.L + 1) * (a.L + 1), Kt = (Lt + 1) * (Lt + 1);
   // this thread's output (order m0 + mi, field b, sign sg); its nine factors are
@@ -409,40 +414,73 @@ __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
   const double x3 = tab(2, l - 1, M + 1), x4 = tab(3, l + 1, M + 1);
   const double x5 = tab(4, l - 1, M), x6 = tab(5, l + 1, M);
   const double u1 = tab(6, l, M - 1), u2 = tab(7, l, M), u3 = tab(8, l, M + 1);
-  double2 x[PER];
-  int off[PER];  // double2 offset of the staged F entry, -1 outside the table
+  // staging: the ROWS x NV entries of one degree are contiguous in the tri layout, so thread
+  // t < ST (row r0 = t / NV, column v = t % NV) reads entry t + ST u of each degree's segment
+  // in pass u (row r0 + RPP u, same column): no per-entry index arithmetic (the divisions of
+  // a flat entry index were two thirds of the kernel's instructions, which was issue bound)
+  constexpr int RPP = CGF_THREADS / NV, ST = RPP * NV, PASSES = (ROWS + RPP - 1) / RPP;
+  const int r0 = threadIdx.x / NV, v = threadIdx.x - r0 * NV;
+  const bool stager = threadIdx.x < ST;
+  const double2* const F2 = reinterpret_cast<const double2*>(Fg);
+  if constexpr (!SPLIT) {
+    // 16-byte cp.async straight into the padded rows (zero fill outside the table): nothing
+    // passes through registers, every copy of the thread is in flight at once
 #pragma unroll
-  for (int u = 0; u < PER; ++u) {  // all loads of the thread in flight before the stores
-    const int e = threadIdx.x + u * CGF_THREADS;
-    x[u] = make_double2(0.0, 0.0);
-    off[u] = -1;
-    if (e < NE) {
-      const int i = e / (ROWS * NV), r = (e / NV) % ROWS, v = e % NV;
-      const int lp = l - 1 + i, mp = m0 - 1 + r;
-      if (lp >= 0 && lp <= Lt && mp >= 0 && mp <= lp) {
-        off[u] = (lp * (lp + 1) / 2 + mp) * NV + v;
-        x[u] = __ldg(reinterpret_cast<const double2*>(Fg) + off[u]);
+    for (int i = 0; i < 3; ++i) {
+      const int lp = l - 1 + i;
+      const bool rowok = lp >= 0 && lp <= Lt;
+      const int base = (lp * (lp + 1) / 2 + m0 - 1) * NV + (int)threadIdx.x;
+#pragma unroll
+      for (int u = 0; u < PASSES; ++u) {
+        const int rr = r0 + RPP * u, mp = m0 - 1 + rr;
+        const bool ok = rowok && mp >= 0 && mp <= lp;
+        if (stager && rr < ROWS) cgs_cp16(&cgf_smem[(i * ROWS + rr) * RS + v], ok ? F2 + base + ST * u : F2, ok);
       }
     }
-  }
-  // split forward launches (SPLIT instantiation only: the unsplit kernel keeps its
-  // 80 registers and three CTAs per SM): add the partial F buffers 1.. in split order
-  if (SPLIT)
-  for (int sp = 1; sp < a.nsplit; ++sp) {
-    const double2* Fp = reinterpret_cast<const double2*>(a.Fx + (sp - 1) * a.fx_stride);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else {
+    // split forward launches: the partial F buffers 1.. are added in split order on the way
+    double2 x[3 * PASSES];
+    unsigned okmask = 0;  // bit i * PASSES + u: entry inside the table
 #pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      if (off[u] >= 0) {
-        const double2 y = __ldg(Fp + off[u]);
-        x[u].x += y.x;
-        x[u].y += y.y;
+    for (int i = 0; i < 3; ++i) {  // all loads of the thread in flight before the stores
+      const int lp = l - 1 + i;
+      const bool rowok = stager && lp >= 0 && lp <= Lt;
+      const int base = (lp * (lp + 1) / 2 + m0 - 1) * NV + (int)threadIdx.x;
+#pragma unroll
+      for (int u = 0; u < PASSES; ++u) {
+        const int mp = m0 - 1 + r0 + RPP * u;
+        const bool ok = rowok && r0 + RPP * u < ROWS && mp >= 0 && mp <= lp;
+        x[i * PASSES + u] = make_double2(0.0, 0.0);
+        if (ok) {
+          x[i * PASSES + u] = __ldg(F2 + base + ST * u);
+          okmask |= 1u << (i * PASSES + u);
+        }
       }
     }
-  }
+    for (int sp = 1; sp < a.nsplit; ++sp) {
+      const double2* Fp = reinterpret_cast<const double2*>(a.Fx + (sp - 1) * a.fx_stride);
 #pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const int e = threadIdx.x + u * CGF_THREADS;
-    if (e < NE) cgf_smem[e / NV * RS + e % NV] = x[u];
+      for (int i = 0; i < 3; ++i) {
+        const int lp = l - 1 + i;
+        const int base = (lp * (lp + 1) / 2 + m0 - 1) * NV + (int)threadIdx.x;
+#pragma unroll
+        for (int u = 0; u < PASSES; ++u) {
+          if (okmask >> (i * PASSES + u) & 1u) {
+            const double2 y = __ldg(Fp + base + ST * u);
+            x[i * PASSES + u].x += y.x;
+            x[i * PASSES + u].y += y.y;
+          }
+        }
+      }
+    }
+    if (stager) {
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int u = 0; u < PASSES; ++u)
+          if (r0 + RPP * u < ROWS) cgf_smem[(i * ROWS + r0 + RPP * u) * RS + v] = x[i * PASSES + u];
+    }
   }
   __syncthreads();
   if (!work) return;
@@ -465,12 +503,6 @@ __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
   const size_t o = (size_t)(b0g + b) * K + (l * l + l + M);
   a.A[o] = make_double2(ar, ai);
   a.Bc[o] = make_double2(br, bi);
-}
-
-// 16-byte cp.async global -> shared; ok == false zero-fills (src-size 0; src must still be a valid address)
-__device__ __forceinline__ void cgs_cp16(void* dst_smem, const void* src, bool ok) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst_smem)), "l"(src), "r"(ok ? 16 : 0)
-               : "memory");
 }
 
 // ---------------------------------------------------------------------------
