@@ -434,7 +434,8 @@ __global__ void __launch_bounds__(CGF_THREADS) cg_fwd_tile_kernel(CgFwdArgs a) {
       for (int u = 0; u < PASSES; ++u) {
         const int rr = r0 + RPP * u, mp = m0 - 1 + rr;
         const bool ok = rowok && mp >= 0 && mp <= lp;
-        if (stager && rr < ROWS) cgs_cp16(&cgf_smem[(i * ROWS + rr) * RS + v], ok ? F2 + base + ST * u : F2, ok);
+        // (an unsigned 32-bit index select, not a pointer select: no 64-bit select / sign extension)
+        if (stager && rr < ROWS) cgs_cp16(&cgf_smem[(i * ROWS + rr) * RS + v], F2 + (ok ? (unsigned)(base + ST * u) : 0u), ok);
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
@@ -757,15 +758,34 @@ __global__ void __launch_bounds__(CGA_THREADS) cg_adj_multi_kernel(CgAdjArgs a, 
   double2* Ds = reinterpret_cast<double2*>(Fs + NO * 18 * 32);    // (d, gamma) [NO][32 rows]
   const int K = (a.L + 1) * (a.L + 1);
   const int lp0 = am0 + c * LC - 1;
-  constexpr int NE = NF * R * 2 * NC;
-  for (int e = threadIdx.x; e < NE; e += CGA_THREADS) {
-    const int j = e % (2 * NC), r = (e / (2 * NC)) % R, bb = e / (2 * NC * R);
-    const int lp = lp0 + r;
+  if constexpr (CGA_THREADS % (2 * NC) == 0 && CGA_THREADS / (2 * NC) <= R) {
+    // thread t: column j = t % 2NC (fixed order mp), staged rows t / 2NC + RP u of the NF x R
+    // (field, degree) rows; (field, degree) advance incrementally (no per-entry divisions)
+    constexpr int RP = CGA_THREADS / (2 * NC), NROW = NF * R;
+    const int j = threadIdx.x % (2 * NC);
     const int mp = j < NC ? am0 - 1 + j : -(am0 + NO) + (j - NC);
-    const bool ok = lp >= 0 && lp <= a.L && abs(mp) <= lp;
-    const size_t o = ok ? (size_t)(b0g + bb) * K + (lp * lp + lp + mp) : 0;
-    cgs_cp16(&As[(bb * R + r) * CS + j], a.A + o, ok);
-    cgs_cp16(&Bs[(bb * R + r) * CS + j], a.Bc + o, ok);
+    const int amp = abs(mp);
+    int row = threadIdx.x / (2 * NC), r = row, bb = 0;  // RP <= R: the first row is in field 0
+    for (; row < NROW; row += RP) {
+      const int lp = lp0 + r;
+      const bool ok = lp >= 0 && lp <= a.L && amp <= lp;
+      const size_t o = ok ? (size_t)(b0g + bb) * K + (lp * lp + lp + mp) : 0;
+      cgs_cp16(&As[row * CS + j], a.A + o, ok);
+      cgs_cp16(&Bs[row * CS + j], a.Bc + o, ok);
+      r += RP;
+      if (r >= R) { r -= R; ++bb; }
+    }
+  } else {
+    constexpr int NE = NF * R * 2 * NC;
+    for (int e = threadIdx.x; e < NE; e += CGA_THREADS) {
+      const int j = e % (2 * NC), r = (e / (2 * NC)) % R, bb = e / (2 * NC * R);
+      const int lp = lp0 + r;
+      const int mp = j < NC ? am0 - 1 + j : -(am0 + NO) + (j - NC);
+      const bool ok = lp >= 0 && lp <= a.L && abs(mp) <= lp;
+      const size_t o = ok ? (size_t)(b0g + bb) * K + (lp * lp + lp + mp) : 0;
+      cgs_cp16(&As[(bb * R + r) * CS + j], a.A + o, ok);
+      cgs_cp16(&Bs[(bb * R + r) * CS + j], a.Bc + o, ok);
+    }
   }
   for (int e = threadIdx.x; e < NO * 18 * 16; e += CGA_THREADS) {
     const int h = e % 16, k = (e / 16) % 18, o = e / (16 * 18);
@@ -779,7 +799,11 @@ __global__ void __launch_bounds__(CGA_THREADS) cg_adj_multi_kernel(CgAdjArgs a, 
     const bool ok = o < no && am + c * LC + idx <= Lt;
     cgs_cp16(&Ds[e], a.dg + (ok ? a.dgofs[am] + c * LC + idx : 0), ok);
   }
-  for (int i = threadIdx.x; i < 2 * C::GBUF; i += CGA_THREADS) Gs[i] = 0.0;
+  // padding columns 12 NF .. 8 NT - 1 are never written below: zero the buffers once (with
+  // 12 NF a multiple of 8 the (row, field, sign) threads write every copied-out entry of a
+  // tile for every order, zeros included)
+  if constexpr ((12 * NF) % 8 != 0)
+    for (int i = threadIdx.x; i < 2 * C::GBUF; i += CGA_THREADS) Gs[i] = 0.0;
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   const int w = threadIdx.x;
